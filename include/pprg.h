@@ -1,0 +1,149 @@
+/* pprg.h — C ABI of the B200-native single-source PPR engine.
+ *
+ * The drop-in boundary for the reference's C++ core API
+ * (/root/reference/proj/core/include/ppr/*.hpp). Plain pointers and sizes, no
+ * C++ or torch types. Each entry point names the reference interface it
+ * replaces (file:line under /root/reference/proj). The C++ shim in
+ * paper_2101_03652_b200/cpp (namespace ppr::) re-exposes these with the
+ * reference's own signatures and exception types; INTEGRATION.md shows the
+ * binding.
+ *
+ * Conventions
+ *   - Graphs are immutable device-resident handles; each handle owns its CUDA
+ *     stream and is safe to share between host threads (calls serialize).
+ *   - Output vectors are CALLER-allocated, query-major: out[q * n + v] for
+ *     query q (k queries per call). Host memory unless the *_device variant or
+ *     PPRG_OUT_DEVICE flag says the pointers are device pointers. NULL skips.
+ *   - Status codes: PPRG_OK, PPRG_EINVAL (std::invalid_argument in the
+ *     reference), PPRG_EDATA (std::runtime_error), PPRG_EINTERNAL
+ *     (std::logic_error), PPRG_ECUDA / PPRG_ENCCL (device / collective).
+ *     pprg_last_error() returns the calling thread's last message.
+ */
+#ifndef PPRG_H
+#define PPRG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPRG_OK 0
+#define PPRG_EINVAL 1
+#define PPRG_EDATA 2
+#define PPRG_EINTERNAL 3
+#define PPRG_ECUDA 4
+#define PPRG_ENCCL 5
+
+#define PPRG_OUT_DEVICE 1u /* output pointers are device pointers on the graph's GPU */
+
+#define PPRG_RNG_PHILOX4X32_10 2u /* PPRW rng-id byte for our walk index (reference uses 1 = mt19937_64, rng.hpp:10) */
+
+typedef struct pprg_graph pprg_graph;
+typedef struct pprg_index pprg_index;
+
+/* Per-query statistics (PPRVector fields, types.hpp:57-65, plus device counters). */
+typedef struct {
+  double achieved_r_sum;   /* PPRVector::achieved_r_sum */
+  uint64_t pushes;         /* PPRVector::pushes: edge pushes, deg_eff per node push */
+  uint64_t walks;          /* PPRVector::walks */
+  uint32_t sweeps;         /* global-phase sweeps (PowerPush) or iterations (PowItr) */
+  uint32_t local_levels;   /* frontier levels of the queue phase */
+  int32_t used_scan_phase; /* PowerPushTrace::used_scan_phase (push.hpp:97-100) */
+  int32_t reserved;
+} pprg_query_stats;
+
+/* Per-call device counters (for the roofline). */
+typedef struct {
+  double device_ms;        /* CUDA-event time of the device section */
+  double sweep_ms;         /* CUDA-event time of the global-sweep kernels */
+  uint64_t alg_bytes;      /* SURVEY 8(d) algorithmic bytes of the global sweeps */
+  uint64_t sweep_launches; /* persistent sweep-kernel launches */
+  uint32_t max_sweeps;
+  uint32_t kernel_launches;/* kernels this library launched for the call */
+} pprg_call_stats;
+
+const char* pprg_last_error(void);
+int pprg_version(void);
+int pprg_device_count(int* count);
+
+/* ---- graphs (graph.hpp) -------------------------------------------------- */
+/* Graph(std::vector<uint64_t> out_offsets, std::vector<NodeId> out_neighbors)
+ * graph.hpp:18, graph.cpp:13-34 (same validation and messages). */
+int pprg_graph_create(const uint64_t* offsets, const uint32_t* neighbors, uint64_t n, int device,
+                      pprg_graph** out);
+/* build_graph_from_edges(edges) graph.hpp:92, graph.cpp:36-63; pairs = 2*count
+ * u64 (src, dst), bit-exact CSR (relabel, input-order neighbours). */
+int pprg_graph_build_from_edges(const uint64_t* pairs, uint64_t count, int device,
+                                pprg_graph** out);
+/* Synthetic inputs (no reference counterpart). Cleaned (self-loops
+ * and duplicates removed), sorted, then built with build_graph_from_edges
+ * semantics. edges_out (optional, capacity draws) receives the canonical
+ * cleaned list as (src << 32 | dst) before relabelling; *edge_count_out its length. */
+int pprg_graph_generate_rmat(int scale, uint64_t edge_factor, double a, double b, double c,
+                             uint64_t seed, int device, uint64_t* edges_out,
+                             uint64_t* edge_count_out, pprg_graph** out);
+int pprg_graph_generate_chung_lu(uint64_t n, uint64_t draws, double beta, uint64_t seed, int device,
+                                 uint64_t* edges_out, uint64_t* edge_count_out, pprg_graph** out);
+/* n(), m(), dead_ends().size() — graph.hpp:20-21,33 */
+int pprg_graph_info(const pprg_graph* g, uint64_t* n, uint64_t* m, uint64_t* dead_ends);
+/* out_offsets()/out_neighbors()/dead_ends() — graph.hpp:31-33 (device -> host) */
+int pprg_graph_export(const pprg_graph* g, uint64_t* offsets, uint32_t* neighbors,
+                      uint32_t* dead_ends);
+/* In-CSR used by the pull sweeps (internal layout, exported for tests). */
+int pprg_graph_export_transpose(pprg_graph* g, uint64_t* in_offsets, uint32_t* in_neighbors);
+void pprg_graph_destroy(pprg_graph* g);
+
+/* ---- high-precision engines (push.hpp) ----------------------------------- */
+/* power_iteration(g, s, alpha, lambda) push.hpp:80-81, push.cpp:81-108, for k sources. */
+int pprg_power_iteration(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                         double lambda, double* reserve_out, double* residue_out, uint32_t flags,
+                         pprg_query_stats* qstats, pprg_call_stats* cstats);
+/* sim_forward_push push.hpp:86-87, push.cpp:110-138 */
+int pprg_sim_forward_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                          double lambda, double* reserve_out, double* residue_out, uint32_t flags,
+                          pprg_query_stats* qstats, pprg_call_stats* cstats);
+/* fifo_forward_push(g, s, alpha, r_max, lambda_stop) push.hpp:92-94, push.cpp:140-149;
+ * lambda_stop <= 0 means none. */
+int pprg_fifo_forward_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                           double r_max, double lambda_stop, double* reserve_out,
+                           double* residue_out, uint32_t flags, pprg_query_stats* qstats,
+                           pprg_call_stats* cstats);
+/* power_push(g, s, alpha, lambda, cfg) push.hpp:105-107, push.cpp:151-206;
+ * scan_threshold < 0 means the default n/4 (types.hpp:25). epoch_r_max_out
+ * (optional, epoch_num doubles) = PowerPushTrace::epoch_r_max. */
+int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                    double lambda, uint32_t epoch_num, int64_t scan_threshold,
+                    double* reserve_out, double* residue_out, uint32_t flags,
+                    pprg_query_stats* qstats, pprg_call_stats* cstats, double* epoch_r_max_out);
+
+/* ---- SpeedPPR (speedppr.hpp, walk_index.hpp) ------------------------------- */
+/* compute_walk_budget(n, eps, mu) speedppr.hpp:16-17 */
+int pprg_walk_budget(uint64_t n, double epsilon, double mu, uint64_t* out);
+/* build_index(g, alpha, seed) walk_index.hpp:50, walk_index.cpp:44-54; Philox
+ * walks keyed (seed, slot) — rng-id PPRG_RNG_PHILOX4X32_10. */
+int pprg_index_build(pprg_graph* g, double alpha, uint64_t seed, pprg_index** out);
+/* WalkIndex(alpha, seed, rng_id, offsets, endpoints) walk_index.hpp:23-24 (offsets
+ * must equal the graph's out-offsets). */
+int pprg_index_from_host(pprg_graph* g, double alpha, uint64_t seed, const uint32_t* endpoints,
+                         pprg_index** out);
+int pprg_index_export(const pprg_index* idx, uint32_t* endpoints);
+void pprg_index_destroy(pprg_index* idx);
+/* speedppr_query(g, s, cfg, index) speedppr.hpp:37-38, speedppr.cpp:74-111;
+ * mu <= 0 means 1/n; idx may be NULL. */
+int pprg_speedppr(pprg_graph* g, const pprg_index* idx, const uint32_t* sources, uint32_t k,
+                  double alpha, double epsilon, double mu, uint64_t seed, double* estimates_out,
+                  uint32_t flags, pprg_query_stats* qstats, pprg_call_stats* cstats);
+/* random_walk(g, start, source, alpha, rng) walk_index.hpp:12 for a batch of
+ * (start_i, k_i, v_i) walk ids under one tag (test hook for the walk stream). */
+int pprg_walk_terminals(pprg_graph* g, const uint32_t* starts, const uint32_t* ks,
+                        const uint32_t* vs, uint64_t count, uint32_t source, uint32_t tag,
+                        double alpha, uint64_t seed, uint32_t* out);
+
+/* ---- device buffers for device-resident outputs (bench / zero-copy) ------- */
+int pprg_device_alloc(int device, uint64_t bytes, void** out);
+int pprg_device_free(int device, void* p);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,384 @@
+// extern "C" boundary (include/pprg.h): argument checks with the reference's
+// error behaviour, exception -> status mapping, per-thread error message.
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pprg.h"
+#include "internal.h"
+
+struct pprg_graph {
+  std::unique_ptr<pprg::Graph> g;
+};
+struct pprg_index {
+  std::unique_ptr<pprg::WalkIndex> w;
+  pprg_graph* owner;
+};
+
+namespace pprg {
+void release_workspaces(const Graph* g);
+}
+
+namespace {
+thread_local std::string t_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return PPRG_OK;
+  } catch (const pprg::Error& e) {
+    t_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    t_err = std::string("out of host memory: ") + e.what();
+    return PPRG_EINTERNAL;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return PPRG_EINTERNAL;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) pprg::fail(PPRG_EINVAL, msg);
+}
+
+void fill_stats(const std::vector<pprg::ColumnStats>& cs, const pprg::CallStats& call, uint32_t k,
+                pprg_query_stats* q, pprg_call_stats* c) {
+  if (q)
+    for (uint32_t i = 0; i < k; ++i) {
+      q[i].achieved_r_sum = cs[i].r_sum;
+      q[i].pushes = cs[i].pushes;
+      q[i].walks = cs[i].walks;
+      q[i].sweeps = cs[i].sweeps;
+      q[i].local_levels = cs[i].local_levels;
+      q[i].used_scan_phase = cs[i].used_scan_phase;
+      q[i].reserved = 0;
+    }
+  if (c) {
+    c->device_ms = call.device_ms;
+    c->sweep_ms = call.sweep_ms;
+    c->alg_bytes = call.alg_bytes;
+    c->sweep_launches = call.sweep_launches;
+    c->max_sweeps = call.max_sweeps;
+    c->kernel_launches = call.kernel_launches;
+  }
+}
+
+// alpha in (0,1): the reference admits alpha = 0 (types.hpp:37) but then never
+// terminates; the device path rejects it instead of spinning.
+void check_alpha(double alpha) {
+  require(alpha > 0.0 && alpha < 1.0, "alpha must be in (0,1)");
+}
+
+int push_engine(pprg_graph* g, pprg::Engine eng, const uint32_t* sources, uint32_t k, double alpha,
+                double lambda, uint32_t epoch_num, int64_t scan_threshold, double r_max,
+                double lambda_stop, double* reserve_out, double* residue_out, uint32_t flags,
+                pprg_query_stats* q, pprg_call_stats* c) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    require(k == 0 || sources, "null sources");
+    check_alpha(alpha);
+    std::vector<pprg::ColumnStats> cs(k);
+    pprg::CallStats call;
+    pprg::Outputs out{reserve_out, residue_out, (flags & PPRG_OUT_DEVICE) != 0};
+    if (k)
+      pprg::run_push_engine(*g->g, eng, sources, k, alpha, lambda, epoch_num, scan_threshold,
+                            r_max, lambda_stop, out, cs.data(), &call);
+    fill_stats(cs, call, k, q, c);
+  });
+}
+}  // namespace
+
+extern "C" {
+
+const char* pprg_last_error(void) { return t_err.c_str(); }
+int pprg_version(void) { return 1; }
+
+int pprg_device_count(int* count) {
+  return guard([&] { PPRG_CUDA(cudaGetDeviceCount(count)); });
+}
+
+int pprg_graph_create(const uint64_t* offsets, const uint32_t* neighbors, uint64_t n, int device,
+                      pprg_graph** out) {
+  return guard([&] {
+    require(out && offsets, "null argument");
+    require(neighbors || offsets[n] == 0, "null neighbors");
+    auto h = new pprg_graph;
+    try {
+      h->g = pprg::graph_from_csr(offsets, neighbors, n, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int pprg_graph_build_from_edges(const uint64_t* pairs, uint64_t count, int device,
+                                pprg_graph** out) {
+  return guard([&] {
+    require(out && (pairs || count == 0), "null argument");
+    auto h = new pprg_graph;
+    try {
+      h->g = pprg::graph_from_edges(pairs, count, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int pprg_graph_generate_rmat(int scale, uint64_t edge_factor, double a, double b, double c,
+                             uint64_t seed, int device, uint64_t* edges_out,
+                             uint64_t* edge_count_out, pprg_graph** out) {
+  return guard([&] {
+    require(out != nullptr, "null argument");
+    std::vector<uint64_t> edges;
+    auto h = new pprg_graph;
+    try {
+      h->g = pprg::graph_rmat(scale, edge_factor, a, b, c, seed, device,
+                              edges_out || edge_count_out ? &edges : nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    if (edges_out) std::memcpy(edges_out, edges.data(), 8 * edges.size());
+    if (edge_count_out) *edge_count_out = edges.size();
+    *out = h;
+  });
+}
+
+int pprg_graph_generate_chung_lu(uint64_t n, uint64_t draws, double beta, uint64_t seed, int device,
+                                 uint64_t* edges_out, uint64_t* edge_count_out, pprg_graph** out) {
+  return guard([&] {
+    require(out != nullptr, "null argument");
+    std::vector<uint64_t> edges;
+    auto h = new pprg_graph;
+    try {
+      h->g = pprg::graph_chung_lu(n, draws, beta, seed, device,
+                                  edges_out || edge_count_out ? &edges : nullptr);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    if (edges_out) std::memcpy(edges_out, edges.data(), 8 * edges.size());
+    if (edge_count_out) *edge_count_out = edges.size();
+    *out = h;
+  });
+}
+
+int pprg_graph_info(const pprg_graph* g, uint64_t* n, uint64_t* m, uint64_t* dead_ends) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    if (n) *n = g->g->n;
+    if (m) *m = g->g->m;
+    if (dead_ends) *dead_ends = g->g->n_dead;
+  });
+}
+
+int pprg_graph_export(const pprg_graph* g, uint64_t* offsets, uint32_t* neighbors,
+                      uint32_t* dead_ends) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    pprg::Graph& G = *g->g;
+    pprg::DeviceGuard dg(G.device);
+    std::lock_guard<std::mutex> lk(G.mu);
+    if (offsets)
+      PPRG_CUDA(cudaMemcpyAsync(offsets, G.off.get(), 8 * (G.n + 1), cudaMemcpyDeviceToHost, G.stream));
+    if (neighbors && G.m)
+      PPRG_CUDA(cudaMemcpyAsync(neighbors, G.nbr.get(), 4 * G.m, cudaMemcpyDeviceToHost, G.stream));
+    if (dead_ends && G.n_dead)
+      PPRG_CUDA(cudaMemcpyAsync(dead_ends, G.dead.get(), 4 * G.n_dead, cudaMemcpyDeviceToHost, G.stream));
+    PPRG_CUDA(cudaStreamSynchronize(G.stream));
+  });
+}
+
+int pprg_graph_export_transpose(pprg_graph* g, uint64_t* in_offsets, uint32_t* in_neighbors) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    pprg::Graph& G = *g->g;
+    pprg::DeviceGuard dg(G.device);
+    std::lock_guard<std::mutex> lk(G.mu);
+    G.ensure_transpose();
+    if (in_offsets)
+      PPRG_CUDA(cudaMemcpyAsync(in_offsets, G.in_off.get(), 8 * (G.n + 1), cudaMemcpyDeviceToHost, G.stream));
+    if (in_neighbors && G.m)
+      PPRG_CUDA(cudaMemcpyAsync(in_neighbors, G.in_nbr.get(), 4 * G.m, cudaMemcpyDeviceToHost, G.stream));
+    PPRG_CUDA(cudaStreamSynchronize(G.stream));
+  });
+}
+
+void pprg_graph_destroy(pprg_graph* g) {
+  if (!g) return;
+  try {
+    pprg::DeviceGuard dg(g->g ? g->g->device : 0);
+    pprg::release_workspaces(g->g.get());
+    g->g.reset();
+  } catch (...) {
+  }
+  delete g;
+}
+
+int pprg_power_iteration(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                         double lambda, double* reserve_out, double* residue_out, uint32_t flags,
+                         pprg_query_stats* q, pprg_call_stats* c) {
+  // power_iteration validates nothing; lambda >= 1 => 0 iterations
+  return push_engine(g, pprg::Engine::PowItr, sources, k, alpha, lambda, 0, -1, 0, 0, reserve_out,
+                     residue_out, flags, q, c);
+}
+
+int pprg_sim_forward_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                          double lambda, double* reserve_out, double* residue_out, uint32_t flags,
+                          pprg_query_stats* q, pprg_call_stats* c) {
+  return push_engine(g, pprg::Engine::SimFwdPush, sources, k, alpha, lambda, 0, -1, 0, 0,
+                     reserve_out, residue_out, flags, q, c);
+}
+
+int pprg_fifo_forward_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                           double r_max, double lambda_stop, double* reserve_out,
+                           double* residue_out, uint32_t flags, pprg_query_stats* q,
+                           pprg_call_stats* c) {
+  if (!(r_max > 0.0)) {  // push.cpp:142
+    t_err = "fifo_forward_push: r_max must be positive";
+    return PPRG_EINVAL;
+  }
+  return push_engine(g, pprg::Engine::Fifo, sources, k, alpha, 0.0, 0, -1, r_max, lambda_stop,
+                     reserve_out, residue_out, flags, q, c);
+}
+
+int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                    double lambda, uint32_t epoch_num, int64_t scan_threshold,
+                    double* reserve_out, double* residue_out, uint32_t flags,
+                    pprg_query_stats* q, pprg_call_stats* c, double* epoch_r_max_out) {
+  if (!(lambda > 0.0 && lambda <= 1.0)) {  // push.cpp:154-155
+    t_err = "power_push: lambda must be in (0,1]";
+    return PPRG_EINVAL;
+  }
+  if (epoch_num == 0) {  // types.hpp:45
+    t_err = "epoch_num must be positive";
+    return PPRG_EINVAL;
+  }
+  const int rc = push_engine(g, pprg::Engine::PowerPush, sources, k, alpha, lambda, epoch_num,
+                             scan_threshold, 0, 0, reserve_out, residue_out, flags, q, c);
+  if (rc == PPRG_OK && epoch_r_max_out) {
+    const double m_eff = (double)g->g->m_eff();
+    for (uint32_t e = 1; e <= epoch_num; ++e)
+      epoch_r_max_out[e - 1] = std::pow(lambda, static_cast<double>(e) / epoch_num) / m_eff;
+  }
+  return rc;
+}
+
+int pprg_walk_budget(uint64_t n, double epsilon, double mu, uint64_t* out) {
+  return guard([&] {
+    // walk_budget_real, speedppr.cpp:8-14 (same checks)
+    require(n >= 2, "walk budget: need n >= 2");
+    require(epsilon > 0.0, "walk budget: epsilon must be positive");
+    require(mu > 0.0 && mu <= 1.0, "walk budget: mu must be in (0,1]");
+    *out = static_cast<uint64_t>(std::ceil(2.0 * (2.0 * epsilon / 3.0 + 2.0) *
+                                           std::log(static_cast<double>(n)) /
+                                           (epsilon * epsilon * mu)));
+  });
+}
+
+int pprg_index_build(pprg_graph* g, double alpha, uint64_t seed, pprg_index** out) {
+  return guard([&] {
+    require(g && g->g && out, "null argument");
+    check_alpha(alpha);
+    auto h = new pprg_index;
+    h->owner = g;
+    try {
+      h->w = pprg::index_build(*g->g, alpha, seed);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int pprg_index_from_host(pprg_graph* g, double alpha, uint64_t seed, const uint32_t* endpoints,
+                         pprg_index** out) {
+  return guard([&] {
+    require(g && g->g && out && (endpoints || g->g->m == 0), "null argument");
+    auto h = new pprg_index;
+    h->owner = g;
+    try {
+      h->w = pprg::index_from_host(*g->g, alpha, seed, endpoints);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int pprg_index_export(const pprg_index* idx, uint32_t* endpoints) {
+  return guard([&] {
+    require(idx && idx->w && endpoints, "null argument");
+    pprg::DeviceGuard dg(idx->w->device);
+    if (idx->w->m)
+      PPRG_CUDA(cudaMemcpy(endpoints, idx->w->endpoints.get(), 4 * idx->w->m, cudaMemcpyDeviceToHost));
+  });
+}
+
+void pprg_index_destroy(pprg_index* idx) {
+  if (!idx) return;
+  try {
+    pprg::DeviceGuard dg(idx->w ? idx->w->device : 0);
+    idx->w.reset();
+  } catch (...) {
+  }
+  delete idx;
+}
+
+int pprg_speedppr(pprg_graph* g, const pprg_index* idx, const uint32_t* sources, uint32_t k,
+                  double alpha, double epsilon, double mu, uint64_t seed, double* estimates_out,
+                  uint32_t flags, pprg_query_stats* q, pprg_call_stats* c) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    require(k == 0 || sources, "null sources");
+    // QueryConfig::validate + speedppr.cpp:76-83
+    require(epsilon > 0.0, "epsilon must be positive");
+    require(!(mu > 0.0) || mu <= 1.0, "mu must be in (0,1]");
+    check_alpha(alpha);
+    if (idx) {
+      if (idx->w->m != g->g->m || idx->owner->g->n != g->g->n)
+        pprg::fail(PPRG_EDATA, "walk index does not match the graph shape");
+      if (idx->w->alpha != alpha) pprg::fail(PPRG_EDATA, "walk index was built for a different alpha");
+    }
+    std::vector<pprg::ColumnStats> cs(k);
+    pprg::CallStats call;
+    if (k)
+      pprg::speedppr(*g->g, idx ? idx->w.get() : nullptr, sources, k, alpha, epsilon, mu, seed,
+                     estimates_out, (flags & PPRG_OUT_DEVICE) != 0, cs.data(), &call);
+    fill_stats(cs, call, k, q, c);
+  });
+}
+
+int pprg_walk_terminals(pprg_graph* g, const uint32_t* starts, const uint32_t* ks,
+                        const uint32_t* vs, uint64_t count, uint32_t source, uint32_t tag,
+                        double alpha, uint64_t seed, uint32_t* out) {
+  return guard([&] {
+    require(g && g->g && out, "null argument");
+    pprg::walk_terminals(*g->g, starts, ks, vs, count, source, tag, alpha, seed, out);
+  });
+}
+
+int pprg_device_alloc(int device, uint64_t bytes, void** out) {
+  return guard([&] {
+    pprg::DeviceGuard dg(device);
+    PPRG_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+  });
+}
+
+int pprg_device_free(int device, void* p) {
+  return guard([&] {
+    pprg::DeviceGuard dg(device);
+    PPRG_CUDA(cudaFree(p));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+// Shared device/host helpers for the PPR engine (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+namespace pprg {
+
+// ---- errors (mapped to PPRG_* codes at the C ABI) --------------------------
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+enum { OK = 0, EINVAL_ = 1, EDATA = 2, EINTERNAL = 3, ECUDA = 4, ENCCL = 5 };
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define PPRG_CUDA(call)                                                              \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      ::pprg::fail(::pprg::ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---- Philox4x32-10 (Salmon et al. SC'11) -----------------------------------
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+__host__ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+#if defined(__CUDA_ARCH__)
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+#else
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c.x, p1 = (uint64_t)0xCD9E8D57u * c.z;
+    const uint32_t lo0 = (uint32_t)p0, hi0 = (uint32_t)(p0 >> 32);
+    const uint32_t lo1 = (uint32_t)p1, hi1 = (uint32_t)(p1 >> 32);
+#endif
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+  }
+  return c;
+}
+
+__host__ __device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) {
+#if defined(__CUDA_ARCH__)
+  return __umul64hi(a, b);
+#else
+  return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// Walk-step randomness, the product's definition:
+// step t of walk (k, v) under tag (source id, or kIndexTag for the index)
+// is Philox(key = seed, ctr = (k, v, tag, t)). Word pair (x,y) gives the
+// 53-bit stop uniform (rng.hpp:21 semantics), (z,w) the 64-bit neighbour
+// draw, bounded by Lemire multiply-high with rejection (rng.hpp:24-35
+// semantics); rejected draws re-key word 3 as t + (retry << 24).
+constexpr uint32_t kIndexTag = 0xFFFFFFFFu;
+
+__host__ __device__ __forceinline__ uint64_t walk_below(uint64_t first, uint64_t bound, uint32_t k,
+                                                        uint32_t v, uint32_t tag, uint32_t t,
+                                                        uint32_t k0, uint32_t k1) {
+  uint64_t hi = mulhi64(first, bound), low = first * bound;
+  if (low < bound) {
+    const uint64_t threshold = (0 - bound) % bound;
+    uint32_t retry = 1;
+    while (low < threshold) {
+      const U4 o = philox4x32_10(U4{k, v, tag, t + (retry++ << 24)}, k0, k1);
+      const uint64_t r = ((uint64_t)o.w << 32) | o.z;
+      hi = mulhi64(r, bound);
+      low = r * bound;
+    }
+  }
+  return hi;
+}
+
+// Full alpha-random walk from `start` (walk_index.cpp:10-17 semantics).
+__host__ __device__ __forceinline__ uint32_t philox_walk(const uint64_t* off, const uint32_t* nbr,
+                                                         uint32_t start, uint32_t source,
+                                                         double alpha, uint64_t seed, uint32_t k,
+                                                         uint32_t v, uint32_t tag) {
+  const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  uint32_t cur = start;
+  for (uint32_t t = 0;; ++t) {
+    const U4 o = philox4x32_10(U4{k, v, tag, t}, k0, k1);
+    const double u = (double)((((uint64_t)o.y << 32) | o.x) >> 11) * 0x1.0p-53;
+    if (!(u >= alpha)) return cur;
+    const uint64_t b = off[cur], d = off[cur + 1] - b;
+    if (d == 0) {
+      cur = source;
+    } else {
+      cur = nbr[b + walk_below(((uint64_t)o.w << 32) | o.z, d, k, v, tag, t, k0, k1)];
+    }
+  }
+}
+
+// ---- device memory helpers -------------------------------------------------
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t count) { alloc(count); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr; o.n = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); p = o.p; n = o.n; o.p = nullptr; o.n = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) PPRG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  T* get() const { return p; }
+};
+
+#if defined(__CUDACC__)
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned ld_acquire32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Sense-free grid barrier over a monotonically increasing counter; `target`
+// = (barrier generation + 1) * gridDim.x. Requires a cooperative launch (all
+// blocks co-resident). The gpu-scope fence also invalidates the SM's L1, so
+// every sweep starts from values at least as new as the previous sweep's.
+__device__ __forceinline__ void grid_barrier(unsigned long long* counter,
+                                             unsigned long long target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(counter, 1ull);
+    while (ld_acquire(counter) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+#endif
+
+}  // namespace pprg

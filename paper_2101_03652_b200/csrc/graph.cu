@@ -1,0 +1,527 @@
+// Graph build and device residency (hot-path subsystem (1)).
+//
+// Reference semantics reproduced bit-exactly (graph.cpp:13-63):
+//   * survivors = sorted unique endpoint ids, new id = rank (:40-51)
+//   * offsets = exclusive scan of per-source counts (:54-56)
+//   * neighbours in input order per source (:58-60) -- a stable radix sort
+//     keyed on the relabelled source gives exactly the cursor scatter order
+//   * dead_ends = ascending ids with out-degree 0 (:19-20); validate (:24-34)
+// Generators (R-MAT, Chung-Lu) are counter-based (Philox keyed by
+// (seed, edge index)) so host and device agree, then cleaned (self-loops and
+// duplicates removed) and sorted before the reference build semantics apply.
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <string>
+
+#include "internal.h"
+
+namespace pprg {
+namespace {
+
+constexpr int TB = 256;
+inline unsigned blocks_for(uint64_t n, int tb = TB) {
+  uint64_t b = (n + tb - 1) / tb;
+  return (unsigned)(b ? (b > 0x7fffffffull ? 0x7fffffffull : b) : 1);
+}
+
+#define GRID_STRIDE(i, cnt) \
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < (cnt); i += (uint64_t)gridDim.x * blockDim.x)
+
+__global__ void k_validate(const uint64_t* off, const uint32_t* nbr, uint64_t n, uint64_t m,
+                           unsigned* bad) {
+  GRID_STRIDE(v, n) {
+    if (off[v + 1] < off[v]) atomicOr(bad, 1u);
+    if (off[v + 1] - off[v] > 0xffffffffull) atomicOr(bad, 4u);
+  }
+  GRID_STRIDE(e, m) {
+    if (nbr[e] >= n) atomicOr(bad, 2u);
+  }
+}
+
+__global__ void k_degrees(const uint64_t* off, uint64_t n, uint32_t* deg, double* inv_deg,
+                          unsigned* dead_flag) {
+  GRID_STRIDE(v, n) {
+    const uint64_t d = off[v + 1] - off[v];
+    deg[v] = (uint32_t)d;
+    inv_deg[v] = 1.0 / (double)(d ? d : 1);
+    dead_flag[v] = d == 0;
+  }
+}
+
+__global__ void k_scatter_flagged(const unsigned* flag, const unsigned* pos, uint64_t n,
+                                  uint32_t* out) {
+  GRID_STRIDE(v, n) {
+    if (flag[v]) out[pos[v]] = (uint32_t)v;
+  }
+}
+
+__global__ void k_expand_rows(const uint64_t* off, uint64_t n, uint32_t* src) {
+  // one warp per row writes the row id over its edge slice
+  const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t v = warp; v < n; v += nw)
+    for (uint64_t e = off[v] + lane; e < off[v + 1]; e += 32) src[e] = (uint32_t)v;
+}
+
+__global__ void k_count(const uint32_t* keys, uint64_t m, unsigned long long* cnt) {
+  GRID_STRIDE(e, m) atomicAdd(cnt + keys[e], 1ull);
+}
+
+__global__ void k_nonempty(const uint64_t* in_off, uint64_t n, unsigned* flag) {
+  GRID_STRIDE(u, n) flag[u] = in_off[u + 1] > in_off[u];
+}
+__global__ void k_compact_rows(const uint64_t* in_off, const unsigned* flag, const unsigned* pos,
+                               uint64_t n, uint64_t m, uint64_t* cin_off, uint32_t* cin_row,
+                               uint64_t n_rows) {
+  GRID_STRIDE(u, n) {
+    if (flag[u]) {
+      cin_off[pos[u]] = in_off[u];
+      cin_row[pos[u]] = (uint32_t)u;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) cin_off[n_rows] = m;
+}
+
+// own_lo[j] = first row u with in_off[u] >= j*T (lower_bound over row starts)
+__global__ void k_tiles(const uint64_t* in_off, uint64_t n, uint64_t ntiles, uint32_t T,
+                        uint32_t* own_lo) {
+  GRID_STRIDE(j, ntiles + 1) {
+    const uint64_t key = j * (uint64_t)T;
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (in_off[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    own_lo[j] = (uint32_t)lo;
+  }
+}
+
+// ---- generators ------------------------------------------------------------
+// R-MAT: edge i descends `scale` levels; level l uses 32-bit word l of the
+// Philox stream ctr = (i_lo, i_hi, 'RMAT', l/4) keyed by seed. Quadrants in
+// the order a (0,0), b (0,1), c (1,0), d (1,1). Key = (u << 32) | v.
+__global__ void k_rmat(uint64_t seed, int scale, uint64_t count, double a, double ab, double abc,
+                       uint64_t* keys) {
+  GRID_STRIDE(i, count) {
+    uint32_t u = 0, v = 0;
+    U4 o{};
+    for (int l = 0; l < scale; ++l) {
+      if ((l & 3) == 0)
+        o = philox4x32_10(U4{(uint32_t)i, (uint32_t)(i >> 32), 0x524D4154u, (uint32_t)(l >> 2)},
+                          (uint32_t)seed, (uint32_t)(seed >> 32));
+      const uint32_t w = (l & 3) == 0 ? o.x : (l & 3) == 1 ? o.y : (l & 3) == 2 ? o.z : o.w;
+      const double p = (double)w * 0x1.0p-32;
+      const uint32_t bu = p >= ab, bv = (p >= a && p < ab) || p >= abc;
+      u = (u << 1) | bu;
+      v = (v << 1) | bv;
+    }
+    keys[i] = ((uint64_t)u << 32) | v;
+  }
+}
+
+// Chung-Lu ball dropping: draw i picks u by inverse CDF of the out-weights
+// and v by inverse CDF of the (permuted) in-weights, from
+// Philox(ctr = (i_lo, i_hi, 'CHLU', 0)) words (x,y) and (z,w) as 53-bit
+// uniforms.
+__device__ __forceinline__ uint32_t inv_cdf(const double* cdf, uint64_t n, double x) {
+  uint64_t lo = 0, hi = n - 1;  // first j with cdf[j] > x
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (cdf[mid] > x) hi = mid; else lo = mid + 1;
+  }
+  return (uint32_t)lo;
+}
+
+__global__ void k_chung_lu(uint64_t seed, uint64_t draws, const double* cdf_out,
+                           const double* cdf_in, uint64_t n, uint64_t* keys) {
+  GRID_STRIDE(i, draws) {
+    const U4 o = philox4x32_10(U4{(uint32_t)i, (uint32_t)(i >> 32), 0x43484C55u, 0u},
+                               (uint32_t)seed, (uint32_t)(seed >> 32));
+    const double x = (double)((((uint64_t)o.y << 32) | o.x) >> 11) * 0x1.0p-53 * cdf_out[n - 1];
+    const double y = (double)((((uint64_t)o.w << 32) | o.z) >> 11) * 0x1.0p-53 * cdf_in[n - 1];
+    keys[i] = ((uint64_t)inv_cdf(cdf_out, n, x) << 32) | inv_cdf(cdf_in, n, y);
+  }
+}
+
+__global__ void k_cl_weights(uint64_t n, double expo, double* w) {
+  GRID_STRIDE(i, n) w[i] = pow((double)(i + 1), -expo);
+}
+__global__ void k_perm_keys(uint64_t seed, uint64_t n, uint64_t* keys, uint32_t* vals) {
+  GRID_STRIDE(i, n) {
+    const U4 o = philox4x32_10(U4{(uint32_t)i, (uint32_t)(i >> 32), 0x5045524Du, 0u},
+                               (uint32_t)seed, (uint32_t)(seed >> 32));
+    keys[i] = ((uint64_t)o.x << 32) | o.y;
+    vals[i] = (uint32_t)i;
+  }
+}
+__global__ void k_gather_w(const double* w, const uint32_t* perm, uint64_t n, double* out) {
+  GRID_STRIDE(i, n) out[i] = w[perm[i]];
+}
+
+// keep[i] = first of its run and not a self-loop
+__global__ void k_clean_flags(const uint64_t* keys, uint64_t cnt, unsigned char* keep) {
+  GRID_STRIDE(i, cnt) {
+    const uint64_t k = keys[i];
+    keep[i] = (i == 0 || keys[i - 1] != k) && ((k >> 32) != (k & 0xffffffffull));
+  }
+}
+__global__ void k_mark_present(const uint64_t* keys, uint64_t cnt, unsigned* present) {
+  GRID_STRIDE(i, cnt) {
+    present[keys[i] >> 32] = 1;
+    present[keys[i] & 0xffffffffull] = 1;
+  }
+}
+__global__ void k_relabel_sorted(const uint64_t* keys, uint64_t cnt, const unsigned* rank,
+                                 uint32_t* src, uint32_t* dst) {
+  GRID_STRIDE(i, cnt) {
+    src[i] = rank[keys[i] >> 32];
+    dst[i] = rank[keys[i] & 0xffffffffull];
+  }
+}
+
+// generic edge list: endpoint ids (2 per pair) and lower_bound relabel
+__global__ void k_split_pairs(const uint64_t* pairs, uint64_t cnt, uint64_t* ids) {
+  GRID_STRIDE(i, 2 * cnt) ids[i] = pairs[i];
+}
+__global__ void k_relabel_search(const uint64_t* pairs, uint64_t cnt, const uint64_t* ids,
+                                 uint64_t n, uint32_t* src, uint32_t* dst) {
+  GRID_STRIDE(i, 2 * cnt) {
+    const uint64_t key = pairs[i];
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (ids[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    if (i & 1) dst[i >> 1] = (uint32_t)lo; else src[i >> 1] = (uint32_t)lo;
+  }
+}
+
+template <typename F>
+void cub_call(F&& f, cudaStream_t st) {
+  size_t bytes = 0;
+  PPRG_CUDA(f(nullptr, bytes));
+  DevBuf<unsigned char> tmp(bytes ? bytes : 1);
+  PPRG_CUDA(f(tmp.get(), bytes));
+  (void)st;
+}
+
+int bits_for(uint64_t maxval) {
+  int b = 1;
+  while (b < 64 && (maxval >> b)) ++b;
+  return b;
+}
+
+// offsets (u64, n+1) from per-row counts of `src` (u32 keys < n)
+void offsets_from_src(const uint32_t* src, uint64_t m, uint64_t n, uint64_t* off, cudaStream_t st) {
+  DevBuf<unsigned long long> cnt(n + 1);
+  PPRG_CUDA(cudaMemsetAsync(cnt.get(), 0, 8 * (n + 1), st));
+  if (m) k_count<<<blocks_for(m), TB, 0, st>>>(src, m, cnt.get());
+  unsigned long long* c = cnt.get();
+  uint64_t* o = off;
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, c, (unsigned long long*)o, (int64_t)(n + 1), st);
+  }, st);
+}
+
+// From a sorted, cleaned key list (u<<32|v): reference build semantics.
+std::unique_ptr<Graph> build_from_sorted_keys(DevBuf<uint64_t>& keys, uint64_t cnt, uint64_t id_space,
+                                              int device, cudaStream_t st) {
+  DevBuf<unsigned> present(id_space + 1), rank(id_space + 1);
+  PPRG_CUDA(cudaMemsetAsync(present.get(), 0, 4 * (id_space + 1), st));
+  k_mark_present<<<blocks_for(cnt), TB, 0, st>>>(keys.get(), cnt, present.get());
+  unsigned* pp = present.get();
+  unsigned* rp = rank.get();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, pp, rp, (int64_t)(id_space + 1), st);
+  }, st);
+  unsigned n32 = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&n32, rank.get() + id_space, 4, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  auto g = std::make_unique<Graph>();
+  g->device = device;
+  g->stream = st;
+  g->n = n32;
+  g->m = cnt;
+  g->nbr.alloc(cnt);
+  g->off.alloc(g->n + 1);
+  DevBuf<uint32_t> src(cnt);
+  k_relabel_sorted<<<blocks_for(cnt), TB, 0, st>>>(keys.get(), cnt, rank.get(), src.get(),
+                                                   g->nbr.get());
+  offsets_from_src(src.get(), cnt, g->n, g->off.get(), st);
+  g->finish_build();
+  return g;
+}
+
+// sort keys, drop duplicates and self-loops (compaction in place)
+uint64_t sort_clean(DevBuf<uint64_t>& keys, uint64_t cnt, int key_bits, cudaStream_t st) {
+  DevBuf<uint64_t> sorted(cnt);
+  uint64_t* in = keys.get();
+  uint64_t* out = sorted.get();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, in, out, (int64_t)cnt, 0, key_bits, st);
+  }, st);
+  DevBuf<unsigned char> keep(cnt);
+  k_clean_flags<<<blocks_for(cnt), TB, 0, st>>>(sorted.get(), cnt, keep.get());
+  DevBuf<unsigned long long> nsel(1);
+  unsigned char* kp = keep.get();
+  unsigned long long* ns = nsel.get();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceSelect::Flagged(t, b, out, kp, in, ns, (int64_t)cnt, st);
+  }, st);
+  unsigned long long h = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&h, ns, 8, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  return h;
+}
+
+}  // namespace
+
+Graph::~Graph() {
+  if (stream) {
+    DeviceGuard dg(device);
+    cudaStreamSynchronize(stream);
+    cudaStreamDestroy(stream);
+  }
+}
+
+void Graph::finish_build() {
+  cudaStream_t st = stream;
+  DevBuf<unsigned> bad(1);
+  PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
+  uint64_t first = 0, last = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&first, off.get(), 8, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaMemcpyAsync(&last, off.get() + n, 8, cudaMemcpyDeviceToHost, st));
+  k_validate<<<blocks_for(n > m ? n : m), TB, 0, st>>>(off.get(), nbr.get(), n, m, bad.get());
+  unsigned hbad = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&hbad, bad.get(), 4, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  // same messages as Graph::validate (graph.cpp:24-34)
+  if (first != 0) fail(EDATA, "graph: offsets must start at 0");
+  if (hbad & 1) fail(EDATA, "graph: offsets must be non-decreasing");
+  if (last != m) fail(EDATA, "graph: offsets must end at m");
+  if (hbad & 2) fail(EDATA, "graph: neighbor id out of range");
+  if (hbad & 4) fail(EDATA, "graph: out-degree exceeds 2^32-1");
+  deg.alloc(n);
+  inv_deg.alloc(n);
+  DevBuf<unsigned> flag(n + 1), pos(n + 1);
+  PPRG_CUDA(cudaMemsetAsync(flag.get() + n, 0, 4, st));
+  k_degrees<<<blocks_for(n), TB, 0, st>>>(off.get(), n, deg.get(), inv_deg.get(), flag.get());
+  unsigned* fp = flag.get();
+  unsigned* pp = pos.get();
+  const uint64_t nn = n;
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, fp, pp, (int64_t)(nn + 1), st);
+  }, st);
+  unsigned nd = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&nd, pos.get() + n, 4, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  n_dead = nd;
+  dead.alloc(n_dead ? n_dead : 1);
+  k_scatter_flagged<<<blocks_for(n), TB, 0, st>>>(flag.get(), pos.get(), n, dead.get());
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  PPRG_CUDA(cudaGetLastError());
+}
+
+void Graph::ensure_transpose() {
+  if (in_off.get()) return;
+  cudaStream_t st = stream;
+  in_off.alloc(n + 1);
+  in_nbr.alloc(m ? m : 1);
+  if (m == 0) {
+    PPRG_CUDA(cudaMemsetAsync(in_off.get(), 0, 8 * (n + 1), st));
+    n_rows = 0;
+    cin_off.alloc(1);
+    cin_row.alloc(1);
+    PPRG_CUDA(cudaMemsetAsync(cin_off.get(), 0, 8, st));
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  DevBuf<uint32_t> src(m), keys_out(m);
+  k_expand_rows<<<blocks_for(n * 32ull), TB, 0, st>>>(off.get(), n, src.get());
+  // stable sort of (dst, src) pairs in out-CSR order => in-neighbours ascending
+  const uint32_t* kin = nbr.get();
+  uint32_t* kout = keys_out.get();
+  const uint32_t* vin = src.get();
+  uint32_t* vout = in_nbr.get();
+  const int bits = bits_for(n);
+  const uint64_t mm = m;
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, vin, vout, (int64_t)mm, 0, bits, st);
+  }, st);
+  offsets_from_src(keys_out.get(), m, n, in_off.get(), st);
+  // compacted row list of the transpose (in-degree > 0)
+  DevBuf<unsigned> flag(n + 1), pos(n + 1);
+  PPRG_CUDA(cudaMemsetAsync(flag.get() + n, 0, 4, st));
+  k_nonempty<<<blocks_for(n), TB, 0, st>>>(in_off.get(), n, flag.get());
+  unsigned* fp = flag.get();
+  unsigned* pp = pos.get();
+  const uint64_t nn = n;
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, fp, pp, (int64_t)(nn + 1), st);
+  }, st);
+  unsigned nr = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&nr, pos.get() + n, 4, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  n_rows = nr;
+  cin_off.alloc(n_rows + 1);
+  cin_row.alloc(n_rows ? n_rows : 1);
+  k_compact_rows<<<blocks_for(n), TB, 0, st>>>(in_off.get(), flag.get(), pos.get(), n, m,
+                                               cin_off.get(), cin_row.get(), n_rows);
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  PPRG_CUDA(cudaGetLastError());
+}
+
+const uint32_t* Graph::tiles(uint32_t T, uint64_t* ntiles) {
+  ensure_transpose();
+  *ntiles = m / T + 1;
+  auto it = tile_lo.find(T);
+  if (it != tile_lo.end()) return it->second.get();
+  DevBuf<uint32_t> lo(*ntiles + 1);
+  k_tiles<<<blocks_for(*ntiles + 1), TB, 0, stream>>>(cin_off.get(), n_rows, *ntiles, T, lo.get());
+  PPRG_CUDA(cudaStreamSynchronize(stream));
+  PPRG_CUDA(cudaGetLastError());
+  const uint32_t* p = lo.get();
+  tile_lo.emplace(T, std::move(lo));
+  return p;
+}
+
+static cudaStream_t make_stream(int device, int* sms) {
+  PPRG_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  PPRG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  PPRG_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, device));
+  return st;
+}
+
+std::unique_ptr<Graph> graph_from_csr(const uint64_t* h_off, const uint32_t* h_nbr, uint64_t n,
+                                      int device) {
+  if (n > 0xffffffffull) fail(EINVAL_, "graph: n exceeds the NodeId range");
+  DeviceGuard dg(device);
+  auto g = std::make_unique<Graph>();
+  g->device = device;
+  g->stream = make_stream(device, &g->sm_count);
+  g->n = n;
+  g->off.alloc(n + 1);
+  PPRG_CUDA(cudaMemcpyAsync(g->off.get(), h_off, 8 * (n + 1), cudaMemcpyHostToDevice, g->stream));
+  g->m = h_off[n];
+  g->nbr.alloc(g->m ? g->m : 1);
+  if (g->m)
+    PPRG_CUDA(cudaMemcpyAsync(g->nbr.get(), h_nbr, 4 * g->m, cudaMemcpyHostToDevice, g->stream));
+  g->finish_build();
+  return g;
+}
+
+std::unique_ptr<Graph> graph_from_edges(const uint64_t* h_pairs, uint64_t count, int device) {
+  if (count == 0) fail(EDATA, "graph is empty after cleaning");  // graph.cpp:37
+  DeviceGuard dg(device);
+  int sms = 0;
+  cudaStream_t st = make_stream(device, &sms);
+  DevBuf<uint64_t> pairs(2 * count), ids(2 * count), ids_sorted(2 * count), uniq(2 * count);
+  PPRG_CUDA(cudaMemcpyAsync(pairs.get(), h_pairs, 16 * count, cudaMemcpyHostToDevice, st));
+  k_split_pairs<<<blocks_for(2 * count), TB, 0, st>>>(pairs.get(), count, ids.get());
+  uint64_t* a = ids.get();
+  uint64_t* b2 = ids_sorted.get();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceRadixSort::SortKeys(t, b, a, b2, (int64_t)(2 * count), 0, 64, st);
+  }, st);
+  DevBuf<unsigned long long> nsel(1);
+  uint64_t* u = uniq.get();
+  unsigned long long* ns = nsel.get();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceSelect::Unique(t, b, b2, u, ns, (int64_t)(2 * count), st);
+  }, st);
+  unsigned long long n = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&n, ns, 8, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  if (n > 0xffffffffull) fail(EINVAL_, "graph: n exceeds the NodeId range");
+  DevBuf<uint32_t> src(count), dst(count), src_sorted(count);
+  k_relabel_search<<<blocks_for(2 * count), TB, 0, st>>>(pairs.get(), count, uniq.get(), n,
+                                                         src.get(), dst.get());
+  auto g = std::make_unique<Graph>();
+  g->device = device;
+  g->stream = st;
+  g->sm_count = sms;
+  g->n = n;
+  g->m = count;
+  g->nbr.alloc(count);
+  g->off.alloc(n + 1);
+  const uint32_t* kin = src.get();
+  uint32_t* kout = src_sorted.get();
+  const uint32_t* vin = dst.get();
+  uint32_t* vout = g->nbr.get();
+  const int bits = bits_for(n);
+  cub_call([&](void* t, size_t& b) {  // stable => input order within a row
+    return cub::DeviceRadixSort::SortPairs(t, b, kin, kout, vin, vout, (int64_t)count, 0, bits, st);
+  }, st);
+  offsets_from_src(src_sorted.get(), count, n, g->off.get(), st);
+  g->finish_build();
+  return g;
+}
+
+std::unique_ptr<Graph> graph_rmat(int scale, uint64_t edge_factor, double a, double b, double c,
+                                  uint64_t seed, int device, std::vector<uint64_t>* h_edges_out) {
+  if (scale < 1 || scale > 31) fail(EINVAL_, "rmat: scale must be in [1,31]");
+  if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) fail(EINVAL_, "rmat: bad quadrant probabilities");
+  DeviceGuard dg(device);
+  int sms = 0;
+  cudaStream_t st = make_stream(device, &sms);
+  const uint64_t draws = edge_factor << scale;
+  DevBuf<uint64_t> keys(draws ? draws : 1);
+  k_rmat<<<blocks_for(draws), TB, 0, st>>>(seed, scale, draws, a, a + b, a + b + c, keys.get());
+  const uint64_t cnt = sort_clean(keys, draws, 32 + scale, st);
+  if (cnt == 0) fail(EDATA, "graph is empty after cleaning");
+  if (h_edges_out) {
+    h_edges_out->resize(cnt);
+    PPRG_CUDA(cudaMemcpyAsync(h_edges_out->data(), keys.get(), 8 * cnt, cudaMemcpyDeviceToHost, st));
+  }
+  auto g = build_from_sorted_keys(keys, cnt, 1ull << scale, device, st);
+  g->sm_count = sms;
+  return g;
+}
+
+std::unique_ptr<Graph> graph_chung_lu(uint64_t n_raw, uint64_t draws, double beta, uint64_t seed,
+                                      int device, std::vector<uint64_t>* h_edges_out) {
+  if (n_raw < 2 || n_raw > 0xffffffffull) fail(EINVAL_, "chung-lu: bad n");
+  if (!(beta > 2.0)) fail(EINVAL_, "chung-lu: beta must exceed 2");
+  DeviceGuard dg(device);
+  int sms = 0;
+  cudaStream_t st = make_stream(device, &sms);
+  // w_i ~ (i+1)^(-1/(beta-1)); in-weights are a seeded permutation of them
+  DevBuf<double> w(n_raw), w_in(n_raw), cdf_out(n_raw), cdf_in(n_raw);
+  k_cl_weights<<<blocks_for(n_raw), TB, 0, st>>>(n_raw, 1.0 / (beta - 1.0), w.get());
+  {
+    DevBuf<uint64_t> pk(n_raw), pk2(n_raw);
+    DevBuf<uint32_t> pv(n_raw), pv2(n_raw);
+    k_perm_keys<<<blocks_for(n_raw), TB, 0, st>>>(seed ^ 0x5A5A5A5A5A5A5A5Aull, n_raw, pk.get(), pv.get());
+    uint64_t* k1 = pk.get();
+    uint64_t* k2 = pk2.get();
+    uint32_t* v1 = pv.get();
+    uint32_t* v2 = pv2.get();
+    cub_call([&](void* t, size_t& b) {
+      return cub::DeviceRadixSort::SortPairs(t, b, k1, k2, v1, v2, (int64_t)n_raw, 0, 64, st);
+    }, st);
+    k_gather_w<<<blocks_for(n_raw), TB, 0, st>>>(w.get(), pv2.get(), n_raw, w_in.get());
+  }
+  double* wp = w.get();
+  double* wi = w_in.get();
+  double* co = cdf_out.get();
+  double* ci = cdf_in.get();
+  cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, wp, co, (int64_t)n_raw, st); }, st);
+  cub_call([&](void* t, size_t& b) { return cub::DeviceScan::InclusiveSum(t, b, wi, ci, (int64_t)n_raw, st); }, st);
+  DevBuf<uint64_t> keys(draws ? draws : 1);
+  k_chung_lu<<<blocks_for(draws), TB, 0, st>>>(seed, draws, cdf_out.get(), cdf_in.get(), n_raw,
+                                               keys.get());
+  const uint64_t cnt = sort_clean(keys, draws, 32 + bits_for(n_raw), st);
+  if (cnt == 0) fail(EDATA, "graph is empty after cleaning");
+  if (h_edges_out) {
+    h_edges_out->resize(cnt);
+    PPRG_CUDA(cudaMemcpyAsync(h_edges_out->data(), keys.get(), 8 * cnt, cudaMemcpyDeviceToHost, st));
+  }
+  auto g = build_from_sorted_keys(keys, cnt, n_raw, device, st);
+  g->sm_count = sms;
+  return g;
+}
+
+}  // namespace pprg

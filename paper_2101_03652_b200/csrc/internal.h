@@ -1,0 +1,130 @@
+// Internal C++ interfaces of the engine (not exported; the C ABI in
+// include/pprg.h is the boundary).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace pprg {
+
+// Device-resident immutable graph. The out-CSR is the canonical, reference-
+// identical layout (graph.hpp:44-46: u64 offsets, u32 neighbours, dead-end
+// list); the transpose and the tile map are derived internal layouts for the
+// pull sweeps.
+struct Graph {
+  int device = 0;
+  int sm_count = 148;
+  uint64_t n = 0, m = 0, n_dead = 0;
+  DevBuf<uint64_t> off;       // out offsets [n+1]
+  DevBuf<uint32_t> nbr;       // out neighbours [m]
+  DevBuf<uint32_t> deg;       // out-degree [n] (0 = dead end)
+  DevBuf<double> inv_deg;     // 1 / effective degree [n]
+  DevBuf<uint32_t> dead;      // dead-end ids ascending [n_dead]
+  DevBuf<uint64_t> in_off;    // transpose offsets [n+1] (lazy)
+  DevBuf<uint32_t> in_nbr;    // transpose neighbours [m], ascending per row
+  // rows of the transpose with in-degree > 0 (the others never receive mass)
+  uint64_t n_rows = 0;
+  DevBuf<uint64_t> cin_off;   // [n_rows+1] offsets of the compacted rows into in_nbr
+  DevBuf<uint32_t> cin_row;   // [n_rows] node id of compacted row
+  std::map<uint32_t, DevBuf<uint32_t>> tile_lo;  // per tile size: first owned compact row of tile j
+  std::mutex mu;
+  cudaStream_t stream = nullptr;
+
+  ~Graph();
+  void finish_build();  // deg / inv_deg / dead-ends from off; validates
+  void ensure_transpose();
+  const uint32_t* tiles(uint32_t edges_per_tile, uint64_t* ntiles);
+  uint64_t m_eff() const { return m + n_dead; }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) PPRG_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+std::unique_ptr<Graph> graph_from_csr(const uint64_t* h_off, const uint32_t* h_nbr, uint64_t n,
+                                      int device);
+std::unique_ptr<Graph> graph_from_edges(const uint64_t* h_pairs, uint64_t count, int device);
+std::unique_ptr<Graph> graph_rmat(int scale, uint64_t edge_factor, double a, double b, double c,
+                                  uint64_t seed, int device, std::vector<uint64_t>* h_edges_out);
+std::unique_ptr<Graph> graph_chung_lu(uint64_t n_raw, uint64_t draws, double beta, uint64_t seed,
+                                      int device, std::vector<uint64_t>* h_edges_out);
+
+// ---- queries --------------------------------------------------------------
+struct ColumnStats {
+  double r_sum = 0;
+  uint64_t pushes = 0;
+  uint64_t walks = 0;
+  uint32_t sweeps = 0;        // global-phase sweeps (powerpush) / iterations (powitr)
+  uint32_t local_levels = 0;  // frontier levels of the local (queue) phase
+  int used_scan_phase = 0;
+};
+
+struct CallStats {
+  double device_ms = 0;       // events around the whole device section
+  double sweep_ms = 0;        // events around the persistent global-sweep kernel(s)
+  uint64_t alg_bytes = 0;     // SURVEY 8(d) algorithmic bytes of the global sweeps
+  uint64_t sweep_launches = 0;
+  uint32_t max_sweeps = 0;
+  uint32_t kernel_launches = 0;
+};
+
+struct Outputs {  // host or device pointers (k x n, query-major); any may be null
+  double* reserve = nullptr;
+  double* residue = nullptr;
+  bool on_device = false;
+};
+
+enum class Engine { PowerPush, PowItr, SimFwdPush, Fifo };
+
+void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, double alpha,
+                     double lambda, uint32_t epoch_num, int64_t scan_threshold, double r_max_fifo,
+                     double lambda_stop_fifo, const Outputs& out, ColumnStats* cols,
+                     CallStats* call);
+
+// Interleaved [u*K + c] state left in the graph workspace by the SpeedPPR push
+// stage (x = pushed mass, res = explicit residues after refine).
+struct PushView {
+  int K = 0;
+  uint32_t k = 0;
+  double* x = nullptr;
+  double* res = nullptr;
+  const uint32_t* d_src = nullptr;
+  std::vector<uint32_t> src;
+};
+void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double alpha,
+                         double lambda, double r_max, ColumnStats* cols, CallStats* call,
+                         PushView* view);
+
+struct WalkIndex {
+  int device = 0;
+  double alpha = 0;
+  uint64_t seed = 0;
+  uint64_t m = 0;
+  DevBuf<uint32_t> endpoints;  // [m], slice v = [off[v], off[v+1])
+};
+
+std::unique_ptr<WalkIndex> index_build(Graph& g, double alpha, uint64_t seed);
+std::unique_ptr<WalkIndex> index_from_host(Graph& g, double alpha, uint64_t seed,
+                                           const uint32_t* h_endpoints);
+void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t k, double alpha,
+              double epsilon, double mu, uint64_t seed, double* est_out, bool out_on_device,
+              ColumnStats* cols, CallStats* call);
+// Walk terminals of walks (k_i, v_i) from start_i under tag (test hook).
+void walk_terminals(Graph& g, const uint32_t* h_start, const uint32_t* h_k, const uint32_t* h_v,
+                    uint64_t count, uint32_t source, uint32_t tag, double alpha, uint64_t seed,
+                    uint32_t* h_out);
+
+}  // namespace pprg

@@ -1,0 +1,338 @@
+// SpeedPPR (hot-path subsystem (4)): Philox alpha-random walks, the
+// epsilon-independent walk index, and the Monte Carlo phase.
+// Reference: speedppr.cpp:8-111, walk_index.cpp:10-54.
+//
+// RNG: the reference draws every walk from one sequential
+// mt19937_64 stream, which cannot be parallelised bit-exactly. Here step t of
+// walk k out of node v is Philox4x32-10(key = seed, ctr = (k, v, tag, t)) with
+// tag = query source (MC walks) or 0xFFFFFFFF (index walks), so every walk is
+// independent and reproducible; terminals are bit-identical to the oracle's
+// restatement (oracle.c og_philox_walk) and the index is byte-identical per
+// seed. Stored index files carry rng-id 2 (PPRG_RNG_PHILOX4X32_10).
+#include <cub/cub.cuh>
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "internal.h"
+
+namespace pprg {
+namespace {
+
+inline unsigned gridn(uint64_t items, int tb = 256) {
+  uint64_t b = (items + tb - 1) / tb;
+  if (b == 0) b = 1;
+  if (b > 65535ull * 64) b = 65535ull * 64;
+  return (unsigned)b;
+}
+
+__device__ __forceinline__ uint64_t row_of(const uint64_t* off, uint64_t n, uint64_t e) {
+  uint64_t lo = 0, hi = n;  // last v with off[v] <= e
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= e) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// build_index (walk_index.cpp:44-54): deg(v) walks from every v with v as
+// its own pseudo-source; one thread per slot, slot k of v keyed (k, v).
+__global__ void k_index(const uint64_t* off, const uint32_t* nbr, uint64_t n, uint64_t m,
+                        double alpha, uint64_t seed, uint32_t* ep) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t v = row_of(off, n, e);
+    ep[e] = philox_walk(off, nbr, (uint32_t)v, (uint32_t)v, alpha, seed, (uint32_t)(e - off[v]),
+                        (uint32_t)v, kIndexTag);
+  }
+}
+
+__global__ void k_check_index(const uint32_t* ep, uint64_t m, uint64_t n, unsigned* bad) {
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < m;
+       e += (uint64_t)gridDim.x * blockDim.x)
+    if (ep[e] >= n) atomicOr(bad, 1u);
+}
+
+__global__ void k_terminals(const uint64_t* off, const uint32_t* nbr, const uint32_t* starts,
+                            const uint32_t* ks, const uint32_t* vs, uint64_t count, uint32_t source,
+                            uint32_t tag, double alpha, uint64_t seed, uint32_t* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < count;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = philox_walk(off, nbr, starts[i], source, alpha, seed, ks[i], vs[i], tag);
+}
+
+// W_v = ceil(r W), clamped to deg_eff within the reference's slack
+// (speedppr.cpp:30-40); counts for padding columns are 0.
+__global__ void k_mc_counts(const double* res, const uint32_t* deg, uint64_t n, int K, int k,
+                            double W, unsigned long long* cnt, unsigned* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * K;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % K);
+    const double r = res[i];
+    unsigned long long wc = 0;
+    if (c < k && r > 0.0) {
+      const uint32_t d = deg[i / K];
+      const double de = d ? (double)d : 1.0;
+      wc = (unsigned long long)ceil(r * W);
+      if ((double)wc > de) {
+        if (r * W > de * (1.0 + 1e-9) + 1e-9) atomicOr(bad, 1u);
+        wc = (unsigned long long)de;
+      }
+    }
+    cnt[i] = wc;
+  }
+}
+
+__global__ void k_est_init(const double* x, uint64_t nk, double alpha, double* est) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nk;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    est[i] = alpha * x[i];
+}
+
+struct McParams {
+  const uint64_t* off;
+  const uint32_t* nbr;
+  const uint32_t* deg;
+  const double* res;
+  const unsigned long long* cnt;
+  const unsigned long long* woff;  // exclusive scan of cnt, [n*K + 1]
+  const uint32_t* index;           // may be null
+  uint64_t nk;
+  unsigned long long total;
+  int K;
+  double alpha;
+  uint64_t seed;
+  double* est;
+  uint32_t src[64];
+};
+
+// One thread per walk: locate its (v, c) by binary search over the scan, then
+// a stored terminal (index prefix, speedppr.cpp:66-71) or a fresh walk.
+__global__ void k_mc_walks(const __grid_constant__ McParams P) {
+  for (unsigned long long w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < P.total;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = P.nk - 1;  // last i with woff[i] <= w
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) >> 1;
+      if (P.woff[mid] <= w) lo = mid; else hi = mid - 1;
+    }
+    const uint64_t i = lo;
+    const uint32_t kk = (uint32_t)(w - P.woff[i]);
+    const uint32_t v = (uint32_t)(i / P.K);
+    const int c = (int)(i % P.K);
+    const double contribution = P.res[i] / (double)P.cnt[i];
+    uint32_t t;
+    if (P.index && P.deg[v]) t = P.index[P.off[v] + kk];
+    else t = philox_walk(P.off, P.nbr, v, P.src[c], P.alpha, P.seed, kk, v, P.src[c]);
+    atomicAdd(P.est + (uint64_t)t * P.K + c, contribution);
+  }
+}
+
+// pure-sampling branch (speedppr.cpp:90-102): W walks from s, weight 1/W
+__global__ void k_mc_pure(const uint64_t* off, const uint32_t* nbr, uint64_t W, int K, int k,
+                          const uint32_t* src, double alpha, uint64_t seed, double* est) {
+  const uint64_t total = W * (uint64_t)k;
+  for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < total;
+       w += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(w / W);
+    const uint32_t kk = (uint32_t)(w % W);
+    const uint32_t s = src[c];
+    const uint32_t t = philox_walk(off, nbr, s, s, alpha, seed, kk, s, s);
+    atomicAdd(est + (uint64_t)t * K + c, 1.0 / (double)W);
+  }
+}
+
+__global__ void k_unpack_est(const double* a, uint64_t n, int K, int k, double* out) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * K;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % K);
+    if (c < k) out[(uint64_t)c * n + i / K] = a[i];
+  }
+}
+
+template <typename F>
+void cub_run(F&& f) {
+  size_t bytes = 0;
+  PPRG_CUDA(f(nullptr, bytes));
+  DevBuf<unsigned char> tmp(bytes ? bytes : 1);
+  PPRG_CUDA(f(tmp.get(), bytes));
+}
+
+}  // namespace
+
+std::unique_ptr<WalkIndex> index_build(Graph& g, double alpha, uint64_t seed) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  auto w = std::make_unique<WalkIndex>();
+  w->device = g.device;
+  w->alpha = alpha;
+  w->seed = seed;
+  w->m = g.m;
+  w->endpoints.alloc(g.m ? g.m : 1);
+  if (g.m)
+    k_index<<<gridn(g.m), 256, 0, g.stream>>>(g.off.get(), g.nbr.get(), g.n, g.m, alpha, seed,
+                                              w->endpoints.get());
+  PPRG_CUDA(cudaGetLastError());
+  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+  return w;
+}
+
+std::unique_ptr<WalkIndex> index_from_host(Graph& g, double alpha, uint64_t seed,
+                                           const uint32_t* h_endpoints) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  auto w = std::make_unique<WalkIndex>();
+  w->device = g.device;
+  w->alpha = alpha;
+  w->seed = seed;
+  w->m = g.m;
+  w->endpoints.alloc(g.m ? g.m : 1);
+  DevBuf<unsigned> bad(1);
+  PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, g.stream));
+  if (g.m) {
+    PPRG_CUDA(cudaMemcpyAsync(w->endpoints.get(), h_endpoints, 4 * g.m, cudaMemcpyHostToDevice, g.stream));
+    k_check_index<<<gridn(g.m), 256, 0, g.stream>>>(w->endpoints.get(), g.m, g.n, bad.get());
+  }
+  unsigned hb = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, g.stream));
+  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+  if (hb) fail(EDATA, "walk index: endpoint id out of range");  // walk_index.cpp:32-33
+  return w;
+}
+
+void walk_terminals(Graph& g, const uint32_t* h_start, const uint32_t* h_k, const uint32_t* h_v,
+                    uint64_t count, uint32_t source, uint32_t tag, double alpha, uint64_t seed,
+                    uint32_t* h_out) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!count) return;
+  DevBuf<uint32_t> s(count), kk(count), v(count), o(count);
+  PPRG_CUDA(cudaMemcpyAsync(s.get(), h_start, 4 * count, cudaMemcpyHostToDevice, g.stream));
+  PPRG_CUDA(cudaMemcpyAsync(kk.get(), h_k, 4 * count, cudaMemcpyHostToDevice, g.stream));
+  PPRG_CUDA(cudaMemcpyAsync(v.get(), h_v, 4 * count, cudaMemcpyHostToDevice, g.stream));
+  k_terminals<<<gridn(count), 256, 0, g.stream>>>(g.off.get(), g.nbr.get(), s.get(), kk.get(),
+                                                  v.get(), count, source, tag, alpha, seed, o.get());
+  PPRG_CUDA(cudaGetLastError());
+  PPRG_CUDA(cudaMemcpyAsync(h_out, o.get(), 4 * count, cudaMemcpyDeviceToHost, g.stream));
+  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+}
+
+void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t k, double alpha,
+              double epsilon, double mu, uint64_t seed, double* est_out, bool out_on_device,
+              ColumnStats* cols, CallStats* call) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  for (uint32_t c = 0; c < k; ++c)
+    if (sources[c] >= g.n) fail(EINVAL_, "speedppr: source out of range");
+  const uint64_t n = g.n;
+  if (n < 2) fail(EINVAL_, "walk budget: need n >= 2");
+  const double mu_eff = mu > 0.0 ? mu : 1.0 / (double)n;
+  const uint64_t W = (uint64_t)std::ceil(2.0 * (2.0 * epsilon / 3.0 + 2.0) * std::log((double)n) /
+                                         (epsilon * epsilon * mu_eff));  // speedppr.cpp:8-18
+  const uint64_t m_eff = g.m_eff();
+  cudaStream_t st = g.stream;
+  const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  cudaEvent_t e0, e1;
+  PPRG_CUDA(cudaEventCreate(&e0));
+  PPRG_CUDA(cudaEventCreate(&e1));
+  PPRG_CUDA(cudaEventRecord(e0, st));
+  for (uint32_t b0 = 0; b0 < k; b0 += 64) {
+    const uint32_t kb = k - b0 < 64u ? k - b0 : 64u;
+    ColumnStats* cs = cols + b0;
+    if (W <= m_eff) {
+      int K = 1;
+      while (K < (int)kb) K <<= 1;
+      DevBuf<double> est(n * K), outb(out_on_device ? 0 : n * kb);
+      DevBuf<uint32_t> dsrc(64);
+      PPRG_CUDA(cudaMemcpyAsync(dsrc.get(), sources + b0, 4 * kb, cudaMemcpyHostToDevice, st));
+      PPRG_CUDA(cudaMemsetAsync(est.get(), 0, 8 * n * K, st));
+      if (W > 0xffffffffull) fail(EINVAL_, "speedppr: walk budget exceeds 2^32 walks per query");
+      k_mc_pure<<<gridn(W * kb), 256, 0, st>>>(g.off.get(), g.nbr.get(), W, K, kb, dsrc.get(), alpha,
+                                              seed, est.get());
+      double* dst = est_out ? (out_on_device ? est_out + (uint64_t)b0 * n : outb.get()) : nullptr;
+      if (dst) k_unpack_est<<<gridn(n * K), 256, 0, st>>>(est.get(), n, K, kb, dst);
+      if (est_out && !out_on_device)
+        PPRG_CUDA(cudaMemcpyAsync(est_out + (uint64_t)b0 * n, outb.get(), 8 * n * kb, kind, st));
+      PPRG_CUDA(cudaStreamSynchronize(st));
+      PPRG_CUDA(cudaGetLastError());
+      call->kernel_launches += 2;
+      for (uint32_t c = 0; c < kb; ++c) {
+        cs[c].walks = W;
+        cs[c].pushes = 0;
+        cs[c].r_sum = 0;
+      }
+      continue;
+    }
+    const double lambda = (double)m_eff / (double)W;
+    const double r_max = 1.0 / (double)W;
+    PushView pv;
+    speedppr_push_stage(g, sources + b0, kb, alpha, lambda, r_max, cs, call, &pv);
+    const int K = pv.K;
+    const uint64_t nk = n * (uint64_t)K;
+    DevBuf<unsigned long long> cnt(nk), woff(nk + 1);
+    DevBuf<double> est(nk), outb(out_on_device ? 0 : n * kb);
+    DevBuf<unsigned> bad(1);
+    PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
+    k_mc_counts<<<gridn(nk), 256, 0, st>>>(pv.res, g.deg.get(), n, K, kb, (double)W, cnt.get(),
+                                          bad.get());
+    unsigned long long* cp = cnt.get();
+    unsigned long long* wp = woff.get();
+    cub_run([&](void* t, size_t& bytes) {
+      return cub::DeviceScan::ExclusiveSum(t, bytes, cp, wp, (int64_t)nk, st);
+    });
+    // total = woff[nk-1] + cnt[nk-1]
+    unsigned long long last_off = 0, last_cnt = 0;
+    unsigned hb = 0;
+    PPRG_CUDA(cudaMemcpyAsync(&last_off, wp + nk - 1, 8, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaMemcpyAsync(&last_cnt, cp + nk - 1, 8, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    if (hb) fail(EINTERNAL, "monte carlo: residue exceeds degree/W, state not refined");
+    const unsigned long long total = last_off + last_cnt;
+    k_est_init<<<gridn(nk), 256, 0, st>>>(pv.x, nk, alpha, est.get());
+    McParams P;
+    std::memset(&P, 0, sizeof P);
+    P.off = g.off.get();
+    P.nbr = g.nbr.get();
+    P.deg = g.deg.get();
+    P.res = pv.res;
+    P.cnt = cnt.get();
+    P.woff = woff.get();
+    P.index = idx ? idx->endpoints.get() : nullptr;
+    P.nk = nk;
+    P.total = total;
+    P.K = K;
+    P.alpha = alpha;
+    P.seed = seed;
+    P.est = est.get();
+    for (int c = 0; c < K; ++c) P.src[c] = pv.src[c];
+    if (total) k_mc_walks<<<gridn(total), 256, 0, st>>>(P);
+    PPRG_CUDA(cudaGetLastError());
+    double* dst = est_out ? (out_on_device ? est_out + (uint64_t)b0 * n : outb.get()) : nullptr;
+    if (dst) k_unpack_est<<<gridn(nk), 256, 0, st>>>(est.get(), n, K, kb, dst);
+    if (est_out && !out_on_device)
+      PPRG_CUDA(cudaMemcpyAsync(est_out + (uint64_t)b0 * n, outb.get(), 8 * n * kb, kind, st));
+    // per-column walk totals
+    std::vector<unsigned long long> hoff(K + 1);
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    call->kernel_launches += 4;
+    for (uint32_t c = 0; c < kb; ++c) cs[c].walks = 0;
+    {
+      // walks per column: sum of counts with i % K == c (small host pass over a reduced copy)
+      std::vector<unsigned long long> hc(nk);
+      PPRG_CUDA(cudaMemcpy(hc.data(), cp, 8 * nk, cudaMemcpyDeviceToHost));
+      for (uint64_t i = 0; i < nk; ++i) cs[i % K].walks += (i % K) < kb ? hc[i] : 0;
+    }
+    for (uint32_t c = 0; c < kb; ++c) cs[c].r_sum = 0;  // speedppr.cpp:47
+  }
+  PPRG_CUDA(cudaEventRecord(e1, st));
+  PPRG_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  PPRG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  call->device_ms += ms;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+}
+
+}  // namespace pprg

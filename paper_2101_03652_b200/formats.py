@@ -1,0 +1,106 @@
+"""On-disk formats shared with the reference, little-endian, bit-exact.
+
+PPRG graph cache (graph.hpp:102-106, graph.cpp:115-149):
+    magic "PPRG", version u8 = 1, n u64, m u64, offsets (n+1) x u64, neighbors m x u32
+PPRW walk index (walk_index.hpp:52-56, walk_index.cpp:57-104):
+    magic "PPRW", version u8 = 1, rng-id u8, alpha f64, seed u64, n u64, m u64,
+    offsets (n+1) x u64, endpoints m x u32
+Our index files carry rng-id 2 (Philox4x32-10); the reference loader accepts
+only 1 (walk_index.cpp:91-93) by design.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from ._abi import DataError, Graph, RNG_ID_PHILOX, WalkIndex
+
+_G_MAGIC, _W_MAGIC, _VERSION = b"PPRG", b"PPRW", 1
+
+
+def save_graph_cache(g: Graph, path: str) -> None:
+    off, nbr = g.out_offsets(), g.out_neighbors()
+    with open(path, "wb") as f:
+        f.write(_G_MAGIC)
+        f.write(bytes([_VERSION]))
+        f.write(np.array([g.n(), g.m()], "<u8").tobytes())
+        f.write(off.astype("<u8").tobytes())
+        f.write(nbr.astype("<u4").tobytes())
+
+
+def is_graph_cache(path: str) -> bool:
+    try:
+        with open(path, "rb") as f:
+            return f.read(4) == _G_MAGIC
+    except OSError:
+        return False
+
+
+def read_graph_cache(path: str):
+    """(offsets, neighbors) host arrays of a PPRG file, with the reference's checks."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise DataError(f"cannot open graph cache: {path}")
+    with f:
+        if f.read(4) != _G_MAGIC:
+            raise DataError(f"{path}: not a graph cache (bad magic)")
+        v = f.read(1)
+        if len(v) != 1 or v[0] != _VERSION:
+            raise DataError(f"{path}: unsupported graph cache version")
+        hdr = f.read(16)
+        if len(hdr) != 16:
+            raise DataError(f"{path}: truncated graph cache")
+        n, m = (int(x) for x in np.frombuffer(hdr, "<u8"))
+        off = np.frombuffer(f.read(8 * (n + 1)), "<u8")
+        nbr = np.frombuffer(f.read(4 * m), "<u4")
+        if off.size != n + 1 or nbr.size != m:
+            raise DataError(f"{path}: truncated graph cache")
+    return off.astype(np.uint64), nbr.astype(np.uint32)
+
+
+def load_graph_cache(path: str, device=None) -> Graph:
+    off, nbr = read_graph_cache(path)
+    return Graph(off, nbr, device=device)
+
+
+def save_index(index: WalkIndex, path: str) -> None:
+    g = index.graph
+    with open(path, "wb") as f:
+        f.write(_W_MAGIC)
+        f.write(bytes([_VERSION, index.rng_id()]))
+        f.write(np.array([index.alpha()], "<f8").tobytes())
+        f.write(np.array([index.seed(), g.n(), g.m()], "<u8").tobytes())
+        f.write(g.out_offsets().astype("<u8").tobytes())
+        f.write(index.endpoints().astype("<u4").tobytes())
+
+
+def read_index(path: str):
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise DataError(f"cannot open walk index: {path}")
+    with f:
+        if f.read(4) != _W_MAGIC:
+            raise DataError(f"{path}: not a walk index (bad magic)")
+        b = f.read(2)
+        if len(b) != 2 or b[0] != _VERSION:
+            raise DataError(f"{path}: unsupported walk index version")
+        if b[1] != RNG_ID_PHILOX:
+            raise DataError(f"{path}: unknown generator id")
+        hdr = f.read(32)
+        if len(hdr) != 32:
+            raise DataError(f"{path}: truncated walk index")
+        alpha = float(np.frombuffer(hdr[:8], "<f8")[0])
+        seed, n, m = (int(x) for x in np.frombuffer(hdr[8:], "<u8"))
+        off = np.frombuffer(f.read(8 * (n + 1)), "<u8")
+        ep = np.frombuffer(f.read(4 * m), "<u4")
+        if off.size != n + 1 or ep.size != m:
+            raise DataError(f"{path}: truncated walk index")
+    return alpha, seed, off.astype(np.uint64), ep.astype(np.uint32)
+
+
+def load_index(path: str, g: Graph) -> WalkIndex:
+    alpha, seed, off, ep = read_index(path)
+    if off.size != g.n() + 1 or ep.size != g.m() or not np.array_equal(off, g.out_offsets()):
+        raise DataError("walk index does not match the graph shape")
+    return WalkIndex.from_endpoints(g, alpha, seed, ep)
