@@ -33,8 +33,11 @@ namespace pprg {
 
 constexpr int KMAX = 64;
 constexpr int EMAX = 64;   // max epochs
-constexpr int NT = 256;    // threads per block for the sweep kernels
-constexpr int SWEEP_ELEMS = 2048;  // edges x columns per tile
+#ifndef PPRG_NT
+#define PPRG_NT 128
+#endif
+constexpr int NT = PPRG_NT;             // threads per block for the sweep kernels
+constexpr int SWEEP_ELEMS = NT * 8;     // edges x columns per tile (8 per thread)
 
 enum SweepMode : int { M_POWERPUSH = 0, M_POWITR = 1, M_SIMFWD = 2, M_FINAL = 3 };
 
@@ -116,7 +119,7 @@ template <int K>
 struct Tile {
   static constexpr int T = SWEEP_ELEMS / K;
   static constexpr int SEG = SWEEP_ELEMS / NT;  // 8
-  static constexpr int RMAX = K == 1 ? 256 : (512 / K > 16 ? 512 / K : 16);
+  static constexpr int RMAX = K == 1 ? NT : ((2 * NT) / K > 16 ? (2 * NT) / K : 16);
   static constexpr int RX = RMAX * K;
   // per buffer: sinv[RMAX] | sx[RX] | sr[RX] | sacc[RX] (f64) | soff[RMAX+1] (i32) | snode, sdeg [RMAX] (u32)
   static constexpr size_t buf_bytes = 8ull * (RMAX + 3 * RX) + 4ull * (RMAX + 1) + 8ull * RMAX;
@@ -428,7 +431,7 @@ __device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* c
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(NT, 4) k_sweeps(const __grid_constant__ SweepParams P) {
+__global__ void __launch_bounds__(NT, 1024 / NT) k_sweeps(const __grid_constant__ SweepParams P) {
   using TC = Tile<K>;
   extern __shared__ __align__(16) char smem_dyn[];
   __shared__ ColSh cs[K];
@@ -606,7 +609,36 @@ struct FrontierParams {
   double thr[KMAX];
 };
 
-__global__ void __launch_bounds__(256) k_frontier(const __grid_constant__ FrontierParams P) {
+struct HeavyEntry {  // a frontier node whose scatter is spread over the grid
+  uint64_t begin;    // first out-edge
+  uint32_t deg;
+  uint32_t c;
+  double share;
+};
+constexpr uint32_t HEAVY_DEG = 2048;
+
+// Append (t, c) to the next frontier once per level when it becomes active
+// (drain_queue's enqueue test, push.cpp:49-53). Warp-aggregated append.
+__device__ __forceinline__ void maybe_append(const FrontierParams& P, bool app, uint64_t ti, int c,
+                                             unsigned mask) {
+  const unsigned bal = __ballot_sync(mask, app);
+  if (app) {
+    const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
+    unsigned long long basepos = 0;
+    if (lane == leader) basepos = atomicAdd(P.next_cnt, (unsigned long long)__popc(bal));
+    basepos = __shfl_sync(bal, basepos, leader);
+    P.next[basepos + __popc(bal & ((1u << lane) - 1u))] = ti;
+    atomicAdd(P.col_cnt + c, 1ull);
+  }
+}
+
+// One warp per frontier entry (v, c): claim r (the FIFO pop, push.cpp:38-41),
+// x += r, then scatter (1-a) r / deg_eff to the effective out-neighbours with
+// fp64 atomics, 4 independent atomics per lane in flight. Entries with more
+// than HEAVY_DEG out-edges are queued for k_frontier_heavy instead, so a hub
+// never serialises one warp.
+__global__ void __launch_bounds__(256) k_frontier(const __grid_constant__ FrontierParams P,
+                                                  HeavyEntry* heavy, unsigned* heavy_cnt) {
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -616,41 +648,78 @@ __global__ void __launch_bounds__(256) k_frontier(const __grid_constant__ Fronti
     const uint32_t v = (uint32_t)(i / K);
     const int c = (int)(i % K);
     if (!((P.col_live >> c) & 1ull)) continue;
-    if (lane == 0) atomicAdd(P.col_proc + c, 1ull);
     double r = 0.0;
-    if (lane == 0) r = __longlong_as_double((long long)atomicExch((unsigned long long*)(P.res + i), 0ull));
-    r = __shfl_sync(0xffffffffu, r, 0);
-    if (!(r > 0.0)) {
-      if (lane == 0 && r < 0.0) atomicAdd(P.res + i, r);  // never expected; keep mass
-      continue;
+    if (lane == 0) {
+      atomicAdd(P.col_proc + c, 1ull);
+      r = __longlong_as_double((long long)atomicExch((unsigned long long*)(P.res + i), 0ull));
     }
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (!(r > 0.0)) continue;
     const uint32_t d = P.deg[v];
     const uint64_t de = d ? d : 1;
     const double share = (1.0 - P.alpha) * r / (double)de;
+    const uint64_t b = P.off[v];
     if (lane == 0) {
       P.x[i] += r;
       atomicAdd(P.col_dr + c, P.alpha * r);
       atomicAdd(P.col_np + c, (unsigned long long)de);
       atomicAdd(P.col_nn + c, 1ull);
+      if (de > HEAVY_DEG) heavy[atomicAdd(heavy_cnt, 1u)] = HeavyEntry{b, d, (uint32_t)c, share};
     }
-    const uint64_t b = P.off[v];
-    for (uint64_t q = lane; q < de; q += 32) {
-      const uint32_t t = d ? __ldg(P.nbr + b + q) : P.src[c];
-      const uint64_t ti = (uint64_t)t * K + c;
-      const double nv = atomicAdd(P.res + ti, share) + share;
-      const uint32_t td = P.deg[t];
-      bool app = false;
-      if (nv > (double)(td ? td : 1) * P.thr[c]) app = atomicExch(P.stamp + ti, P.level_tag) != P.level_tag;
-      const unsigned bal = __ballot_sync(__activemask(), app);
-      if (app) {
-        const int leader = __ffs(bal) - 1;
-        unsigned long long basepos = 0;
-        if (lane == leader) basepos = atomicAdd(P.next_cnt, (unsigned long long)__popc(bal));
-        basepos = __shfl_sync(bal, basepos, leader);
-        P.next[basepos + __popc(bal & ((1u << lane) - 1u))] = ti;
-        atomicAdd(P.col_cnt + c, 1ull);
+    if (de > HEAVY_DEG) continue;
+    for (uint64_t q0 = 0; q0 < de; q0 += 128) {
+      uint64_t ti[4];
+      double nv[4];
+      uint32_t td[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint64_t q = q0 + lane + 32 * k;
+        ti[k] = q < de ? (uint64_t)(d ? __ldg(P.nbr + b + q) : P.src[c]) * K + c : ~0ull;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (ti[k] != ~0ull) {
+          nv[k] = atomicAdd(P.res + ti[k], share) + share;
+          td[k] = __ldg(P.deg + ti[k] / K);
+        }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        bool app = false;
+        if (ti[k] != ~0ull && nv[k] > (double)(td[k] ? td[k] : 1) * P.thr[c])
+          app = atomicExch(P.stamp + ti[k], P.level_tag) != P.level_tag;
+        maybe_append(P, app, ti[k], c, 0xffffffffu);
       }
     }
+  }
+}
+
+// The scatter of heavy entries, one thread per out-edge over all of them.
+__global__ void __launch_bounds__(256) k_frontier_heavy(const __grid_constant__ FrontierParams P,
+                                                        const HeavyEntry* heavy,
+                                                        const unsigned long long* prefix,
+                                                        unsigned nheavy, unsigned long long total) {
+  const int K = P.K;
+  for (unsigned long long e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+       e - threadIdx.x < total; e += (uint64_t)gridDim.x * blockDim.x) {
+    const bool ok = e < total;
+    uint64_t ti = 0;
+    int c = 0;
+    bool app = false;
+    if (ok) {
+      unsigned lo = 0, hi = nheavy;  // last h with prefix[h] <= e
+      while (lo + 1 < hi) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (prefix[mid] <= e) lo = mid; else hi = mid;
+      }
+      const HeavyEntry h = heavy[lo];
+      c = (int)h.c;
+      ti = (uint64_t)__ldg(P.nbr + h.begin + (e - prefix[lo])) * K + c;
+      const double nv = atomicAdd(P.res + ti, h.share) + h.share;
+      const uint32_t td = __ldg(P.deg + ti / K);
+      if (nv > (double)(td ? td : 1) * P.thr[c])
+        app = atomicExch(P.stamp + ti, P.level_tag) != P.level_tag;
+    }
+    maybe_append(P, app, ti, c, 0xffffffffu);
   }
 }
 
@@ -739,6 +808,9 @@ struct Workspace {
   DevBuf<unsigned long long> counters;  // next_cnt + col_cnt[K] + col_np[K] + col_nn[K]
   DevBuf<double> dcols;                 // col_dr[K], colsum[K], D[K]
   DevBuf<uint32_t> d_src;
+  DevBuf<HeavyEntry> heavy;
+  DevBuf<unsigned> heavy_cnt;
+  DevBuf<unsigned long long> heavy_prefix;
   unsigned level_tag = 0;
   uint64_t ntiles_alloc = 0;
 };
@@ -769,6 +841,8 @@ static Workspace& workspace(Graph& g, int K, uint64_t ntiles) {
     w.counters.alloc(1 + 4 * KMAX);
     w.dcols.alloc(3 * KMAX);
     w.d_src.alloc(KMAX);
+    w.heavy.alloc((g.m / HEAVY_DEG + 1) * (uint64_t)K + 1);
+    w.heavy_cnt.alloc(1);
   }
   Workspace& w = *slot;
   if (ntiles > w.ntiles_alloc) {
@@ -1032,9 +1106,29 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
       F.col_proc = col_proc;
       F.col_live = live;
       F.level_tag = tag;
-      k_frontier<<<grid_for(chunk * 32), 256, 0, st>>>(F);
+      PPRG_CUDA(cudaMemsetAsync(w.heavy_cnt.get(), 0, 4, st));
+      k_frontier<<<grid_for(chunk * 32), 256, 0, st>>>(F, w.heavy.get(), w.heavy_cnt.get());
       PPRG_CUDA(cudaGetLastError());
       call->kernel_launches += 1;
+      unsigned nheavy = 0;
+      PPRG_CUDA(cudaMemcpyAsync(&nheavy, w.heavy_cnt.get(), 4, cudaMemcpyDeviceToHost, st));
+      PPRG_CUDA(cudaStreamSynchronize(st));
+      if (nheavy) {
+        std::vector<HeavyEntry> hv(nheavy);
+        PPRG_CUDA(cudaMemcpyAsync(hv.data(), w.heavy.get(), sizeof(HeavyEntry) * nheavy,
+                                  cudaMemcpyDeviceToHost, st));
+        PPRG_CUDA(cudaStreamSynchronize(st));
+        std::vector<unsigned long long> pre(nheavy + 1, 0);
+        for (unsigned h = 0; h < nheavy; ++h) pre[h + 1] = pre[h] + hv[h].deg;
+        w.heavy_prefix.ensure(nheavy + 1);
+        PPRG_CUDA(cudaMemcpyAsync(w.heavy_prefix.get(), pre.data(), 8 * (nheavy + 1),
+                                  cudaMemcpyHostToDevice, st));
+        k_frontier_heavy<<<grid_for(pre[nheavy]), 256, 0, st>>>(F, w.heavy.get(),
+                                                                w.heavy_prefix.get(), nheavy,
+                                                                pre[nheavy]);
+        PPRG_CUDA(cudaGetLastError());
+        call->kernel_launches += 1;
+      }
       PPRG_CUDA(cudaMemcpyAsync(hc.data(), w.counters.get(), 8 * NC, cudaMemcpyDeviceToHost, st));
       PPRG_CUDA(cudaMemcpyAsync(hdr.data(), col_dr, 8 * KMAX, cudaMemcpyDeviceToHost, st));
       PPRG_CUDA(cudaStreamSynchronize(st));
@@ -1240,7 +1334,7 @@ uint32_t block_columns(uint64_t n, uint32_t k) {
     if (v >= 1 && v <= KMAX) return (uint32_t)v;
   }
   uint32_t K = KMAX;
-  while (K > 1 && 16.0 * (double)n * K > 80e6) K >>= 1;
+  while (K > 1 && 8.0 * (double)n * K > 80e6) K >>= 1;
   return K < k ? K : (k ? k : 1);
 }
 
