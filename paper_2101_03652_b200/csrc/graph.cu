@@ -84,6 +84,43 @@ __global__ void k_compact_rows(const uint64_t* in_off, const unsigned* flag, con
   if (blockIdx.x == 0 && threadIdx.x == 0) cin_off[n_rows] = m;
 }
 
+__global__ void k_row_degs(const uint32_t* cin_row, uint64_t n_rows, const uint32_t* deg,
+                           const double* inv_deg, uint32_t* cdeg, double* cinv) {
+  GRID_STRIDE(r, n_rows) {
+    cdeg[r] = deg[cin_row[r]];
+    cinv[r] = inv_deg[cin_row[r]];
+  }
+}
+
+// Tile descriptor: (first compact row touching tile j, number of rows) where
+// the rows are the continuation of a row begun in an earlier tile (if any)
+// plus the rows starting in [jT, (j+1)T).
+__device__ __forceinline__ uint64_t lb_rows(const uint64_t* off, uint64_t n, uint64_t key) {
+  uint64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (off[mid] < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__global__ void k_tile_desc(const uint64_t* cin_off, uint64_t n_rows, uint64_t m, uint64_t ntiles,
+                            uint32_t T, uint2* desc) {
+  GRID_STRIDE(j, ntiles) {
+    const uint64_t base = j * (uint64_t)T;
+    const uint64_t lo = lb_rows(cin_off, n_rows, base);
+    const uint64_t hi = lb_rows(cin_off, n_rows, base + T);
+    const bool has_head = lo > 0 && base < m && cin_off[lo] > base;
+    const uint64_t first = has_head ? lo - 1 : lo;
+    desc[j] = make_uint2((uint32_t)first, (uint32_t)(hi - first));
+  }
+}
+
+// Rows spanning more than one tile (their partials are combined after the
+// sweep's grid barrier).
+__global__ void k_split_flags(const uint64_t* cin_off, uint64_t n_rows, uint32_t T, unsigned* flag) {
+  GRID_STRIDE(r, n_rows) flag[r] = (cin_off[r] / T) != ((cin_off[r + 1] - 1) / T);
+}
+
 // own_lo[j] = first row u with in_off[u] >= j*T (lower_bound over row starts)
 __global__ void k_tiles(const uint64_t* in_off, uint64_t n, uint64_t ntiles, uint32_t T,
                         uint32_t* own_lo) {
@@ -334,6 +371,8 @@ void Graph::ensure_transpose() {
     n_rows = 0;
     cin_off.alloc(1);
     cin_row.alloc(1);
+    cin_deg.alloc(1);
+    cin_inv.alloc(1);
     PPRG_CUDA(cudaMemsetAsync(cin_off.get(), 0, 8, st));
     PPRG_CUDA(cudaStreamSynchronize(st));
     return;
@@ -369,8 +408,58 @@ void Graph::ensure_transpose() {
   cin_row.alloc(n_rows ? n_rows : 1);
   k_compact_rows<<<blocks_for(n), TB, 0, st>>>(in_off.get(), flag.get(), pos.get(), n, m,
                                                cin_off.get(), cin_row.get(), n_rows);
+  cin_deg.alloc(n_rows ? n_rows : 1);
+  cin_inv.alloc(n_rows ? n_rows : 1);
+  if (n_rows)
+    k_row_degs<<<blocks_for(n_rows), TB, 0, st>>>(cin_row.get(), n_rows, deg.get(), inv_deg.get(),
+                                                  cin_deg.get(), cin_inv.get());
   PPRG_CUDA(cudaStreamSynchronize(st));
   PPRG_CUDA(cudaGetLastError());
+}
+
+const uint2* Graph::tile_desc(uint32_t T, uint64_t* ntiles) {
+  ensure_transpose();
+  *ntiles = m / T + 1;
+  auto it = tile_d.find(T);
+  if (it != tile_d.end()) return it->second.get();
+  DevBuf<uint2> d(*ntiles);
+  k_tile_desc<<<blocks_for(*ntiles), TB, 0, stream>>>(cin_off.get(), n_rows, m, *ntiles, T, d.get());
+  PPRG_CUDA(cudaStreamSynchronize(stream));
+  PPRG_CUDA(cudaGetLastError());
+  const uint2* p = d.get();
+  tile_d.emplace(T, std::move(d));
+  return p;
+}
+
+const uint32_t* Graph::split_rows(uint32_t T, uint64_t* count) {
+  ensure_transpose();
+  auto it = tile_split.find(T);
+  if (it != tile_split.end()) {
+    *count = it->second.n;
+    return it->second.get();
+  }
+  cudaStream_t st = stream;
+  const uint64_t nr = n_rows;
+  DevBuf<unsigned> flag(nr + 1), pos(nr + 1);
+  PPRG_CUDA(cudaMemsetAsync(flag.get(), 0, 4 * (nr + 1), st));
+  if (nr) k_split_flags<<<blocks_for(nr), TB, 0, st>>>(cin_off.get(), nr, T, flag.get());
+  unsigned* fp = flag.get();
+  unsigned* pp = pos.get();
+  cub_call([&](void* t, size_t& b) {
+    return cub::DeviceScan::ExclusiveSum(t, b, fp, pp, (int64_t)(nr + 1), st);
+  }, st);
+  unsigned cnt = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&cnt, pos.get() + nr, 4, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  DevBuf<uint32_t> list(cnt ? cnt : 1);
+  if (nr) k_scatter_flagged<<<blocks_for(nr), TB, 0, st>>>(flag.get(), pos.get(), nr, list.get());
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  PPRG_CUDA(cudaGetLastError());
+  list.n = cnt;
+  *count = cnt;
+  const uint32_t* p = list.get();
+  tile_split.emplace(T, std::move(list));
+  return p;
 }
 
 const uint32_t* Graph::tiles(uint32_t T, uint64_t* ntiles) {

@@ -73,11 +73,14 @@ struct SweepParams {
   uint64_t n, m;
   const uint64_t* in_off;      // compacted transpose rows (in-degree > 0)
   const uint32_t* crow;        // node id of each compacted row
+  const uint32_t* cdeg;        // out-degree of each compacted row's node
+  const double* cinv;          // 1 / effective out-degree of each compacted row's node
   const uint64_t* in_off_full; // transpose offsets per node
   const uint32_t* in_nbr;
   const uint32_t* deg;
   const double* inv_deg;
   const uint32_t* tile_lo;
+  const uint2* desc;           // per tile: (first compact row, rows)
   uint64_t ntiles;
   uint32_t T;
   int k_live;  // real columns (<= K)
@@ -91,6 +94,9 @@ struct SweepParams {
   double* carry_head;
   double* carry_tail;
   unsigned* split_cnt;
+  const uint32_t* split_list;  // compact rows spanning tiles
+  uint64_t n_split;
+  double* split_acc;           // [2][ntiles+1][K] per-sweep partial sums of split rows
   SweepCtl* ctl;
   double* out_reserve;         // finalize outputs, query-major [c*n + u]
   double* out_residue;
@@ -110,21 +116,24 @@ struct ColSh {
   unsigned long long pushes;
 };
 
-// Tile geometry. A tile is T = 2048/K consecutive in-edges; thread t owns
-// column c = t % K and the SEG = 8 consecutive edges [8 (t/K), 8 (t/K) + 8)
-// of the tile, so every thread does identical gather work. Rows (the
-// transpose's rows with in-degree > 0, so none is empty) are staged in chunks
-// of RMAX, double-buffered between consecutive tiles.
+// Tile geometry. A tile is T = SWEEP_ELEMS/K consecutive in-edges; thread t
+// owns column c = t % K and the SEG = 8 consecutive edges [8 (t/K), 8 (t/K) + 8)
+// of the tile, so every thread does identical gather work. The gathered values
+// of two tiles (current, next) live in shared memory in an owner-private
+// layout vals[i*NT + t]; rows (the transpose's rows with in-degree > 0, so
+// none is empty) are staged in chunks of RMAX, double-buffered.
 template <int K>
 struct Tile {
   static constexpr int T = SWEEP_ELEMS / K;
   static constexpr int SEG = SWEEP_ELEMS / NT;  // 8
-  static constexpr int RMAX = K == 1 ? NT : ((2 * NT) / K > 16 ? (2 * NT) / K : 16);
+  static constexpr int RMAX_ = (2 * NT) / K > 16 ? (2 * NT) / K : 16;
+  static constexpr int RMAX = RMAX_ < NT - 1 ? RMAX_ : NT - 1;  // nr + 1 offsets fit one per thread
   static constexpr int RX = RMAX * K;
-  // per buffer: sinv[RMAX] | sx[RX] | sr[RX] | sacc[RX] (f64) | soff[RMAX+1] (i32) | snode, sdeg [RMAX] (u32)
+  // per staging buffer: sinv[RMAX] | sx[RX] | sr[RX] | sacc[RX] (f64) | soff[RMAX+1] (i32) | snode, sdeg [RMAX] (u32)
   static constexpr size_t buf_bytes = 8ull * (RMAX + 3 * RX) + 4ull * (RMAX + 1) + 8ull * RMAX;
   static constexpr size_t buf_stride = (buf_bytes + 15) / 16 * 16;
-  static constexpr size_t bytes = 2 * buf_stride;
+  static constexpr size_t vals_bytes = 8ull * SWEEP_ELEMS;
+  static constexpr size_t bytes = 2 * vals_bytes + 2 * buf_stride;
 };
 
 struct Acc {  // per-thread sweep counters for the thread's column
@@ -139,6 +148,18 @@ struct BlockAcc {  // shared, per column
   unsigned long long* nn;
   unsigned long long* et;
 };
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 8 : 0;  // src-size 0 zero-fills
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 
 // The per-(row, column) decision: push form of push.cpp:182-193 in pull
 // representation, the PowItr update of push.cpp:90-99, or the final explicit
@@ -200,216 +221,279 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
   }
 }
 
-// A row straddling tiles: publish this tile's per-column partials; the last
-// tile to arrive sums all partials in tile order and decides the row. Kept
-// out of line so the common path stays register-lean. `rb`/`re` are the
-// row's global edge range.
-template <int K, int MODE>
-__device__ __noinline__ void split_row(const SweepParams& P, uint64_t j, uint32_t r, uint64_t rb,
-                                       uint64_t re, const uint32_t* snode, const double* sx,
-                                       const double* sr, const double* sacc, const uint32_t* sdeg,
-                                       const double* sinv, const ColSh* cs, const double* thr_cur,
-                                       const double* yg, double* rnxt, double* ynxt,
-                                       const BlockAcc& ba) {
+// A row straddling tiles adds this tile's per-column partial into the sweep's
+// accumulator (fire-and-forget RED, keyed by the row's first tile); the row is
+// decided after the grid barrier by split_decide.
+template <int K>
+__device__ __noinline__ void post_split(const SweepParams& P, uint32_t cr, uint32_t r,
+                                        const double* sacc, uint32_t parity) {
   constexpr int T = Tile<K>::T;
-  const uint64_t base = j * (uint64_t)T;
-  const uint64_t ft = rb / T, lt = (re - 1) / T;
-  double* slot = (rb < base ? P.carry_head : P.carry_tail) + j * K;
-  for (int cc = 0; cc < K; ++cc) __stcg(slot + cc, sacc[r * K + cc]);
-  // release-ordered arrival (MEMBAR.GPU, no L1 invalidation); partials are
-  // read back from L2 (ld.cg) by the last arriver.
-  unsigned old;
-  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
-               : "=r"(old) : "l"(P.split_cnt + ft) : "memory");
-  if (old != (unsigned)(lt - ft)) return;
-  P.split_cnt[ft] = 0;
-  for (int cc = 0; cc < K; ++cc) {
-    double sum = __ldcg(P.carry_tail + ft * K + cc);
-    for (uint64_t t = ft + 1; t <= lt; ++t) sum += __ldcg(P.carry_head + t * K + cc);
-    Acc b;
-    decide<K, MODE>(P, cs, thr_cur, snode[r], cc, sum, sx[r * K + cc],
-                    (MODE == M_POWITR || MODE == M_SIMFWD) ? sr[r * K + cc] : 0.0, sdeg[r],
-                    sinv[r], yg, rnxt, ynxt, b);
-    if (b.push != 0.0) atomicAdd(&ba.push[cc], b.push);
-    if (b.d != 0.0) atomicAdd(&ba.d[cc], b.d);
-    if (b.np) atomicAdd(&ba.np[cc], b.np);
-    if (b.nn) atomicAdd(&ba.nn[cc], b.nn);
-    if (b.et) atomicAdd(&ba.et[cc], b.et);
+  const uint64_t ft = __ldg(P.in_off + cr) / T;
+  double* acc = P.split_acc + ((uint64_t)parity * (P.ntiles + 1) + ft) * K;
+  for (int cc = 0; cc < K; ++cc) atomicAdd(acc + cc, sacc[r * K + cc]);
+}
+
+// Decide every split row from the accumulated partials of sweep `parity`
+// (grid-stride; thread column = tid % K as everywhere), and clear them.
+template <int K, int MODE>
+__device__ __forceinline__ void split_decide(const SweepParams& P, uint32_t parity, const ColSh* cs,
+                                             const double* thr_cur, const double* yg,
+                                             const double* rcur, double* rnxt, double* ynxt,
+                                             Acc& a) {
+  constexpr int T = Tile<K>::T;
+  const uint64_t total = P.n_split * K;
+  for (uint64_t idx = blockIdx.x * (uint64_t)NT + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * NT) {
+    const uint32_t cr = P.split_list[idx / K];
+    const int c = (int)(idx % K);
+    const uint64_t ft = __ldg(P.in_off + cr) / T;
+    double* slot = P.split_acc + ((uint64_t)parity * (P.ntiles + 1) + ft) * K + c;
+    const double acc = __ldcg(slot);
+    *slot = 0.0;
+    const uint32_t u = __ldg(P.crow + cr);
+    const uint64_t ix = (uint64_t)u * K + c;
+    decide<K, MODE>(P, cs, thr_cur, u, c, acc, __ldcg(P.x + ix),
+                    (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0,
+                    __ldg(P.cdeg + cr), __ldg(P.cinv + cr), yg, rnxt, ynxt, a);
   }
 }
 
-// One tile of in-edges [j*T, (j+1)*T).
-//   1. every thread loads its 8 in-neighbour ids (one 32-byte vector load),
-//      issues its 8 independent gathers of y, and the block stages the tile's
-//      rows (offsets, node ids, degrees, state) -- one memory latency for all;
-//   2. segmented reduction: each thread walks its 8 edges across row ends
-//      (rows are never empty, so at most one boundary per edge); rows wholly
-//      inside the segment are stored directly, rows shared by consecutive
-//      segments are combined by a segmented shuffle scan over the lanes of the
-//      same column, and only rows crossing a warp boundary use a shared atomic;
-//   3. one thread per (row, column) decides. Rows straddling tiles (at most
-//      the first and the last) go through split_row.
+// The in-neighbour ids of my 8 edges of tile j (one 32-byte vector load).
+template <int K>
+__device__ __forceinline__ void load_ids(const SweepParams& P, uint64_t j, uint32_t (&id)[8]) {
+  constexpr int T = Tile<K>::T, SEG = Tile<K>::SEG;
+  const int32_t seg0 = (threadIdx.x / K) * SEG;
+  const uint64_t base = j * (uint64_t)T;
+  const int32_t ne = base < P.m ? (int32_t)(P.m - base < (uint64_t)T ? P.m - base : (uint64_t)T) : 0;
+  if (seg0 + SEG <= ne) {
+    const uint4* p4 = reinterpret_cast<const uint4*>(P.in_nbr + base + seg0);
+    const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1);
+    id[0] = q0.x; id[1] = q0.y; id[2] = q0.z; id[3] = q0.w;
+    id[4] = q1.x; id[5] = q1.y; id[6] = q1.z; id[7] = q1.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < SEG; ++i) id[i] = seg0 + i < ne ? __ldg(P.in_nbr + base + seg0 + i) : ~0u;
+  }
+}
+
+// Issue my 8 gathers of y for tile j as cp.async into my private slots.
+template <int K>
+__device__ __forceinline__ void issue_gathers(const double* yg, const uint32_t (&id)[8],
+                                              double* vals) {
+  const int c = threadIdx.x % K;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const bool ok = id[i] != ~0u;
+    cp_async8(vals + i * NT + threadIdx.x, yg + (ok ? (uint64_t)id[i] * K + c : 0), ok);
+  }
+}
+
+// Row data of one tile's first chunk, prefetched into registers one tile ahead
+// (thread t holds row t; thread nr holds only the end offset).
+struct RowPre {
+  uint64_t off = 0;
+  uint32_t node = 0, deg = 0;
+  double inv = 0.0;
+};
+
+template <int K>
+__device__ __forceinline__ void load_rows(const SweepParams& P, uint2 d, RowPre& rp) {
+  constexpr int RMAX = Tile<K>::RMAX;
+  const uint32_t nr = d.y < (uint32_t)RMAX ? d.y : RMAX;
+  const uint32_t t = threadIdx.x;
+  if (t <= nr) rp.off = __ldg(P.in_off + d.x + t);
+  if (t < nr) {
+    rp.node = __ldg(P.crow + d.x + t);
+    rp.deg = __ldg(P.cdeg + d.x + t);
+    rp.inv = __ldg(P.cinv + d.x + t);
+  }
+}
+
+// Stage rows [cr0, cr0 + nr) of tile `base` into a staging buffer.
+template <int K>
+__device__ __forceinline__ void stage_rows_from(const RowPre& rp, uint32_t nr, uint64_t base,
+                                                char* buf) {
+  using TC = Tile<K>;
+  constexpr int T = TC::T, RMAX = TC::RMAX, RX = TC::RX;
+  double* sinv = reinterpret_cast<double*>(buf);
+  double* sacc = sinv + RMAX + 2 * RX;
+  int32_t* soff = reinterpret_cast<int32_t*>(sacc + RX);
+  uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
+  uint32_t* sdeg = snode + RMAX;
+  const uint32_t t = threadIdx.x;
+  if (t <= nr) {
+    const int64_t d = (int64_t)rp.off - (int64_t)base;
+    soff[t] = d < 0 ? -1 : (d > T ? T + 1 : (int32_t)d);
+  }
+  if (t < nr) {
+    snode[t] = rp.node;
+    sdeg[t] = rp.deg;
+    sinv[t] = rp.inv;
+#pragma unroll
+    for (int cc = 0; cc < K; ++cc) sacc[t * K + cc] = 0.0;
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void stage_rows_sync(const SweepParams& P, uint32_t cr0, uint32_t nr,
+                                                uint64_t base, char* buf) {
+  for (uint32_t t0 = 0; t0 <= nr; t0 += NT) {
+    RowPre rp;
+    const uint32_t t = t0 + threadIdx.x;
+    if (t <= nr) rp.off = __ldg(P.in_off + cr0 + t);
+    if (t < nr) {
+      rp.node = __ldg(P.crow + cr0 + t);
+      rp.deg = __ldg(P.cdeg + cr0 + t);
+      rp.inv = __ldg(P.cinv + cr0 + t);
+    }
+    // stage_rows_from uses threadIdx.x as the row; emulate the offset t0
+    using TC = Tile<K>;
+    constexpr int T = TC::T, RMAX = TC::RMAX, RX = TC::RX;
+    double* sinv = reinterpret_cast<double*>(buf);
+    double* sacc = sinv + RMAX + 2 * RX;
+    int32_t* soff = reinterpret_cast<int32_t*>(sacc + RX);
+    uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
+    uint32_t* sdeg = snode + RMAX;
+    if (t <= nr) {
+      const int64_t d = (int64_t)rp.off - (int64_t)base;
+      soff[t] = d < 0 ? -1 : (d > T ? T + 1 : (int32_t)d);
+    }
+    if (t < nr) {
+      snode[t] = rp.node;
+      sdeg[t] = rp.deg;
+      sinv[t] = rp.inv;
+      for (int cc = 0; cc < K; ++cc) sacc[t * K + cc] = 0.0;
+    }
+  }
+}
+
+// Reduce + decide one staged chunk (rows [cr0, cr0+nr)) of tile j whose
+// gathered values are in `vals`. Called after the staging barrier.
 template <int K, int MODE>
-__device__ __forceinline__ void process_tile(const SweepParams& P, uint64_t j, char* smem_buf,
-                                             const ColSh* cs, const double* thr_cur,
-                                             const double* yg, const double* rcur, double* rnxt,
-                                             double* ynxt, Acc& a, const BlockAcc& ba) {
+__device__ __forceinline__ void chunk_compute(const SweepParams& P, uint64_t j, const double* vals,
+                                              char* smem_buf, uint32_t cr0, uint32_t nr,
+                                              bool first_chunk, bool last_chunk, uint32_t parity,
+                                              const ColSh* cs,
+                                              const double* thr_cur, const double* yg,
+                                              const double* rcur, double* rnxt, double* ynxt,
+                                              Acc& a, const BlockAcc& ba) {
   using TC = Tile<K>;
   constexpr int T = TC::T, SEG = TC::SEG, RMAX = TC::RMAX, RX = TC::RX;
   double* sinv = reinterpret_cast<double*>(smem_buf);
-  double* sx = sinv + RMAX;
-  double* sr = sx + RX;
+  double* sr = sinv + RMAX + RX;
   double* sacc = sr + RX;
-  int32_t* soff = reinterpret_cast<int32_t*>(sacc + RX);  // tile-local, clamped to [-1, T+1]
+  int32_t* soff = reinterpret_cast<int32_t*>(sacc + RX);
   uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
   uint32_t* sdeg = snode + RMAX;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int c = tid % K;
-  const int32_t seg0 = (tid / K) * SEG;  // tile-local first edge
+  const int32_t seg0 = (tid / K) * SEG;
   const uint64_t base = j * (uint64_t)T;
   const int32_t ne = base < P.m ? (int32_t)(P.m - base < (uint64_t)T ? P.m - base : (uint64_t)T) : 0;
-  const uint32_t lo = P.tile_lo[j], hi = P.tile_lo[j + 1];
-  const bool has_head = lo > 0 && ne > 0 && __ldg(P.in_off + lo) > base;
-  const uint32_t r_first = has_head ? lo - 1 : lo;
-  const uint32_t nrows_all = hi - r_first;
 
-  // ---- 1a. ids + gathers (registers) ---------------------------------------
-  double v[SEG];
-  {
-    uint32_t id[SEG];
-    if (seg0 + SEG <= ne) {
-      const uint4* p4 = reinterpret_cast<const uint4*>(P.in_nbr + base + seg0);
-      const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1);
-      id[0] = q0.x; id[1] = q0.y; id[2] = q0.z; id[3] = q0.w;
-      id[4] = q1.x; id[5] = q1.y; id[6] = q1.z; id[7] = q1.w;
-    } else {
-#pragma unroll
-      for (int i = 0; i < SEG; ++i)
-        id[i] = seg0 + i < ne ? __ldg(P.in_nbr + base + seg0 + i) : 0u;
-    }
-#pragma unroll
-    for (int i = 0; i < SEG; ++i)
-      v[i] = seg0 + i < ne ? yg[(uint64_t)id[i] * K + c] : 0.0;
+  // prefetch the state of my first decision (lands during the reduction)
+  double xo0 = 0.0, rc0 = 0.0;
+  if ((uint32_t)tid < nr * K) {
+    const uint64_t ix = (uint64_t)snode[tid / K] * K + c;
+    xo0 = __ldcg(P.x + ix);
+    if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) rc0 = __ldcg(rcur + ix);
   }
+  if (first_chunk) cp_async_wait<1>();  // my gathers of this tile have landed
 
-  for (uint32_t row0 = 0; row0 < nrows_all || row0 == 0; row0 += RMAX) {
-    const uint32_t nr = nrows_all - row0 < (uint32_t)RMAX ? nrows_all - row0 : RMAX;
-    const uint32_t cr0 = r_first + row0;  // first compact row of the chunk
-    // ---- 1b. stage rows --------------------------------------------------
-    for (uint32_t t = tid; t <= nr; t += NT) {
-      const int64_t d = (int64_t)__ldg(P.in_off + cr0 + t) - (int64_t)base;
-      soff[t] = d < 0 ? -1 : (d > T ? T + 1 : (int32_t)d);
-    }
-    for (uint32_t t = tid; t < nr; t += NT) {
-      const uint32_t u = __ldg(P.crow + cr0 + t);
-      snode[t] = u;
-      sdeg[t] = __ldg(P.deg + u);
-      sinv[t] = __ldg(P.inv_deg + u);
-    }
-    for (uint32_t f = tid; f < nr * K; f += NT) {
-      const uint64_t ix = (uint64_t)__ldg(P.crow + cr0 + f / K) * K + f % K;
-      sx[f] = __ldcg(P.x + ix);
-      if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) sr[f] = __ldcg(rcur + ix);
-      sacc[f] = 0.0;
-    }
-    __syncthreads();
-
-    // ---- 2. segmented reduction over my 8 edges -----------------------------
-    {
-      constexpr uint32_t SENT = 0xFFFFFFFFu;
-      double hp = 0.0, tp = 0.0;
-      uint32_t f = SENT, l = SENT;
-      bool started = false, cont = false, have = false;
-      if (nr > 0) {
-        const int32_t cbeg = soff[0] < 0 ? 0 : soff[0];
-        int32_t e_hi = seg0 + SEG;
-        if (e_hi > ne) e_hi = ne;
-        if (e_hi > soff[nr]) e_hi = soff[nr];
-        const int32_t e_lo = seg0 > cbeg ? seg0 : cbeg;
-        if (e_lo < e_hi) {
-          have = true;
-          uint32_t lo_r = 0, hi_r = nr;  // last row r with soff[r] <= e_lo
-          while (lo_r + 1 < hi_r) {
-            const uint32_t mid = (lo_r + hi_r) >> 1;
-            if (soff[mid] <= e_lo) lo_r = mid; else hi_r = mid;
-          }
-          uint32_t r = lo_r;
-          f = r;
-          started = soff[r] < e_lo;
-          int32_t rend = soff[r + 1];
-          double part = 0.0;
+  // ---- segmented reduction over my 8 edges ---------------------------------
+  {
+    constexpr uint32_t SENT = 0xFFFFFFFFu;
+    double hp = 0.0, tp = 0.0;
+    uint32_t f = SENT, l = SENT;
+    bool started = false, cont = false, have = false;
+    if (nr > 0) {
+      const int32_t cbeg = soff[0] < 0 ? 0 : soff[0];
+      int32_t e_hi = seg0 + SEG;
+      if (e_hi > ne) e_hi = ne;
+      if (e_hi > soff[nr]) e_hi = soff[nr];
+      const int32_t e_lo = seg0 > cbeg ? seg0 : cbeg;
+      if (e_lo < e_hi) {
+        have = true;
+        uint32_t lo_r = 0, hi_r = nr;  // last row r with soff[r] <= e_lo
+        while (lo_r + 1 < hi_r) {
+          const uint32_t mid = (lo_r + hi_r) >> 1;
+          if (soff[mid] <= e_lo) lo_r = mid; else hi_r = mid;
+        }
+        uint32_t r = lo_r;
+        f = r;
+        started = soff[r] < e_lo;
+        int32_t rend = soff[r + 1];
+        double part = 0.0;
 #pragma unroll
-          for (int i = 0; i < SEG; ++i) {
-            const int32_t e = seg0 + i;
-            if (e >= e_lo && e < e_hi) {
-              if (e >= rend) {  // row r ended at e - 1 (rows are never empty)
-                if (r == f) hp = part;
-                else sacc[r * K + c] = part;  // started and ended inside the segment
-                part = 0.0;
-                ++r;
-                rend = soff[r + 1];
-              }
-              part += v[i];
+        for (int i = 0; i < SEG; ++i) {
+          const int32_t e = seg0 + i;
+          if (e >= e_lo && e < e_hi) {
+            if (e >= rend) {  // row r ended at e - 1 (rows are never empty)
+              if (r == f) hp = part;
+              else sacc[r * K + c] = part;  // started and ended inside the segment
+              part = 0.0;
+              ++r;
+              rend = soff[r + 1];
             }
+            part += vals[i * NT + tid];
           }
-          l = r;
-          cont = rend > e_hi;
-          if (l == f) hp = part; else tp = part;
-          if (l != f && !cont) sacc[l * K + c] = tp;
-          if (!started && (l != f || !cont)) sacc[f * K + c] = hp;
         }
+        l = r;
+        cont = rend > e_hi;
+        if (l == f) hp = part; else tp = part;
+        if (l != f && !cont) sacc[l * K + c] = tp;
+        if (!started && (l != f || !cont)) sacc[f * K + c] = hp;
       }
-      const double carry = cont ? (l == f ? hp : tp) : 0.0;
-      const uint32_t key = have ? l : SENT;
-      double S = carry;
-      double carry_in = 0.0;
-      uint32_t f_next = SENT;  // first row of the next segment of my column
-      if constexpr (K < 32) {
+    }
+    const double carry = cont ? (l == f ? hp : tp) : 0.0;
+    const uint32_t key = have ? l : SENT;
+    double S = carry;
+    double carry_in = 0.0;
+    uint32_t f_next = SENT;  // first row of the next segment of my column
+    if constexpr (K < 32) {
 #pragma unroll
-        for (int d = K; d < 32; d <<= 1) {
-          const double Sd = __shfl_up_sync(0xffffffffu, S, d);
-          const uint32_t kd = __shfl_up_sync(0xffffffffu, key, d);
-          if (lane >= d && kd == key) S += Sd;
-        }
-        const double Sp = __shfl_up_sync(0xffffffffu, S, K);
-        const uint32_t kp = __shfl_up_sync(0xffffffffu, key, K);
-        if (lane >= K && kp == f) carry_in = Sp;
-        f_next = __shfl_down_sync(0xffffffffu, f, K);
+      for (int d = K; d < 32; d <<= 1) {
+        const double Sd = __shfl_up_sync(0xffffffffu, S, d);
+        const uint32_t kd = __shfl_up_sync(0xffffffffu, key, d);
+        if (lane >= d && kd == key) S += Sd;
       }
-      const int first_lane = K < 32 ? lane % K : lane;
-      const uint32_t f_first = __shfl_sync(0xffffffffu, f, first_lane);
-      const bool st_first = __shfl_sync(0xffffffffu, started, first_lane);
-      if (have && started && !(l == f && cont)) {  // I finish row f
-        const double val = hp + carry_in;
-        if (f == f_first && st_first) atomicAdd(&sacc[f * K + c], val);  // began in an earlier warp
-        else sacc[f * K + c] = val;
-      }
-      if (have && cont && (lane + K >= 32 || f_next != key))
-        atomicAdd(&sacc[l * K + c], S);  // row l continues past this warp / chunk
+      const double Sp = __shfl_up_sync(0xffffffffu, S, K);
+      const uint32_t kp = __shfl_up_sync(0xffffffffu, key, K);
+      if (lane >= K && kp == f) carry_in = Sp;
+      f_next = __shfl_down_sync(0xffffffffu, f, K);
     }
-    __syncthreads();
+    const int first_lane = K < 32 ? lane % K : lane;
+    const uint32_t f_first = __shfl_sync(0xffffffffu, f, first_lane);
+    const bool st_first = __shfl_sync(0xffffffffu, started, first_lane);
+    if (have && started && !(l == f && cont)) {  // I finish row f
+      const double val = hp + carry_in;
+      if (f == f_first && st_first) atomicAdd(&sacc[f * K + c], val);  // began in an earlier warp
+      else sacc[f * K + c] = val;
+    }
+    if (have && cont && (lane + K >= 32 || f_next != key))
+      atomicAdd(&sacc[l * K + c], S);  // row l continues past this warp / chunk
+  }
+  __syncthreads();
 
-    // ---- 3. decisions -------------------------------------------------------
-    const bool last_chunk = row0 + nr >= nrows_all;
-    for (uint32_t f = tid; f < nr * K; f += NT) {
-      const uint32_t r = f / K;
-      if (soff[r] < 0 || soff[r + 1] > T) continue;  // straddles the tile: split_row
-      decide<K, MODE>(P, cs, thr_cur, snode[r], c, sacc[f], sx[f],
-                      (MODE == M_POWITR || MODE == M_SIMFWD) ? sr[f] : 0.0, sdeg[r], sinv[r], yg,
-                      rnxt, ynxt, a);
+  // ---- rows straddling the tile: post partials --------------------------
+  const uint32_t rl = nr ? nr - 1 : 0;
+  const bool first_split = first_chunk && nr > 0 && (soff[0] < 0 || soff[1] > T);
+  const bool last_split = last_chunk && nr > 0 && !(first_chunk && rl == 0) && soff[rl + 1] > T;
+  if (tid == 0 && first_split) post_split<K>(P, cr0, 0, sacc, parity);
+  if (tid == 32 && last_split) post_split<K>(P, cr0 + rl, rl, sacc, parity);
+  // ---- decisions --------------------------------------------------------
+  for (uint32_t fi = tid; fi < nr * K; fi += NT) {
+    const uint32_t r = fi / K;
+    if (soff[r] < 0 || soff[r + 1] > T) continue;  // straddles the tile: split_row
+    double xo = xo0, rc = rc0;
+    if (fi != (uint32_t)tid) {
+      const uint64_t ix = (uint64_t)snode[r] * K + c;
+      xo = __ldcg(P.x + ix);
+      if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) rc = __ldcg(rcur + ix);
     }
-    const uint32_t rl = nr ? nr - 1 : 0;
-    const bool first_split = row0 == 0 && nr > 0 && (soff[0] < 0 || soff[1] > T);
-    const bool last_split = last_chunk && nr > 0 && !(row0 == 0 && rl == 0) && soff[rl + 1] > T;
-    if ((tid == 0 && first_split) || (tid == 32 && last_split)) {
-      const uint32_t r = tid == 0 ? 0 : rl;
-      const uint64_t rb = __ldg(P.in_off + cr0 + r), re = __ldg(P.in_off + cr0 + r + 1);
-      split_row<K, MODE>(P, j, r, rb, re, snode, sx, sr, sacc, sdeg, sinv, cs, thr_cur, yg, rnxt,
-                         ynxt, ba);
-    }
-    if (!last_chunk) __syncthreads();  // the next chunk restages this buffer
-    if (nrows_all == 0) break;
+    decide<K, MODE>(P, cs, thr_cur, snode[r], c, sacc[fi], xo, rc, sdeg[r], sinv[r], yg, rnxt,
+                    ynxt, a);
   }
 }
 
@@ -431,7 +515,10 @@ __device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* c
 }
 
 template <int K, int MODE>
-__global__ void __launch_bounds__(NT, 1024 / NT) k_sweeps(const __grid_constant__ SweepParams P) {
+#ifndef PPRG_MINB
+#define PPRG_MINB 6
+#endif
+__global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant__ SweepParams P) {
   using TC = Tile<K>;
   extern __shared__ __align__(16) char smem_dyn[];
   __shared__ ColSh cs[K];
@@ -491,17 +578,73 @@ __global__ void __launch_bounds__(NT, 1024 / NT) k_sweeps(const __grid_constant_
     double* rnxt = P.r[(sweep + 1) & 1];
     double* ynxt = P.y[(sweep + 1) & 1];
     Acc a;
-    // Tickets are fetched two tiles ahead into a 3-slot ring, and row staging
-    // is double-buffered, so consecutive tiles need no block barrier between
-    // them: warps that finish a tile's decisions start the next tile's gathers.
+    if (MODE == M_POWERPUSH && sweep > 0)  // rows straddling tiles, from the last sweep
+      split_decide<K, MODE>(P, (sweep - 1) & 1, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+    // Software pipeline. Tickets are fetched two tiles ahead into a 3-slot
+    // ring; the ids of tile it+2 are loaded during tile it; the gathers of
+    // tile it+1 are issued (cp.async, owner-private slots) before tile it is
+    // reduced. Row staging is double-buffered, so consecutive tiles need no
+    // block barrier between them.
+    uint32_t ids[8];
+    RowPre rp;  // rows (first chunk) of the tile about to be processed
+    uint2 dcur = make_uint2(0, 0), dnext = make_uint2(0, 0);
+    double* vals0 = reinterpret_cast<double*>(smem_dyn);
+    double* vals1 = vals0 + SWEEP_ELEMS;
+    char* stage0 = smem_dyn + 2 * TC::vals_bytes;
+    {
+      const unsigned long long j0 = sh_tile[0], j1 = sh_tile[1];
+      if (j0 < P.ntiles) {
+        dcur = P.desc[j0];
+        load_rows<K>(P, dcur, rp);
+        load_ids<K>(P, j0, ids);
+        issue_gathers<K>(yg, ids, vals0);
+      }
+      cp_async_commit();
+      if (j1 < P.ntiles) {
+        dnext = P.desc[j1];
+        load_ids<K>(P, j1, ids);
+      }
+    }
     for (uint32_t it = 0;; ++it) {
       const unsigned long long j = sh_tile[it % 3];
       if (j >= P.ntiles) break;
+      const unsigned long long jn = sh_tile[(it + 1) % 3];
+      if (jn < P.ntiles) issue_gathers<K>(yg, ids, (it & 1) ? vals0 : vals1);
+      cp_async_commit();
       if (tid == 0) sh_tile[(it + 2) % 3] = atomicAdd(&ctl->ticket[buf], 1u);
-      process_tile<K, MODE>(P, j, smem_dyn + (it & 1) * TC::buf_stride, cs, thr_cur, yg, rcur,
-                            rnxt, ynxt, a, ba);
+      char* sbuf = stage0 + (it & 1) * TC::buf_stride;
+      const uint64_t base = j * (uint64_t)TC::T;
+      const uint2 dthis = dcur;
+      const uint32_t nr0 = dthis.y < (uint32_t)TC::RMAX ? dthis.y : TC::RMAX;
+      stage_rows_from<K>(rp, nr0, base, sbuf);
+      __syncthreads();
+      // prefetch: rows of tile it+1, descriptor and ids of tile it+2
+      const unsigned long long j2 = sh_tile[(it + 2) % 3];
+      if (jn < P.ntiles) load_rows<K>(P, dnext, rp);
+      dcur = dnext;
+      if (j2 < P.ntiles) {
+        dnext = P.desc[j2];
+        load_ids<K>(P, j2, ids);
+      }
+      const double* vals = (it & 1) ? vals1 : vals0;
+      chunk_compute<K, MODE>(P, j, vals, sbuf, dthis.x, nr0, true, dthis.y <= (uint32_t)TC::RMAX,
+                             sweep & 1, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba);
+      for (uint32_t row0 = TC::RMAX; row0 < dthis.y; row0 += TC::RMAX) {  // rare: many rows
+        __syncthreads();
+        const uint32_t nr = dthis.y - row0 < (uint32_t)TC::RMAX ? dthis.y - row0 : TC::RMAX;
+        stage_rows_sync<K>(P, dthis.x + row0, nr, base, sbuf);
+        __syncthreads();
+        chunk_compute<K, MODE>(P, j, vals, sbuf, dthis.x + row0, nr, false,
+                               row0 + nr >= dthis.y, sweep & 1, cs, thr_cur, yg, rcur, rnxt, ynxt,
+                               a, ba);
+      }
     }
+    cp_async_wait<0>();
     source_rows<K, MODE>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+    if (MODE != M_POWERPUSH) {  // synchronous modes finish their split rows this sweep
+      grid_barrier(&ctl->barrier, (++gen) * gridDim.x);
+      split_decide<K, MODE>(P, sweep & 1, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+    }
     // block-level flush of this sweep's accumulators: reduce over the lanes of
     // the same column first (shuffles), then one shared atomic per warp/column
     {
@@ -804,6 +947,7 @@ struct Workspace {
   DevBuf<uint64_t> fa, fb;
   DevBuf<double> carry_h, carry_t;
   DevBuf<unsigned> split_cnt;
+  DevBuf<double> split_acc;
   DevBuf<SweepCtl> ctl;
   DevBuf<unsigned long long> counters;  // next_cnt + col_cnt[K] + col_np[K] + col_nn[K]
   DevBuf<double> dcols;                 // col_dr[K], colsum[K], D[K]
@@ -850,6 +994,7 @@ static Workspace& workspace(Graph& g, int K, uint64_t ntiles) {
     w.carry_t.alloc((ntiles + 1) * K);
     w.split_cnt.alloc(ntiles + 1);
     PPRG_CUDA(cudaMemsetAsync(w.split_cnt.get(), 0, 4 * (ntiles + 1), g.stream));
+    w.split_acc.alloc(2 * (ntiles + 1) * K);
     w.ntiles_alloc = ntiles;
   }
   return w;
@@ -871,6 +1016,8 @@ inline unsigned grid_for(uint64_t items, int tb = 256) {
 
 template <int K, int MODE>
 void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
+  if (P.split_acc)
+    PPRG_CUDA(cudaMemsetAsync(P.split_acc, 0, sizeof(double) * 2 * (P.ntiles + 1) * K, g.stream));
   const size_t smem = Tile<K>::bytes;
   auto kern = k_sweeps<K, MODE>;
   static bool attr_set = false;
@@ -945,6 +1092,9 @@ struct Block {
   uint32_t k;
   uint64_t ntiles = 0;
   const uint32_t* tile_lo = nullptr;
+  const uint2* desc = nullptr;
+  const uint32_t* split_list = nullptr;
+  uint64_t n_split = 0;
   double alpha;
   std::vector<uint32_t> src;
   std::vector<double> r_sum;
@@ -962,11 +1112,17 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   const int K = round_k(k);
   uint64_t ntiles = 0;
   const uint32_t* tl = nullptr;
-  if (need_pull) tl = g.tiles(SWEEP_ELEMS / K, &ntiles);
+  const uint2* dsc = nullptr;
+  if (need_pull) {
+    tl = g.tiles(SWEEP_ELEMS / K, &ntiles);
+    dsc = g.tile_desc(SWEEP_ELEMS / K, &ntiles);
+  }
   Workspace& w = workspace(g, K, ntiles);
   Block b(g, w, K, k, alpha);
   b.ntiles = ntiles;
   b.tile_lo = tl;
+  b.desc = dsc;
+  if (need_pull) b.split_list = g.split_rows(SWEEP_ELEMS / K, &b.n_split);
   for (uint32_t c = 0; c < k; ++c) b.src[c] = sources[c];
   for (int c = k; c < K; ++c) b.src[c] = sources[0];  // padding columns are inert
   PPRG_CUDA(cudaMemcpyAsync(w.d_src.get(), b.src.data(), 4 * KMAX, cudaMemcpyHostToDevice, g.stream));
@@ -988,14 +1144,20 @@ SweepParams base_params(Block& b) {
   for (int c = 0; c < b.K; ++c) P.src[c] = b.src[c];
   P.in_off = g.cin_off.get();
   P.crow = g.cin_row.get();
+  P.cdeg = g.cin_deg.get();
+  P.cinv = g.cin_inv.get();
   P.in_off_full = g.in_off.get();
   P.in_nbr = g.in_nbr.get();
   P.tile_lo = b.tile_lo;
+  P.desc = b.desc;
   P.ntiles = b.ntiles;
   P.T = SWEEP_ELEMS / b.K;
   P.carry_head = b.w.carry_h.get();
   P.carry_tail = b.w.carry_t.get();
   P.split_cnt = b.w.split_cnt.get();
+  P.split_acc = b.w.split_acc.get();
+  P.split_list = b.split_list;
+  P.n_split = b.n_split;
   return P;
 }
 
@@ -1284,7 +1446,7 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
     Q.init[c].D = b.D[c];
   }
   PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
-  dispatch_sweeps<M_FINAL>(g, b.K, Q, false);
+  dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
   call->kernel_launches += 1;
   SweepCtl fc;
   PPRG_CUDA(cudaMemcpyAsync(&fc, w.ctl.get(), sizeof fc, cudaMemcpyDeviceToHost, st));
