@@ -56,6 +56,8 @@ typedef struct {
 typedef struct {
   double device_ms;        /* CUDA-event time of the device section */
   double sweep_ms;         /* CUDA-event time of the global-sweep kernels */
+  double local_ms;         /* CUDA-event time of the local (queue) phase */
+  double final_ms;         /* CUDA-event time of the final residue pass */
   uint64_t alg_bytes;      /* SURVEY 8(d) algorithmic bytes of the global sweeps */
   uint64_t sweep_launches; /* persistent sweep-kernel launches */
   uint32_t max_sweeps;

@@ -43,7 +43,8 @@ class QStats(C.Structure):
 
 
 class CStats(C.Structure):
-    _fields_ = [("device_ms", C.c_double), ("sweep_ms", C.c_double), ("alg_bytes", C.c_uint64),
+    _fields_ = [("device_ms", C.c_double), ("sweep_ms", C.c_double), ("local_ms", C.c_double),
+                ("final_ms", C.c_double), ("alg_bytes", C.c_uint64),
                 ("sweep_launches", C.c_uint64), ("max_sweeps", C.c_uint32),
                 ("kernel_launches", C.c_uint32)]
 
@@ -52,6 +53,8 @@ class CStats(C.Structure):
 class CallStats:
     device_ms: float = 0.0
     sweep_ms: float = 0.0
+    local_ms: float = 0.0
+    final_ms: float = 0.0
     alg_bytes: int = 0
     sweep_launches: int = 0
     max_sweeps: int = 0
@@ -59,8 +62,8 @@ class CallStats:
 
     @classmethod
     def of(cls, c: CStats) -> "CallStats":
-        return cls(c.device_ms, c.sweep_ms, c.alg_bytes, c.sweep_launches, c.max_sweeps,
-                   c.kernel_launches)
+        return cls(c.device_ms, c.sweep_ms, c.local_ms, c.final_ms, c.alg_bytes,
+                   c.sweep_launches, c.max_sweeps, c.kernel_launches)
 
 
 _lib = None

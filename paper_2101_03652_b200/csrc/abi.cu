@@ -59,6 +59,8 @@ void fill_stats(const std::vector<pprg::ColumnStats>& cs, const pprg::CallStats&
   if (c) {
     c->device_ms = call.device_ms;
     c->sweep_ms = call.sweep_ms;
+    c->local_ms = call.local_ms;
+    c->final_ms = call.final_ms;
     c->alg_bytes = call.alg_bytes;
     c->sweep_launches = call.sweep_launches;
     c->max_sweeps = call.max_sweeps;

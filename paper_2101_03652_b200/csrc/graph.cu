@@ -11,8 +11,10 @@
 // duplicates removed) and sorted before the reference build semantics apply.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cmath>
 #include <string>
+#include <vector>
 
 #include "internal.h"
 
@@ -460,6 +462,58 @@ const uint32_t* Graph::split_rows(uint32_t T, uint64_t* count) {
   const uint32_t* p = list.get();
   tile_split.emplace(T, std::move(list));
   return p;
+}
+
+// Greedy row-aligned packing in id order (so sweeps stay id-ordered): rows are
+// added to the current tile while it keeps <= T in-edges and <= R rows; a row
+// with more than T in-edges becomes ceil(deg/T) hub pieces of its own.
+const Graph::Plan& Graph::tile_plan(uint32_t T, uint32_t R) {
+  ensure_transpose();
+  const uint64_t key = ((uint64_t)T << 32) | R;
+  auto it = plans.find(key);
+  if (it != plans.end()) return it->second;
+  std::vector<uint64_t> h_off(n_rows + 1);
+  PPRG_CUDA(cudaMemcpyAsync(h_off.data(), cin_off.get(), 8 * (n_rows + 1), cudaMemcpyDeviceToHost, stream));
+  PPRG_CUDA(cudaStreamSynchronize(stream));
+  std::vector<TileDesc> tl;
+  tl.reserve(m / T + n_rows / R + 16);
+  uint32_t nhubs = 0;
+  TileDesc cur{0, 0, 0, 0, 0, 0, 1};
+  auto close = [&] {
+    if (cur.nr) tl.push_back(cur);
+    cur = TileDesc{0, 0, 0, 0, 0, 0, 1};
+  };
+  for (uint64_t r = 0; r < n_rows; ++r) {
+    const uint64_t d = h_off[r + 1] - h_off[r];
+    if (d > T) {
+      close();
+      const uint32_t np = (uint32_t)((d + T - 1) / T);
+      for (uint32_t p = 0; p < np; ++p) {
+        const uint64_t e0 = h_off[r] + (uint64_t)p * T;
+        const uint64_t ne = std::min<uint64_t>(T, h_off[r + 1] - e0);
+        tl.push_back(TileDesc{e0, (uint32_t)ne, (uint32_t)r, 1, nhubs, p, np});
+      }
+      ++nhubs;
+      continue;
+    }
+    if (cur.nr && (cur.ne + d > T || cur.nr >= R)) close();
+    if (!cur.nr) {
+      cur.e0 = h_off[r];
+      cur.r0 = (uint32_t)r;
+    }
+    cur.ne += (uint32_t)d;
+    cur.nr += 1;
+  }
+  close();
+  Plan pl;
+  pl.ntiles = tl.size();
+  pl.nhubs = nhubs;
+  pl.tiles.alloc(tl.size() ? tl.size() : 1);
+  if (!tl.empty())
+    PPRG_CUDA(cudaMemcpyAsync(pl.tiles.get(), tl.data(), sizeof(TileDesc) * tl.size(),
+                              cudaMemcpyHostToDevice, stream));
+  PPRG_CUDA(cudaStreamSynchronize(stream));
+  return plans.emplace(key, std::move(pl)).first->second;
 }
 
 const uint32_t* Graph::tiles(uint32_t T, uint64_t* ntiles) {

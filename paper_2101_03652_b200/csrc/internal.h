@@ -13,6 +13,14 @@
 
 namespace pprg {
 
+// Row-aligned tile of the transpose for the pull sweeps: rows [r0, r0+nr)
+// with their contiguous in-edges [e0, e0+ne); or, for a row with more in-edges
+// than a tile holds ("hub"), piece `piece` of `npieces` of that row.
+struct TileDesc {
+  uint64_t e0;
+  uint32_t ne, r0, nr, hub, piece, npieces;
+};
+
 // Device-resident immutable graph. The out-CSR is the canonical, reference-
 // identical layout (graph.hpp:44-46: u64 offsets, u32 neighbours, dead-end
 // list); the transpose and the tile map are derived internal layouts for the
@@ -46,6 +54,12 @@ struct Graph {
   const uint32_t* tiles(uint32_t edges_per_tile, uint64_t* ntiles);
   const uint2* tile_desc(uint32_t edges_per_tile, uint64_t* ntiles);
   const uint32_t* split_rows(uint32_t edges_per_tile, uint64_t* count);
+  struct Plan {
+    DevBuf<TileDesc> tiles;
+    uint64_t ntiles = 0, nhubs = 0;
+  };
+  std::map<uint64_t, Plan> plans;  // key: (T << 32) | RMAX
+  const Plan& tile_plan(uint32_t max_edges, uint32_t max_rows);
   uint64_t m_eff() const { return m + n_dead; }
 };
 
@@ -81,6 +95,8 @@ struct ColumnStats {
 struct CallStats {
   double device_ms = 0;       // events around the whole device section
   double sweep_ms = 0;        // events around the persistent global-sweep kernel(s)
+  double local_ms = 0;        // local (queue) phase incl. its exact r_sum
+  double final_ms = 0;        // final explicit-residue pass
   uint64_t alg_bytes = 0;     // SURVEY 8(d) algorithmic bytes of the global sweeps
   uint64_t sweep_launches = 0;
   uint32_t max_sweeps = 0;

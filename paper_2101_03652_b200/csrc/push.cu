@@ -80,7 +80,9 @@ struct SweepParams {
   const uint32_t* deg;
   const double* inv_deg;
   const uint32_t* tile_lo;
-  const uint2* desc;           // per tile: (first compact row, rows)
+  const TileDesc* desc;        // row-aligned tile plan
+  double* hub_acc;             // [nhubs][K] partial sums of hub rows
+  unsigned* hub_cnt;           // [nhubs] arrived pieces
   uint64_t ntiles;
   uint32_t T;
   int k_live;  // real columns (<= K)
@@ -94,9 +96,7 @@ struct SweepParams {
   double* carry_head;
   double* carry_tail;
   unsigned* split_cnt;
-  const uint32_t* split_list;  // compact rows spanning tiles
-  uint64_t n_split;
-  double* split_acc;           // [2][ntiles+1][K] per-sweep partial sums of split rows
+
   SweepCtl* ctl;
   double* out_reserve;         // finalize outputs, query-major [c*n + u]
   double* out_residue;
@@ -116,24 +116,17 @@ struct ColSh {
   unsigned long long pushes;
 };
 
-// Tile geometry. A tile is T = SWEEP_ELEMS/K consecutive in-edges; thread t
-// owns column c = t % K and the SEG = 8 consecutive edges [8 (t/K), 8 (t/K) + 8)
-// of the tile, so every thread does identical gather work. The gathered values
-// of two tiles (current, next) live in shared memory in an owner-private
-// layout vals[i*NT + t]; rows (the transpose's rows with in-degree > 0, so
-// none is empty) are staged in chunks of RMAX, double-buffered.
+// Tile geometry: a row-aligned tile holds at most T = SWEEP_ELEMS/K in-edges
+// and at most RMAX rows (host-built plan, Graph::tile_plan). Its gathered
+// values vals[e*K + c] and its row data live in shared memory.
 template <int K>
 struct Tile {
   static constexpr int T = SWEEP_ELEMS / K;
-  static constexpr int SEG = SWEEP_ELEMS / NT;  // 8
-  static constexpr int RMAX_ = (2 * NT) / K > 16 ? (2 * NT) / K : 16;
-  static constexpr int RMAX = RMAX_ < NT - 1 ? RMAX_ : NT - 1;  // nr + 1 offsets fit one per thread
-  static constexpr int RX = RMAX * K;
-  // per staging buffer: sinv[RMAX] | sx[RX] | sr[RX] | sacc[RX] (f64) | soff[RMAX+1] (i32) | snode, sdeg [RMAX] (u32)
-  static constexpr size_t buf_bytes = 8ull * (RMAX + 3 * RX) + 4ull * (RMAX + 1) + 8ull * RMAX;
-  static constexpr size_t buf_stride = (buf_bytes + 15) / 16 * 16;
-  static constexpr size_t vals_bytes = 8ull * SWEEP_ELEMS;
-  static constexpr size_t bytes = 2 * vals_bytes + 2 * buf_stride;
+  static constexpr int RMAX = T < 256 ? T : 256;
+  static constexpr int LONG = K == 1 ? 32 : 16;  // rows longer than this: warp per row
+  // vals[SWEEP_ELEMS] f64 | sinv[RMAX] f64 | hub[NT/32 * K] f64 | soff[RMAX+1] i32 | snode, sdeg, slong [RMAX] u32
+  static constexpr size_t bytes = 8ull * (SWEEP_ELEMS + RMAX + (NT / 32) * K) +
+                                  4ull * (RMAX + 1) + 12ull * RMAX + 16;
 };
 
 struct Acc {  // per-thread sweep counters for the thread's column
@@ -148,18 +141,6 @@ struct BlockAcc {  // shared, per column
   unsigned long long* nn;
   unsigned long long* et;
 };
-
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 8 : 0;  // src-size 0 zero-fills
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(gmem), "r"(sz)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
 
 // The per-(row, column) decision: push form of push.cpp:182-193 in pull
 // representation, the PowItr update of push.cpp:90-99, or the final explicit
@@ -221,280 +202,182 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
   }
 }
 
-// A row straddling tiles adds this tile's per-column partial into the sweep's
-// accumulator (fire-and-forget RED, keyed by the row's first tile); the row is
-// decided after the grid barrier by split_decide.
-template <int K>
-__device__ __noinline__ void post_split(const SweepParams& P, uint32_t cr, uint32_t r,
-                                        const double* sacc, uint32_t parity) {
-  constexpr int T = Tile<K>::T;
-  const uint64_t ft = __ldg(P.in_off + cr) / T;
-  double* acc = P.split_acc + ((uint64_t)parity * (P.ntiles + 1) + ft) * K;
-  for (int cc = 0; cc < K; ++cc) atomicAdd(acc + cc, sacc[r * K + cc]);
-}
-
-// Decide every split row from the accumulated partials of sweep `parity`
-// (grid-stride; thread column = tid % K as everywhere), and clear them.
 template <int K, int MODE>
-__device__ __forceinline__ void split_decide(const SweepParams& P, uint32_t parity, const ColSh* cs,
-                                             const double* thr_cur, const double* yg,
-                                             const double* rcur, double* rnxt, double* ynxt,
-                                             Acc& a) {
-  constexpr int T = Tile<K>::T;
-  const uint64_t total = P.n_split * K;
-  for (uint64_t idx = blockIdx.x * (uint64_t)NT + threadIdx.x; idx < total;
-       idx += (uint64_t)gridDim.x * NT) {
-    const uint32_t cr = P.split_list[idx / K];
-    const int c = (int)(idx % K);
-    const uint64_t ft = __ldg(P.in_off + cr) / T;
-    double* slot = P.split_acc + ((uint64_t)parity * (P.ntiles + 1) + ft) * K + c;
-    const double acc = __ldcg(slot);
-    *slot = 0.0;
-    const uint32_t u = __ldg(P.crow + cr);
-    const uint64_t ix = (uint64_t)u * K + c;
-    decide<K, MODE>(P, cs, thr_cur, u, c, acc, __ldcg(P.x + ix),
-                    (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0,
-                    __ldg(P.cdeg + cr), __ldg(P.cinv + cr), yg, rnxt, ynxt, a);
-  }
+__device__ __forceinline__ void decide_at(const SweepParams& P, const ColSh* cs,
+                                          const double* thr_cur, uint32_t u, int c, double acc,
+                                          uint32_t dg, double inv, const double* yg,
+                                          const double* rcur, double* rnxt, double* ynxt, Acc& a) {
+  const uint64_t ix = (uint64_t)u * K + c;
+  decide<K, MODE>(P, cs, thr_cur, u, c, acc, __ldcg(P.x + ix),
+                  (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0, dg, inv, yg,
+                  rnxt, ynxt, a);
 }
 
-// The in-neighbour ids of my 8 edges of tile j (one 32-byte vector load).
-template <int K>
-__device__ __forceinline__ void load_ids(const SweepParams& P, uint64_t j, uint32_t (&id)[8]) {
-  constexpr int T = Tile<K>::T, SEG = Tile<K>::SEG;
-  const int32_t seg0 = (threadIdx.x / K) * SEG;
-  const uint64_t base = j * (uint64_t)T;
-  const int32_t ne = base < P.m ? (int32_t)(P.m - base < (uint64_t)T ? P.m - base : (uint64_t)T) : 0;
-  if (seg0 + SEG <= ne) {
-    const uint4* p4 = reinterpret_cast<const uint4*>(P.in_nbr + base + seg0);
-    const uint4 q0 = __ldg(p4), q1 = __ldg(p4 + 1);
-    id[0] = q0.x; id[1] = q0.y; id[2] = q0.z; id[3] = q0.w;
-    id[4] = q1.x; id[5] = q1.y; id[6] = q1.z; id[7] = q1.w;
-  } else {
-#pragma unroll
-    for (int i = 0; i < SEG; ++i) id[i] = seg0 + i < ne ? __ldg(P.in_nbr + base + seg0 + i) : ~0u;
-  }
-}
-
-// Issue my 8 gathers of y for tile j as cp.async into my private slots.
-template <int K>
-__device__ __forceinline__ void issue_gathers(const double* yg, const uint32_t (&id)[8],
-                                              double* vals) {
-  const int c = threadIdx.x % K;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool ok = id[i] != ~0u;
-    cp_async8(vals + i * NT + threadIdx.x, yg + (ok ? (uint64_t)id[i] * K + c : 0), ok);
-  }
-}
-
-// Row data of one tile's first chunk, prefetched into registers one tile ahead
-// (thread t holds row t; thread nr holds only the end offset).
-struct RowPre {
-  uint64_t off = 0;
-  uint32_t node = 0, deg = 0;
-  double inv = 0.0;
-};
-
-template <int K>
-__device__ __forceinline__ void load_rows(const SweepParams& P, uint2 d, RowPre& rp) {
-  constexpr int RMAX = Tile<K>::RMAX;
-  const uint32_t nr = d.y < (uint32_t)RMAX ? d.y : RMAX;
-  const uint32_t t = threadIdx.x;
-  if (t <= nr) rp.off = __ldg(P.in_off + d.x + t);
-  if (t < nr) {
-    rp.node = __ldg(P.crow + d.x + t);
-    rp.deg = __ldg(P.cdeg + d.x + t);
-    rp.inv = __ldg(P.cinv + d.x + t);
-  }
-}
-
-// Stage rows [cr0, cr0 + nr) of tile `base` into a staging buffer.
-template <int K>
-__device__ __forceinline__ void stage_rows_from(const RowPre& rp, uint32_t nr, uint64_t base,
-                                                char* buf) {
-  using TC = Tile<K>;
-  constexpr int T = TC::T, RMAX = TC::RMAX, RX = TC::RX;
-  double* sinv = reinterpret_cast<double*>(buf);
-  double* sacc = sinv + RMAX + 2 * RX;
-  int32_t* soff = reinterpret_cast<int32_t*>(sacc + RX);
-  uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
-  uint32_t* sdeg = snode + RMAX;
-  const uint32_t t = threadIdx.x;
-  if (t <= nr) {
-    const int64_t d = (int64_t)rp.off - (int64_t)base;
-    soff[t] = d < 0 ? -1 : (d > T ? T + 1 : (int32_t)d);
-  }
-  if (t < nr) {
-    snode[t] = rp.node;
-    sdeg[t] = rp.deg;
-    sinv[t] = rp.inv;
-#pragma unroll
-    for (int cc = 0; cc < K; ++cc) sacc[t * K + cc] = 0.0;
-  }
-}
-
-template <int K>
-__device__ __forceinline__ void stage_rows_sync(const SweepParams& P, uint32_t cr0, uint32_t nr,
-                                                uint64_t base, char* buf) {
-  for (uint32_t t0 = 0; t0 <= nr; t0 += NT) {
-    RowPre rp;
-    const uint32_t t = t0 + threadIdx.x;
-    if (t <= nr) rp.off = __ldg(P.in_off + cr0 + t);
-    if (t < nr) {
-      rp.node = __ldg(P.crow + cr0 + t);
-      rp.deg = __ldg(P.cdeg + cr0 + t);
-      rp.inv = __ldg(P.cinv + cr0 + t);
-    }
-    // stage_rows_from uses threadIdx.x as the row; emulate the offset t0
-    using TC = Tile<K>;
-    constexpr int T = TC::T, RMAX = TC::RMAX, RX = TC::RX;
-    double* sinv = reinterpret_cast<double*>(buf);
-    double* sacc = sinv + RMAX + 2 * RX;
-    int32_t* soff = reinterpret_cast<int32_t*>(sacc + RX);
-    uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
-    uint32_t* sdeg = snode + RMAX;
-    if (t <= nr) {
-      const int64_t d = (int64_t)rp.off - (int64_t)base;
-      soff[t] = d < 0 ? -1 : (d > T ? T + 1 : (int32_t)d);
-    }
-    if (t < nr) {
-      snode[t] = rp.node;
-      sdeg[t] = rp.deg;
-      sinv[t] = rp.inv;
-      for (int cc = 0; cc < K; ++cc) sacc[t * K + cc] = 0.0;
-    }
-  }
-}
-
-// Reduce + decide one staged chunk (rows [cr0, cr0+nr)) of tile j whose
-// gathered values are in `vals`. Called after the staging barrier.
+// One piece of a hub row (more in-edges than a tile holds): the block sums its
+// edges per column, adds the piece total into the row's accumulator, and the
+// last piece to arrive decides the row (release-ordered counter; the partials
+// are read back from L2). Only hub pieces pay this protocol.
 template <int K, int MODE>
-__device__ __forceinline__ void chunk_compute(const SweepParams& P, uint64_t j, const double* vals,
-                                              char* smem_buf, uint32_t cr0, uint32_t nr,
-                                              bool first_chunk, bool last_chunk, uint32_t parity,
-                                              const ColSh* cs,
-                                              const double* thr_cur, const double* yg,
-                                              const double* rcur, double* rnxt, double* ynxt,
-                                              Acc& a, const BlockAcc& ba) {
-  using TC = Tile<K>;
-  constexpr int T = TC::T, SEG = TC::SEG, RMAX = TC::RMAX, RX = TC::RX;
-  double* sinv = reinterpret_cast<double*>(smem_buf);
-  double* sr = sinv + RMAX + RX;
-  double* sacc = sr + RX;
-  int32_t* soff = reinterpret_cast<int32_t*>(sacc + RX);
-  uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
-  uint32_t* sdeg = snode + RMAX;
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
+__device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, double* hubsh,
+                                       int* flag, const ColSh* cs, const double* thr_cur,
+                                       const double* yg, const double* rcur, double* rnxt,
+                                       double* ynxt, Acc& a) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = tid % K;
-  const int32_t seg0 = (tid / K) * SEG;
-  const uint64_t base = j * (uint64_t)T;
-  const int32_t ne = base < P.m ? (int32_t)(P.m - base < (uint64_t)T ? P.m - base : (uint64_t)T) : 0;
-
-  // prefetch the state of my first decision (lands during the reduction)
-  double xo0 = 0.0, rc0 = 0.0;
-  if ((uint32_t)tid < nr * K) {
-    const uint64_t ix = (uint64_t)snode[tid / K] * K + c;
-    xo0 = __ldcg(P.x + ix);
-    if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) rc0 = __ldcg(rcur + ix);
+  const uint64_t total = (uint64_t)d.ne * K;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  uint64_t f = tid;
+  for (; f + 3 * NT < total; f += 4 * NT) {
+    const uint32_t i0 = __ldg(P.in_nbr + d.e0 + f / K);
+    const uint32_t i1 = __ldg(P.in_nbr + d.e0 + (f + NT) / K);
+    const uint32_t i2 = __ldg(P.in_nbr + d.e0 + (f + 2 * NT) / K);
+    const uint32_t i3 = __ldg(P.in_nbr + d.e0 + (f + 3 * NT) / K);
+    s0 += yg[(uint64_t)i0 * K + c];
+    s1 += yg[(uint64_t)i1 * K + c];
+    s2 += yg[(uint64_t)i2 * K + c];
+    s3 += yg[(uint64_t)i3 * K + c];
   }
-  if (first_chunk) cp_async_wait<1>();  // my gathers of this tile have landed
-
-  // ---- segmented reduction over my 8 edges ---------------------------------
-  {
-    constexpr uint32_t SENT = 0xFFFFFFFFu;
-    double hp = 0.0, tp = 0.0;
-    uint32_t f = SENT, l = SENT;
-    bool started = false, cont = false, have = false;
-    if (nr > 0) {
-      const int32_t cbeg = soff[0] < 0 ? 0 : soff[0];
-      int32_t e_hi = seg0 + SEG;
-      if (e_hi > ne) e_hi = ne;
-      if (e_hi > soff[nr]) e_hi = soff[nr];
-      const int32_t e_lo = seg0 > cbeg ? seg0 : cbeg;
-      if (e_lo < e_hi) {
-        have = true;
-        uint32_t lo_r = 0, hi_r = nr;  // last row r with soff[r] <= e_lo
-        while (lo_r + 1 < hi_r) {
-          const uint32_t mid = (lo_r + hi_r) >> 1;
-          if (soff[mid] <= e_lo) lo_r = mid; else hi_r = mid;
-        }
-        uint32_t r = lo_r;
-        f = r;
-        started = soff[r] < e_lo;
-        int32_t rend = soff[r + 1];
-        double part = 0.0;
+  for (; f < total; f += NT) s0 += yg[(uint64_t)__ldg(P.in_nbr + d.e0 + f / K) * K + c];
+  double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
-        for (int i = 0; i < SEG; ++i) {
-          const int32_t e = seg0 + i;
-          if (e >= e_lo && e < e_hi) {
-            if (e >= rend) {  // row r ended at e - 1 (rows are never empty)
-              if (r == f) hp = part;
-              else sacc[r * K + c] = part;  // started and ended inside the segment
-              part = 0.0;
-              ++r;
-              rend = soff[r + 1];
-            }
-            part += vals[i * NT + tid];
-          }
-        }
-        l = r;
-        cont = rend > e_hi;
-        if (l == f) hp = part; else tp = part;
-        if (l != f && !cont) sacc[l * K + c] = tp;
-        if (!started && (l != f || !cont)) sacc[f * K + c] = hp;
-      }
-    }
-    const double carry = cont ? (l == f ? hp : tp) : 0.0;
-    const uint32_t key = have ? l : SENT;
-    double S = carry;
-    double carry_in = 0.0;
-    uint32_t f_next = SENT;  // first row of the next segment of my column
-    if constexpr (K < 32) {
-#pragma unroll
-      for (int d = K; d < 32; d <<= 1) {
-        const double Sd = __shfl_up_sync(0xffffffffu, S, d);
-        const uint32_t kd = __shfl_up_sync(0xffffffffu, key, d);
-        if (lane >= d && kd == key) S += Sd;
-      }
-      const double Sp = __shfl_up_sync(0xffffffffu, S, K);
-      const uint32_t kp = __shfl_up_sync(0xffffffffu, key, K);
-      if (lane >= K && kp == f) carry_in = Sp;
-      f_next = __shfl_down_sync(0xffffffffu, f, K);
-    }
-    const int first_lane = K < 32 ? lane % K : lane;
-    const uint32_t f_first = __shfl_sync(0xffffffffu, f, first_lane);
-    const bool st_first = __shfl_sync(0xffffffffu, started, first_lane);
-    if (have && started && !(l == f && cont)) {  // I finish row f
-      const double val = hp + carry_in;
-      if (f == f_first && st_first) atomicAdd(&sacc[f * K + c], val);  // began in an earlier warp
-      else sacc[f * K + c] = val;
-    }
-    if (have && cont && (lane + K >= 32 || f_next != key))
-      atomicAdd(&sacc[l * K + c], S);  // row l continues past this warp / chunk
+  for (int o = 16; o >= K && o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int i = tid; i < (NT / 32) * K; i += NT) hubsh[i] = 0.0;
+  __syncthreads();
+  if (lane < K) hubsh[warp * K + c] = s;  // the lanes holding this warp's per-column sums
+  __syncthreads();
+  if (tid < K) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += hubsh[w * K + tid];
+    atomicAdd(P.hub_acc + (uint64_t)d.hub * K + tid, t);
   }
   __syncthreads();
+  if (tid == 0) {
+    unsigned old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
+    *flag = old == d.npieces - 1;
+    if (*flag) P.hub_cnt[d.hub] = 0;
+  }
+  __syncthreads();
+  if (*flag && tid < K) {
+    double* slot = P.hub_acc + (uint64_t)d.hub * K + tid;
+    const double acc = __ldcg(slot);
+    *slot = 0.0;
+    const uint32_t u = __ldg(P.crow + d.r0);
+    decide_at<K, MODE>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
+                       rcur, rnxt, ynxt, a);
+  }
+}
 
-  // ---- rows straddling the tile: post partials --------------------------
-  const uint32_t rl = nr ? nr - 1 : 0;
-  const bool first_split = first_chunk && nr > 0 && (soff[0] < 0 || soff[1] > T);
-  const bool last_split = last_chunk && nr > 0 && !(first_chunk && rl == 0) && soff[rl + 1] > T;
-  if (tid == 0 && first_split) post_split<K>(P, cr0, 0, sacc, parity);
-  if (tid == 32 && last_split) post_split<K>(P, cr0 + rl, rl, sacc, parity);
-  // ---- decisions --------------------------------------------------------
+// One row-aligned tile: gather y of every in-edge into shared memory (all
+// loads of the tile issued together), then one thread per (row, column) sums
+// its row and decides; rows longer than LONG are summed by a whole warp.
+template <int K, int MODE>
+__device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& d, char* smem,
+                                          const ColSh* cs, const double* thr_cur, const double* yg,
+                                          const double* rcur, double* rnxt, double* ynxt, Acc& a,
+                                          const BlockAcc& ba, uint32_t* nlong,
+                                          const unsigned long long* dn_slot, TileDesc* dn) {
+  using TC = Tile<K>;
+  constexpr int RMAX = TC::RMAX;
+  double* vals = reinterpret_cast<double*>(smem);
+  double* sinv = vals + SWEEP_ELEMS;
+  int32_t* soff = reinterpret_cast<int32_t*>(sinv + RMAX + (NT / 32) * K);
+  uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
+  uint32_t* sdeg = snode + RMAX;
+  uint32_t* slong = sdeg + RMAX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = tid % K;
+  const uint32_t nr = d.nr;
+  // ---- stage rows and gather (one memory latency) -------------------------
+  for (uint32_t t = tid; t <= nr; t += NT) soff[t] = (int32_t)(__ldg(P.in_off + d.r0 + t) - d.e0);
+  for (uint32_t t = tid; t < nr; t += NT) {
+    snode[t] = __ldg(P.crow + d.r0 + t);
+    sdeg[t] = __ldg(P.cdeg + d.r0 + t);
+    sinv[t] = __ldg(P.cinv + d.r0 + t);
+    const uint64_t len = __ldg(P.in_off + d.r0 + t + 1) - __ldg(P.in_off + d.r0 + t);
+    if (len > (uint64_t)TC::LONG) slong[atomicAdd(nlong, 1u)] = t;
+  }
+  {
+    const uint32_t total = d.ne * K;
+    constexpr int U = 8;
+    for (uint32_t f0 = 0; f0 < total; f0 += U * NT) {
+      uint32_t id[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t f = f0 + tid + i * NT;
+        id[i] = f < total ? __ldg(P.in_nbr + d.e0 + f / K) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t f = f0 + tid + i * NT;
+        if (f < total) vals[f] = yg[(uint64_t)id[i] * K + (f % K)];
+      }
+    }
+  }
+  __syncthreads();
+  if (dn_slot) *dn = P.desc[*dn_slot < P.ntiles ? *dn_slot : 0];  // next tile's descriptor
+  // ---- short rows: one thread per (row, column) ------------------------------
   for (uint32_t fi = tid; fi < nr * K; fi += NT) {
     const uint32_t r = fi / K;
-    if (soff[r] < 0 || soff[r + 1] > T) continue;  // straddles the tile: split_row
-    double xo = xo0, rc = rc0;
-    if (fi != (uint32_t)tid) {
-      const uint64_t ix = (uint64_t)snode[r] * K + c;
-      xo = __ldcg(P.x + ix);
-      if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) rc = __ldcg(rcur + ix);
+    const int32_t b = soff[r], e = soff[r + 1];
+    if (e - b > TC::LONG) continue;
+    const uint32_t u = snode[r];
+    const uint64_t ix = (uint64_t)u * K + c;
+    const double xo = __ldcg(P.x + ix);  // issued before the sum: lands meanwhile
+    const double rc = (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0;
+    double s0 = 0.0, s1 = 0.0;
+    int32_t q = b;
+    for (; q + 1 < e; q += 2) {
+      s0 += vals[q * K + c];
+      s1 += vals[(q + 1) * K + c];
     }
-    decide<K, MODE>(P, cs, thr_cur, snode[r], c, sacc[fi], xo, rc, sdeg[r], sinv[r], yg, rnxt,
-                    ynxt, a);
+    if (q < e) s0 += vals[q * K + c];
+    decide<K, MODE>(P, cs, thr_cur, u, c, s0 + s1, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a);
   }
+  // ---- long rows: one warp per row -----------------------------------------
+  {
+    constexpr int KC = K < 32 ? K : 32;
+    constexpr int CPL = K / KC;
+    constexpr int ES = 32 / KC;  // edge slots per warp
+    const int es = lane / KC, kc = lane % KC;
+    const uint32_t nl = *nlong;
+    for (uint32_t li = warp; li < nl; li += NT / 32) {
+      const uint32_t r = slong[li];
+      const int32_t b = soff[r], e = soff[r + 1];
+      double s[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) s[q] = 0.0;
+      for (int32_t p = b + es; p < e; p += ES)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) s[q] += vals[p * K + kc + q * KC];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+      if (es == 0) {
+        if constexpr (CPL == 1) {
+          decide_at<K, MODE>(P, cs, thr_cur, snode[r], kc, s[0], sdeg[r], sinv[r], yg, rcur, rnxt,
+                             ynxt, a);
+        } else {  // K = 64: lane kc decides columns kc and kc+32; counters via shared atomics
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            Acc b2;
+            const int cc = kc + q * KC;
+            decide_at<K, MODE>(P, cs, thr_cur, snode[r], cc, s[q], sdeg[r], sinv[r], yg, rcur,
+                               rnxt, ynxt, b2);
+            if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
+            if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
+            if (b2.np) atomicAdd(&ba.np[cc], b2.np);
+            if (b2.nn) atomicAdd(&ba.nn[cc], b2.nn);
+            if (b2.et) atomicAdd(&ba.et[cc], b2.et);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *nlong = 0;
 }
 
 // Sources with in-degree 0 are not rows of the compacted transpose; their
@@ -516,7 +399,7 @@ __device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* c
 
 template <int K, int MODE>
 #ifndef PPRG_MINB
-#define PPRG_MINB 6
+#define PPRG_MINB 10
 #endif
 __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant__ SweepParams P) {
   using TC = Tile<K>;
@@ -527,6 +410,9 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
   __shared__ unsigned long long sh_np[K], sh_nn[K], sh_et[K];
   __shared__ unsigned long long sh_tile[3];
   __shared__ int sh_any;
+  __shared__ double sh_hub[(NT / 32) * K];
+  __shared__ int sh_flag;
+  __shared__ uint32_t sh_nlong;
   const int tid = threadIdx.x;
   SweepCtl* ctl = P.ctl;
   if (tid < K) {
@@ -547,10 +433,8 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
       int any = 0;
       for (int cc = 0; cc < K; ++cc) any |= !cs[cc].done;
       sh_any = any && (MODE == M_FINAL ? sweep == 0 : sweep < P.max_sweeps);
-      if (sh_any) {
-        sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
-        sh_tile[1] = atomicAdd(&ctl->ticket[buf], 1u);
-      }
+      if (sh_any) sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
+      sh_nlong = 0;
     }
     if (tid < K) {
       thr_cur[tid] = (MODE == M_POWERPUSH && !cs[tid].done) ? P.thr[cs[tid].epoch] : 0.0;
@@ -578,73 +462,26 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
     double* rnxt = P.r[(sweep + 1) & 1];
     double* ynxt = P.y[(sweep + 1) & 1];
     Acc a;
-    if (MODE == M_POWERPUSH && sweep > 0)  // rows straddling tiles, from the last sweep
-      split_decide<K, MODE>(P, (sweep - 1) & 1, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
-    // Software pipeline. Tickets are fetched two tiles ahead into a 3-slot
-    // ring; the ids of tile it+2 are loaded during tile it; the gathers of
-    // tile it+1 are issued (cp.async, owner-private slots) before tile it is
-    // reduced. Row staging is double-buffered, so consecutive tiles need no
-    // block barrier between them.
-    uint32_t ids[8];
-    RowPre rp;  // rows (first chunk) of the tile about to be processed
-    uint2 dcur = make_uint2(0, 0), dnext = make_uint2(0, 0);
-    double* vals0 = reinterpret_cast<double*>(smem_dyn);
-    double* vals1 = vals0 + SWEEP_ELEMS;
-    char* stage0 = smem_dyn + 2 * TC::vals_bytes;
-    {
-      const unsigned long long j0 = sh_tile[0], j1 = sh_tile[1];
-      if (j0 < P.ntiles) {
-        dcur = P.desc[j0];
-        load_rows<K>(P, dcur, rp);
-        load_ids<K>(P, j0, ids);
-        issue_gathers<K>(yg, ids, vals0);
-      }
-      cp_async_commit();
-      if (j1 < P.ntiles) {
-        dnext = P.desc[j1];
-        load_ids<K>(P, j1, ids);
-      }
-    }
+    // Tiles in ticket (= id) order; the next ticket is fetched one tile ahead
+    // and the next descriptor is loaded inside the current tile.
+    unsigned long long j = sh_tile[0];
+    TileDesc d = P.desc[j < P.ntiles ? j : 0];
     for (uint32_t it = 0;; ++it) {
-      const unsigned long long j = sh_tile[it % 3];
       if (j >= P.ntiles) break;
-      const unsigned long long jn = sh_tile[(it + 1) % 3];
-      if (jn < P.ntiles) issue_gathers<K>(yg, ids, (it & 1) ? vals0 : vals1);
-      cp_async_commit();
-      if (tid == 0) sh_tile[(it + 2) % 3] = atomicAdd(&ctl->ticket[buf], 1u);
-      char* sbuf = stage0 + (it & 1) * TC::buf_stride;
-      const uint64_t base = j * (uint64_t)TC::T;
-      const uint2 dthis = dcur;
-      const uint32_t nr0 = dthis.y < (uint32_t)TC::RMAX ? dthis.y : TC::RMAX;
-      stage_rows_from<K>(rp, nr0, base, sbuf);
-      __syncthreads();
-      // prefetch: rows of tile it+1, descriptor and ids of tile it+2
-      const unsigned long long j2 = sh_tile[(it + 2) % 3];
-      if (jn < P.ntiles) load_rows<K>(P, dnext, rp);
-      dcur = dnext;
-      if (j2 < P.ntiles) {
-        dnext = P.desc[j2];
-        load_ids<K>(P, j2, ids);
-      }
-      const double* vals = (it & 1) ? vals1 : vals0;
-      chunk_compute<K, MODE>(P, j, vals, sbuf, dthis.x, nr0, true, dthis.y <= (uint32_t)TC::RMAX,
-                             sweep & 1, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba);
-      for (uint32_t row0 = TC::RMAX; row0 < dthis.y; row0 += TC::RMAX) {  // rare: many rows
+      if (tid == 0) sh_tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
+      TileDesc dn = d;
+      if (d.npieces > 1) {
+        hub_piece<K, MODE>(P, d, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+        dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
         __syncthreads();
-        const uint32_t nr = dthis.y - row0 < (uint32_t)TC::RMAX ? dthis.y - row0 : TC::RMAX;
-        stage_rows_sync<K>(P, dthis.x + row0, nr, base, sbuf);
-        __syncthreads();
-        chunk_compute<K, MODE>(P, j, vals, sbuf, dthis.x + row0, nr, false,
-                               row0 + nr >= dthis.y, sweep & 1, cs, thr_cur, yg, rcur, rnxt, ynxt,
-                               a, ba);
+      } else {
+        tile_rows<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba, &sh_nlong,
+                           &sh_tile[(it + 1) & 1], &dn);
       }
+      j = sh_tile[(it + 1) & 1];
+      d = dn;
     }
-    cp_async_wait<0>();
     source_rows<K, MODE>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
-    if (MODE != M_POWERPUSH) {  // synchronous modes finish their split rows this sweep
-      grid_barrier(&ctl->barrier, (++gen) * gridDim.x);
-      split_decide<K, MODE>(P, sweep & 1, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
-    }
     // block-level flush of this sweep's accumulators: reduce over the lanes of
     // the same column first (shuffles), then one shared atomic per warp/column
     {
@@ -938,6 +775,11 @@ __global__ void k_unpack(const double* a, uint64_t n, int K, int k_live, double 
   }
 }
 
+inline uint32_t tile_rmax(int K) {
+  const int T = SWEEP_ELEMS / K;
+  return T < 256 ? T : 256;
+}
+
 // ---- per-graph workspace --------------------------------------------------
 struct Workspace {
   int K = 0;
@@ -947,7 +789,24 @@ struct Workspace {
   DevBuf<uint64_t> fa, fb;
   DevBuf<double> carry_h, carry_t;
   DevBuf<unsigned> split_cnt;
-  DevBuf<double> split_acc;
+  DevBuf<double> hub_acc;
+  DevBuf<unsigned> hub_cnt;
+  // host-output staging: finalize writes slot s while the copy stream drains
+  // slot s^1 to the caller's host buffers (overlaps D2H with the next block)
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  DevBuf<double> stage_res[2], stage_rsd[2];
+  unsigned stage_slot = 0;
+  ~Workspace() {
+    if (copy_st) {
+      cudaStreamSynchronize(copy_st);
+      cudaStreamDestroy(copy_st);
+      for (int i = 0; i < 2; ++i) {
+        cudaEventDestroy(ev_ready[i]);
+        cudaEventDestroy(ev_done[i]);
+      }
+    }
+  }
   DevBuf<SweepCtl> ctl;
   DevBuf<unsigned long long> counters;  // next_cnt + col_cnt[K] + col_np[K] + col_nn[K]
   DevBuf<double> dcols;                 // col_dr[K], colsum[K], D[K]
@@ -962,7 +821,7 @@ struct Workspace {
 static std::mutex g_ws_mu;
 static std::map<const Graph*, std::map<int, std::unique_ptr<Workspace>>> g_ws;
 
-static Workspace& workspace(Graph& g, int K, uint64_t ntiles) {
+static Workspace& workspace(Graph& g, int K, uint64_t ntiles, uint64_t nhubs) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
   auto& slot = g_ws[&g][K];
   if (!slot) {
@@ -994,10 +853,24 @@ static Workspace& workspace(Graph& g, int K, uint64_t ntiles) {
     w.carry_t.alloc((ntiles + 1) * K);
     w.split_cnt.alloc(ntiles + 1);
     PPRG_CUDA(cudaMemsetAsync(w.split_cnt.get(), 0, 4 * (ntiles + 1), g.stream));
-    w.split_acc.alloc(2 * (ntiles + 1) * K);
     w.ntiles_alloc = ntiles;
   }
+  if (nhubs + 1 > w.hub_cnt.n) {
+    w.hub_acc.alloc((nhubs + 1) * K);
+    w.hub_cnt.alloc(nhubs + 1);
+    PPRG_CUDA(cudaMemsetAsync(w.hub_acc.get(), 0, 8 * (nhubs + 1) * K, g.stream));
+    PPRG_CUDA(cudaMemsetAsync(w.hub_cnt.get(), 0, 4 * (nhubs + 1), g.stream));
+  }
   return w;
+}
+
+// Wait for every pending host-output copy of this graph's workspaces.
+static void sync_host_copies(const Graph& g) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto it = g_ws.find(&g);
+  if (it == g_ws.end()) return;
+  for (auto& kv : it->second)
+    if (kv.second && kv.second->copy_st) PPRG_CUDA(cudaStreamSynchronize(kv.second->copy_st));
 }
 
 void release_workspaces(const Graph* g) {
@@ -1016,8 +889,7 @@ inline unsigned grid_for(uint64_t items, int tb = 256) {
 
 template <int K, int MODE>
 void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
-  if (P.split_acc)
-    PPRG_CUDA(cudaMemsetAsync(P.split_acc, 0, sizeof(double) * 2 * (P.ntiles + 1) * K, g.stream));
+
   const size_t smem = Tile<K>::bytes;
   auto kern = k_sweeps<K, MODE>;
   static bool attr_set = false;
@@ -1092,9 +964,8 @@ struct Block {
   uint32_t k;
   uint64_t ntiles = 0;
   const uint32_t* tile_lo = nullptr;
-  const uint2* desc = nullptr;
-  const uint32_t* split_list = nullptr;
-  uint64_t n_split = 0;
+  const TileDesc* desc = nullptr;
+  uint64_t nhubs = 0;
   double alpha;
   std::vector<uint32_t> src;
   std::vector<double> r_sum;
@@ -1112,17 +983,20 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   const int K = round_k(k);
   uint64_t ntiles = 0;
   const uint32_t* tl = nullptr;
-  const uint2* dsc = nullptr;
+  const TileDesc* dsc = nullptr;
+  uint64_t nhubs = 0;
   if (need_pull) {
-    tl = g.tiles(SWEEP_ELEMS / K, &ntiles);
-    dsc = g.tile_desc(SWEEP_ELEMS / K, &ntiles);
+    const Graph::Plan& pl = g.tile_plan(SWEEP_ELEMS / K, tile_rmax(K));
+    dsc = pl.tiles.get();
+    ntiles = pl.ntiles;
+    nhubs = pl.nhubs;
   }
-  Workspace& w = workspace(g, K, ntiles);
+  Workspace& w = workspace(g, K, ntiles, nhubs);
   Block b(g, w, K, k, alpha);
   b.ntiles = ntiles;
   b.tile_lo = tl;
   b.desc = dsc;
-  if (need_pull) b.split_list = g.split_rows(SWEEP_ELEMS / K, &b.n_split);
+  b.nhubs = nhubs;
   for (uint32_t c = 0; c < k; ++c) b.src[c] = sources[c];
   for (int c = k; c < K; ++c) b.src[c] = sources[0];  // padding columns are inert
   PPRG_CUDA(cudaMemcpyAsync(w.d_src.get(), b.src.data(), 4 * KMAX, cudaMemcpyHostToDevice, g.stream));
@@ -1155,9 +1029,8 @@ SweepParams base_params(Block& b) {
   P.carry_head = b.w.carry_h.get();
   P.carry_tail = b.w.carry_t.get();
   P.split_cnt = b.w.split_cnt.get();
-  P.split_acc = b.w.split_acc.get();
-  P.split_list = b.split_list;
-  P.n_split = b.n_split;
+  P.hub_acc = b.w.hub_acc.get();
+  P.hub_cnt = b.w.hub_cnt.get();
   return P;
 }
 
@@ -1427,12 +1300,24 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
     return;
   }
   SweepParams Q = base_params(b);
-  DevBuf<double> o_res, o_rsd;
   const bool direct = out.on_device;  // write straight into the caller's device buffers
-  if (out.reserve && !direct) o_res.alloc(n * k);
-  if (out.residue && !direct) o_rsd.alloc(n * k);
-  Q.out_reserve = out.reserve ? (direct ? out.reserve : o_res.get()) : nullptr;
-  Q.out_residue = out.residue ? (direct ? out.residue : o_rsd.get()) : nullptr;
+  int slot = 0;
+  if (!direct && (out.reserve || out.residue)) {
+    if (!w.copy_st) {
+      PPRG_CUDA(cudaStreamCreateWithFlags(&w.copy_st, cudaStreamNonBlocking));
+      for (int i = 0; i < 2; ++i) {
+        PPRG_CUDA(cudaEventCreateWithFlags(&w.ev_ready[i], cudaEventDisableTiming));
+        PPRG_CUDA(cudaEventCreateWithFlags(&w.ev_done[i], cudaEventDisableTiming));
+        PPRG_CUDA(cudaEventRecord(w.ev_done[i], w.copy_st));
+      }
+    }
+    slot = (int)(w.stage_slot++ & 1);
+    PPRG_CUDA(cudaStreamWaitEvent(st, w.ev_done[slot], 0));  // the slot's previous D2H is done
+    if (out.reserve) w.stage_res[slot].ensure(n * b.K);
+    if (out.residue) w.stage_rsd[slot].ensure(n * b.K);
+  }
+  Q.out_reserve = out.reserve ? (direct ? out.reserve : w.stage_res[slot].get()) : nullptr;
+  Q.out_residue = out.residue ? (direct ? out.residue : w.stage_rsd[slot].get()) : nullptr;
   // rows with in-degree 0 (other than sources) are never visited: they hold 0
   if (Q.out_reserve) PPRG_CUDA(cudaMemsetAsync(Q.out_reserve, 0, 8 * n * k, st));
   if (Q.out_residue) PPRG_CUDA(cudaMemsetAsync(Q.out_residue, 0, 8 * n * k, st));
@@ -1446,13 +1331,24 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
     Q.init[c].D = b.D[c];
   }
   PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+  EventTimer tf(st);
+  tf.start();
   dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
+  tf.stop();
   call->kernel_launches += 1;
   SweepCtl fc;
   PPRG_CUDA(cudaMemcpyAsync(&fc, w.ctl.get(), sizeof fc, cudaMemcpyDeviceToHost, st));
-  if (out.reserve && !direct) PPRG_CUDA(cudaMemcpyAsync(out.reserve, o_res.get(), 8 * n * k, kind, st));
-  if (out.residue && !direct) PPRG_CUDA(cudaMemcpyAsync(out.residue, o_rsd.get(), 8 * n * k, kind, st));
+  if (!direct && (out.reserve || out.residue)) {
+    PPRG_CUDA(cudaEventRecord(w.ev_ready[slot], st));
+    PPRG_CUDA(cudaStreamWaitEvent(w.copy_st, w.ev_ready[slot], 0));
+    if (out.reserve)
+      PPRG_CUDA(cudaMemcpyAsync(out.reserve, Q.out_reserve, 8 * n * k, cudaMemcpyDeviceToHost, w.copy_st));
+    if (out.residue)
+      PPRG_CUDA(cudaMemcpyAsync(out.residue, Q.out_residue, 8 * n * k, cudaMemcpyDeviceToHost, w.copy_st));
+    PPRG_CUDA(cudaEventRecord(w.ev_done[slot], w.copy_st));
+  }
   PPRG_CUDA(cudaStreamSynchronize(st));
+  call->final_ms += tf.ms();
   for (uint32_t c = 0; c < k; ++c) {
     if (!b.scan[c]) continue;
     const double exact = fc.pushed[0][c];
@@ -1474,9 +1370,13 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
   const uint64_t limit = scan_threshold < 0 ? b.g.n / 4 : (uint64_t)scan_threshold;
   std::vector<int> state(KMAX, 2);
   for (uint32_t c = 0; c < b.k; ++c) state[c] = 0;
+  EventTimer tl(st);
+  tl.start();
   drain_levels(b, r_max, lambda, limit, false, state, call);
   std::vector<int> all(KMAX, 1);
   exact_rsum(b, all);
+  tl.stop();
+  call->local_ms += tl.ms();
   bool any = false;
   for (uint32_t c = 0; c < b.k; ++c) {
     b.scan[c] = b.r_sum[c] > lambda;  // push.cpp:168
@@ -1496,7 +1396,7 @@ uint32_t block_columns(uint64_t n, uint32_t k) {
     if (v >= 1 && v <= KMAX) return (uint32_t)v;
   }
   uint32_t K = KMAX;
-  while (K > 1 && 8.0 * (double)n * K > 80e6) K >>= 1;
+  while (K > 1 && 8.0 * (double)n * K > 320e6) K >>= 1;
   return K < k ? K : (k ? k : 1);
 }
 
@@ -1600,6 +1500,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
     }
     tdev.stop();
     call->device_ms += tdev.ms();
+    if (b0 + kb >= k) sync_host_copies(g);
     if (eng == Engine::PowerPush || eng == Engine::Fifo)
       for (uint32_t c = 0; c < kb; ++c) {
         cs[c].r_sum = b.r_sum[c];

@@ -42,6 +42,7 @@ for _ in range(a.reps):
     wall = (time.perf_counter() - t0) * 1e3
     print(f"wall {wall:.2f} ms  device {cs.device_ms:.2f} ms  sweeps_kernel {cs.sweep_ms:.2f} ms  "
           f"alg {cs.alg_bytes / 1e9:.2f} GB  {cs.alg_bytes / max(cs.sweep_ms, 1e-9) / 1e6:.1f} GB/s  "
+          f"local {cs.local_ms:.2f} ms final {cs.final_ms:.2f} ms "
           f"max_sweeps {cs.max_sweeps} launches {cs.kernel_launches}  "
           f"r_sum_max {max(o.achieved_r_sum for o in outs):.3e} "
           f"levels {outs[0].local_levels} pushes/m {outs[0].pushes / g.m():.2f}")
