@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -565,6 +566,9 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
 // Entry = linear index i = u*K + c. One warp per entry: claim r with
 // atomicExch (the FIFO pop, push.cpp:38-41), x += r, scatter (1-a) r / deg_eff
 // with fp64 RED, and append newly active (t, c) once per level (stamp).
+// Frontier of one level: per column c a FIFO segment
+// cur[c*seg_cap, c*seg_cap + q_c) of node ids, so an entry's position in its
+// segment is the number of pops of column c before it.
 struct FrontierParams {
   const uint64_t* off;
   const uint32_t* nbr;
@@ -572,19 +576,22 @@ struct FrontierParams {
   double* res;
   double* x;
   unsigned* stamp;
-  const uint64_t* cur;
-  uint64_t ncur;
-  uint64_t* next;
-  unsigned long long* next_cnt;
-  unsigned long long* col_cnt;   // [K] entries appended per column
-  double* col_dr;                // [K] alpha * sum r pushed
-  unsigned long long* col_np;    // [K] edge pushes
-  unsigned long long* col_nn;    // [K] node pushes
-  unsigned long long* col_proc;  // [K] entries of live columns processed
-  unsigned long long col_live;   // bit c set: column c still in this phase
+  const uint32_t* cur;
+  uint32_t* next;
+  uint64_t seg_cap;
+  uint64_t total;                 // sum of q_c
+  unsigned long long* col_cnt;    // [K] appends per column this level (= next segment length)
+  double* col_dr;                 // [K] alpha * sum r pushed
+  unsigned long long* col_np;     // [K] edge pushes
+  unsigned long long* col_nn;     // [K] node pushes
+  unsigned* col_stop;             // [K] set when the queue outgrows `limit` (push.cpp:38)
+  unsigned long long* col_resv;   // [K] out-degrees reserved by this level's pops
+  unsigned long long limit;
+  unsigned long long col_live;    // bit c set: column c still in this phase
   unsigned level_tag;
   int K;
   double alpha;
+  uint64_t pre[KMAX + 1];         // segment prefix: column c owns [pre[c], pre[c+1])
   uint32_t src[KMAX];
   double thr[KMAX];
 };
@@ -597,79 +604,103 @@ struct HeavyEntry {  // a frontier node whose scatter is spread over the grid
 };
 constexpr uint32_t HEAVY_DEG = 2048;
 
-// Append (t, c) to the next frontier once per level when it becomes active
-// (drain_queue's enqueue test, push.cpp:49-53). Warp-aggregated append.
-__device__ __forceinline__ void maybe_append(const FrontierParams& P, bool app, uint64_t ti, int c,
+// Append t to column c's next segment once per level when it becomes active
+// (drain_queue's enqueue test, push.cpp:49-53); one atomic per ballot group.
+__device__ __forceinline__ void maybe_append(const FrontierParams& P, bool app, uint32_t t, int c,
                                              unsigned mask) {
   const unsigned bal = __ballot_sync(mask, app);
   if (app) {
     const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
     unsigned long long basepos = 0;
-    if (lane == leader) basepos = atomicAdd(P.next_cnt, (unsigned long long)__popc(bal));
+    if (lane == leader) basepos = atomicAdd(P.col_cnt + c, (unsigned long long)__popc(bal));
     basepos = __shfl_sync(bal, basepos, leader);
-    P.next[basepos + __popc(bal & ((1u << lane) - 1u))] = ti;
-    atomicAdd(P.col_cnt + c, 1ull);
+    P.next[(uint64_t)c * P.seg_cap + basepos + __popc(bal & ((1u << lane) - 1u))] = t;
   }
 }
 
-// One warp per frontier entry (v, c): claim r (the FIFO pop, push.cpp:38-41),
-// x += r, then scatter (1-a) r / deg_eff to the effective out-neighbours with
-// fp64 atomics, 4 independent atomics per lane in flight. Entries with more
-// than HEAVY_DEG out-edges are queued for k_frontier_heavy instead, so a hub
-// never serialises one warp.
+__device__ __forceinline__ void relax_scatter(const FrontierParams& P, uint32_t t, int c,
+                                              double share, bool ok, unsigned mask) {
+  bool app = false;
+  if (ok) {
+    const uint64_t ti = (uint64_t)t * P.K + c;
+    const double nv = atomicAdd(P.res + ti, share) + share;
+    const uint32_t td = __ldg(P.deg + t);
+    if (nv > (double)(td ? td : 1) * P.thr[c])
+      app = atomicExch(P.stamp + ti, P.level_tag) != P.level_tag;
+  }
+  maybe_append(P, app, t, c, mask);
+}
+
+// One warp per frontier entry (v, c): check drain_queue's loop condition
+// (queue size <= limit before the pop, push.cpp:38), claim r (the pop,
+// push.cpp:40-43), x += r, then scatter (1-a) r / deg_eff to the effective
+// out-neighbours with fp64 atomics, 4 independent atomics per lane in flight.
+// Entries with more than HEAVY_DEG out-edges are queued for k_frontier_heavy,
+// so a hub never serialises one warp. Per-column counters accumulate in
+// shared memory and are flushed once per block.
 __global__ void __launch_bounds__(256) k_frontier(const __grid_constant__ FrontierParams P,
                                                   HeavyEntry* heavy, unsigned* heavy_cnt) {
+  __shared__ double sh_dr[KMAX];
+  __shared__ unsigned long long sh_np[KMAX], sh_nn[KMAX];
+  const int K = P.K;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) sh_dr[i] = 0, sh_np[i] = 0, sh_nn[i] = 0;
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const int K = P.K;
-  for (uint64_t w = w0; w < P.ncur; w += nw) {
-    const uint64_t i = P.cur[w];
-    const uint32_t v = (uint32_t)(i / K);
-    const int c = (int)(i % K);
+  for (uint64_t w = w0; w < P.total; w += nw) {
+    int c = 0;
+    while (w >= P.pre[c + 1]) ++c;
     if (!((P.col_live >> c) & 1ull)) continue;
+    const uint64_t pos = w - P.pre[c];
+    const uint32_t v = P.cur[(uint64_t)c * P.seg_cap + pos];
+    const uint64_t i = (uint64_t)v * K + c;
+    const uint32_t d = P.deg[v];
     double r = 0.0;
     if (lane == 0) {
-      atomicAdd(P.col_proc + c, 1ull);
-      r = __longlong_as_double((long long)atomicExch((unsigned long long*)(P.res + i), 0ull));
+      bool stop = *(volatile unsigned*)(P.col_stop + c) != 0;
+      if (!stop && P.limit != ~0ull) {
+        // appends of the pops before this one are bounded by their out-degrees,
+        // reserved at pop time, so concurrent warps see the queue growth at once
+        const unsigned long long reserved = atomicAdd(P.col_resv + c, (unsigned long long)(d ? d : 1));
+        const unsigned long long q = P.pre[c + 1] - P.pre[c];
+        if (q - pos + reserved > P.limit) {
+          stop = true;
+          P.col_stop[c] = 1;
+        }
+      }
+      if (!stop)
+        r = __longlong_as_double((long long)atomicExch((unsigned long long*)(P.res + i), 0ull));
     }
     r = __shfl_sync(0xffffffffu, r, 0);
     if (!(r > 0.0)) continue;
-    const uint32_t d = P.deg[v];
     const uint64_t de = d ? d : 1;
     const double share = (1.0 - P.alpha) * r / (double)de;
     const uint64_t b = P.off[v];
     if (lane == 0) {
       P.x[i] += r;
-      atomicAdd(P.col_dr + c, P.alpha * r);
-      atomicAdd(P.col_np + c, (unsigned long long)de);
-      atomicAdd(P.col_nn + c, 1ull);
+      atomicAdd(&sh_dr[c], P.alpha * r);
+      atomicAdd(&sh_np[c], (unsigned long long)de);
+      atomicAdd(&sh_nn[c], 1ull);
       if (de > HEAVY_DEG) heavy[atomicAdd(heavy_cnt, 1u)] = HeavyEntry{b, d, (uint32_t)c, share};
     }
     if (de > HEAVY_DEG) continue;
     for (uint64_t q0 = 0; q0 < de; q0 += 128) {
-      uint64_t ti[4];
-      double nv[4];
-      uint32_t td[4];
+      uint32_t t[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint64_t q = q0 + lane + 32 * k;
-        ti[k] = q < de ? (uint64_t)(d ? __ldg(P.nbr + b + q) : P.src[c]) * K + c : ~0ull;
+        t[k] = q < de ? (d ? __ldg(P.nbr + b + q) : P.src[c]) : 0xFFFFFFFFu;
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        if (ti[k] != ~0ull) {
-          nv[k] = atomicAdd(P.res + ti[k], share) + share;
-          td[k] = __ldg(P.deg + ti[k] / K);
-        }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        bool app = false;
-        if (ti[k] != ~0ull && nv[k] > (double)(td[k] ? td[k] : 1) * P.thr[c])
-          app = atomicExch(P.stamp + ti[k], P.level_tag) != P.level_tag;
-        maybe_append(P, app, ti[k], c, 0xffffffffu);
-      }
+      for (int k = 0; k < 4; ++k) relax_scatter(P, t[k], c, share, t[k] != 0xFFFFFFFFu, 0xffffffffu);
     }
+  }
+  __syncthreads();
+  for (int cc = threadIdx.x; cc < K; cc += blockDim.x) {
+    if (sh_dr[cc] != 0.0) atomicAdd(P.col_dr + cc, sh_dr[cc]);
+    if (sh_np[cc]) atomicAdd(P.col_np + cc, sh_np[cc]);
+    if (sh_nn[cc]) atomicAdd(P.col_nn + cc, sh_nn[cc]);
   }
 }
 
@@ -678,13 +709,12 @@ __global__ void __launch_bounds__(256) k_frontier_heavy(const __grid_constant__ 
                                                         const HeavyEntry* heavy,
                                                         const unsigned long long* prefix,
                                                         unsigned nheavy, unsigned long long total) {
-  const int K = P.K;
   for (unsigned long long e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
        e - threadIdx.x < total; e += (uint64_t)gridDim.x * blockDim.x) {
     const bool ok = e < total;
-    uint64_t ti = 0;
+    uint32_t t = 0;
     int c = 0;
-    bool app = false;
+    double share = 0.0;
     if (ok) {
       unsigned lo = 0, hi = nheavy;  // last h with prefix[h] <= e
       while (lo + 1 < hi) {
@@ -693,35 +723,38 @@ __global__ void __launch_bounds__(256) k_frontier_heavy(const __grid_constant__ 
       }
       const HeavyEntry h = heavy[lo];
       c = (int)h.c;
-      ti = (uint64_t)__ldg(P.nbr + h.begin + (e - prefix[lo])) * K + c;
-      const double nv = atomicAdd(P.res + ti, h.share) + h.share;
-      const uint32_t td = __ldg(P.deg + ti / K);
-      if (nv > (double)(td ? td : 1) * P.thr[c])
-        app = atomicExch(P.stamp + ti, P.level_tag) != P.level_tag;
+      share = h.share;
+      t = __ldg(P.nbr + h.begin + (e - prefix[lo]));
     }
-    maybe_append(P, app, ti, c, 0xffffffffu);
+    // all lanes of a ballot group must share the column: group by column
+    const unsigned same = __match_any_sync(0xffffffffu, ok ? c : -1);
+    if (ok) relax_scatter(P, t, c, share, true, same);
   }
 }
 
-// Enqueue every active (u, c) in id order (refine, push.cpp:212-218).
+// Enqueue every active (u, c) in id order (refine, push.cpp:212-218) into
+// column c's segment. Order within a segment follows warp-aggregated appends
+// over ascending ids.
 __global__ void k_scan_active(const double* res, const uint32_t* deg, uint64_t n, int K,
                               const double* thr, unsigned long long col_live, unsigned* stamp,
-                              unsigned tag, uint64_t* out, unsigned long long* cnt,
+                              unsigned tag, uint32_t* out, uint64_t seg_cap,
                               unsigned long long* col_cnt) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * K;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(i % K);
-    const uint32_t d = deg[i / K];
-    const bool a = ((col_live >> c) & 1ull) && res[i] > (double)(d ? d : 1) * thr[c];
-    const unsigned bal = __ballot_sync(0xffffffffu, a);
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x; i0 < n * K;
+       i0 += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool in = i < n * K;
+    const int c = in ? (int)(i % K) : -1;
+    const uint32_t d = in ? deg[i / K] : 0;
+    const bool a = in && ((col_live >> c) & 1ull) && res[i] > (double)(d ? d : 1) * thr[c];
+    const unsigned grp = __match_any_sync(0xffffffffu, c);
+    const unsigned bal = __ballot_sync(0xffffffffu, a) & grp;
     if (a) {
       stamp[i] = tag;
       const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
       unsigned long long b = 0;
-      if (lane == leader) b = atomicAdd(cnt, (unsigned long long)__popc(bal));
+      if (lane == leader) b = atomicAdd(col_cnt + c, (unsigned long long)__popc(bal));
       b = __shfl_sync(bal, b, leader);
-      out[b + __popc(bal & ((1u << lane) - 1u))] = i;
-      atomicAdd(col_cnt + c, 1ull);
+      out[(uint64_t)c * seg_cap + b + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)(i / K);
     }
   }
 }
@@ -786,7 +819,7 @@ struct Workspace {
   uint64_t n = 0;
   DevBuf<double> x, y0, y1, r0, r1, res;
   DevBuf<unsigned> stamp;
-  DevBuf<uint64_t> fa, fb;
+  DevBuf<uint32_t> fa, fb;  // frontier segments [K][n] of node ids
   DevBuf<double> carry_h, carry_t;
   DevBuf<unsigned> split_cnt;
   DevBuf<double> hub_acc;
@@ -813,6 +846,7 @@ struct Workspace {
   DevBuf<uint32_t> d_src;
   DevBuf<HeavyEntry> heavy;
   DevBuf<unsigned> heavy_cnt;
+  DevBuf<unsigned> col_stop;
   DevBuf<unsigned long long> heavy_prefix;
   unsigned level_tag = 0;
   uint64_t ntiles_alloc = 0;
@@ -841,7 +875,8 @@ static Workspace& workspace(Graph& g, int K, uint64_t ntiles, uint64_t nhubs) {
     w.fa.alloc(nk + 1);
     w.fb.alloc(nk + 1);
     w.ctl.alloc(1);
-    w.counters.alloc(1 + 4 * KMAX);
+    w.counters.alloc(1 + 5 * KMAX);
+    w.col_stop.alloc(KMAX);
     w.dcols.alloc(3 * KMAX);
     w.d_src.alloc(KMAX);
     w.heavy.alloc((g.m / HEAVY_DEG + 1) * (uint64_t)K + 1);
@@ -1058,21 +1093,21 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
   F.stamp = w.stamp.get();
   F.K = K;
   F.alpha = b.alpha;
+  F.seg_cap = n;
+  F.limit = limit == UINT64_MAX ? ~0ull : (unsigned long long)limit;
   for (int c = 0; c < K; ++c) {
     F.src[c] = b.src[c];
     F.thr[c] = r_max;
   }
-  const int NC = 1 + 4 * KMAX;
-  unsigned long long* next_cnt = w.counters.get();
-  unsigned long long* col_cnt = next_cnt + 1;
+  const int NC = 1 + 5 * KMAX;
+  unsigned long long* col_cnt = w.counters.get() + 1;
   unsigned long long* col_np = col_cnt + KMAX;
   unsigned long long* col_nn = col_np + KMAX;
-  unsigned long long* col_proc = col_nn + KMAX;
   double* col_dr = w.dcols.get();
-  uint64_t* cur = w.fa.get();
-  uint64_t* nxt = w.fb.get();
+  unsigned* d_stop = w.col_stop.get();
+  uint32_t* cur = w.fa.get();
+  uint32_t* nxt = w.fb.get();
   std::vector<uint64_t> qsize(K, 0);
-  uint64_t ncur = 0;
   auto next_tag = [&] {
     if (++w.level_tag == 0) {
       PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, st));
@@ -1089,11 +1124,9 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     PPRG_CUDA(cudaMemcpyAsync(w.dcols.get() + KMAX, thr.data(), 8 * KMAX, cudaMemcpyHostToDevice, st));
     PPRG_CUDA(cudaMemsetAsync(w.counters.get(), 0, 8 * NC, st));
     k_scan_active<<<grid_for(nk), 256, 0, st>>>(w.res.get(), g.deg.get(), n, K, w.dcols.get() + KMAX,
-                                                live0, w.stamp.get(), next_tag(), cur, next_cnt,
-                                                col_cnt);
+                                                live0, w.stamp.get(), next_tag(), cur, n, col_cnt);
     PPRG_CUDA(cudaMemcpyAsync(hc.data(), w.counters.get(), 8 * NC, cudaMemcpyDeviceToHost, st));
     PPRG_CUDA(cudaStreamSynchronize(st));
-    ncur = hc[0];
     for (int c = 0; c < K; ++c) qsize[c] = hc[1 + c];
     call->kernel_launches += 1;
   } else {
@@ -1101,18 +1134,14 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     for (int c = 0; c < K; ++c)
       PPRG_CUDA(cudaMemcpyAsync(&hdeg[c], g.deg.get() + b.src[c], 4, cudaMemcpyDeviceToHost, st));
     PPRG_CUDA(cudaStreamSynchronize(st));
-    std::vector<uint64_t> h;
-    for (uint32_t c = 0; c < b.k; ++c)
+    for (uint32_t c = 0; c < b.k; ++c)  // seed_source, push.cpp:61-66
       if (state[c] == 0 && 1.0 > (double)(hdeg[c] ? hdeg[c] : 1) * r_max) {
-        h.push_back((uint64_t)b.src[c] * K + c);
+        PPRG_CUDA(cudaMemcpyAsync(cur + (uint64_t)c * n, &b.src[c], 4, cudaMemcpyHostToDevice, st));
         qsize[c] = 1;
       }
-    ncur = h.size();
-    if (ncur) PPRG_CUDA(cudaMemcpyAsync(cur, h.data(), 8 * ncur, cudaMemcpyHostToDevice, st));
   }
-  const bool bounded = limit != UINT64_MAX;
-  const uint64_t chunk_max = bounded ? std::max<uint64_t>(4096, limit / 16) : UINT64_MAX;
   std::vector<double> hdr(KMAX);
+  std::vector<unsigned> hstop(KMAX);
   unsigned long long live = 0;
   auto still_live = [&](uint32_t c, uint64_t queued) {
     return queued > 0 && queued <= limit && !(lam_stop > 0 && b.r_sum[c] <= lam_stop);
@@ -1122,74 +1151,77 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     if (still_live(c, qsize[c])) live |= 1ull << c;
     else state[c] = 1;
   }
-  while (live && ncur) {
+  while (live) {
+    uint64_t total = 0;
+    for (int c = 0; c < K; ++c) {
+      F.pre[c] = total;
+      total += ((live >> c) & 1ull) ? qsize[c] : 0;
+    }
+    F.pre[K] = total;
+    for (int c = K + 1; c <= KMAX; ++c) F.pre[c] = total;
+    if (!total) break;
     PPRG_CUDA(cudaMemsetAsync(w.counters.get(), 0, 8 * NC, st));
-    const unsigned tag = next_tag();
-    uint64_t pos = 0;
-    while (pos < ncur && live) {
-      const uint64_t chunk = std::min<uint64_t>(chunk_max, ncur - pos);
-      PPRG_CUDA(cudaMemsetAsync(col_dr, 0, 8 * KMAX, st));
-      PPRG_CUDA(cudaMemsetAsync(col_np, 0, 8 * 2 * KMAX, st));
-      F.cur = cur + pos;
-      F.ncur = chunk;
-      F.next = nxt;
-      F.next_cnt = next_cnt;
-      F.col_cnt = col_cnt;
-      F.col_dr = col_dr;
-      F.col_np = col_np;
-      F.col_nn = col_nn;
-      F.col_proc = col_proc;
-      F.col_live = live;
-      F.level_tag = tag;
-      PPRG_CUDA(cudaMemsetAsync(w.heavy_cnt.get(), 0, 4, st));
-      k_frontier<<<grid_for(chunk * 32), 256, 0, st>>>(F, w.heavy.get(), w.heavy_cnt.get());
+    PPRG_CUDA(cudaMemsetAsync(col_dr, 0, 8 * KMAX, st));
+    PPRG_CUDA(cudaMemsetAsync(d_stop, 0, 4 * KMAX, st));
+    PPRG_CUDA(cudaMemsetAsync(w.heavy_cnt.get(), 0, 4, st));
+    // the segments of the live columns are read in place (pre[] skips the others)
+    F.cur = cur;
+    F.next = nxt;
+    F.total = total;
+    F.col_cnt = col_cnt;
+    F.col_dr = col_dr;
+    F.col_np = col_np;
+    F.col_nn = col_nn;
+    F.col_stop = d_stop;
+    F.col_resv = col_nn + KMAX;
+    F.col_live = live;
+    F.level_tag = next_tag();
+    // live columns are contiguous in pre[] but their segments sit at c*n: the
+    // kernel maps (c, pos) -> cur[c*n + pos]
+    k_frontier<<<grid_for(total * 32), 256, 0, st>>>(F, w.heavy.get(), w.heavy_cnt.get());
+    PPRG_CUDA(cudaGetLastError());
+    call->kernel_launches += 1;
+    unsigned nheavy = 0;
+    PPRG_CUDA(cudaMemcpyAsync(&nheavy, w.heavy_cnt.get(), 4, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    if (nheavy) {
+      std::vector<HeavyEntry> hv(nheavy);
+      PPRG_CUDA(cudaMemcpyAsync(hv.data(), w.heavy.get(), sizeof(HeavyEntry) * nheavy,
+                                cudaMemcpyDeviceToHost, st));
+      PPRG_CUDA(cudaStreamSynchronize(st));
+      std::vector<unsigned long long> pre(nheavy + 1, 0);
+      for (unsigned h = 0; h < nheavy; ++h) pre[h + 1] = pre[h] + hv[h].deg;
+      w.heavy_prefix.ensure(nheavy + 1);
+      PPRG_CUDA(cudaMemcpyAsync(w.heavy_prefix.get(), pre.data(), 8 * (nheavy + 1),
+                                cudaMemcpyHostToDevice, st));
+      k_frontier_heavy<<<grid_for(pre[nheavy]), 256, 0, st>>>(F, w.heavy.get(),
+                                                              w.heavy_prefix.get(), nheavy,
+                                                              pre[nheavy]);
       PPRG_CUDA(cudaGetLastError());
       call->kernel_launches += 1;
-      unsigned nheavy = 0;
-      PPRG_CUDA(cudaMemcpyAsync(&nheavy, w.heavy_cnt.get(), 4, cudaMemcpyDeviceToHost, st));
-      PPRG_CUDA(cudaStreamSynchronize(st));
-      if (nheavy) {
-        std::vector<HeavyEntry> hv(nheavy);
-        PPRG_CUDA(cudaMemcpyAsync(hv.data(), w.heavy.get(), sizeof(HeavyEntry) * nheavy,
-                                  cudaMemcpyDeviceToHost, st));
-        PPRG_CUDA(cudaStreamSynchronize(st));
-        std::vector<unsigned long long> pre(nheavy + 1, 0);
-        for (unsigned h = 0; h < nheavy; ++h) pre[h + 1] = pre[h] + hv[h].deg;
-        w.heavy_prefix.ensure(nheavy + 1);
-        PPRG_CUDA(cudaMemcpyAsync(w.heavy_prefix.get(), pre.data(), 8 * (nheavy + 1),
-                                  cudaMemcpyHostToDevice, st));
-        k_frontier_heavy<<<grid_for(pre[nheavy]), 256, 0, st>>>(F, w.heavy.get(),
-                                                                w.heavy_prefix.get(), nheavy,
-                                                                pre[nheavy]);
-        PPRG_CUDA(cudaGetLastError());
-        call->kernel_launches += 1;
-      }
-      PPRG_CUDA(cudaMemcpyAsync(hc.data(), w.counters.get(), 8 * NC, cudaMemcpyDeviceToHost, st));
-      PPRG_CUDA(cudaMemcpyAsync(hdr.data(), col_dr, 8 * KMAX, cudaMemcpyDeviceToHost, st));
-      PPRG_CUDA(cudaStreamSynchronize(st));
-      pos += chunk;
-      for (uint32_t c = 0; c < b.k; ++c) {
-        if (!((live >> c) & 1ull)) continue;
-        b.r_sum[c] -= hdr[c];
-        b.pushes[c] += hc[1 + KMAX + c];
-        const uint64_t queued = (qsize[c] - hc[1 + 3 * KMAX + c]) + hc[1 + c];
-        if (pos < ncur && !still_live(c, queued)) {
-          live &= ~(1ull << c);
-          state[c] = 1;
-        }
-      }
+    }
+    PPRG_CUDA(cudaMemcpyAsync(hc.data(), w.counters.get(), 8 * NC, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaMemcpyAsync(hdr.data(), col_dr, 8 * KMAX, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaMemcpyAsync(hstop.data(), d_stop, 4 * KMAX, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    if (std::getenv("PPRG_DEBUG_LOCAL")) {
+      unsigned long long nn = 0, np = 0, app = 0;
+      for (uint32_t c = 0; c < b.k; ++c) nn += hc[1 + 2 * KMAX + c], np += hc[1 + KMAX + c], app += hc[1 + c];
+      std::fprintf(stderr, "level: entries %llu heavy %u node_pushes %llu edge_pushes %llu appended %llu\n",
+                   (unsigned long long)total, nheavy, nn, np, app);
     }
     for (uint32_t c = 0; c < b.k; ++c) {
       if (!((live >> c) & 1ull)) continue;
+      b.r_sum[c] -= hdr[c];
+      b.pushes[c] += hc[1 + KMAX + c];
       b.levels[c] += 1;
       qsize[c] = hc[1 + c];
-      if (!still_live(c, qsize[c])) {
+      if (hstop[c] || !still_live(c, qsize[c])) {
         live &= ~(1ull << c);
         state[c] = 1;
       }
     }
     std::swap(cur, nxt);
-    ncur = hc[0];
   }
   for (uint32_t c = 0; c < b.k; ++c)
     if (state[c] == 0) state[c] = 1;
