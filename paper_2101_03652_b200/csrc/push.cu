@@ -381,6 +381,111 @@ __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& 
   if (tid == 0) *nlong = 0;
 }
 
+// Wide column blocks (K >= WIDE_K): tiles of up to WIDE_T in-edges and
+// RMAX_W rows; warps take rows from a shared counter and gather each in-edge's
+// K contiguous values straight into registers (lanes = edge slots x columns),
+// so no value staging in shared memory and no per-tile hub split below WIDE_T.
+constexpr int WIDE_K = 4;
+constexpr uint32_t WIDE_T = 4096;
+constexpr uint32_t RMAX_W = 256;
+
+template <int K, int MODE>
+__device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileDesc& d, char* smem,
+                                               const ColSh* cs, const double* thr_cur,
+                                               const double* yg, const double* rcur, double* rnxt,
+                                               double* ynxt, Acc& a, const BlockAcc& ba,
+                                               uint32_t* rowctr,
+                                               const unsigned long long* dn_slot, TileDesc* dn) {
+  uint64_t* soff = reinterpret_cast<uint64_t*>(smem);
+  double* sinv = reinterpret_cast<double*>(soff + RMAX_W + 1);
+  uint32_t* snode = reinterpret_cast<uint32_t*>(sinv + RMAX_W);
+  uint32_t* sdeg = snode + RMAX_W;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const uint32_t nr = d.nr;
+  for (uint32_t t = tid; t <= nr; t += NT) soff[t] = __ldg(P.in_off + d.r0 + t);
+  for (uint32_t t = tid; t < nr; t += NT) {
+    snode[t] = __ldg(P.crow + d.r0 + t);
+    sdeg[t] = __ldg(P.cdeg + d.r0 + t);
+    sinv[t] = __ldg(P.cinv + d.r0 + t);
+  }
+  __syncthreads();
+  if (dn_slot) *dn = P.desc[*dn_slot < P.ntiles ? *dn_slot : 0];  // next tile's descriptor
+  constexpr int KC = K < 32 ? K : 32;  // column lanes
+  constexpr int CPL = K / KC;          // contiguous columns per lane (2 for K = 64)
+  constexpr int ES = 32 / KC;          // edge slots per warp step
+  constexpr int U = 4;                 // independent steps in flight
+  const int es = lane / KC, kc = lane % KC;
+  for (;;) {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(rowctr, 1u);
+    r = __shfl_sync(0xffffffffu, r, 0);
+    if (r >= nr) break;
+    const uint64_t b = soff[r], e = soff[r + 1];
+    const uint32_t u = snode[r];
+    // issue the decision state early; it lands during the edge loop
+    double xo[CPL], rc[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
+      xo[q] = es == 0 ? __ldcg(P.x + ix) : 0.0;
+      rc[q] = (es == 0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
+    }
+    double acc[CPL][U];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+#pragma unroll
+      for (int k = 0; k < U; ++k) acc[q][k] = 0.0;
+    for (uint64_t p0 = b; p0 < e; p0 += ES * U) {
+      uint32_t id[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint64_t p = p0 + es + k * ES;
+        id[k] = p < e ? __ldg(P.in_nbr + p) : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (id[k] == 0xFFFFFFFFu) continue;
+        const double* src = yg + (uint64_t)id[k] * K + kc * CPL;
+        if constexpr (CPL == 2) {
+          const double2 v2 = *reinterpret_cast<const double2*>(src);
+          acc[0][k] += v2.x;
+          acc[1][k] += v2.y;
+        } else {
+          acc[0][k] += *src;
+        }
+      }
+    }
+    double s[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      s[q] = (acc[q][0] + acc[q][1]) + (acc[q][2] + acc[q][3]);
+#pragma unroll
+      for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+    }
+    if (es == 0) {
+      if constexpr (CPL == 1) {
+        decide<K, MODE>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], sdeg[r], sinv[r], yg, rnxt,
+                        ynxt, a);
+      } else {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) {
+          Acc b2;
+          const int cc = kc * CPL + q;
+          decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], sdeg[r], sinv[r], yg, rnxt,
+                          ynxt, b2);
+          if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
+          if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
+          if (b2.np) atomicAdd(&ba.np[cc], b2.np);
+          if (b2.nn) atomicAdd(&ba.nn[cc], b2.nn);
+          if (b2.et) atomicAdd(&ba.et[cc], b2.et);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *rowctr = 0;
+}
+
 // Sources with in-degree 0 are not rows of the compacted transpose; their
 // only inflow is the unit start mass plus the dead-end mass D (block 0).
 template <int K, int MODE>
@@ -475,6 +580,9 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
         hub_piece<K, MODE>(P, d, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
         dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
         __syncthreads();
+      } else if constexpr (K >= WIDE_K) {
+        tile_rows_wide<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba,
+                                &sh_nlong, &sh_tile[(it + 1) & 1], &dn);
       } else {
         tile_rows<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba, &sh_nlong,
                            &sh_tile[(it + 1) & 1], &dn);
@@ -808,7 +916,9 @@ __global__ void k_unpack(const double* a, uint64_t n, int K, int k_live, double 
   }
 }
 
+inline uint32_t tile_edges(int K) { return K >= WIDE_K ? WIDE_T : (uint32_t)(SWEEP_ELEMS / K); }
 inline uint32_t tile_rmax(int K) {
+  if (K >= WIDE_K) return RMAX_W;
   const int T = SWEEP_ELEMS / K;
   return T < 256 ? T : 256;
 }
@@ -925,7 +1035,8 @@ inline unsigned grid_for(uint64_t items, int tb = 256) {
 template <int K, int MODE>
 void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
 
-  const size_t smem = Tile<K>::bytes;
+  const size_t wide_bytes = 8ull * (RMAX_W + 1) + 8ull * RMAX_W + 8ull * RMAX_W + 16;
+  const size_t smem = K >= WIDE_K ? wide_bytes : Tile<K>::bytes;
   auto kern = k_sweeps<K, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1021,7 +1132,7 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   const TileDesc* dsc = nullptr;
   uint64_t nhubs = 0;
   if (need_pull) {
-    const Graph::Plan& pl = g.tile_plan(SWEEP_ELEMS / K, tile_rmax(K));
+    const Graph::Plan& pl = g.tile_plan(tile_edges(K), tile_rmax(K));
     dsc = pl.tiles.get();
     ntiles = pl.ntiles;
     nhubs = pl.nhubs;
@@ -1428,7 +1539,7 @@ uint32_t block_columns(uint64_t n, uint32_t k) {
     if (v >= 1 && v <= KMAX) return (uint32_t)v;
   }
   uint32_t K = KMAX;
-  while (K > 1 && 8.0 * (double)n * K > 320e6) K >>= 1;
+  while (K > 1 && 8.0 * (double)n * K > 1.6e9) K >>= 1;  // x, y, res, ... are n*K doubles each
   return K < k ? K : (k ? k : 1);
 }
 
