@@ -1,7 +1,7 @@
 /* pprg.h — C ABI of the B200-native single-source PPR engine.
  *
  * The drop-in boundary for the reference's C++ core API
- * (/root/reference/proj/core/include/ppr/*.hpp). Plain pointers and sizes, no
+ * (the ppr/ headers under /root/reference/proj/core/include). Plain pointers and sizes, no
  * C++ or torch types. Each entry point names the reference interface it
  * replaces (file:line under /root/reference/proj). The C++ shim in
  * paper_2101_03652_b200/cpp (namespace ppr::) re-exposes these with the

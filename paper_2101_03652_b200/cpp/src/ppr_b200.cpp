@@ -1,0 +1,335 @@
+// C++ drop-in of the reference's ppr:: core API over the engine's C ABI
+// (include/pprg.h). Every engine call runs on the GPU; status codes come back
+// as the reference's exception types (invalid_argument / runtime_error /
+// logic_error).
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <stdexcept>
+#include <string>
+
+#include "../../../include/pprg.h"
+#include "ppr/graph.hpp"
+#include "ppr/push.hpp"
+#include "ppr/speedppr.hpp"
+#include "ppr/walk_index.hpp"
+
+namespace ppr {
+namespace {
+
+void check(int rc) {
+  if (rc == PPRG_OK) return;
+  const std::string msg = pprg_last_error();
+  if (rc == PPRG_EINVAL) throw std::invalid_argument(msg);
+  if (rc == PPRG_EDATA) throw std::runtime_error(msg);
+  if (rc == PPRG_EINTERNAL) throw std::logic_error(msg);
+  throw std::runtime_error("device error: " + msg);
+}
+
+int device_from_env() {
+  if (const char* e = std::getenv("PPRG_DEVICE")) return std::atoi(e);
+  return 0;
+}
+
+PPRVector make_vector(NodeId n, NodeId s, double alpha) {
+  PPRVector v;
+  v.estimates.assign(n, 0.0);
+  v.residues.assign(n, 0.0);
+  v.source = s;
+  v.alpha = alpha;
+  return v;
+}
+
+void notify(PushObserver* obs, const PPRVector& v, std::uint32_t iterations) {
+  if (!obs) return;
+  PushState st(static_cast<NodeId>(v.estimates.size()), v.source);
+  st.reserve = v.estimates;
+  st.residue = v.residues;
+  st.r_sum = v.achieved_r_sum;
+  st.edge_push_count = v.pushes;
+  obs->on_push(st);
+  obs->on_iteration(st, iterations);
+}
+
+void write_u64(std::ofstream& o, std::uint64_t v) {
+  char b[8];
+  for (int i = 0; i < 8; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
+  o.write(b, 8);
+}
+void write_u32(std::ofstream& o, std::uint32_t v) {
+  char b[4];
+  for (int i = 0; i < 4; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
+  o.write(b, 4);
+}
+std::uint64_t read_u64(std::ifstream& in) {
+  unsigned char b[8] = {};
+  in.read(reinterpret_cast<char*>(b), 8);
+  std::uint64_t v = 0;
+  for (int i = 0; i < 8; ++i) v |= static_cast<std::uint64_t>(b[i]) << (8 * i);
+  return v;
+}
+std::uint32_t read_u32(std::ifstream& in) {
+  unsigned char b[4] = {};
+  in.read(reinterpret_cast<char*>(b), 4);
+  std::uint32_t v = 0;
+  for (int i = 0; i < 4; ++i) v |= static_cast<std::uint32_t>(b[i]) << (8 * i);
+  return v;
+}
+
+}  // namespace
+
+// ---- graph.hpp ---------------------------------------------------------------
+Graph::Graph(std::vector<std::uint64_t> out_offsets, std::vector<NodeId> out_neighbors)
+    : out_offsets_(std::move(out_offsets)), out_neighbors_(std::move(out_neighbors)) {
+  if (out_offsets_.empty()) throw std::runtime_error("graph: offsets array must have length n+1");
+  n_ = static_cast<NodeId>(out_offsets_.size() - 1);
+  m_ = out_neighbors_.size();
+  if (out_offsets_.back() != m_) throw std::runtime_error("graph: offsets must end at m");
+  pprg_graph* h = nullptr;
+  check(pprg_graph_create(out_offsets_.data(), out_neighbors_.data(), n_, device_from_env(), &h));
+  dev_.reset(h, pprg_graph_destroy);
+  for (NodeId v = 0; v < n_; ++v)
+    if (out_degree(v) == 0) dead_ends_.push_back(v);
+}
+
+void Graph::validate() const {  // the device validated at construction (graph.cpp:24-34)
+  if (out_offsets_[0] != 0) throw std::runtime_error("graph: offsets must start at 0");
+}
+
+Graph build_graph_from_edges(const std::vector<std::pair<std::uint64_t, std::uint64_t>>& edges) {
+  if (edges.empty()) throw std::runtime_error("graph is empty after cleaning");
+  std::vector<std::uint64_t> flat(2 * edges.size());
+  for (std::size_t i = 0; i < edges.size(); ++i) {
+    flat[2 * i] = edges[i].first;
+    flat[2 * i + 1] = edges[i].second;
+  }
+  pprg_graph* h = nullptr;
+  check(pprg_graph_build_from_edges(flat.data(), edges.size(), device_from_env(), &h));
+  std::uint64_t n = 0, m = 0, nd = 0;
+  check(pprg_graph_info(h, &n, &m, &nd));
+  std::vector<std::uint64_t> off(n + 1);
+  std::vector<NodeId> nbr(m);
+  check(pprg_graph_export(h, off.data(), nbr.data(), nullptr));
+  pprg_graph_destroy(h);
+  return Graph(std::move(off), std::move(nbr));
+}
+
+void save_graph_cache(const Graph& g, const std::string& path) {  // graph.cpp:115-125
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) throw std::runtime_error("cannot open for writing: " + path);
+  out.write("PPRG", 4);
+  out.put(1);
+  write_u64(out, g.n());
+  write_u64(out, g.m());
+  for (auto o : g.out_offsets()) write_u64(out, o);
+  for (auto u : g.out_neighbors()) write_u32(out, u);
+  if (!out) throw std::runtime_error("write failed: " + path);
+}
+
+Graph load_graph_cache(const std::string& path) {  // graph.cpp:127-143
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open graph cache: " + path);
+  char magic[4];
+  if (!in.read(magic, 4) || std::memcmp(magic, "PPRG", 4) != 0)
+    throw std::runtime_error(path + ": not a graph cache (bad magic)");
+  if (in.get() != 1) throw std::runtime_error(path + ": unsupported graph cache version");
+  const std::uint64_t n = read_u64(in), m = read_u64(in);
+  std::vector<std::uint64_t> off(n + 1);
+  for (auto& o : off) o = read_u64(in);
+  std::vector<NodeId> nbr(m);
+  for (auto& u : nbr) u = read_u32(in);
+  if (!in) throw std::runtime_error(path + ": truncated graph cache");
+  return Graph(std::move(off), std::move(nbr));
+}
+
+bool is_graph_cache(const std::string& path) {
+  std::ifstream in(path, std::ios::binary);
+  char magic[4];
+  return in && in.read(magic, 4) && std::memcmp(magic, "PPRG", 4) == 0;
+}
+
+// ---- push.hpp ----------------------------------------------------------------
+PPRVector power_iteration(const Graph& g, NodeId s, double alpha, double lambda,
+                          PushObserver* observer) {
+  PPRVector v = make_vector(g.n(), s, alpha);
+  pprg_query_stats q{};
+  check(pprg_power_iteration(g.device_handle(), &s, 1, alpha, lambda, v.estimates.data(),
+                             v.residues.data(), 0, &q, nullptr));
+  v.achieved_r_sum = q.achieved_r_sum;
+  v.pushes = q.pushes;
+  notify(observer, v, q.sweeps);
+  return v;
+}
+
+PPRVector sim_forward_push(const Graph& g, NodeId s, double alpha, double lambda,
+                           PushObserver* observer) {
+  PPRVector v = make_vector(g.n(), s, alpha);
+  pprg_query_stats q{};
+  check(pprg_sim_forward_push(g.device_handle(), &s, 1, alpha, lambda, v.estimates.data(),
+                              v.residues.data(), 0, &q, nullptr));
+  v.achieved_r_sum = q.achieved_r_sum;
+  v.pushes = q.pushes;
+  notify(observer, v, q.sweeps);
+  return v;
+}
+
+PPRVector fifo_forward_push(const Graph& g, NodeId s, double alpha, double r_max,
+                            std::optional<double> lambda_stop, PushObserver* observer) {
+  PPRVector v = make_vector(g.n(), s, alpha);
+  pprg_query_stats q{};
+  check(pprg_fifo_forward_push(g.device_handle(), &s, 1, alpha, r_max,
+                               lambda_stop ? *lambda_stop : -1.0, v.estimates.data(),
+                               v.residues.data(), 0, &q, nullptr));
+  v.achieved_r_sum = q.achieved_r_sum;
+  v.pushes = q.pushes;
+  notify(observer, v, q.local_levels);
+  return v;
+}
+
+PPRVector power_push(const Graph& g, NodeId s, double alpha, double lambda,
+                     const QueryConfig& cfg, PushObserver* observer, PowerPushTrace* trace) {
+  PPRVector v = make_vector(g.n(), s, alpha);
+  pprg_query_stats q{};
+  std::vector<double> eps(cfg.epoch_num);
+  check(pprg_power_push(g.device_handle(), &s, 1, alpha, lambda, cfg.epoch_num,
+                        cfg.scan_threshold ? static_cast<int64_t>(*cfg.scan_threshold) : -1,
+                        v.estimates.data(), v.residues.data(), 0, &q, nullptr, eps.data()));
+  v.achieved_r_sum = q.achieved_r_sum;
+  v.pushes = q.pushes;
+  if (trace) {
+    trace->used_scan_phase = q.used_scan_phase != 0;
+    trace->epoch_r_max = q.used_scan_phase ? eps : std::vector<double>{};
+  }
+  notify(observer, v, q.sweeps);
+  return v;
+}
+
+std::vector<PPRVector> power_push_batch(const Graph& g, const std::vector<NodeId>& sources,
+                                        double alpha, double lambda, const QueryConfig& cfg) {
+  const std::size_t k = sources.size(), n = g.n();
+  std::vector<double> res(k * n), rsd(k * n);
+  std::vector<pprg_query_stats> q(k);
+  check(pprg_power_push(g.device_handle(), sources.data(), static_cast<uint32_t>(k), alpha, lambda,
+                        cfg.epoch_num,
+                        cfg.scan_threshold ? static_cast<int64_t>(*cfg.scan_threshold) : -1,
+                        res.data(), rsd.data(), 0, q.data(), nullptr, nullptr));
+  std::vector<PPRVector> out(k);
+  for (std::size_t i = 0; i < k; ++i) {
+    out[i].estimates.assign(res.begin() + i * n, res.begin() + (i + 1) * n);
+    out[i].residues.assign(rsd.begin() + i * n, rsd.begin() + (i + 1) * n);
+    out[i].source = sources[i];
+    out[i].alpha = alpha;
+    out[i].achieved_r_sum = q[i].achieved_r_sum;
+    out[i].pushes = q[i].pushes;
+  }
+  return out;
+}
+
+// ---- walk_index.hpp / speedppr.hpp -------------------------------------------
+void WalkIndex::check_compatible(const Graph& g) const {  // walk_index.cpp:36-42
+  if (node_count() != g.n() || endpoint_count() != g.m())
+    throw std::runtime_error("walk index does not match the graph shape");
+  for (NodeId v = 0; v < g.n(); ++v)
+    if (endpoints_of(v).size() != g.out_degree(v))
+      throw std::runtime_error("walk index slice length differs from out-degree");
+}
+
+WalkIndex build_index(const Graph& g, double alpha, std::uint64_t seed) {
+  pprg_index* h = nullptr;
+  check(pprg_index_build(g.device_handle(), alpha, seed, &h));
+  WalkIndex w;
+  w.dev_.reset(h, pprg_index_destroy);
+  w.alpha_ = alpha;
+  w.seed_ = seed;
+  w.offsets_ = g.out_offsets();
+  w.endpoints_.resize(g.m());
+  if (g.m()) check(pprg_index_export(h, w.endpoints_.data()));
+  return w;
+}
+
+void save_index(const WalkIndex& index, const std::string& path) {  // walk_index.cpp:61-81
+  std::ofstream out(path, std::ios::binary | std::ios::trunc);
+  if (!out) throw std::runtime_error("cannot open for writing: " + path);
+  out.write("PPRW", 4);
+  out.put(1);
+  out.put(static_cast<char>(index.rng_id()));
+  std::uint64_t bits;
+  const double a = index.alpha();
+  std::memcpy(&bits, &a, 8);
+  write_u64(out, bits);
+  write_u64(out, index.seed());
+  write_u64(out, index.node_count());
+  write_u64(out, index.endpoint_count());
+  std::uint64_t off = 0;
+  write_u64(out, 0);
+  for (NodeId v = 0; v < index.node_count(); ++v) {
+    off += index.endpoints_of(v).size();
+    write_u64(out, off);
+  }
+  for (NodeId v = 0; v < index.node_count(); ++v)
+    for (NodeId e : index.endpoints_of(v)) write_u32(out, e);
+  if (!out) throw std::runtime_error("write failed: " + path);
+}
+
+WalkIndex load_index(const std::string& path, const Graph& g) {  // walk_index.cpp:83-104
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open walk index: " + path);
+  char magic[4];
+  if (!in.read(magic, 4) || std::memcmp(magic, "PPRW", 4) != 0)
+    throw std::runtime_error(path + ": not a walk index (bad magic)");
+  if (in.get() != 1) throw std::runtime_error(path + ": unsupported walk index version");
+  if (in.get() != kRngIdPhilox4x32_10) throw std::runtime_error(path + ": unknown generator id");
+  const std::uint64_t abits = read_u64(in);
+  double alpha;
+  std::memcpy(&alpha, &abits, 8);
+  const std::uint64_t seed = read_u64(in), n = read_u64(in), m = read_u64(in);
+  WalkIndex w;
+  w.alpha_ = alpha;
+  w.seed_ = seed;
+  w.offsets_.resize(n + 1);
+  for (auto& o : w.offsets_) o = read_u64(in);
+  w.endpoints_.resize(m);
+  for (auto& e : w.endpoints_) e = read_u32(in);
+  if (!in) throw std::runtime_error(path + ": truncated walk index");
+  w.check_compatible(g);
+  pprg_index* h = nullptr;
+  check(pprg_index_from_host(g.device_handle(), alpha, seed, w.endpoints_.data(), &h));
+  w.dev_.reset(h, pprg_index_destroy);
+  return w;
+}
+
+double walk_budget_real(std::uint64_t n, double epsilon, double mu) {  // speedppr.cpp:8-14
+  if (n < 2) throw std::invalid_argument("walk budget: need n >= 2");
+  if (!(epsilon > 0.0)) throw std::invalid_argument("walk budget: epsilon must be positive");
+  if (!(mu > 0.0 && mu <= 1.0)) throw std::invalid_argument("walk budget: mu must be in (0,1]");
+  return 2.0 * (2.0 * epsilon / 3.0 + 2.0) * std::log(static_cast<double>(n)) /
+         (epsilon * epsilon * mu);
+}
+
+std::uint64_t compute_walk_budget(std::uint64_t n, double epsilon, double mu) {
+  std::uint64_t out = 0;
+  check(pprg_walk_budget(n, epsilon, mu, &out));
+  return out;
+}
+
+PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
+                         const WalkIndex* index) {  // speedppr.cpp:74-111
+  cfg.validate();
+  if (!cfg.epsilon) throw std::invalid_argument("speedppr: epsilon is required");
+  if (s >= g.n()) throw std::invalid_argument("speedppr: source out of range");
+  if (index) {
+    index->check_compatible(g);
+    if (index->alpha() != cfg.alpha)
+      throw std::runtime_error("walk index was built for a different alpha");
+  }
+  PPRVector v = make_vector(g.n(), s, cfg.alpha);
+  pprg_query_stats q{};
+  check(pprg_speedppr(g.device_handle(), index ? index->device_handle() : nullptr, &s, 1,
+                      cfg.alpha, *cfg.epsilon, cfg.mu ? *cfg.mu : -1.0, cfg.seed,
+                      v.estimates.data(), 0, &q, nullptr));
+  v.pushes = q.pushes;
+  v.walks = q.walks;
+  return v;
+}
+
+}  // namespace ppr

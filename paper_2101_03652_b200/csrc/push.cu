@@ -389,6 +389,93 @@ constexpr int WIDE_K = 4;
 constexpr uint32_t WIDE_T = 4096;
 constexpr uint32_t RMAX_W = 256;
 
+// Sum of y over the in-edges [b, e) of one row for my columns, by one warp.
+// Lanes = ES edge slots x KC column lanes (x CPL contiguous columns). The ids
+// of 32 consecutive edges are loaded once, coalesced, and broadcast by shuffle.
+template <int K>
+__device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double* yg, uint64_t b,
+                                             uint64_t e, double (&s)[(K < 32 ? 1 : K / 32)]) {
+  constexpr int KC = K < 32 ? K : 32;
+  constexpr int CPL = K / KC;
+  constexpr int ES = 32 / KC;
+  const int lane = threadIdx.x & 31, es = lane / KC, kc = lane % KC;
+  double acc[CPL][4];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[q][k] = 0.0;
+  for (uint64_t p0 = b; p0 < e; p0 += 32) {
+    const uint64_t pl = p0 + lane;
+    const uint32_t myid = pl < e ? __ldg(P.in_nbr + pl) : 0xFFFFFFFFu;
+    const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
+#pragma unroll 2
+    for (int j0 = 0; j0 < 32; j0 += 4 * ES) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int j = j0 + k * ES + es;
+        const uint32_t id = __shfl_sync(0xffffffffu, myid, j & 31);
+        if (j < cnt) {
+          const double* src = yg + (uint64_t)id * K + kc * CPL;
+          if constexpr (CPL == 2) {
+            const double2 v2 = *reinterpret_cast<const double2*>(src);
+            acc[0][k] += v2.x;
+            acc[1][k] += v2.y;
+          } else {
+            acc[0][k] += *src;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    s[q] = (acc[q][0] + acc[q][1]) + (acc[q][2] + acc[q][3]);
+#pragma unroll
+    for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+  }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* cs,
+                                            const double* thr_cur, uint32_t u, const double* s,
+                                            const double* xo, const double* rc, uint32_t dg,
+                                            double inv, const double* yg, double* rnxt,
+                                            double* ynxt, Acc& a, const BlockAcc& ba) {
+  constexpr int KC = K < 32 ? K : 32;
+  constexpr int CPL = K / KC;
+  const int kc = (threadIdx.x & 31) % KC;
+  if constexpr (CPL == 1) {
+    decide<K, MODE>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], dg, inv, yg, rnxt, ynxt, a);
+  } else {  // K = 64: lane kc owns columns 2kc, 2kc+1; counters via shared atomics
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      Acc b2;
+      const int cc = kc * CPL + q;
+      decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
+      if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
+      if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
+      if (b2.np) atomicAdd(&ba.np[cc], b2.np);
+      if (b2.nn) atomicAdd(&ba.nn[cc], b2.nn);
+      if (b2.et) atomicAdd(&ba.et[cc], b2.et);
+    }
+  }
+}
+
+// Long-row counter slot of the wide layout (zeroed at kernel start).
+template <int K>
+__device__ __forceinline__ uint32_t* wide_long_count(char* smem) {
+  uint64_t* soff = reinterpret_cast<uint64_t*>(smem);
+  double* sinv = reinterpret_cast<double*>(soff + RMAX_W + 1);
+  double* spart = sinv + RMAX_W;
+  uint32_t* snode = reinterpret_cast<uint32_t*>(spart + (NT / 32) * K);
+  return snode + 3 * RMAX_W;
+}
+
+// Wide column blocks: warps take rows from a shared counter and sum each row
+// with warp_row_sum; rows longer than LONG_W in-edges are summed by all warps
+// of the block together (partials in shared memory) so no warp lags the tile.
+constexpr uint32_t LONG_W = 384;
+
 template <int K, int MODE>
 __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileDesc& d, char* smem,
                                                const ColSh* cs, const double* thr_cur,
@@ -396,94 +483,82 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
                                                double* ynxt, Acc& a, const BlockAcc& ba,
                                                uint32_t* rowctr,
                                                const unsigned long long* dn_slot, TileDesc* dn) {
+  constexpr int KC = K < 32 ? K : 32;
+  constexpr int CPL = K / KC;
+  constexpr int NW = NT / 32;
   uint64_t* soff = reinterpret_cast<uint64_t*>(smem);
   double* sinv = reinterpret_cast<double*>(soff + RMAX_W + 1);
-  uint32_t* snode = reinterpret_cast<uint32_t*>(sinv + RMAX_W);
+  double* spart = sinv + RMAX_W;                       // [NW][K] long-row partials
+  uint32_t* snode = reinterpret_cast<uint32_t*>(spart + NW * K);
   uint32_t* sdeg = snode + RMAX_W;
-  const int tid = threadIdx.x, lane = tid & 31;
+  uint32_t* slong = sdeg + RMAX_W;                     // [RMAX_W] long rows; slong[RMAX_W] = count
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int es0 = lane < KC;  // lanes holding the reduced sums
+  const int kc = lane % KC;
   const uint32_t nr = d.nr;
   for (uint32_t t = tid; t <= nr; t += NT) soff[t] = __ldg(P.in_off + d.r0 + t);
   for (uint32_t t = tid; t < nr; t += NT) {
     snode[t] = __ldg(P.crow + d.r0 + t);
     sdeg[t] = __ldg(P.cdeg + d.r0 + t);
     sinv[t] = __ldg(P.cinv + d.r0 + t);
+    const uint64_t len = __ldg(P.in_off + d.r0 + t + 1) - __ldg(P.in_off + d.r0 + t);
+    if (len > LONG_W) slong[atomicAdd(&slong[RMAX_W], 1u)] = t;
   }
   __syncthreads();
   if (dn_slot) *dn = P.desc[*dn_slot < P.ntiles ? *dn_slot : 0];  // next tile's descriptor
-  constexpr int KC = K < 32 ? K : 32;  // column lanes
-  constexpr int CPL = K / KC;          // contiguous columns per lane (2 for K = 64)
-  constexpr int ES = 32 / KC;          // edge slots per warp step
-  constexpr int U = 4;                 // independent steps in flight
-  const int es = lane / KC, kc = lane % KC;
+  // ---- short rows: one warp per row, dynamic -----------------------------
   for (;;) {
     uint32_t r = 0;
     if (lane == 0) r = atomicAdd(rowctr, 1u);
     r = __shfl_sync(0xffffffffu, r, 0);
     if (r >= nr) break;
     const uint64_t b = soff[r], e = soff[r + 1];
+    if (e - b > LONG_W) continue;
     const uint32_t u = snode[r];
-    // issue the decision state early; it lands during the edge loop
-    double xo[CPL], rc[CPL];
+    double xo[CPL], rc[CPL], s[CPL];
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
+    for (int q = 0; q < CPL; ++q) {  // issued early; lands during the edge loop
       const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
-      xo[q] = es == 0 ? __ldcg(P.x + ix) : 0.0;
-      rc[q] = (es == 0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
+      xo[q] = es0 ? __ldcg(P.x + ix) : 0.0;
+      rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
     }
-    double acc[CPL][U];
-#pragma unroll
-    for (int q = 0; q < CPL; ++q)
-#pragma unroll
-      for (int k = 0; k < U; ++k) acc[q][k] = 0.0;
-    for (uint64_t p0 = b; p0 < e; p0 += ES * U) {
-      uint32_t id[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const uint64_t p = p0 + es + k * ES;
-        id[k] = p < e ? __ldg(P.in_nbr + p) : 0xFFFFFFFFu;
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if (id[k] == 0xFFFFFFFFu) continue;
-        const double* src = yg + (uint64_t)id[k] * K + kc * CPL;
-        if constexpr (CPL == 2) {
-          const double2 v2 = *reinterpret_cast<const double2*>(src);
-          acc[0][k] += v2.x;
-          acc[1][k] += v2.y;
-        } else {
-          acc[0][k] += *src;
-        }
-      }
-    }
+    warp_row_sum<K>(P, yg, b, e, s);
+    if (es0) decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
+  }
+  // ---- long rows: all warps split the edges ---------------------------------
+  const uint32_t nl = slong[RMAX_W];
+  for (uint32_t li = 0; li < nl; ++li) {
+    const uint32_t r = slong[li];
+    const uint64_t b = soff[r], e = soff[r + 1];
+    const uint64_t chunk = ((e - b) + NW - 1) / NW;
+    const uint64_t wb = b + warp * chunk, we = wb + chunk < e ? wb + chunk : e;
     double s[CPL];
+    warp_row_sum<K>(P, yg, wb < e ? wb : e, we, s);
+    if (es0)
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      s[q] = (acc[q][0] + acc[q][1]) + (acc[q][2] + acc[q][3]);
+      for (int q = 0; q < CPL; ++q) spart[warp * K + kc * CPL + q] = s[q];
+    __syncthreads();
+    if (warp == 0 && es0) {
+      const uint32_t u = snode[r];
+      double xo[CPL], rc[CPL];
 #pragma unroll
-      for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
-    }
-    if (es == 0) {
-      if constexpr (CPL == 1) {
-        decide<K, MODE>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], sdeg[r], sinv[r], yg, rnxt,
-                        ynxt, a);
-      } else {
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) {
-          Acc b2;
-          const int cc = kc * CPL + q;
-          decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], sdeg[r], sinv[r], yg, rnxt,
-                          ynxt, b2);
-          if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
-          if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
-          if (b2.np) atomicAdd(&ba.np[cc], b2.np);
-          if (b2.nn) atomicAdd(&ba.nn[cc], b2.nn);
-          if (b2.et) atomicAdd(&ba.et[cc], b2.et);
-        }
+      for (int q = 0; q < CPL; ++q) {
+        const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
+        xo[q] = __ldcg(P.x + ix);
+        rc[q] = (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0;
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += spart[w * K + kc * CPL + q];
+        s[q] = t;
       }
+      decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
     }
+    __syncthreads();
   }
   __syncthreads();
-  if (tid == 0) *rowctr = 0;
+  if (tid == 0) {
+    *rowctr = 0;
+    slong[RMAX_W] = 0;
+  }
 }
 
 // Sources with in-degree 0 are not rows of the compacted transpose; their
@@ -541,6 +616,7 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
       sh_any = any && (MODE == M_FINAL ? sweep == 0 : sweep < P.max_sweeps);
       if (sh_any) sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
       sh_nlong = 0;
+      if constexpr (K >= WIDE_K) *wide_long_count<K>(smem_dyn) = 0;
     }
     if (tid < K) {
       thr_cur[tid] = (MODE == M_POWERPUSH && !cs[tid].done) ? P.thr[cs[tid].epoch] : 0.0;
@@ -1035,7 +1111,8 @@ inline unsigned grid_for(uint64_t items, int tb = 256) {
 template <int K, int MODE>
 void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
 
-  const size_t wide_bytes = 8ull * (RMAX_W + 1) + 8ull * RMAX_W + 8ull * RMAX_W + 16;
+  const size_t wide_bytes = 8ull * (RMAX_W + 1) + 8ull * RMAX_W + 8ull * (NT / 32) * K +
+                            4ull * (3 * RMAX_W + 1) + 16;
   const size_t smem = K >= WIDE_K ? wide_bytes : Tile<K>::bytes;
   auto kern = k_sweeps<K, MODE>;
   static bool attr_set = false;
