@@ -1435,13 +1435,16 @@ void exact_rsum(Block& b, const std::vector<int>& which) {
 
 // Global phase: epochs of asynchronous pull sweeps in one persistent
 // cooperative kernel (push.cpp:168-197) for the columns with scan[c] set.
-void global_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
+// refine_rmax > 0 appends a refine epoch (push.cpp:208-222): threshold
+// refine_rmax, no r_sum target, ends at the sweep that pushes nothing — the
+// fixpoint where every residue is <= deg_eff * refine_rmax, refine's postcondition.
+void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double refine_rmax = 0.0) {
   Graph& g = b.g;
   Workspace& w = b.w;
   cudaStream_t st = g.stream;
   const uint64_t nk = g.n * (uint64_t)b.K;
   const double m_eff = (double)g.m_eff();
-  if (E > EMAX) fail(EINVAL_, "epoch_num exceeds 64");
+  if (E + (refine_rmax > 0.0) > EMAX) fail(EINVAL_, "epoch_num exceeds 64");
   PPRG_CUDA(cudaMemsetAsync(w.dcols.get() + 2 * KMAX, 0, 8 * KMAX, st));
   k_init_pull<<<grid_for(nk), 256, 0, st>>>(w.x.get(), g.deg.get(), g.inv_deg.get(), g.n, b.K,
                                             b.alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
@@ -1454,15 +1457,20 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
     P.lam[e] = el;
     P.thr[e] = el / m_eff;
   }
+  const int Et = (int)E + (refine_rmax > 0.0);
+  if (refine_rmax > 0.0) {
+    P.lam[E] = -1.0;
+    P.thr[E] = refine_rmax;
+  }
   for (int c = 0; c < b.K; ++c) {
     P.init[c].r_sum = b.r_sum[c];
     P.init[c].D = b.D[c];
     int ep = 0;
-    while (ep < (int)E && !(b.r_sum[c] > P.lam[ep])) ++ep;
+    while (ep < Et && !(b.r_sum[c] > P.lam[ep])) ++ep;
     P.init[c].epoch = ep;
-    P.init[c].done = !b.scan[c] || ep >= (int)E;
+    P.init[c].done = !b.scan[c] || ep >= Et;
   }
-  P.E = (int)E;
+  P.E = Et;
   P.x = w.x.get();
   P.y[0] = P.y[1] = w.y0.get();
   EventTimer tm(st);
@@ -1579,7 +1587,7 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
 }
 
 void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_threshold,
-                      CallStats* call) {
+                      CallStats* call, double refine_rmax = 0.0) {
   const double m_eff = (double)b.g.m_eff();
   const uint64_t nk = b.g.n * (uint64_t)b.K;
   cudaStream_t st = b.g.stream;
@@ -1599,10 +1607,10 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
   call->local_ms += tl.ms();
   bool any = false;
   for (uint32_t c = 0; c < b.k; ++c) {
-    b.scan[c] = b.r_sum[c] > lambda;  // push.cpp:168
+    b.scan[c] = b.r_sum[c] > lambda || refine_rmax > 0.0;  // push.cpp:168
     any |= b.scan[c] != 0;
   }
-  if (any) global_phase(b, lambda, epoch_num, call);
+  if (any) global_phase(b, lambda, epoch_num, call, refine_rmax);
 }
 
 }  // namespace
@@ -1740,15 +1748,12 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
                          PushView* view) {
   g.ensure_transpose();
   Block b = make_block(g, sources, k, alpha, true);
-  power_push_block(b, lambda, 8, -1, call);
+  // PowerPush to lambda, then refine (push.cpp:208-222) as a final sweep
+  // epoch at r_max run to its fixpoint, so the refine is pull sweeps over the
+  // tile plan rather than a scattered frontier over millions of nodes.
+  power_push_block(b, lambda, 8, -1, call, r_max);
   Outputs none;
   finalize(b, none, true, call);
-  // refine (push.cpp:208-222): every active node in id order, drain, recompute
-  std::vector<int> state(KMAX, 2);
-  for (uint32_t c = 0; c < k; ++c) state[c] = 0;
-  drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);
-  std::vector<int> all(KMAX, 1);
-  exact_rsum(b, all);
   for (uint32_t c = 0; c < k; ++c) {
     cols[c].r_sum = b.r_sum[c];
     cols[c].pushes = b.pushes[c];

@@ -63,9 +63,14 @@ __global__ void k_terminals(const uint64_t* off, const uint32_t* nbr, const uint
 }
 
 // W_v = ceil(r W), clamped to deg_eff within the reference's slack
-// (speedppr.cpp:30-40); counts for padding columns are 0.
+// (speedppr.cpp:30-40); counts for padding columns are 0. Per-column walk
+// totals accumulate in shared memory (K <= 64), flushed once per block.
 __global__ void k_mc_counts(const double* res, const uint32_t* deg, uint64_t n, int K, int k,
-                            double W, unsigned long long* cnt, unsigned* bad) {
+                            double W, unsigned long long* cnt, unsigned* bad,
+                            unsigned long long* colw) {
+  __shared__ unsigned long long s_w[64];
+  for (int c = threadIdx.x; c < 64; c += blockDim.x) s_w[c] = 0;
+  __syncthreads();
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * K;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % K);
@@ -79,9 +84,13 @@ __global__ void k_mc_counts(const double* res, const uint32_t* deg, uint64_t n, 
         if (r * W > de * (1.0 + 1e-9) + 1e-9) atomicOr(bad, 1u);
         wc = (unsigned long long)de;
       }
+      if (wc) atomicAdd(&s_w[c], wc);
     }
     cnt[i] = wc;
   }
+  __syncthreads();
+  for (int c = threadIdx.x; c < K; c += blockDim.x)
+    if (s_w[c]) atomicAdd(colw + c, s_w[c]);
 }
 
 __global__ void k_est_init(const double* x, uint64_t nk, double alpha, double* est) {
@@ -96,10 +105,8 @@ struct McParams {
   const uint32_t* deg;
   const double* res;
   const unsigned long long* cnt;
-  const unsigned long long* woff;  // exclusive scan of cnt, [n*K + 1]
   const uint32_t* index;           // may be null
   uint64_t nk;
-  unsigned long long total;
   int K;
   double alpha;
   uint64_t seed;
@@ -107,25 +114,47 @@ struct McParams {
   uint32_t src[64];
 };
 
-// One thread per walk: locate its (v, c) by binary search over the scan, then
-// a stored terminal (index prefix, speedppr.cpp:66-71) or a fresh walk.
-__global__ void k_mc_walks(const __grid_constant__ McParams P) {
-  for (unsigned long long w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < P.total;
-       w += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t lo = 0, hi = P.nk - 1;  // last i with woff[i] <= w
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi + 1) >> 1;
-      if (P.woff[mid] <= w) lo = mid; else hi = mid - 1;
+// One walk's terminal: a stored index terminal (index prefix,
+// speedppr.cpp:66-71) or a fresh Philox walk keyed (seed, source, (k, v)).
+__device__ __forceinline__ uint32_t mc_terminal(const McParams& P, uint32_t v, int c, uint32_t kk) {
+  if (P.index && P.deg[v]) return P.index[P.off[v] + kk];
+  return philox_walk(P.off, P.nbr, v, P.src[c], P.alpha, P.seed, kk, v, P.src[c]);
+}
+
+// Entries (v, c) with W_v <= 32 walks: one thread each, its walks in a loop;
+// larger entries go to a list for k_mc_big (warp per entry).
+__global__ void k_mc_entries(const __grid_constant__ McParams P, uint64_t* big,
+                             unsigned long long* nbig) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < P.nk;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long wc = P.cnt[i];
+    if (!wc) continue;
+    if (wc > 32) {
+      big[atomicAdd(nbig, 1ull)] = i;
+      continue;
     }
-    const uint64_t i = lo;
-    const uint32_t kk = (uint32_t)(w - P.woff[i]);
     const uint32_t v = (uint32_t)(i / P.K);
     const int c = (int)(i % P.K);
-    const double contribution = P.res[i] / (double)P.cnt[i];
-    uint32_t t;
-    if (P.index && P.deg[v]) t = P.index[P.off[v] + kk];
-    else t = philox_walk(P.off, P.nbr, v, P.src[c], P.alpha, P.seed, kk, v, P.src[c]);
-    atomicAdd(P.est + (uint64_t)t * P.K + c, contribution);
+    const double contribution = P.res[i] / (double)wc;  // speedppr.cpp:41
+    for (uint32_t kk = 0; kk < (uint32_t)wc; ++kk)
+      atomicAdd(P.est + (uint64_t)mc_terminal(P, v, c, kk) * P.K + c, contribution);
+  }
+}
+
+__global__ void k_mc_big(const __grid_constant__ McParams P, const uint64_t* big,
+                         const unsigned long long* nbig_p) {
+  const unsigned long long nbig = *nbig_p;
+  const int lane = threadIdx.x & 31;
+  const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = w0; w < nbig; w += nw) {
+    const uint64_t i = big[w];
+    const uint32_t v = (uint32_t)(i / P.K);
+    const int c = (int)(i % P.K);
+    const unsigned long long wc = P.cnt[i];
+    const double contribution = P.res[i] / (double)wc;
+    for (unsigned long long kk = lane; kk < wc; kk += 32)
+      atomicAdd(P.est + (uint64_t)mc_terminal(P, v, c, (uint32_t)kk) * P.K + c, contribution);
   }
 }
 
@@ -270,26 +299,15 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
     speedppr_push_stage(g, sources + b0, kb, alpha, lambda, r_max, cs, call, &pv);
     const int K = pv.K;
     const uint64_t nk = n * (uint64_t)K;
-    DevBuf<unsigned long long> cnt(nk), woff(nk + 1);
+    DevBuf<unsigned long long> cnt(nk), colw(64 + 1);
+    DevBuf<uint64_t> big(nk);
     DevBuf<double> est(nk), outb(out_on_device ? 0 : n * kb);
     DevBuf<unsigned> bad(1);
+    unsigned long long* nbig = colw.get() + 64;
     PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
+    PPRG_CUDA(cudaMemsetAsync(colw.get(), 0, 8 * 65, st));
     k_mc_counts<<<gridn(nk), 256, 0, st>>>(pv.res, g.deg.get(), n, K, kb, (double)W, cnt.get(),
-                                          bad.get());
-    unsigned long long* cp = cnt.get();
-    unsigned long long* wp = woff.get();
-    cub_run([&](void* t, size_t& bytes) {
-      return cub::DeviceScan::ExclusiveSum(t, bytes, cp, wp, (int64_t)nk, st);
-    });
-    // total = woff[nk-1] + cnt[nk-1]
-    unsigned long long last_off = 0, last_cnt = 0;
-    unsigned hb = 0;
-    PPRG_CUDA(cudaMemcpyAsync(&last_off, wp + nk - 1, 8, cudaMemcpyDeviceToHost, st));
-    PPRG_CUDA(cudaMemcpyAsync(&last_cnt, cp + nk - 1, 8, cudaMemcpyDeviceToHost, st));
-    PPRG_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, st));
-    PPRG_CUDA(cudaStreamSynchronize(st));
-    if (hb) fail(EINTERNAL, "monte carlo: residue exceeds degree/W, state not refined");
-    const unsigned long long total = last_off + last_cnt;
+                                          bad.get(), colw.get());
     k_est_init<<<gridn(nk), 256, 0, st>>>(pv.x, nk, alpha, est.get());
     McParams P;
     std::memset(&P, 0, sizeof P);
@@ -298,32 +316,30 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
     P.deg = g.deg.get();
     P.res = pv.res;
     P.cnt = cnt.get();
-    P.woff = woff.get();
     P.index = idx ? idx->endpoints.get() : nullptr;
     P.nk = nk;
-    P.total = total;
     P.K = K;
     P.alpha = alpha;
     P.seed = seed;
     P.est = est.get();
     for (int c = 0; c < K; ++c) P.src[c] = pv.src[c];
-    if (total) k_mc_walks<<<gridn(total), 256, 0, st>>>(P);
+    // Entries run thread-per-(v, c); entries over 32 walks are queued and run
+    // warp-per-entry by a fixed-size grid that reads the queue length on device.
+    k_mc_entries<<<gridn(nk), 256, 0, st>>>(P, big.get(), nbig);
+    k_mc_big<<<g.sm_count * 8, 256, 0, st>>>(P, big.get(), nbig);
     PPRG_CUDA(cudaGetLastError());
     double* dst = est_out ? (out_on_device ? est_out + (uint64_t)b0 * n : outb.get()) : nullptr;
     if (dst) k_unpack_est<<<gridn(nk), 256, 0, st>>>(est.get(), n, K, kb, dst);
     if (est_out && !out_on_device)
       PPRG_CUDA(cudaMemcpyAsync(est_out + (uint64_t)b0 * n, outb.get(), 8 * n * kb, kind, st));
-    // per-column walk totals
-    std::vector<unsigned long long> hoff(K + 1);
+    unsigned long long hw[65];
+    unsigned hb = 0;
+    PPRG_CUDA(cudaMemcpyAsync(hw, colw.get(), 8 * 65, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, st));
     PPRG_CUDA(cudaStreamSynchronize(st));
-    call->kernel_launches += 4;
-    for (uint32_t c = 0; c < kb; ++c) cs[c].walks = 0;
-    {
-      // walks per column: sum of counts with i % K == c (small host pass over a reduced copy)
-      std::vector<unsigned long long> hc(nk);
-      PPRG_CUDA(cudaMemcpy(hc.data(), cp, 8 * nk, cudaMemcpyDeviceToHost));
-      for (uint64_t i = 0; i < nk; ++i) cs[i % K].walks += (i % K) < kb ? hc[i] : 0;
-    }
+    if (hb) fail(EINTERNAL, "monte carlo: residue exceeds degree/W, state not refined");
+    call->kernel_launches += 5;
+    for (uint32_t c = 0; c < kb; ++c) cs[c].walks = hw[c];
     for (uint32_t c = 0; c < kb; ++c) cs[c].r_sum = 0;  // speedppr.cpp:47
   }
   PPRG_CUDA(cudaEventRecord(e1, st));

@@ -324,3 +324,24 @@ def test_speedppr_unbiased(P, oracle):
                      for s in range(300)])
     se = runs.std(axis=0, ddof=1) / math.sqrt(len(runs))
     assert np.all(np.abs(runs.mean(axis=0) - truth) <= 4 * se + 1e-12)
+
+
+@pytest.mark.parametrize("use_index", [False, True])
+def test_speedppr_batch_push_branch(P, oracle, use_index):
+    """64 sources as one column block on a skewed graph where W > m_eff (push +
+    refine + MC branch, speedppr.cpp:103-110): every query sums to 1 and at
+    most one in 20 has a node with pi >= 1/n off by more than epsilon."""
+    g = P.generate_rmat(11, 8, 21)
+    n = g.n()
+    c = gcsr(g)
+    src = P.sample_sources(np.diff(g.out_offsets()), 64, 21)
+    idx = P.build_index(g, 0.2, 8) if use_index else None
+    outs, _ = P.speedppr_batch(g, src, P.QueryConfig(epsilon=0.5, seed=5), idx)
+    assert P.compute_walk_budget(n, 0.5, 1.0 / n) > g.m() + len(g.dead_ends())
+    clean = 0
+    for q in range(0, 64, 4):
+        est = outs[q].estimates
+        assert abs(est.sum() - 1.0) < 1e-9 and outs[q].pushes > 0 and outs[q].walks > 0
+        truth = oracle.exact_ppr(c, int(src[q]), 0.2)
+        clean += oracle.compare_to_truth(est, truth, 1.0 / n, 0.5).violations == 0
+    assert clean >= 15
