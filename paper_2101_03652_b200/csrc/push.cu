@@ -103,6 +103,7 @@ struct SweepParams {
   double* out_residue;
   double* res_inter;           // finalize: explicit residues back into [u*K + c] (SpeedPPR)
   uint32_t max_sweeps;
+  unsigned long long handoff_np;  // refine epoch: hand off to the frontier below this many edge pushes
   uint32_t src[KMAX];
   int final_pull[KMAX];        // finalize: 1 = residue from pull form
   double thr[EMAX];            // epoch r_max (lambda is per call, so shared by columns)
@@ -712,6 +713,7 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
         if (MODE == M_POWERPUSH) {
           cs[cc].r_sum -= P.alpha * pushed;
           if (np == 0) cs[cc].epoch += 1;  // fixpoint: nothing active at this threshold
+          else if (cs[cc].epoch == P.E - 1 && np < P.handoff_np) cs[cc].epoch += 1;  // refine tail
           while (cs[cc].epoch < P.E && !(cs[cc].r_sum > P.lam[cs[cc].epoch])) cs[cc].epoch += 1;
           if (cs[cc].epoch >= P.E) cs[cc].done = 1;
         } else {
@@ -1461,6 +1463,11 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   if (refine_rmax > 0.0) {
     P.lam[E] = -1.0;
     P.thr[E] = refine_rmax;
+    // a sweep costs a pass over every in-edge; once the refine tail pushes
+    // fewer than m_eff/64 edges per sweep the frontier kernels finish it
+    double f = 1.0 / 64;
+    if (const char* e = std::getenv("PPRG_REFINE_HANDOFF")) f = std::atof(e);
+    P.handoff_np = (unsigned long long)(f * m_eff);
   }
   for (int c = 0; c < b.K; ++c) {
     P.init[c].r_sum = b.r_sum[c];
@@ -1754,6 +1761,16 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
   power_push_block(b, lambda, 8, -1, call, r_max);
   Outputs none;
   finalize(b, none, true, call);
+  // the tail: every node still above deg_eff * r_max in id order, drained
+  std::vector<int> state(KMAX, 2);
+  for (uint32_t c = 0; c < k; ++c) state[c] = 0;
+  EventTimer tl(g.stream);
+  tl.start();
+  drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);
+  std::vector<int> all(KMAX, 1);
+  exact_rsum(b, all);
+  tl.stop();
+  call->local_ms += tl.ms();
   for (uint32_t c = 0; c < k; ++c) {
     cols[c].r_sum = b.r_sum[c];
     cols[c].pushes = b.pushes[c];
