@@ -317,7 +317,7 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(P, g, int(os.environ.get("PPRG_COLUMNS", "0")) or None),
+            "config": workload_config(P, g, g.block_columns(k)),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 4 * k,
                     "d2h_bytes_per_step": 16 * k * n},
             "gpu_launches": launches,

@@ -118,6 +118,10 @@ int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double a
                     double* reserve_out, double* residue_out, uint32_t flags,
                     pprg_query_stats* qstats, pprg_call_stats* cstats, double* epoch_r_max_out);
 
+/* Columns (sources) per device block for a k-source call: the batch width the
+ * engines use (a power of two, padding columns inert). Not in the reference. */
+int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out);
+
 /* ---- SpeedPPR (speedppr.hpp, walk_index.hpp) ------------------------------- */
 /* compute_walk_budget(n, eps, mu) speedppr.hpp:16-17 */
 int pprg_walk_budget(uint64_t n, double epsilon, double mu, uint64_t* out);

@@ -10,7 +10,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-lib_path = os.path.join(_HERE, "lib", "libpprg.so")
+lib_path = os.path.abspath(os.environ.get("PPRG_LIB") or "") if os.environ.get("PPRG_LIB") else os.path.join(_HERE, "lib", "libpprg.so")
 
 KINDEX_TAG = 0xFFFFFFFF
 RNG_ID_PHILOX = 2
@@ -102,6 +102,7 @@ def load_library(path: str = lib_path):
     L.pprg_power_push.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
                                   C.c_int64, vp, vp, C.c_uint32, vp, vp, vp]
     L.pprg_walk_budget.argtypes = [C.c_uint64, C.c_double, C.c_double, u64p]
+    L.pprg_block_columns.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint32)]
     L.pprg_index_build.argtypes = [vp, C.c_double, C.c_uint64, C.POINTER(vp)]
     L.pprg_index_from_host.argtypes = [vp, C.c_double, C.c_uint64, vp, C.POINTER(vp)]
     L.pprg_index_export.argtypes = [vp, vp]
@@ -262,6 +263,12 @@ class Graph:
     def dead_ends(self) -> np.ndarray:
         self._export()
         return self._dead
+
+    def block_columns(self, k: int) -> int:
+        """Columns per device block the engines use for a k-source call."""
+        out = C.c_uint32()
+        _check(load_library().pprg_block_columns(self.handle, k, C.byref(out)))
+        return out.value
 
     def out_degree(self, v: int) -> int:
         off = self.out_offsets()

@@ -273,6 +273,13 @@ int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double a
   return rc;
 }
 
+int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out) {
+  return guard([&] {
+    require(g != nullptr && out != nullptr, "block columns: null argument");
+    *out = pprg::block_width(g->g->n, k);
+  });
+}
+
 int pprg_walk_budget(uint64_t n, double epsilon, double mu, uint64_t* out) {
   return guard([&] {
     // walk_budget_real, speedppr.cpp:8-14 (same checks)

@@ -134,6 +134,68 @@ struct DevBuf {
 
 #if defined(__CUDACC__)
 __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+
+// L2 eviction-priority hints for the sweep streams. Per sweep the in-edge ids,
+// row data and the state x are touched once (streams, > L2), while the gathered
+// operand y is re-read once per out-edge of its node; marking the streams
+// evict-first keeps L2 for y. PPRG_HINTS: 0 = none, 1 = streams evict-first,
+// 2 = 1 + y gathers evict-last.
+#ifndef PPRG_HINTS
+#define PPRG_HINTS 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_evict_last() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) {
+#if PPRG_HINTS >= 1
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+#else
+  return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double ld_state(const double* p) {  // coherent (L2), streamed
+#if PPRG_HINTS >= 1
+  double v;
+  asm volatile("ld.global.cg.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_first()));
+  return v;
+#else
+  return __ldcg(p);
+#endif
+}
+__device__ __forceinline__ void st_state(double* p, double v) {
+#if PPRG_HINTS >= 1
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(l2_evict_first()) : "memory");
+#else
+  *p = v;
+#endif
+}
+__device__ __forceinline__ double2 ld_gather2(const double* p) {
+#if PPRG_HINTS >= 2
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(l2_evict_last()));
+  return v;
+#else
+  return *reinterpret_cast<const double2*>(p);
+#endif
+}
+__device__ __forceinline__ double ld_gather(const double* p) {
+#if PPRG_HINTS >= 2
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_last()));
+  return v;
+#else
+  return *p;
+#endif
+}
 __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");

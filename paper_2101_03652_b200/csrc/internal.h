@@ -126,6 +126,7 @@ struct PushView {
   const uint32_t* d_src = nullptr;
   std::vector<uint32_t> src;
 };
+uint32_t block_width(uint64_t n, uint32_t k);  // padded columns per block for k queries
 void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double alpha,
                          double lambda, double r_max, ColumnStats* cols, CallStats* call,
                          PushView* view);

@@ -160,7 +160,7 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
     const double inflow = acc + (is_src ? 1.0 + cs[c].D : 0.0);
     const double r = inflow - xo;
     if (r > (dg ? (double)dg : 1.0) * thr_cur[c]) {
-      P.x[ix] = inflow;
+      st_state(P.x + ix, inflow);
       if (dg) P.y[0][ix] = oma * inflow * inv;
       a.push += r;
       a.np += dg ? dg : 1;
@@ -392,45 +392,55 @@ constexpr uint32_t RMAX_W = 256;
 
 // Sum of y over the in-edges [b, e) of one row for my columns, by one warp.
 // Lanes = ES edge slots x KC column lanes (x CPL contiguous columns). The ids
-// of 32 consecutive edges are loaded once, coalesced, and broadcast by shuffle.
+// of 32 consecutive edges are loaded once, coalesced, and broadcast by shuffle;
+// the gathers are then issued G at a time into registers before any add, so
+// each warp keeps G row-loads in flight (tail slots re-load the last edge and
+// are masked out of the sum).
+#ifndef PPRG_G
+#define PPRG_G 8
+#endif
 template <int K>
 __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double* yg, uint64_t b,
                                              uint64_t e, double (&s)[(K < 32 ? 1 : K / 32)]) {
   constexpr int KC = K < 32 ? K : 32;
   constexpr int CPL = K / KC;
   constexpr int ES = 32 / KC;
+  constexpr int G = PPRG_G;
   const int lane = threadIdx.x & 31, es = lane / KC, kc = lane % KC;
-  double acc[CPL][4];
+  const double* ybase = yg + kc * CPL;
+  double acc[CPL][2];
 #pragma unroll
-  for (int q = 0; q < CPL; ++q)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc[q][k] = 0.0;
+  for (int q = 0; q < CPL; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (uint64_t p0 = b; p0 < e; p0 += 32) {
     const uint64_t pl = p0 + lane;
-    const uint32_t myid = pl < e ? __ldg(P.in_nbr + pl) : 0xFFFFFFFFu;
+    const uint32_t myid = pl < e ? ld_stream(P.in_nbr + pl) : 0u;
     const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
-#pragma unroll 2
-    for (int j0 = 0; j0 < 32; j0 += 4 * ES) {
+    for (int j0 = 0; j0 < cnt; j0 += G * ES) {
+      double v[G][CPL];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int j = j0 + k * ES + es;
-        const uint32_t id = __shfl_sync(0xffffffffu, myid, j & 31);
-        if (j < cnt) {
-          const double* src = yg + (uint64_t)id * K + kc * CPL;
-          if constexpr (CPL == 2) {
-            const double2 v2 = *reinterpret_cast<const double2*>(src);
-            acc[0][k] += v2.x;
-            acc[1][k] += v2.y;
-          } else {
-            acc[0][k] += *src;
-          }
+      for (int g = 0; g < G; ++g) {
+        const int j = j0 + g * ES + es;
+        const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
+        const double* src = ybase + (uint64_t)id * K;
+        if constexpr (CPL == 2) {
+          const double2 v2 = ld_gather2(src);
+          v[g][0] = v2.x;
+          v[g][1] = v2.y;
+        } else {
+          v[g][0] = ld_gather(src);
         }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const bool ok = j0 + g * ES + es < cnt;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) acc[q][g & 1] += ok ? v[g][q] : 0.0;
       }
     }
   }
 #pragma unroll
   for (int q = 0; q < CPL; ++q) {
-    s[q] = (acc[q][0] + acc[q][1]) + (acc[q][2] + acc[q][3]);
+    s[q] = acc[q][0] + acc[q][1];
 #pragma unroll
     for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
   }
@@ -520,7 +530,7 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {  // issued early; lands during the edge loop
       const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
-      xo[q] = es0 ? __ldcg(P.x + ix) : 0.0;
+      xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
       rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
     }
     warp_row_sum<K>(P, yg, b, e, s);
@@ -581,7 +591,7 @@ __device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* c
 
 template <int K, int MODE>
 #ifndef PPRG_MINB
-#define PPRG_MINB 10
+#define PPRG_MINB 8
 #endif
 __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant__ SweepParams P) {
   using TC = Tile<K>;
@@ -1622,9 +1632,9 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
 
 }  // namespace
 
-// Columns per block: the gathered operand y (n*K doubles) and the state x
-// should stay L2-resident (126 MB), so K shrinks as n grows. PPRG_COLUMNS
-// overrides (power of two <= 64).
+// Columns per block: wider blocks amortise the in-edge stream over more
+// queries; the per-block state (x, y, residues: n*K doubles each) is capped
+// at 1.6 GB per array, so K shrinks as n grows. PPRG_COLUMNS overrides.
 uint32_t block_columns(uint64_t n, uint32_t k) {
   if (const char* e = std::getenv("PPRG_COLUMNS")) {
     const long v = std::strtol(e, nullptr, 10);
@@ -1634,6 +1644,8 @@ uint32_t block_columns(uint64_t n, uint32_t k) {
   while (K > 1 && 8.0 * (double)n * K > 1.6e9) K >>= 1;  // x, y, res, ... are n*K doubles each
   return K < k ? K : (k ? k : 1);
 }
+
+uint32_t block_width(uint64_t n, uint32_t k) { return (uint32_t)round_k(block_columns(n, k)); }
 
 void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, double alpha,
                      double lambda, uint32_t epoch_num, int64_t scan_threshold, double r_max_fifo,
