@@ -40,6 +40,7 @@ extern "C" {
 
 typedef struct pprg_graph pprg_graph;
 typedef struct pprg_index pprg_index;
+typedef struct pprg_part pprg_part;
 
 /* Per-query statistics (PPRVector fields, types.hpp:57-65, plus device counters). */
 typedef struct {
@@ -117,6 +118,52 @@ int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double a
                     double lambda, uint32_t epoch_num, int64_t scan_threshold,
                     double* reserve_out, double* residue_out, uint32_t flags,
                     pprg_query_stats* qstats, pprg_call_stats* cstats, double* epoch_r_max_out);
+
+/* ---- vertex-partitioned power_push (BASELINE configs[4]) ------
+ * One session per (part, source block) on a graph resident on this part's
+ * GPU. Part p of nparts owns the pull-sweep rows [node_lo, node_hi), cut at
+ * row-aligned tiles so every part holds ~m/nparts in-edges (every part
+ * computes the same cut). The caller moves data between parts:
+ *   begin -> all-reduce(partial_sums, 2*64 doubles) -> start
+ *   while need_sweeps: all-gather y row slices [lo*C, hi*C) (C = columns)
+ *                      -> sweep -> all-reduce(counters, 5*C doubles, device)
+ *                      -> advance(summed counters, host) until done
+ *   finish -> all-reduce(residue_sums) = exact r_sum per source.
+ * The epoch rule is power_push's (push.cpp:168-197): r_sum = 1 - alpha*sum(x)
+ * and the push counters come from every part, so all parts take identical
+ * decisions. finish writes this part's rows [node_lo, node_hi) of the
+ * query-major outputs (k x n) and leaves other rows untouched. */
+/* Per-column global-phase state and the host epoch rule the sessions use
+ * (push.cpp:168-197 restated over summed counters; host-only, no GPU). */
+typedef struct {
+  double r_sum;
+  double D;        /* (1 - alpha) * sum of x over dead ends */
+  int32_t epoch;
+  int32_t done;
+  uint32_t sweeps;
+  uint64_t pushes;
+} pprg_column_state;
+int pprg_epoch_init(pprg_column_state* cols, uint32_t columns, const double* sum_x,
+                    const double* sum_dead_x, const double* epoch_lambda, uint32_t epoch_num,
+                    double alpha, int* need_sweeps);
+/* summed = [pushed mass | edge pushes | node pushes | dead-end mass | pushed out-degree] x columns */
+int pprg_epoch_advance(pprg_column_state* cols, uint32_t columns, const double* summed,
+                       const double* epoch_lambda, uint32_t epoch_num, double alpha, int* done);
+
+int pprg_part_begin(pprg_graph* g, uint32_t nparts, uint32_t part, const uint32_t* sources,
+                    uint32_t k, double alpha, double lambda, uint32_t epoch_num,
+                    int64_t scan_threshold, double* partial_sums, uint64_t* node_lo,
+                    uint64_t* node_hi, pprg_part** out);
+int pprg_part_start(pprg_part* p, const double* summed, int* need_sweeps);
+/* device pointers: y [n * columns] (interleaved u*columns + c) and counters [5 * columns] */
+int pprg_part_buffers(pprg_part* p, double** y, uint32_t* columns, double** counters);
+/* one global sweep over this part's rows; local_counters (host, optional) gets a copy */
+int pprg_part_sweep(pprg_part* p, double* local_counters);
+int pprg_part_advance(pprg_part* p, const double* summed, int* done);
+int pprg_part_finish(pprg_part* p, double* reserve_out, double* residue_out, uint32_t flags,
+                     double* residue_sums);
+int pprg_part_stats(const pprg_part* p, pprg_query_stats* qstats, pprg_call_stats* cstats);
+void pprg_part_destroy(pprg_part* p);
 
 /* Columns (sources) per device block for a k-source call: the batch width the
  * engines use (a power of two, padding columns inert). Not in the reference. */

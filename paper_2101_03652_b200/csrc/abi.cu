@@ -11,6 +11,11 @@
 struct pprg_graph {
   std::unique_ptr<pprg::Graph> g;
 };
+struct pprg_part {
+  pprg::PartSession* s = nullptr;
+  pprg_graph* owner = nullptr;
+  uint32_t k = 0;
+};
 struct pprg_index {
   std::unique_ptr<pprg::WalkIndex> w;
   pprg_graph* owner;
@@ -271,6 +276,102 @@ int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double a
       epoch_r_max_out[e - 1] = std::pow(lambda, static_cast<double>(e) / epoch_num) / m_eff;
   }
   return rc;
+}
+
+static_assert(sizeof(pprg_column_state) == sizeof(pprg::ColInit), "column state layout");
+
+int pprg_epoch_init(pprg_column_state* cols, uint32_t columns, const double* sum_x,
+                    const double* sum_dead_x, const double* epoch_lambda, uint32_t epoch_num,
+                    double alpha, int* need_sweeps) {
+  return guard([&] {
+    require(cols && sum_x && sum_dead_x && epoch_lambda && need_sweeps, "epoch: null argument");
+    require(columns >= 1 && columns <= 64 && epoch_num >= 1 && epoch_num <= 64, "epoch: bad sizes");
+    *need_sweeps = pprg::epoch_init(reinterpret_cast<pprg::ColInit*>(cols), (int)columns, sum_x,
+                                    sum_dead_x, epoch_lambda, epoch_num, alpha);
+  });
+}
+
+int pprg_epoch_advance(pprg_column_state* cols, uint32_t columns, const double* summed,
+                       const double* epoch_lambda, uint32_t epoch_num, double alpha, int* done) {
+  return guard([&] {
+    require(cols && summed && epoch_lambda && done, "epoch: null argument");
+    require(columns >= 1 && columns <= 64 && epoch_num >= 1 && epoch_num <= 64, "epoch: bad sizes");
+    *done = pprg::epoch_advance(reinterpret_cast<pprg::ColInit*>(cols), (int)columns, summed,
+                                epoch_lambda, epoch_num, alpha);
+  });
+}
+
+int pprg_part_begin(pprg_graph* g, uint32_t nparts, uint32_t part, const uint32_t* sources,
+                    uint32_t k, double alpha, double lambda, uint32_t epoch_num,
+                    int64_t scan_threshold, double* partial_sums, uint64_t* node_lo,
+                    uint64_t* node_hi, pprg_part** out) {
+  return guard([&] {
+    require(g && sources && partial_sums && node_lo && node_hi && out, "partition: null argument");
+    auto h = new pprg_part;
+    try {
+      h->s = pprg::part_begin(*g->g, nparts, part, sources, k, alpha, lambda, epoch_num,
+                              scan_threshold, partial_sums, node_lo, node_hi);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    h->owner = g;
+    h->k = k;
+    *out = h;
+  });
+}
+
+int pprg_part_start(pprg_part* p, const double* summed, int* need_sweeps) {
+  return guard([&] {
+    require(p && summed && need_sweeps, "partition: null argument");
+    *need_sweeps = pprg::part_start(p->s, summed) ? 1 : 0;
+  });
+}
+
+int pprg_part_buffers(pprg_part* p, double** y, uint32_t* columns, double** counters) {
+  return guard([&] {
+    require(p && y && columns && counters, "partition: null argument");
+    *y = pprg::part_y(p->s, columns);
+    *counters = pprg::part_counters(p->s);
+  });
+}
+
+int pprg_part_sweep(pprg_part* p, double* local_counters) {
+  return guard([&] {
+    require(p != nullptr, "partition: null argument");
+    pprg::part_sweep(p->s, local_counters);
+  });
+}
+
+int pprg_part_advance(pprg_part* p, const double* summed, int* done) {
+  return guard([&] {
+    require(p && summed && done, "partition: null argument");
+    *done = pprg::part_advance(p->s, summed) ? 1 : 0;
+  });
+}
+
+int pprg_part_finish(pprg_part* p, double* reserve_out, double* residue_out, uint32_t flags,
+                     double* residue_sums) {
+  return guard([&] {
+    require(p && residue_sums, "partition: null argument");
+    pprg::part_finish(p->s, reserve_out, residue_out, (flags & PPRG_OUT_DEVICE) != 0, residue_sums);
+  });
+}
+
+int pprg_part_stats(const pprg_part* p, pprg_query_stats* q, pprg_call_stats* c) {
+  return guard([&] {
+    require(p != nullptr, "partition: null argument");
+    std::vector<pprg::ColumnStats> cs(p->k);
+    pprg::CallStats call;
+    pprg::part_stats(p->s, cs.data(), &call);
+    fill_stats(cs, call, p->k, q, c);
+  });
+}
+
+void pprg_part_destroy(pprg_part* p) {
+  if (!p) return;
+  pprg::part_destroy(p->s);
+  delete p;
 }
 
 int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out) {

@@ -513,6 +513,7 @@ const Graph::Plan& Graph::tile_plan(uint32_t T, uint32_t R) {
     PPRG_CUDA(cudaMemcpyAsync(pl.tiles.get(), tl.data(), sizeof(TileDesc) * tl.size(),
                               cudaMemcpyHostToDevice, stream));
   PPRG_CUDA(cudaStreamSynchronize(stream));
+  pl.host = std::move(tl);
   return plans.emplace(key, std::move(pl)).first->second;
 }
 

@@ -56,6 +56,7 @@ struct Graph {
   const uint32_t* split_rows(uint32_t edges_per_tile, uint64_t* count);
   struct Plan {
     DevBuf<TileDesc> tiles;
+    std::vector<TileDesc> host;  // same list (partition cuts)
     uint64_t ntiles = 0, nhubs = 0;
   };
   std::map<uint64_t, Plan> plans;  // key: (T << 32) | RMAX
@@ -130,6 +131,34 @@ uint32_t block_width(uint64_t n, uint32_t k);  // padded columns per block for k
 void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double alpha,
                          double lambda, double r_max, ColumnStats* cols, CallStats* call,
                          PushView* view);
+
+// Per-column global-phase state (layout = pprg_column_state).
+struct ColInit {
+  double r_sum;
+  double D;
+  int epoch;
+  int done;
+  uint32_t sweeps;
+  uint64_t pushes;
+};
+bool epoch_init(ColInit* st, int K, const double* sum_x, const double* sum_dead_x,
+                const double* lam, uint32_t E, double alpha);
+bool epoch_advance(ColInit* st, int K, const double* summed, const double* lam, uint32_t E,
+                   double alpha);
+
+// Vertex-partitioned PowerPush session (push.cu; BASELINE configs[4]).
+struct PartSession;
+PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t* sources,
+                        uint32_t k, double alpha, double lambda, uint32_t E, int64_t scan_threshold,
+                        double* partial_host, uint64_t* lo_out, uint64_t* hi_out);
+bool part_start(PartSession* s, const double* summed);
+void part_sweep(PartSession* s, double* local_host);
+bool part_advance(PartSession* s, const double* summed);
+void part_finish(PartSession* s, double* reserve, double* residue, bool on_device, double* rpart);
+void part_stats(const PartSession* s, ColumnStats* cols, CallStats* call);
+double* part_y(PartSession* s, uint32_t* K);
+double* part_counters(PartSession* s);
+void part_destroy(PartSession* s);
 
 struct WalkIndex {
   int device = 0;

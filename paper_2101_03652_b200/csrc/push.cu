@@ -61,15 +61,6 @@ struct SweepCtl {
   unsigned total_sweeps;
 };
 
-struct ColInit {
-  double r_sum;
-  double D;
-  int epoch;
-  int done;
-  uint32_t sweeps;
-  uint64_t pushes;
-};
-
 struct SweepParams {
   uint64_t n, m;
   const uint64_t* in_off;      // compacted transpose rows (in-degree > 0)
@@ -103,6 +94,7 @@ struct SweepParams {
   double* out_residue;
   double* res_inter;           // finalize: explicit residues back into [u*K + c] (SpeedPPR)
   uint32_t max_sweeps;
+  uint64_t own_lo, own_hi;      // node range this launch owns (vertex partition; else [0, n))
   unsigned long long handoff_np;  // refine epoch: hand off to the frontier below this many edge pushes
   uint32_t src[KMAX];
   int final_pull[KMAX];        // finalize: 1 = residue from pull form
@@ -582,6 +574,7 @@ __device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* c
   const int tid = threadIdx.x;
   if (blockIdx.x != 0 || tid >= K) return;
   const uint32_t u = P.src[tid];
+  if (u < P.own_lo || u >= P.own_hi) return;  // another partition's row
   if (__ldg(P.in_off_full + u + 1) != __ldg(P.in_off_full + u)) return;
   const uint64_t ix = (uint64_t)u * K + tid;
   decide<K, MODE>(P, cs, thr_cur, u, tid, 0.0, __ldcg(P.x + ix),
@@ -1053,34 +1046,31 @@ struct Workspace {
 static std::mutex g_ws_mu;
 static std::map<const Graph*, std::map<int, std::unique_ptr<Workspace>>> g_ws;
 
-static Workspace& workspace(Graph& g, int K, uint64_t ntiles, uint64_t nhubs) {
-  std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto& slot = g_ws[&g][K];
-  if (!slot) {
-    slot = std::make_unique<Workspace>();
-    Workspace& w = *slot;
-    w.K = K;
-    w.n = g.n;
-    const uint64_t nk = g.n * (uint64_t)K;
-    w.x.alloc(nk);
-    w.y0.alloc(nk);
-    w.y1.alloc(nk);
-    w.r0.alloc(nk);
-    w.r1.alloc(nk);
-    w.res.alloc(nk);
-    w.stamp.alloc(nk);
-    PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, g.stream));
-    w.fa.alloc(nk + 1);
-    w.fb.alloc(nk + 1);
-    w.ctl.alloc(1);
-    w.counters.alloc(1 + 5 * KMAX);
-    w.col_stop.alloc(KMAX);
-    w.dcols.alloc(3 * KMAX);
-    w.d_src.alloc(KMAX);
-    w.heavy.alloc((g.m / HEAVY_DEG + 1) * (uint64_t)K + 1);
-    w.heavy_cnt.alloc(1);
-  }
-  Workspace& w = *slot;
+static void ws_alloc(Workspace& w, Graph& g, int K) {
+  w.K = K;
+  w.n = g.n;
+  const uint64_t nk = g.n * (uint64_t)K;
+  w.x.alloc(nk);
+  w.y0.alloc(nk);
+  w.y1.alloc(nk);
+  w.r0.alloc(nk);
+  w.r1.alloc(nk);
+  w.res.alloc(nk);
+  w.stamp.alloc(nk);
+  PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, g.stream));
+  w.fa.alloc(nk + 1);
+  w.fb.alloc(nk + 1);
+  w.ctl.alloc(1);
+  w.counters.alloc(1 + 5 * KMAX);
+  w.col_stop.alloc(KMAX);
+  w.dcols.alloc(3 * KMAX);
+  w.d_src.alloc(KMAX);
+  w.heavy.alloc((g.m / HEAVY_DEG + 1) * (uint64_t)K + 1);
+  w.heavy_cnt.alloc(1);
+}
+
+static void ws_tiles(Workspace& w, Graph& g, uint64_t ntiles, uint64_t nhubs) {
+  const int K = w.K;
   if (ntiles > w.ntiles_alloc) {
     w.carry_h.alloc((ntiles + 1) * K);
     w.carry_t.alloc((ntiles + 1) * K);
@@ -1094,7 +1084,17 @@ static Workspace& workspace(Graph& g, int K, uint64_t ntiles, uint64_t nhubs) {
     PPRG_CUDA(cudaMemsetAsync(w.hub_acc.get(), 0, 8 * (nhubs + 1) * K, g.stream));
     PPRG_CUDA(cudaMemsetAsync(w.hub_cnt.get(), 0, 4 * (nhubs + 1), g.stream));
   }
-  return w;
+}
+
+static Workspace& workspace(Graph& g, int K, uint64_t ntiles, uint64_t nhubs) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto& slot = g_ws[&g][K];
+  if (!slot) {
+    slot = std::make_unique<Workspace>();
+    ws_alloc(*slot, g, K);
+  }
+  ws_tiles(*slot, g, ntiles, nhubs);
+  return *slot;
 }
 
 // Wait for every pending host-output copy of this graph's workspaces.
@@ -1214,7 +1214,8 @@ struct Block {
         levels(KMAX, 0), D(KMAX, 0.0), scan(KMAX, 0), sweeps(KMAX, 0) {}
 };
 
-Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bool need_pull) {
+Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bool need_pull,
+                 Workspace* own = nullptr) {
   const int K = round_k(k);
   uint64_t ntiles = 0;
   const uint32_t* tl = nullptr;
@@ -1226,7 +1227,11 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
     ntiles = pl.ntiles;
     nhubs = pl.nhubs;
   }
-  Workspace& w = workspace(g, K, ntiles, nhubs);
+  if (own) {
+    if (!own->K) ws_alloc(*own, g, K);
+    ws_tiles(*own, g, ntiles, nhubs);
+  }
+  Workspace& w = own ? *own : workspace(g, K, ntiles, nhubs);
   Block b(g, w, K, k, alpha);
   b.ntiles = ntiles;
   b.tile_lo = tl;
@@ -1250,6 +1255,8 @@ SweepParams base_params(Block& b) {
   P.ctl = b.w.ctl.get();
   P.k_live = (int)b.k;
   P.max_sweeps = 200000;
+  P.own_lo = 0;
+  P.own_hi = g.n;
   for (int c = 0; c < b.K; ++c) P.src[c] = b.src[c];
   P.in_off = g.cin_off.get();
   P.crow = g.cin_row.get();
@@ -1796,6 +1803,367 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
   view->res = b.w.res.get();
   view->d_src = b.w.d_src.get();
   view->src = b.src;
+}
+
+// ---- vertex-partitioned PowerPush (BASELINE configs[4]) ------
+// Partition `part` of `nparts` owns a contiguous range of destination rows of
+// the pull sweep, cut at row-aligned tile boundaries of the tile plan so each
+// part holds ~m/nparts in-edges. Per global sweep a part pushes its own rows
+// (x, y updated in place) from the gathered operand y of the previous
+// exchange; the caller then all-gathers y's row slices and all-reduces the
+// per-column sweep counters, and every part advances the identical epoch
+// state (push.cpp:168-197) from the summed counters. Stale remote y only
+// under-estimates inflow, and r_sum = 1 - alpha * sum(x) is exact whatever
+// the staleness, so the result obeys the same lambda bounds. The local queue
+// phase (push.cpp:163-166) runs on every part over its resident full graph
+// (it is <= 0.05 m work); each part keeps only its own rows of it.
+namespace {
+
+__global__ void k_part_sums(const double* x, const uint32_t* deg, uint64_t lo, uint64_t hi, int K,
+                            double* out) {
+  __shared__ double sx[KMAX], sd[KMAX];
+  if (threadIdx.x < KMAX) sx[threadIdx.x] = sd[threadIdx.x] = 0.0;
+  __syncthreads();
+  double ax = 0.0, ad = 0.0;
+  // blockDim and the grid stride are multiples of K: a thread keeps one column
+  for (uint64_t i = lo * K + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi * K;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    ax += v;
+    if (deg[i / K] == 0) ad += v;
+  }
+  const int c = threadIdx.x % K;
+  if (ax != 0.0) atomicAdd(&sx[c], ax);
+  if (ad != 0.0) atomicAdd(&sd[c], ad);
+  __syncthreads();
+  if (threadIdx.x < K) {
+    if (sx[threadIdx.x] != 0.0) atomicAdd(out + threadIdx.x, sx[threadIdx.x]);
+    if (sd[threadIdx.x] != 0.0) atomicAdd(out + KMAX + threadIdx.x, sd[threadIdx.x]);
+  }
+}
+
+__global__ void k_part_y(const double* x, const double* inv_deg, uint64_t lo, uint64_t hi, int K,
+                         double alpha, double* y) {
+  for (uint64_t i = lo * K + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi * K;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    y[i] = (1.0 - alpha) * x[i] * inv_deg[i / K];
+}
+
+__global__ void k_pack_counters(const SweepCtl* ctl, int K, double* out) {
+  const int c = threadIdx.x;
+  if (c >= K) return;
+  out[c] = ctl->pushed[0][c];
+  out[K + c] = (double)ctl->npush[0][c];
+  out[2 * K + c] = (double)ctl->nnode[0][c];
+  out[3 * K + c] = ctl->dsum[0][c];
+  out[4 * K + c] = (double)ctl->et[0][c];
+}
+
+__global__ void k_zero_rows(double* out, uint64_t n, uint32_t k, uint64_t lo, uint64_t hi) {
+  const uint64_t w = hi - lo;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < w * k;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    out[(i / w) * n + lo + i % w] = 0.0;
+}
+
+}  // namespace
+
+// The global-phase epoch rule on the host, over summed counters. Identical to
+// the device rule of k_sweeps (M_POWERPUSH): r_sum -= alpha * pushed; an
+// epoch ends when r_sum <= its lambda, or at a fixpoint (no pushes).
+bool epoch_init(ColInit* st, int K, const double* sum_x, const double* sum_dead_x,
+                const double* lam, uint32_t E, double alpha) {
+  bool any = false;
+  for (int c = 0; c < K; ++c) {
+    ColInit& ci = st[c];
+    ci = ColInit{};
+    ci.r_sum = 1.0 - alpha * sum_x[c];  // sum_u r_u = 1 - alpha sum_u x_u
+    ci.D = (1.0 - alpha) * sum_dead_x[c];
+    int ep = 0;
+    while (ep < (int)E && !(ci.r_sum > lam[ep])) ++ep;
+    ci.epoch = ep;
+    ci.done = ep >= (int)E;
+    any |= !ci.done;
+  }
+  return any;
+}
+
+bool epoch_advance(ColInit* st, int K, const double* summed, const double* lam, uint32_t E,
+                   double alpha) {
+  bool all_done = true;
+  for (int c = 0; c < K; ++c) {
+    ColInit& ci = st[c];
+    if (!ci.done) {
+      const double pushed = summed[c];
+      const uint64_t np = (uint64_t)summed[K + c];
+      ci.sweeps += 1;
+      ci.pushes += np;
+      ci.D = summed[3 * K + c];
+      ci.r_sum -= alpha * pushed;
+      if (np == 0) ci.epoch += 1;
+      while (ci.epoch < (int)E && !(ci.r_sum > lam[ci.epoch])) ci.epoch += 1;
+      if (ci.epoch >= (int)E) ci.done = 1;
+    }
+    all_done &= ci.done != 0;
+  }
+  return all_done;
+}
+
+struct PartSession {
+  Graph* g = nullptr;
+  Workspace w;
+  std::unique_ptr<Block> b;
+  uint32_t nparts = 1, part = 0, E = 8;
+  uint64_t t0 = 0, t1 = 0, lo = 0, hi = 0;
+  const TileDesc* desc = nullptr;
+  double lambda = 0;
+  std::vector<double> lam, thr;
+  std::vector<ColInit> st;
+  std::vector<int> used_scan;
+  DevBuf<double> sums, counters;
+  CallStats call;
+  uint64_t own_alg_bytes = 0;
+  uint32_t sweeps = 0;
+};
+
+PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t* sources,
+                        uint32_t k, double alpha, double lambda, uint32_t E, int64_t scan_threshold,
+                        double* partial_host, uint64_t* lo_out, uint64_t* hi_out) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (nparts < 1 || part >= nparts) fail(EINVAL_, "partition: part must be < nparts");
+  if (k < 1 || k > KMAX) fail(EINVAL_, "partition: 1..64 sources per session");
+  if (!(lambda > 0.0 && lambda <= 1.0)) fail(EINVAL_, "power_push: lambda must be in (0,1]");
+  if (!(alpha > 0.0 && alpha < 1.0)) fail(EINVAL_, "alpha must be in (0,1)");
+  if (E < 1 || E > EMAX) fail(EINVAL_, "epoch_num must be in 1..64");
+  for (uint32_t c = 0; c < k; ++c)
+    if (sources[c] >= g.n) fail(EINVAL_, "source out of range");
+  g.ensure_transpose();
+  auto s = std::make_unique<PartSession>();
+  s->g = &g;
+  s->nparts = nparts;
+  s->part = part;
+  s->E = E;
+  s->lambda = lambda;
+  s->b = std::make_unique<Block>(make_block(g, sources, k, alpha, true, &s->w));
+  Block& b = *s->b;
+  const int K = b.K;
+  // ---- the cut: row-start tiles, balanced on in-edges ------------------------
+  const Graph::Plan& pl = g.tile_plan(tile_edges(K), tile_rmax(K));
+  const std::vector<TileDesc>& tl = pl.host;
+  uint64_t total = 0;
+  for (const TileDesc& t : tl) total += t.ne;
+  std::vector<uint64_t> cut(nparts + 1, 0);
+  cut[nparts] = tl.size();
+  {
+    uint64_t acc = 0, t = 0;
+    for (uint32_t p = 1; p < nparts; ++p) {
+      const double target = (double)total * p / nparts;
+      while (t < tl.size() && ((double)acc < target || tl[t].piece != 0)) acc += tl[t++].ne;
+      cut[p] = t;
+    }
+  }
+  auto node_of_tile = [&](uint64_t t) -> uint64_t {
+    if (t >= tl.size()) return g.n;
+    uint32_t u = 0;
+    PPRG_CUDA(cudaMemcpy(&u, g.cin_row.get() + tl[t].r0, 4, cudaMemcpyDeviceToHost));
+    return u;
+  };
+  s->t0 = cut[part];
+  s->t1 = cut[part + 1];
+  s->lo = part == 0 ? 0 : node_of_tile(s->t0);
+  s->hi = part + 1 == nparts ? g.n : node_of_tile(s->t1);
+  if (s->hi < s->lo) s->hi = s->lo;
+  s->desc = pl.tiles.get() + s->t0;
+  // ---- local phase (push.cpp:163-166) on the full graph -----------------------
+  cudaStream_t st = g.stream;
+  const uint64_t nk = g.n * (uint64_t)K;
+  PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, st));
+  PPRG_CUDA(cudaMemsetAsync(b.w.res.get(), 0, 8 * nk, st));
+  k_seed<<<1, KMAX, 0, st>>>(b.w.res.get(), b.w.d_src.get(), K, 1.0);
+  const double r_max = lambda / (double)g.m_eff();
+  const uint64_t limit = scan_threshold < 0 ? g.n / 4 : (uint64_t)scan_threshold;
+  std::vector<int> state(KMAX, 2);
+  for (uint32_t c = 0; c < k; ++c) state[c] = 0;
+  EventTimer tl_(st);
+  tl_.start();
+  drain_levels(b, r_max, lambda, limit, false, state, &s->call);
+  tl_.stop();
+  s->call.local_ms += tl_.ms();
+  // ---- this part's share of sum(x) and sum over dead ends -------------------
+  s->sums.alloc(2 * KMAX);
+  s->counters.alloc(5 * KMAX);
+  PPRG_CUDA(cudaMemsetAsync(s->sums.get(), 0, 16 * KMAX, st));
+  if (s->hi > s->lo)
+    k_part_sums<<<grid_for((s->hi - s->lo) * K), 256, 0, st>>>(b.w.x.get(), g.deg.get(), s->lo,
+                                                               s->hi, K, s->sums.get());
+  PPRG_CUDA(cudaGetLastError());
+  PPRG_CUDA(cudaMemcpyAsync(partial_host, s->sums.get(), 16 * KMAX, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  s->call.kernel_launches += 2;
+  *lo_out = s->lo;
+  *hi_out = s->hi;
+  return s.release();
+}
+
+bool part_start(PartSession* s, const double* summed) {
+  Graph& g = *s->g;
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  Block& b = *s->b;
+  const int K = b.K;
+  const double m_eff = (double)g.m_eff();
+  s->lam.assign(EMAX, 0.0);
+  s->thr.assign(EMAX, 0.0);
+  for (uint32_t e = 0; e < s->E; ++e) {
+    s->lam[e] = std::pow(s->lambda, static_cast<double>(e + 1) / s->E);  // push.cpp:176-178
+    s->thr[e] = s->lam[e] / m_eff;
+  }
+  s->st.assign(KMAX, ColInit{});
+  s->used_scan.assign(KMAX, 0);
+  std::vector<double> sx(summed, summed + K), sd(summed + KMAX, summed + KMAX + K);
+  const bool any = epoch_init(s->st.data(), K, sx.data(), sd.data(), s->lam.data(), s->E, b.alpha);
+  for (int c = 0; c < K; ++c) s->used_scan[c] = s->st[c].r_sum > s->lambda;  // push.cpp:168
+  if (s->hi > s->lo)
+    k_part_y<<<grid_for((s->hi - s->lo) * K), 256, 0, g.stream>>>(b.w.x.get(), g.inv_deg.get(), s->lo,
+                                                                  s->hi, K, b.alpha, b.w.y0.get());
+  PPRG_CUDA(cudaGetLastError());
+  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+  s->call.kernel_launches += 1;
+  return any;
+}
+
+static SweepParams part_params(PartSession* s) {
+  Block& b = *s->b;
+  SweepParams P = base_params(b);
+  P.desc = s->desc;
+  P.ntiles = s->t1 - s->t0;
+  P.own_lo = s->lo;
+  P.own_hi = s->hi;
+  P.x = b.w.x.get();
+  P.y[0] = P.y[1] = b.w.y0.get();
+  for (int c = 0; c < b.K; ++c) P.init[c] = s->st[c];
+  return P;
+}
+
+void part_sweep(PartSession* s, double* local_host) {
+  Graph& g = *s->g;
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  Block& b = *s->b;
+  const int K = b.K;
+  SweepParams P = part_params(s);
+  P.max_sweeps = 1;
+  P.E = (int)s->E;
+  for (uint32_t e = 0; e < s->E; ++e) {
+    P.lam[e] = s->lam[e];
+    P.thr[e] = s->thr[e];
+  }
+  cudaStream_t st = g.stream;
+  PPRG_CUDA(cudaMemsetAsync(b.w.ctl.get(), 0, sizeof(SweepCtl), st));
+  EventTimer tm(st);
+  tm.start();
+  dispatch_sweeps<M_POWERPUSH>(g, K, P, true);
+  tm.stop();
+  k_pack_counters<<<1, KMAX, 0, st>>>(b.w.ctl.get(), K, s->counters.get());
+  PPRG_CUDA(cudaGetLastError());
+  std::vector<double> loc(5 * KMAX, 0.0);
+  PPRG_CUDA(cudaMemcpyAsync(loc.data(), s->counters.get(), 8 * 5 * K, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  if (local_host) std::memcpy(local_host, loc.data(), 8 * 5 * K);
+  // this part's algorithmic bytes (SURVEY 8(d) over its own rows)
+  uint64_t pt = 0, et = 0;
+  for (uint32_t c = 0; c < b.k; ++c) {
+    pt += (uint64_t)loc[2 * K + c];
+    et = std::max<uint64_t>(et, (uint64_t)loc[4 * K + c]);
+  }
+  const uint64_t nown = s->hi - s->lo;
+  s->own_alg_bytes += 8ull * (nown + 1) + 8ull * b.k * nown + 4ull * et + 24ull * pt;
+  s->call.sweep_ms += tm.ms();
+  s->call.sweep_launches += 1;
+  s->call.kernel_launches += 2;
+  s->sweeps += 1;
+}
+
+bool part_advance(PartSession* s, const double* summed) {
+  const bool all_done = epoch_advance(s->st.data(), s->b->K, summed, s->lam.data(), s->E, s->b->alpha);
+  if (!all_done && s->sweeps >= 200000) fail(EINTERNAL, "power push: sweep limit reached");
+  return all_done;
+}
+
+void part_finish(PartSession* s, double* reserve, double* residue, bool on_device, double* rpart) {
+  Graph& g = *s->g;
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  Block& b = *s->b;
+  cudaStream_t st = g.stream;
+  const uint64_t n = g.n;
+  const uint32_t k = b.k;
+  SweepParams Q = part_params(s);
+  DevBuf<double> tr, tq;
+  if (!on_device) {
+    if (reserve) tr.alloc(n * k);
+    if (residue) tq.alloc(n * k);
+  }
+  Q.out_reserve = reserve ? (on_device ? reserve : tr.get()) : nullptr;
+  Q.out_residue = residue ? (on_device ? residue : tq.get()) : nullptr;
+  const uint64_t w = s->hi - s->lo;
+  for (double* o : {Q.out_reserve, Q.out_residue})
+    if (o && w) k_zero_rows<<<grid_for(w * k), 256, 0, st>>>(o, n, k, s->lo, s->hi);
+  Q.res_inter = nullptr;
+  Q.push_res = b.w.res.get();
+  for (int c = 0; c < b.K; ++c) {
+    Q.final_pull[c] = 1;
+    Q.init[c].done = 0;  // the final pass visits every column
+  }
+  PPRG_CUDA(cudaMemsetAsync(b.w.ctl.get(), 0, sizeof(SweepCtl), st));
+  EventTimer tf(st);
+  tf.start();
+  dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
+  tf.stop();
+  SweepCtl fc;
+  PPRG_CUDA(cudaMemcpyAsync(&fc, b.w.ctl.get(), sizeof fc, cudaMemcpyDeviceToHost, st));
+  if (!on_device && w) {
+    for (uint32_t c = 0; c < k; ++c) {
+      if (reserve)
+        PPRG_CUDA(cudaMemcpyAsync(reserve + c * n + s->lo, tr.get() + c * n + s->lo, 8 * w,
+                                  cudaMemcpyDeviceToHost, st));
+      if (residue)
+        PPRG_CUDA(cudaMemcpyAsync(residue + c * n + s->lo, tq.get() + c * n + s->lo, 8 * w,
+                                  cudaMemcpyDeviceToHost, st));
+    }
+  }
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  s->call.final_ms += tf.ms();
+  s->call.kernel_launches += 3;
+  for (uint32_t c = 0; c < k; ++c) rpart[c] = fc.pushed[0][c];
+}
+
+void part_stats(const PartSession* s, ColumnStats* cols, CallStats* call) {
+  const Block& b = *s->b;
+  for (uint32_t c = 0; c < b.k; ++c) {
+    cols[c].pushes = b.pushes[c] + s->st[c].pushes;
+    cols[c].sweeps = s->st[c].sweeps;
+    cols[c].local_levels = b.levels[c];
+    cols[c].used_scan_phase = s->used_scan[c];
+    cols[c].r_sum = s->st[c].r_sum;
+  }
+  *call = s->call;
+  call->alg_bytes = s->own_alg_bytes;
+  call->max_sweeps = s->sweeps;
+  call->device_ms = s->call.local_ms + s->call.sweep_ms + s->call.final_ms;
+}
+
+double* part_y(PartSession* s, uint32_t* K) {
+  *K = (uint32_t)s->b->K;
+  return s->b->w.y0.get();
+}
+double* part_counters(PartSession* s) { return s->counters.get(); }
+
+void part_destroy(PartSession* s) {
+  if (!s) return;
+  DeviceGuard dg(s->g->device);
+  delete s;
 }
 
 }  // namespace pprg

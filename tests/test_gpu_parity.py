@@ -345,3 +345,69 @@ def test_speedppr_batch_push_branch(P, oracle, use_index):
         truth = oracle.exact_ppr(c, int(src[q]), 0.2)
         clean += oracle.compare_to_truth(est, truth, 1.0 / n, 0.5).violations == 0
     assert clean >= 15
+
+
+# ---- (5) vertex-partitioned power_push (configs[4]) ----------------
+@pytest.mark.parametrize("nparts,k", [(2, 1), (3, 4), (8, 1), (8, 64)])
+def test_partitioned_power_push_virtual(P, oracle, nparts, k):
+    """P parts of one block on one GPU (sequential, slices copied between
+    them) against the oracle's power_push: per node |diff| <= lambda, and the
+    exact all-part r_sum <= lambda."""
+    from paper_2101_03652_b200.partition import run_virtual_parts
+    g = P.generate_rmat(13, 8, 31)
+    c = gcsr(g)
+    lam = 1e-8
+    src = P.sample_sources(np.diff(g.out_offsets()), k, 31)
+    res, rsd, rs, sweeps, parts = run_virtual_parts(g, nparts, src, 0.2, lam)
+    bounds = [(p.lo, p.hi) for p in parts]
+    assert bounds[0][0] == 0 and bounds[-1][1] == g.n()
+    assert all(bounds[i][1] == bounds[i + 1][0] for i in range(nparts - 1))
+    assert sweeps > 0
+    for q in range(0, k, max(1, k // 4)):
+        ref = oracle.power_push(c, int(src[q]), 0.2, lam)
+        assert rs[q] <= lam
+        assert abs(rsd[q].sum() - rs[q]) < 1e-12
+        assert np.max(np.abs(res[q] - ref.estimates)) <= lam
+        assert abs(res[q].sum() + rs[q] - 1.0) < 1e-9
+    for p in parts:
+        p.close()
+
+
+def test_partitioned_local_phase_only(P, oracle):
+    """lambda reached by the queue phase: no sweeps, outputs still exact."""
+    from paper_2101_03652_b200.partition import run_virtual_parts
+    g = dev(P, oracle.random_graph(400, 1, 6, 9))
+    c = gcsr(g)
+    res, rsd, rs, sweeps, parts = run_virtual_parts(g, 3, [5], 0.2, 1e-2,
+                                                    scan_threshold=10 ** 9)
+    ref = oracle.power_push(c, 5, 0.2, 1e-2, scan_threshold=10 ** 9)
+    assert sweeps == 0 and rs[0] <= 1e-2
+    assert np.max(np.abs(res[0] - ref.estimates)) <= 1e-2
+    q, _ = parts[0].stats()
+    assert q[0].used_scan_phase == 0
+
+
+def test_partitioned_single_rank_nccl(P, oracle):
+    """The torch.distributed protocol at world size 1 over NCCL (the exchange
+    degenerates to self-broadcasts, the sweeps are the real ones)."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2101_03652_b200.partition import GpuPart, run_partitioned
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        g = P.generate_rmat(12, 8, 5)
+        c = gcsr(g)
+        part = GpuPart(g, 1, 0, [int(np.argmax(np.diff(g.out_offsets())))], 0.2, 1e-8)
+        n = g.n()
+        out = np.zeros(n)
+        r = run_partitioned(part, comm_device="cuda:0",
+                            finish_kwargs=dict(reserve_ptr=out.ctypes.data))
+        ref = oracle.power_push(c, int(part.src[0]), 0.2, 1e-8)
+        assert r.r_sum[0] <= 1e-8 and r.bounds == [(0, n)]
+        assert np.max(np.abs(out - ref.estimates)) <= 1e-8
+        part.close()
+    finally:
+        dist.destroy_process_group()
