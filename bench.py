@@ -261,7 +261,7 @@ def main():
     torch.cuda.synchronize()
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sweep_ms = dev_ms = 0.0
-    alg = launches = 0
+    alg = launches = sweep_launches = 0
     sweeps = []
     with ClockSampler(local) as clk:
         start.record()
@@ -271,6 +271,7 @@ def main():
             dev_ms += cs.device_ms
             alg += cs.alg_bytes
             launches += cs.kernel_launches
+            sweep_launches += cs.sweep_launches
             sweeps.append(cs.max_sweeps)
         stop.record()
         torch.cuda.synchronize()
@@ -325,6 +326,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic_for("config3"),
                          "peak_kind": peak_kind, "kernel": "k_sweeps<K,POWERPUSH>",
                          "alg_bytes_per_step": alg / args.steps,
+                         "alg_bytes_per_launch": alg / max(sweep_launches, 1),
                          "sweep_ms_per_step": sweep_ms / args.steps,
                          "sweeps_per_block": sweeps[-1]},
             "clocks": clk.summary()}

@@ -1113,6 +1113,14 @@ void release_workspaces(const Graph* g) {
 
 namespace {
 
+// Reductions that flush per-block partials with global atomics: a bounded,
+// grid-stride grid (a few blocks per SM) keeps those atomics few.
+inline unsigned grid_reduce(uint64_t items, int tb = 256) {
+  uint64_t b = (items + tb - 1) / tb;
+  if (b == 0) b = 1;
+  return (unsigned)(b < 148ull * 8 ? b : 148ull * 8);
+}
+
 inline unsigned grid_for(uint64_t items, int tb = 256) {
   uint64_t b = (items + tb - 1) / tb;
   if (b == 0) b = 1;
@@ -1440,7 +1448,7 @@ void exact_rsum(Block& b, const std::vector<int>& which) {
   cudaStream_t st = g.stream;
   const uint64_t nk = g.n * (uint64_t)b.K;
   PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
-  k_colsum<<<grid_for(nk), 256, 0, st>>>(b.w.res.get(), g.n, b.K, b.w.dcols.get() + KMAX);
+  k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), g.n, b.K, b.w.dcols.get() + KMAX);
   std::vector<double> exact(KMAX);
   PPRG_CUDA(cudaMemcpyAsync(exact.data(), b.w.dcols.get() + KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
   PPRG_CUDA(cudaStreamSynchronize(st));
@@ -1465,7 +1473,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   const double m_eff = (double)g.m_eff();
   if (E + (refine_rmax > 0.0) > EMAX) fail(EINVAL_, "epoch_num exceeds 64");
   PPRG_CUDA(cudaMemsetAsync(w.dcols.get() + 2 * KMAX, 0, 8 * KMAX, st));
-  k_init_pull<<<grid_for(nk), 256, 0, st>>>(w.x.get(), g.deg.get(), g.inv_deg.get(), g.n, b.K,
+  k_init_pull<<<grid_reduce(nk), 256, 0, st>>>(w.x.get(), g.deg.get(), g.inv_deg.get(), g.n, b.K,
                                             b.alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
   PPRG_CUDA(cudaMemcpyAsync(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
   PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
@@ -1684,7 +1692,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       PPRG_CUDA(cudaMemsetAsync(w.y1.get(), 0, 8 * nk, st));
       PPRG_CUDA(cudaMemsetAsync(w.dcols.get() + 2 * KMAX, 0, 8 * KMAX, st));
       k_seed<<<1, KMAX, 0, st>>>(w.r0.get(), w.d_src.get(), b.K, 1.0);
-      k_init_pull<<<grid_for(nk), 256, 0, st>>>(w.r0.get(), g.deg.get(), g.inv_deg.get(), n, b.K,
+      k_init_pull<<<grid_reduce(nk), 256, 0, st>>>(w.r0.get(), g.deg.get(), g.inv_deg.get(), n, b.K,
                                                 alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
       PPRG_CUDA(cudaMemcpyAsync(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
       PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
@@ -1995,7 +2003,7 @@ PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t
   s->counters.alloc(5 * KMAX);
   PPRG_CUDA(cudaMemsetAsync(s->sums.get(), 0, 16 * KMAX, st));
   if (s->hi > s->lo)
-    k_part_sums<<<grid_for((s->hi - s->lo) * K), 256, 0, st>>>(b.w.x.get(), g.deg.get(), s->lo,
+    k_part_sums<<<grid_reduce((s->hi - s->lo) * K), 256, 0, st>>>(b.w.x.get(), g.deg.get(), s->lo,
                                                                s->hi, K, s->sums.get());
   PPRG_CUDA(cudaGetLastError());
   PPRG_CUDA(cudaMemcpyAsync(partial_host, s->sums.get(), 16 * KMAX, cudaMemcpyDeviceToHost, st));

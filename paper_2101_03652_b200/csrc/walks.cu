@@ -9,6 +9,7 @@
 // independent and reproducible; terminals are bit-identical to the oracle's
 // restatement (oracle.c og_philox_walk) and the index is byte-identical per
 // seed. Stored index files carry rng-id 2 (PPRG_RNG_PHILOX4X32_10).
+#include <algorithm>
 #include <cub/cub.cuh>
 
 #include <cmath>
@@ -306,7 +307,7 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
     unsigned long long* nbig = colw.get() + 64;
     PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
     PPRG_CUDA(cudaMemsetAsync(colw.get(), 0, 8 * 65, st));
-    k_mc_counts<<<gridn(nk), 256, 0, st>>>(pv.res, g.deg.get(), n, K, kb, (double)W, cnt.get(),
+    k_mc_counts<<<std::min<unsigned>(gridn(nk), g.sm_count * 8), 256, 0, st>>>(pv.res, g.deg.get(), n, K, kb, (double)W, cnt.get(),
                                           bad.get(), colw.get());
     k_est_init<<<gridn(nk), 256, 0, st>>>(pv.x, nk, alpha, est.get());
     McParams P;
