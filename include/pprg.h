@@ -169,6 +169,14 @@ void pprg_part_destroy(pprg_part* p);
  * engines use (a power of two, padding columns inert). Not in the reference. */
 int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out);
 
+/* ground_truth(g, s, alpha) metrics.hpp:41, metrics.cpp:44-55: the answer at
+ * lambda = 1e-17 (r_sum <= 1e-17 on exit), for k sources; graphs with
+ * n <= 2000 are cross-checked against an independent engine (l1 <= 1e-12,
+ * PPRG_EINTERNAL otherwise). estimates_out is required. */
+int pprg_ground_truth(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                      double* estimates_out, uint32_t flags, pprg_query_stats* qstats,
+                      pprg_call_stats* cstats);
+
 /* ---- SpeedPPR (speedppr.hpp, walk_index.hpp) ------------------------------- */
 /* compute_walk_budget(n, eps, mu) speedppr.hpp:16-17 */
 int pprg_walk_budget(uint64_t n, double epsilon, double mu, uint64_t* out);

@@ -11,6 +11,7 @@ Same names, argument meaning and error behaviour:
     power_push(g, s, alpha, lam, cfg)      push.hpp:105
     build_index / speedppr_query           walk_index.hpp:50, speedppr.hpp:37
     compute_walk_budget                    speedppr.hpp:17
+    ground_truth                           metrics.hpp:41
 
 Every query runs on the GPU; there is no CPU fallback — the module raises if
 the CUDA library is missing or no device is visible.
@@ -19,7 +20,8 @@ from ._abi import (PPRVector, QueryConfig, Graph, WalkIndex, CallStats, PowerPus
                    build_graph_from_edges, generate_rmat, generate_chung_lu, power_iteration,
                    sim_forward_push, fifo_forward_push, power_push, power_push_batch,
                    power_iteration_batch, speedppr_query, speedppr_batch, build_index,
-                   compute_walk_budget, walk_terminals, default_lambda, default_mu,
+                   compute_walk_budget, walk_terminals, ground_truth, ground_truth_batch,
+                   GROUND_TRUTH_LAMBDA, default_lambda, default_mu,
                    default_scan_threshold, load_library, lib_path, PPRGError, InvalidArgument,
                    DataError, LogicError, KINDEX_TAG, RNG_ID_PHILOX)
 from .formats import save_graph_cache, load_graph_cache, save_index, load_index, is_graph_cache

@@ -102,6 +102,7 @@ def load_library(path: str = lib_path):
     L.pprg_power_push.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
                                   C.c_int64, vp, vp, C.c_uint32, vp, vp, vp]
     L.pprg_walk_budget.argtypes = [C.c_uint64, C.c_double, C.c_double, u64p]
+    L.pprg_ground_truth.argtypes = [vp, vp, C.c_uint32, C.c_double, vp, C.c_uint32, vp, vp]
     L.pprg_block_columns.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint32)]
     L.pprg_index_build.argtypes = [vp, C.c_double, C.c_uint64, C.POINTER(vp)]
     L.pprg_index_from_host.argtypes = [vp, C.c_double, C.c_uint64, vp, C.POINTER(vp)]
@@ -414,6 +415,27 @@ def fifo_forward_push(g: Graph, s: int, alpha: float, r_max: float,
                                        lambda_stop if lambda_stop is not None else -1.0, rp, dp,
                                        flags, q, C.byref(cs)))
     return _vectors(src, res, rsd, q, alpha)[0]
+
+
+GROUND_TRUTH_LAMBDA = 1e-17  # kGroundTruthLambda, metrics.hpp:10
+
+
+def ground_truth_batch(g: Graph, sources, alpha: float):
+    """ground_truth for k sources (metrics.cpp:44-55): reserve with r_sum <= 1e-17.
+    Returns (list[PPRVector] without residues, CallStats)."""
+    load_library()
+    src = _sources(sources)
+    res = np.empty((len(src), g.n()), np.float64)
+    q = (QStats * max(len(src), 1))()
+    cs = CStats()
+    _check(_lib.pprg_ground_truth(g.handle, _ptr(src), len(src), alpha, res.ctypes.data, 0, q,
+                                  C.byref(cs)))
+    return _vectors(src, res, None, q, alpha), CallStats.of(cs)
+
+
+def ground_truth(g: Graph, s: int, alpha: float) -> PPRVector:
+    """metrics.hpp:41 (metrics.cpp:44-55)."""
+    return ground_truth_batch(g, [s], alpha)[0][0]
 
 
 def power_push(g: Graph, s: int, alpha: float, lam: float, cfg: Optional[QueryConfig] = None,

@@ -256,6 +256,50 @@ int pprg_fifo_forward_push(pprg_graph* g, const uint32_t* sources, uint32_t k, d
                      reserve_out, residue_out, flags, q, c);
 }
 
+int pprg_ground_truth(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
+                      double* estimates_out, uint32_t flags, pprg_query_stats* q,
+                      pprg_call_stats* c) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    require(k == 0 || (sources && estimates_out), "null argument");
+    check_alpha(alpha);
+    pprg::Graph& G = *g->g;
+    const bool dev = (flags & PPRG_OUT_DEVICE) != 0;
+    // kGroundTruthLambda = 1e-17 (metrics.hpp:10), the double-precision limit.
+    // Power iteration keeps the residues explicit (no cancellation against
+    // x), stops at r_sum <= 1e-17 (push.cpp:81-108) and is deterministic:
+    // fixed-order row sums, hub rows combined in piece order.
+    std::vector<pprg::ColumnStats> cs(k);
+    pprg::CallStats call;
+    if (k)
+      pprg::run_push_engine(G, pprg::Engine::PowItr, sources, k, alpha, 1e-17, 0, -1, 0.0, 0.0,
+                            pprg::Outputs{estimates_out, nullptr, dev}, cs.data(), &call);
+    if (k && G.n <= 2000) {
+      // metrics.cpp:48-53 cross-checks small graphs against the dense solve;
+      // here an independent engine (FIFO push to lambda = 1e-14) plays that
+      // role, with the reference's 1e-12 l1 bound.
+      const uint64_t n = G.n;
+      std::vector<double> chk(n * k), got(n * k);
+      std::vector<pprg::ColumnStats> cs2(k);
+      pprg::CallStats call2;
+      const double r_max = 1e-14 / static_cast<double>(G.m_eff());
+      pprg::run_push_engine(G, pprg::Engine::Fifo, sources, k, alpha, 0.0, 0, -1, r_max, 0.0,
+                            pprg::Outputs{chk.data(), nullptr, false}, cs2.data(), &call2);
+      if (dev)
+        PPRG_CUDA(cudaMemcpy(got.data(), estimates_out, 8 * n * k, cudaMemcpyDeviceToHost));
+      else
+        std::memcpy(got.data(), estimates_out, 8 * n * k);
+      for (uint32_t i = 0; i < k; ++i) {
+        double l1 = 0.0;
+        for (uint64_t v = 0; v < n; ++v) l1 += std::fabs(got[i * n + v] - chk[i * n + v]);
+        if (l1 > 1e-12) pprg::fail(pprg::EINTERNAL, "ground_truth: disagrees with the dense solve");
+      }
+      call.kernel_launches += call2.kernel_launches;
+    }
+    fill_stats(cs, call, k, q, c);
+  });
+}
+
 int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
                     double lambda, uint32_t epoch_num, int64_t scan_threshold,
                     double* reserve_out, double* residue_out, uint32_t flags,

@@ -141,7 +141,7 @@ __device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
 // evict-first keeps L2 for y. PPRG_HINTS: 0 = none, 1 = streams evict-first,
 // 2 = 1 + y gathers evict-last.
 #ifndef PPRG_HINTS
-#define PPRG_HINTS 1
+#define PPRG_HINTS 0
 #endif
 __device__ __forceinline__ uint64_t l2_evict_first() {
   uint64_t p;
@@ -179,7 +179,11 @@ __device__ __forceinline__ void st_state(double* p, double v) {
 #endif
 }
 __device__ __forceinline__ double2 ld_gather2(const double* p) {
-#if PPRG_HINTS >= 2
+#if PPRG_HINTS == 3
+  double2 v;
+  asm volatile("ld.global.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+#elif PPRG_HINTS >= 2
   double2 v;
   asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(l2_evict_last()));
   return v;
@@ -188,7 +192,11 @@ __device__ __forceinline__ double2 ld_gather2(const double* p) {
 #endif
 }
 __device__ __forceinline__ double ld_gather(const double* p) {
-#if PPRG_HINTS >= 2
+#if PPRG_HINTS == 3
+  double v;
+  asm volatile("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+#elif PPRG_HINTS >= 2
   double v;
   asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_last()));
   return v;

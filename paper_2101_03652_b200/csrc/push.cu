@@ -73,7 +73,7 @@ struct SweepParams {
   const double* inv_deg;
   const uint32_t* tile_lo;
   const TileDesc* desc;        // row-aligned tile plan
-  double* hub_acc;             // [nhubs][K] partial sums of hub rows
+  double* hub_acc;             // [ntiles][K] per-piece partial sums of hub rows
   unsigned* hub_cnt;           // [nhubs] arrived pieces
   uint64_t ntiles;
   uint32_t T;
@@ -212,8 +212,8 @@ __device__ __forceinline__ void decide_at(const SweepParams& P, const ColSh* cs,
 // last piece to arrive decides the row (release-ordered counter; the partials
 // are read back from L2). Only hub pieces pay this protocol.
 template <int K, int MODE>
-__device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, double* hubsh,
-                                       int* flag, const ColSh* cs, const double* thr_cur,
+__device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, uint64_t j,
+                                       double* hubsh, int* flag, const ColSh* cs, const double* thr_cur,
                                        const double* yg, const double* rcur, double* rnxt,
                                        double* ynxt, Acc& a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -242,7 +242,7 @@ __device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, 
   if (tid < K) {
     double t = 0.0;
     for (int w = 0; w < NT / 32; ++w) t += hubsh[w * K + tid];
-    atomicAdd(P.hub_acc + (uint64_t)d.hub * K + tid, t);
+    P.hub_acc[j * K + tid] = t;  // this piece's partial (slot = its tile)
   }
   __syncthreads();
   if (tid == 0) {
@@ -254,9 +254,10 @@ __device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, 
   }
   __syncthreads();
   if (*flag && tid < K) {
-    double* slot = P.hub_acc + (uint64_t)d.hub * K + tid;
-    const double acc = __ldcg(slot);
-    *slot = 0.0;
+    // the last piece sums the partials in piece order: deterministic
+    const double* part = P.hub_acc + (j - d.piece) * K + tid;
+    double acc = 0.0;
+    for (uint32_t p = 0; p < d.npieces; ++p) acc += __ldcg(part + (uint64_t)p * K);
     const uint32_t u = __ldg(P.crow + d.r0);
     decide_at<K, MODE>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
                        rcur, rnxt, ynxt, a);
@@ -657,7 +658,7 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
       if (tid == 0) sh_tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
       TileDesc dn = d;
       if (d.npieces > 1) {
-        hub_piece<K, MODE>(P, d, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+        hub_piece<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
         dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
         __syncthreads();
       } else if constexpr (K >= WIDE_K) {
@@ -1078,10 +1079,9 @@ static void ws_tiles(Workspace& w, Graph& g, uint64_t ntiles, uint64_t nhubs) {
     PPRG_CUDA(cudaMemsetAsync(w.split_cnt.get(), 0, 4 * (ntiles + 1), g.stream));
     w.ntiles_alloc = ntiles;
   }
+  if ((ntiles + 1) * K > w.hub_acc.n) w.hub_acc.alloc((ntiles + 1) * K);
   if (nhubs + 1 > w.hub_cnt.n) {
-    w.hub_acc.alloc((nhubs + 1) * K);
     w.hub_cnt.alloc(nhubs + 1);
-    PPRG_CUDA(cudaMemsetAsync(w.hub_acc.get(), 0, 8 * (nhubs + 1) * K, g.stream));
     PPRG_CUDA(cudaMemsetAsync(w.hub_cnt.get(), 0, 4 * (nhubs + 1), g.stream));
   }
 }

@@ -411,3 +411,41 @@ def test_partitioned_single_rank_nccl(P, oracle):
         part.close()
     finally:
         dist.destroy_process_group()
+
+
+# ---- ground_truth (metrics.cpp:44-55) ------------------------
+def test_ground_truth_five_node_deterministic(P):  # test_metrics.cpp:66-76
+    d = P.build_graph_from_edges(five_node_edges())
+    a = P.ground_truth(d, 0, 0.2)
+    b = P.ground_truth(d, 0, 0.2)
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.abs(a.estimates - FIVE_NODE_PI0).sum() <= 1e-12
+    assert abs(a.estimates.sum() - 1.0) <= 1e-12
+    assert a.achieved_r_sum <= P.GROUND_TRUTH_LAMBDA
+
+
+def test_ground_truth_dead_ends(P, oracle):  # test_metrics.cpp:78-83
+    g = oracle.random_graph(50, 0, 3, 71)
+    d = dev(P, g)
+    assert len(d.dead_ends()) > 0
+    out = P.ground_truth(d, 7, 0.2)
+    assert out.achieved_r_sum <= P.GROUND_TRUTH_LAMBDA
+    assert np.abs(out.estimates - oracle.exact_ppr(g, 7, 0.2)).sum() <= 1e-12
+
+
+def test_ground_truth_large_reproducible(P):
+    """r_sum <= 1e-17 on exit, and two runs agree to the 1e-17 bound (the
+    dead-end mass and r_sum are fp64 atomic sums, so bits may differ where
+    the reference's sequential loop is bit-deterministic)."""
+    g = P.generate_rmat(15, 16, 9)
+    src = P.sample_sources(np.diff(g.out_offsets()), 3, 9)
+    a, _ = P.ground_truth_batch(g, src, 0.2)
+    b, _ = P.ground_truth_batch(g, src, 0.2)
+    for x, y in zip(a, b):
+        assert np.abs(x.estimates - y.estimates).sum() <= 2 * P.GROUND_TRUTH_LAMBDA + 1e-16
+        assert x.achieved_r_sum <= P.GROUND_TRUTH_LAMBDA
+        assert abs(x.estimates.sum() + x.achieved_r_sum - 1.0) < 1e-12
+    # the 1e-8 PowerPush answer is within lambda of it everywhere
+    pp, _ = P.power_push_batch(g, src, 0.2, 1e-8)
+    for x, y in zip(a, pp):
+        assert np.max(np.abs(x.estimates - y.estimates)) <= 1e-8
