@@ -169,6 +169,25 @@ void pprg_part_destroy(pprg_part* p);
  * engines use (a power of two, padding columns inert). Not in the reference. */
 int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out);
 
+/* One high-precision query with its progress series: the reference's
+ * run_high_precision + CheckpointRecorder (sweep.cpp:25-61), recorded at
+ * global-sweep / iteration / frontier-level granularity (pushes = cumulative
+ * edge pushes, r_sum after that step, time_ns since the call started). FIFO
+ * uses r_max = lambda / m_eff and power_push the default config, as
+ * sweep.cpp:55-60. *count = points written (<= capacity). */
+#define PPRG_ALGO_POWITR 0
+#define PPRG_ALGO_SIMFWDPUSH 1
+#define PPRG_ALGO_FIFO 2
+#define PPRG_ALGO_POWERPUSH 3
+typedef struct {
+  uint64_t pushes;
+  double r_sum;
+  uint64_t time_ns;
+} pprg_checkpoint;
+int pprg_run_traced(pprg_graph* g, int algo, uint32_t source, double alpha, double lambda,
+                    double* estimates_out, pprg_query_stats* qstats, pprg_checkpoint* points,
+                    uint32_t capacity, uint32_t* count);
+
 /* ground_truth(g, s, alpha) metrics.hpp:41, metrics.cpp:44-55: the answer at
  * lambda = 1e-17 (r_sum <= 1e-17 on exit), for k sources; graphs with
  * n <= 2000 are cross-checked against an independent engine (l1 <= 1e-12,

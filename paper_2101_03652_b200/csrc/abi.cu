@@ -1,5 +1,6 @@
 // extern "C" boundary (include/pprg.h): argument checks with the reference's
 // error behaviour, exception -> status mapping, per-thread error message.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -254,6 +255,55 @@ int pprg_fifo_forward_push(pprg_graph* g, const uint32_t* sources, uint32_t k, d
   }
   return push_engine(g, pprg::Engine::Fifo, sources, k, alpha, 0.0, 0, -1, r_max, lambda_stop,
                      reserve_out, residue_out, flags, q, c);
+}
+
+int pprg_run_traced(pprg_graph* g, int algo, uint32_t source, double alpha, double lambda,
+                    double* estimates_out, pprg_query_stats* q, pprg_checkpoint* points,
+                    uint32_t capacity, uint32_t* count) {
+  return guard([&] {
+    require(g && g->g && count, "null argument");
+    require(algo >= PPRG_ALGO_POWITR && algo <= PPRG_ALGO_POWERPUSH, "unknown algorithm");
+    check_alpha(alpha);
+    require(lambda > 0.0 && lambda <= 1.0, "lambda must be in (0,1]");
+    pprg::Graph& G = *g->g;
+    pprg::TraceSink sink;
+    sink.dev_t0 = pprg::device_now_ns(G);
+    sink.host_t0 = pprg::host_now_ns();
+    struct Reset {
+      ~Reset() { pprg::g_trace = nullptr; }
+    } reset;
+    pprg::g_trace = &sink;
+    std::vector<pprg::ColumnStats> cs(1);
+    pprg::CallStats call;
+    pprg::Outputs out{estimates_out, nullptr, false};
+    // run_high_precision (sweep.cpp:50-61)
+    switch (algo) {
+      case PPRG_ALGO_POWITR:
+        pprg::run_push_engine(G, pprg::Engine::PowItr, &source, 1, alpha, lambda, 0, -1, 0, 0, out,
+                              cs.data(), &call);
+        break;
+      case PPRG_ALGO_SIMFWDPUSH:
+        pprg::run_push_engine(G, pprg::Engine::SimFwdPush, &source, 1, alpha, lambda, 0, -1, 0, 0,
+                              out, cs.data(), &call);
+        break;
+      case PPRG_ALGO_FIFO:
+        pprg::run_push_engine(G, pprg::Engine::Fifo, &source, 1, alpha, 0.0, 0, -1,
+                              lambda / static_cast<double>(G.m_eff()), 0.0, out, cs.data(), &call);
+        break;
+      default:
+        pprg::run_push_engine(G, pprg::Engine::PowerPush, &source, 1, alpha, lambda, 8, -1, 0, 0,
+                              out, cs.data(), &call);
+    }
+    pprg::g_trace = nullptr;
+    const uint32_t n = (uint32_t)std::min<size_t>(sink.pts.size(), capacity);
+    for (uint32_t i = 0; i < n && points; ++i) {
+      points[i].pushes = sink.pts[i].pushes;
+      points[i].r_sum = sink.pts[i].r_sum;
+      points[i].time_ns = sink.pts[i].time_ns;
+    }
+    *count = n;
+    fill_stats(cs, call, 1, q, nullptr);
+  });
 }
 
 int pprg_ground_truth(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,

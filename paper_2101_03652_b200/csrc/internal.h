@@ -132,6 +132,23 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
                          double lambda, double r_max, ColumnStats* cols, CallStats* call,
                          PushView* view);
 
+// Progress trace of a traced single-source call (the reference's
+// CheckpointRecorder, sweep.hpp:30-45, at sweep / level granularity). A
+// thread-local sink, set by pprg_run_traced for the duration of one call.
+struct TracePoint {
+  uint64_t pushes;
+  double r_sum;
+  uint64_t time_ns;
+};
+struct TraceSink {
+  std::vector<TracePoint> pts;
+  uint64_t host_t0 = 0;    // steady-clock ns at the call start
+  uint64_t dev_t0 = 0;     // %globaltimer at the call start
+};
+extern thread_local TraceSink* g_trace;
+uint64_t host_now_ns();
+uint64_t device_now_ns(Graph& g);
+
 // Per-column global-phase state (layout = pprg_column_state).
 struct ColInit {
   double r_sum;

@@ -17,6 +17,7 @@
 // atomic ticket, so rows processed later in a sweep see earlier rows' pushes.
 // The local phase and refine use push form (atomicExch claim + fp64 RED
 // scatter) over frontier levels, since their frontiers are sparse.
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <algorithm>
@@ -41,6 +42,14 @@ constexpr int NT = PPRG_NT;             // threads per block for the sweep kerne
 constexpr int SWEEP_ELEMS = NT * 8;     // edges x columns per tile (8 per thread)
 
 enum SweepMode : int { M_POWERPUSH = 0, M_POWITR = 1, M_SIMFWD = 2, M_FINAL = 3 };
+
+thread_local TraceSink* g_trace = nullptr;
+
+uint64_t host_now_ns() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
 
 struct SweepCtl {
   unsigned long long barrier;
@@ -94,6 +103,8 @@ struct SweepParams {
   double* out_residue;
   double* res_inter;           // finalize: explicit residues back into [u*K + c] (SpeedPPR)
   uint32_t max_sweeps;
+  TracePoint* trace;            // per-sweep progress of column 0 (traced calls), or null
+  uint32_t trace_cap;
   uint64_t own_lo, own_hi;      // node range this launch owns (vertex partition; else [0, n))
   unsigned long long handoff_np;  // refine epoch: hand off to the frontier below this many edge pushes
   uint32_t src[KMAX];
@@ -714,6 +725,12 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
         cs[cc].sweeps += 1;
         cs[cc].pushes += np;
         cs[cc].D = __ldcg(&ctl->dsum[buf][cc]);
+        if (P.trace && cc == 0 && blockIdx.x == 0 && sweep < P.trace_cap) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          const double rs = MODE == M_POWERPUSH ? cs[cc].r_sum - P.alpha * pushed : pushed;
+          P.trace[sweep] = TracePoint{cs[cc].pushes, rs, t};
+        }
         if (MODE == M_POWERPUSH) {
           cs[cc].r_sum -= P.alpha * pushed;
           if (np == 0) cs[cc].epoch += 1;  // fixpoint: nothing active at this threshold
@@ -1174,6 +1191,53 @@ int round_k(uint32_t k) {
   return K;
 }
 
+__global__ void k_stamp(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
+}
+
+// Device trace buffer for one sweep launch of a traced call; `fold` appends
+// its points to the sink with a push offset / scale.
+struct SweepTrace {
+  DevBuf<TracePoint> buf;
+  uint32_t cap = 0;
+  void attach(SweepParams& P) {
+    if (!g_trace) return;
+    cap = 1u << 16;
+    buf.alloc(cap);
+    P.trace = buf.get();
+    P.trace_cap = cap;
+  }
+  void fold(cudaStream_t st, uint32_t nsweeps, uint64_t push_base, uint64_t per_sweep_pushes) {
+    if (!g_trace || !cap) return;
+    const uint32_t n = nsweeps < cap ? nsweeps : cap;
+    std::vector<TracePoint> h(n);
+    if (n) PPRG_CUDA(cudaMemcpyAsync(h.data(), buf.get(), sizeof(TracePoint) * n, cudaMemcpyDeviceToHost, st));
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t i = 0; i < n; ++i) {
+      TracePoint t = h[i];
+      t.pushes = per_sweep_pushes ? push_base + (uint64_t)(i + 1) * per_sweep_pushes
+                                  : push_base + t.pushes;
+      t.time_ns = t.time_ns > g_trace->dev_t0 ? t.time_ns - g_trace->dev_t0 : 0;
+      g_trace->pts.push_back(t);
+    }
+  }
+};
+
+}  // namespace
+
+uint64_t device_now_ns(Graph& g) {
+  DevBuf<unsigned long long> t(1);
+  k_stamp<<<1, 1, 0, g.stream>>>(t.get());
+  unsigned long long h = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&h, t.get(), 8, cudaMemcpyDeviceToHost, g.stream));
+  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+  return h;
+}
+
+namespace {
+
 struct EventTimer {
   cudaEvent_t a{}, b{};
   cudaStream_t st;
@@ -1430,6 +1494,8 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
       b.r_sum[c] -= hdr[c];
       b.pushes[c] += hc[1 + KMAX + c];
       b.levels[c] += 1;
+      if (g_trace && c == 0)
+        g_trace->pts.push_back(TracePoint{b.pushes[0], b.r_sum[0], host_now_ns() - g_trace->host_t0});
       qsize[c] = hc[1 + c];
       if (hstop[c] || !still_live(c, qsize[c])) {
         live &= ~(1ull << c);
@@ -1505,6 +1571,8 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   P.E = Et;
   P.x = w.x.get();
   P.y[0] = P.y[1] = w.y0.get();
+  SweepTrace trace;
+  trace.attach(P);
   EventTimer tm(st);
   tm.start();
   dispatch_sweeps<M_POWERPUSH>(g, b.K, P, true);
@@ -1512,6 +1580,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   SweepCtl hc;
   PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
   call->sweep_ms += tm.ms();
+  trace.fold(st, hc.total_sweeps, b.pushes[0], 0);
   call->alg_bytes += hc.alg_bytes;
   call->sweep_launches += 1;
   call->kernel_launches += 2;
@@ -1709,6 +1778,8 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       P.r[1] = w.r1.get();
       P.y[0] = w.y0.get();
       P.y[1] = w.y1.get();
+      SweepTrace trace;
+      trace.attach(P);
       EventTimer tm(st);
       tm.start();
       if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, P, true);
@@ -1717,6 +1788,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       SweepCtl hc;
       PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
       call->sweep_ms += tm.ms();
+      trace.fold(st, hc.total_sweeps, 0, eng == Engine::PowItr ? g.m_eff() : 0);
       call->alg_bytes += hc.alg_bytes;
       call->sweep_launches += 1;
       call->kernel_launches += 4;

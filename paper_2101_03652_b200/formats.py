@@ -104,3 +104,61 @@ def load_index(path: str, g: Graph) -> WalkIndex:
     if off.size != g.n() + 1 or ep.size != g.m() or not np.array_equal(off, g.out_offsets()):
         raise DataError("walk index does not match the graph shape")
     return WalkIndex.from_endpoints(g, alpha, seed, ep)
+
+
+# ---- edge-list text files (graph.cpp:66-101) --------------------------------------
+def parse_edge_list(path: str, undirected: bool = False) -> np.ndarray:
+    """Pairs (src, dst) as uint64 [count, 2], with the reference's rules and
+    messages: blank lines and '#' comments skipped, two non-negative integers
+    per line separated by spaces/tabs, nothing after them; `undirected` adds
+    the reverse of every pair right after it."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise DataError("cannot open graph file: " + path)
+    out = []
+    with f:
+        for line_no, raw in enumerate(f, 1):
+            line = raw.rstrip(b"\n")
+            p, end = 0, len(line)
+
+            def fail(what):
+                raise DataError(f"{path}:{line_no}: {what}")
+
+            while p < end and line[p] in b" \t\r":
+                p += 1
+            if p == end or line[p:p + 1] == b"#":
+                continue
+            vals = []
+            for what in ("expected non-negative integer source id",
+                         "expected non-negative integer target id"):
+                q = p
+                while q < end and 48 <= line[q] <= 57:
+                    q += 1
+                if q == p:
+                    fail(what)
+                v = int(line[p:q])
+                if v >= 1 << 64:
+                    fail(what)
+                vals.append(v)
+                p = q
+                while p < end and line[p] in b" \t\r":
+                    p += 1
+            if p != end:
+                fail("trailing content after edge pair")
+            out.append(vals)
+            if undirected:
+                out.append(vals[::-1])
+    if not out:
+        raise DataError(path + ": graph is empty after cleaning")
+    return np.asarray(out, dtype=np.uint64)
+
+
+def load_edge_list(path: str, device=None) -> Graph:  # graph.hpp:97
+    from ._abi import build_graph_from_edges
+    return build_graph_from_edges(parse_edge_list(path), device=device)
+
+
+def undirected_to_directed(path: str, device=None) -> Graph:  # graph.hpp:100
+    from ._abi import build_graph_from_edges
+    return build_graph_from_edges(parse_edge_list(path, undirected=True), device=device)

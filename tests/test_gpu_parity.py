@@ -449,3 +449,21 @@ def test_ground_truth_large_reproducible(P):
     pp, _ = P.power_push_batch(g, src, 0.2, 1e-8)
     for x, y in zip(a, pp):
         assert np.max(np.abs(x.estimates - y.estimates)) <= 1e-8
+
+
+# ---- sweep harness progress series (sweep.cpp:25-61) --------------------------------
+@pytest.mark.parametrize("algo", ["powerpush", "powitr", "simfwdpush", "fwdpush-fifo"])
+def test_traced_progress_series(P, oracle, algo):
+    from paper_2101_03652_b200 import harness
+    g = P.generate_rmat(12, 8, 4)
+    s = int(np.argmax(np.diff(g.out_offsets())))
+    got, pts = harness.run_traced(g, algo, s, 0.2, 1e-8)
+    assert len(pts) >= 5 and got.achieved_r_sum <= 1e-8
+    push = [p.pushes for p in pts]
+    assert push == sorted(push) and push[-1] <= got.pushes
+    assert pts[-1].r_sum <= 1.0 and pts[0].r_sum <= 1.0
+    assert all(b.time_ns >= a.time_ns for a, b in zip(pts, pts[1:]))
+    ref = oracle.power_push(gcsr(g), s, 0.2, 1e-8)
+    assert np.max(np.abs(got.estimates - ref.estimates)) <= 1e-8
+    cp = harness.cadence_filter(pts, 4 * g.m())
+    assert all(b.pushes - a.pushes >= 0 for a, b in zip(cp, cp[1:]))
