@@ -2,14 +2,18 @@
 // (include/pprg.h). Every engine call runs on the GPU; status codes come back
 // as the reference's exception types (invalid_argument / runtime_error /
 // logic_error).
+#include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <stdexcept>
 #include <string>
 
 #include "../../../include/pprg.h"
+#include "ppr/csv.hpp"
 #include "ppr/graph.hpp"
+#include "ppr/metrics.hpp"
 #include "ppr/push.hpp"
 #include "ppr/speedppr.hpp"
 #include "ppr/walk_index.hpp"
@@ -330,6 +334,84 @@ PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
   v.pushes = q.pushes;
   v.walks = q.walks;
   return v;
+}
+
+// ---- metrics.hpp (metrics.cpp:11-55) ---------------------------------------------
+double l1_error(std::span<const double> estimate, std::span<const double> truth) {
+  if (estimate.size() != truth.size())
+    throw std::invalid_argument("l1_error: vector lengths differ");
+  double total = 0.0;
+  for (std::size_t i = 0; i < estimate.size(); ++i) total += std::abs(estimate[i] - truth[i]);
+  return total;
+}
+
+double l1_error(const PPRVector& estimate, const PPRVector& truth) {
+  if (estimate.source != truth.source)
+    throw std::invalid_argument("l1_error: results are for different sources");
+  return l1_error(std::span<const double>(estimate.estimates),
+                  std::span<const double>(truth.estimates));
+}
+
+ErrorReport compare_to_truth(std::span<const double> estimate, std::span<const double> truth,
+                             double mu, double epsilon) {
+  if (estimate.size() != truth.size())
+    throw std::invalid_argument("compare_to_truth: vector lengths differ");
+  ErrorReport r;
+  for (std::size_t i = 0; i < estimate.size(); ++i) {
+    const double d = std::abs(estimate[i] - truth[i]);
+    r.l1 += d;
+    if (truth[i] >= mu) {
+      ++r.nodes_above_mu;
+      r.max_rel_above_mu = std::max(r.max_rel_above_mu, d / truth[i]);
+      if (d / truth[i] > epsilon) ++r.violations;
+    }
+  }
+  return r;
+}
+
+PPRVector ground_truth(const Graph& g, NodeId s, double alpha) {
+  if (s >= g.n()) throw std::invalid_argument("source out of range");
+  PPRVector v = make_vector(g.n(), s, alpha);
+  pprg_query_stats qs{};
+  check(pprg_ground_truth(g.device_handle(), &s, 1, alpha, v.estimates.data(), 0, &qs, nullptr));
+  v.achieved_r_sum = qs.achieved_r_sum;
+  v.pushes = qs.pushes;
+  return v;
+}
+
+// ---- csv.hpp (csv.cpp:9-43) --------------------------------------------------------
+std::string format_double(double value) {
+  char buffer[40];
+  std::snprintf(buffer, sizeof(buffer), "%.17g", value);
+  return buffer;
+}
+
+void write_ppr_csv(const std::string& path, std::span<const double> values) {
+  std::ofstream out(path, std::ios::trunc);
+  if (!out) throw std::runtime_error("cannot open for writing: " + path);
+  out << "node,ppr\n";
+  for (std::size_t v = 0; v < values.size(); ++v) out << v << ',' << format_double(values[v]) << '\n';
+  if (!out) throw std::runtime_error("write failed: " + path);
+}
+
+std::vector<double> read_ppr_csv(const std::string& path) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open: " + path);
+  std::string line;
+  if (!std::getline(in, line) || line != "node,ppr")
+    throw std::runtime_error(path + ": missing node,ppr header");
+  std::vector<double> values;
+  std::uint64_t expected = 0;
+  while (std::getline(in, line)) {
+    if (line.empty()) continue;
+    const auto comma = line.find(',');
+    if (comma == std::string::npos) throw std::runtime_error(path + ": malformed row: " + line);
+    if (std::stoull(line.substr(0, comma)) != expected)
+      throw std::runtime_error(path + ": node ids must be consecutive from 0");
+    values.push_back(std::stod(line.substr(comma + 1)));
+    ++expected;
+  }
+  return values;
 }
 
 }  // namespace ppr

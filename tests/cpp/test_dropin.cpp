@@ -9,7 +9,9 @@
 #include <string>
 #include <vector>
 
+#include "ppr/csv.hpp"
 #include "ppr/graph.hpp"
+#include "ppr/metrics.hpp"
 #include "ppr/push.hpp"
 #include "ppr/speedppr.hpp"
 #include "ppr/walk_index.hpp"
@@ -142,5 +144,22 @@ int main() {
     CHECK_THROWS_AS(speedppr_query(g, 0, c2, &other), std::runtime_error);
   }
   std::printf("%s: %d failure(s)\n", failures ? "FAILED" : "OK", failures);
+  {  // test_metrics.cpp:66-76, 85-93
+    const PPRVector a = ground_truth(g, 0, 0.2);
+    const PPRVector b = ground_truth(g, 0, 0.2);
+    CHECK(a.estimates == b.estimates);
+    const double pi0[5] = {0.29366106080206994, 0.27166882276843485, 0.23285899094437276,
+                           0.1474773609314361, 0.054333764553686985};
+    double l1 = 0.0, total = 0.0;
+    for (int v = 0; v < 5; ++v) l1 += std::fabs(a.estimates[v] - pi0[v]), total += a.estimates[v];
+    CHECK(l1 <= 1e-12);
+    CHECK(std::fabs(total - 1.0) <= 1e-12);
+    CHECK(a.achieved_r_sum <= kGroundTruthLambda);
+    CHECK(compare_to_truth(a.estimates, a.estimates, 0.2, 0.0).violations == 0);
+    const std::vector<double> vals = {0.29366106080206994, 1e-17, 0.0, 2.0 / 3.0, 5.4333764553686985e-2};
+    write_ppr_csv("/tmp/pprg_dropin_vals.csv", vals);
+    CHECK(read_ppr_csv("/tmp/pprg_dropin_vals.csv") == vals);
+    std::remove("/tmp/pprg_dropin_vals.csv");
+  }
   return failures;
 }
