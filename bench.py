@@ -183,6 +183,7 @@ def run_reference_arm(args, world, rank):
     # the timed region is the reference's own power_push on its own Graph.
     g, srcs = make_graph(P, 0)
     off, nbr = g.out_offsets().copy(), g.out_neighbors().copy()
+    cfg = workload_config(P, g, g.block_columns(len(srcs)))
     del g
     from oracle.pyoracle import CSR, Ref
     ref = Ref()
@@ -204,7 +205,7 @@ def run_reference_arm(args, world, rank):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(P, None, 0),
+            "config": cfg,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": f"{per_step} power_push queries per step on {threads} "
                                        f"threads (reference libppr_core, -O3)"},
