@@ -164,6 +164,16 @@ int pprg_part_finish(pprg_part* p, double* reserve_out, double* residue_out, uin
                      double* residue_sums);
 int pprg_part_stats(const pprg_part* p, pprg_query_stats* qstats, pprg_call_stats* cstats);
 void pprg_part_destroy(pprg_part* p);
+/* Fused exchange (instead of the y all-gather): the sweep kernel stores every
+ * pushed y row of this part straight into the peers' y buffers (other GPUs'
+ * buffers over NVLink via the IPC calls below, or other parts' buffers on the
+ * same device). Set before pprg_part_start; up to 15 peers. With peers set
+ * the per-sweep y exchange is skipped (counters are still all-reduced, which
+ * also orders every part's sweep before the next). */
+int pprg_part_set_peers(pprg_part* p, double* const* peer_y, uint32_t npeers);
+int pprg_part_ipc_handle(pprg_part* p, void* handle /* 64 bytes, cudaIpcMemHandle_t */);
+int pprg_ipc_open(int device, const void* handle, void** ptr);
+int pprg_ipc_close(int device, void* ptr);
 
 /* Columns (sources) per device block for a k-source call: the batch width the
  * engines use (a power of two, padding columns inert). Not in the reference. */

@@ -462,6 +462,41 @@ int pprg_part_stats(const pprg_part* p, pprg_query_stats* q, pprg_call_stats* c)
   });
 }
 
+int pprg_part_set_peers(pprg_part* p, double* const* peer_y, uint32_t npeers) {
+  return guard([&] {
+    require(p && (npeers == 0 || peer_y), "partition: null argument");
+    pprg::part_set_peers(p->s, peer_y, npeers);
+  });
+}
+
+int pprg_part_ipc_handle(pprg_part* p, void* handle) {
+  return guard([&] {
+    require(p && handle, "partition: null argument");
+    pprg::DeviceGuard dg(pprg::part_device(p->s));
+    uint32_t cols = 0;
+    cudaIpcMemHandle_t h;
+    PPRG_CUDA(cudaIpcGetMemHandle(&h, pprg::part_y(p->s, &cols)));
+    std::memcpy(handle, &h, sizeof h);
+  });
+}
+
+int pprg_ipc_open(int device, const void* handle, void** ptr) {
+  return guard([&] {
+    require(handle && ptr, "ipc: null argument");
+    pprg::DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    PPRG_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+int pprg_ipc_close(int device, void* ptr) {
+  return guard([&] {
+    pprg::DeviceGuard dg(device);
+    PPRG_CUDA(cudaIpcCloseMemHandle(ptr));
+  });
+}
+
 void pprg_part_destroy(pprg_part* p) {
   if (!p) return;
   pprg::part_destroy(p->s);

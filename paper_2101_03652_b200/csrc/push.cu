@@ -38,7 +38,8 @@ constexpr int EMAX = 64;   // max epochs
 #ifndef PPRG_NT
 #define PPRG_NT 128
 #endif
-constexpr int NT = PPRG_NT;             // threads per block for the sweep kernels
+constexpr int NT = PPRG_NT;
+#define PPRG_MAX_PEERS 15             // threads per block for the sweep kernels
 constexpr int SWEEP_ELEMS = NT * 8;     // edges x columns per tile (8 per thread)
 
 enum SweepMode : int { M_POWERPUSH = 0, M_POWITR = 1, M_SIMFWD = 2, M_FINAL = 3 };
@@ -103,6 +104,8 @@ struct SweepParams {
   double* out_residue;
   double* res_inter;           // finalize: explicit residues back into [u*K + c] (SpeedPPR)
   uint32_t max_sweeps;
+  double* peer_y[PPRG_MAX_PEERS];  // fused exchange: other parts' y buffers (P2P / same device)
+  int npeers;
   TracePoint* trace;            // per-sweep progress of column 0 (traced calls), or null
   uint32_t trace_cap;
   uint64_t own_lo, own_hi;      // node range this launch owns (vertex partition; else [0, n))
@@ -164,7 +167,11 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
     const double r = inflow - xo;
     if (r > (dg ? (double)dg : 1.0) * thr_cur[c]) {
       st_state(P.x + ix, inflow);
-      if (dg) P.y[0][ix] = oma * inflow * inv;
+      if (dg) {
+        const double yv = oma * inflow * inv;
+        P.y[0][ix] = yv;
+        for (int p = 0; p < P.npeers; ++p) P.peer_y[p][ix] = yv;  // fused exchange
+      }
       a.push += r;
       a.np += dg ? dg : 1;
       a.nn += 1;
@@ -1922,11 +1929,19 @@ __global__ void k_part_sums(const double* x, const uint32_t* deg, uint64_t lo, u
   }
 }
 
+struct PeerSet {
+  double* y[PPRG_MAX_PEERS];
+  int n;
+};
+
 __global__ void k_part_y(const double* x, const double* inv_deg, uint64_t lo, uint64_t hi, int K,
-                         double alpha, double* y) {
+                         double alpha, double* y, const PeerSet peers) {
   for (uint64_t i = lo * K + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi * K;
-       i += (uint64_t)gridDim.x * blockDim.x)
-    y[i] = (1.0 - alpha) * x[i] * inv_deg[i / K];
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = (1.0 - alpha) * x[i] * inv_deg[i / K];
+    y[i] = v;
+    for (int p = 0; p < peers.n; ++p) peers.y[p][i] = v;
+  }
 }
 
 __global__ void k_pack_counters(const SweepCtl* ctl, int K, double* out) {
@@ -2004,6 +2019,7 @@ struct PartSession {
   CallStats call;
   uint64_t own_alg_bytes = 0;
   uint32_t sweeps = 0;
+  std::vector<double*> peers;  // fused exchange targets (other parts' y)
 };
 
 PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t* sources,
@@ -2060,6 +2076,7 @@ PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t
   const uint64_t nk = g.n * (uint64_t)K;
   PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, st));
   PPRG_CUDA(cudaMemsetAsync(b.w.res.get(), 0, 8 * nk, st));
+  PPRG_CUDA(cudaMemsetAsync(b.w.y0.get(), 0, 8 * nk, st));  // y = 0 is a valid stale value
   k_seed<<<1, KMAX, 0, st>>>(b.w.res.get(), b.w.d_src.get(), K, 1.0);
   const double r_max = lambda / (double)g.m_eff();
   const uint64_t limit = scan_threshold < 0 ? g.n / 4 : (uint64_t)scan_threshold;
@@ -2104,9 +2121,12 @@ bool part_start(PartSession* s, const double* summed) {
   std::vector<double> sx(summed, summed + K), sd(summed + KMAX, summed + KMAX + K);
   const bool any = epoch_init(s->st.data(), K, sx.data(), sd.data(), s->lam.data(), s->E, b.alpha);
   for (int c = 0; c < K; ++c) s->used_scan[c] = s->st[c].r_sum > s->lambda;  // push.cpp:168
+  PeerSet ps{};
+  ps.n = (int)s->peers.size();
+  for (int p = 0; p < ps.n; ++p) ps.y[p] = s->peers[p];
   if (s->hi > s->lo)
     k_part_y<<<grid_for((s->hi - s->lo) * K), 256, 0, g.stream>>>(b.w.x.get(), g.inv_deg.get(), s->lo,
-                                                                  s->hi, K, b.alpha, b.w.y0.get());
+                                                                  s->hi, K, b.alpha, b.w.y0.get(), ps);
   PPRG_CUDA(cudaGetLastError());
   PPRG_CUDA(cudaStreamSynchronize(g.stream));
   s->call.kernel_launches += 1;
@@ -2123,7 +2143,14 @@ static SweepParams part_params(PartSession* s) {
   P.x = b.w.x.get();
   P.y[0] = P.y[1] = b.w.y0.get();
   for (int c = 0; c < b.K; ++c) P.init[c] = s->st[c];
+  P.npeers = (int)s->peers.size();
+  for (int p = 0; p < P.npeers; ++p) P.peer_y[p] = s->peers[p];
   return P;
+}
+
+void part_set_peers(PartSession* s, double* const* peer_y, uint32_t npeers) {
+  if (npeers > PPRG_MAX_PEERS) fail(EINVAL_, "partition: too many peers");
+  s->peers.assign(peer_y, peer_y + npeers);
 }
 
 void part_sweep(PartSession* s, double* local_host) {
@@ -2239,6 +2266,7 @@ double* part_y(PartSession* s, uint32_t* K) {
   return s->b->w.y0.get();
 }
 double* part_counters(PartSession* s) { return s->counters.get(); }
+int part_device(const PartSession* s) { return s->g->device; }
 
 void part_destroy(PartSession* s) {
   if (!s) return;

@@ -63,6 +63,10 @@ def _bind(L):
     L.pprg_part_stats.argtypes = [vp, vp, vp]
     L.pprg_part_destroy.argtypes = [vp]
     L.pprg_part_destroy.restype = None
+    L.pprg_part_set_peers.argtypes = [vp, vp, C.c_uint32]
+    L.pprg_part_ipc_handle.argtypes = [vp, vp]
+    L.pprg_ipc_open.argtypes = [C.c_int, vp, C.POINTER(vp)]
+    L.pprg_ipc_close.argtypes = [C.c_int, vp]
     L.pprg_epoch_init.argtypes = [vp, C.c_uint32, vp, vp, vp, C.c_uint32, C.c_double,
                                   C.POINTER(C.c_int)]
     L.pprg_epoch_advance.argtypes = [vp, C.c_uint32, vp, vp, C.c_uint32, C.c_double,
@@ -153,6 +157,21 @@ class GpuPart:
         _check(_lib().pprg_part_start(self.h, _p(s), C.byref(need)))
         return bool(need.value)
 
+    def set_peers(self, ptrs: Sequence[int]):
+        """Fused exchange: this part's sweeps store pushed y rows into these
+        device buffers (other parts' y) instead of a per-sweep all-gather."""
+        arr = (C.c_void_p * max(len(ptrs), 1))(*ptrs)
+        _check(_lib().pprg_part_set_peers(self.h, arr, len(ptrs)))
+        self.fused = len(ptrs) > 0
+
+    def y_ptr(self) -> int:
+        return self._y
+
+    def ipc_handle(self) -> bytes:
+        buf = (C.c_ubyte * 64)()
+        _check(_lib().pprg_part_ipc_handle(self.h, buf))
+        return bytes(buf)
+
     def y_view(self):
         return _device_view(self._y, self.n * self.columns, self.g.device)
 
@@ -201,10 +220,34 @@ class PartitionResult:
     local_stats: object = None
 
 
-def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None) -> PartitionResult:
+def _open_peer_buffers(part, group, dev):
+    """IPC-map every other rank's y buffer on this GPU (fused exchange)."""
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    mine = torch.tensor(list(part.ipc_handle()), dtype=torch.uint8, device=dev)
+    allh = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(allh, mine, group=group)
+    L = _lib()
+    ptrs = []
+    for r in range(world):
+        if r == rank:
+            continue
+        h = bytes(allh[r].cpu().numpy().tolist())
+        p = C.c_void_p()
+        _check(L.pprg_ipc_open(part.g.device, h, C.byref(p)))
+        ptrs.append(p.value)
+    return ptrs
+
+
+def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None,
+                    fused: bool = False) -> PartitionResult:
     """Drive one part through the exchange protocol with torch.distributed.
     `part` exposes begin/start/y_view/counters_view/sweep/advance/finish and
-    lo/hi/columns; tensors live on `comm_device` (cuda for NCCL, cpu for gloo)."""
+    lo/hi/columns; tensors live on `comm_device` (cuda for NCCL, cpu for gloo).
+    fused=True (GPU parts, one GPU per rank): the sweeps store pushed y rows
+    straight into the peers' IPC-mapped y buffers, and the per-sweep y
+    all-gather is skipped."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
@@ -217,6 +260,9 @@ def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None) -> P
         return t.cpu().numpy()
 
     partial = part.begin()
+    peers = _open_peer_buffers(part, group, dev) if fused else []
+    if fused:
+        part.set_peers(peers)
     need = part.start(allreduce_np(partial))
     mine = torch.tensor([part.lo, part.hi], dtype=torch.int64, device=dev)
     allb = [torch.empty_like(mine) for _ in range(world)]
@@ -227,6 +273,8 @@ def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None) -> P
     y = part.y_view()
 
     def exchange():  # all-gather-v of the y row slices; the final pass needs it too
+        if fused:
+            return
         for p, (lo, hi) in enumerate(bounds):
             if hi > lo:
                 dist.broadcast(y[lo * Cw:hi * Cw], src=ranks[p], group=group)
@@ -243,19 +291,28 @@ def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None) -> P
         exchange()
         sweeps += 1
     rs = allreduce_np(part.finish(**(finish_kwargs or {})))
+    if fused:
+        dist.barrier(group=group)  # every rank's final pass has read the peers' y
+        for p in peers:
+            _check(_lib().pprg_ipc_close(part.g.device, p))
     return PartitionResult(rs, sweeps, (part.lo, part.hi), bounds)
 
 
 def run_virtual_parts(g: _abi.Graph, nparts: int, sources: Sequence[int], alpha: float, lam: float,
-                      epoch_num: int = 8, scan_threshold: Optional[int] = None):
+                      epoch_num: int = 8, scan_threshold: Optional[int] = None,
+                      fused: bool = False):
     """P parts of one query block on ONE GPU, run one after another each sweep;
-    the exchange is device copies between the parts' y buffers and host sums
-    of their counters. Returns (reserve [k, n], residue [k, n], r_sum [k],
-    sweeps, parts). No part ever waits on another."""
+    the exchange is device copies between the parts' y buffers (or, fused,
+    each part's sweep storing its pushed rows into the others' buffers) and
+    host sums of their counters. Returns (reserve [k, n], residue [k, n],
+    r_sum [k], sweeps, parts). No part ever waits on another."""
     import torch
     parts = [GpuPart(g, nparts, p, sources, alpha, lam, epoch_num, scan_threshold)
              for p in range(nparts)]
     partial = sum(p.begin() for p in parts)
+    if fused:
+        for p in parts:
+            p.set_peers([q.y_ptr() for q in parts if q is not p])
     need = [p.start(partial) for p in parts]
     assert len(set(need)) == 1
     need = need[0]
@@ -263,6 +320,9 @@ def run_virtual_parts(g: _abi.Graph, nparts: int, sources: Sequence[int], alpha:
     ys = [p.y_view() for p in parts]
 
     def exchange():
+        if fused:
+            torch.cuda.synchronize(g.device)
+            return
         for src in parts:
             if src.hi > src.lo:
                 sl = slice(src.lo * Cw, src.hi * Cw)

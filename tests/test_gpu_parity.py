@@ -348,8 +348,9 @@ def test_speedppr_batch_push_branch(P, oracle, use_index):
 
 
 # ---- (5) vertex-partitioned power_push (configs[4]) ----------------
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("nparts,k", [(2, 1), (3, 4), (8, 1), (8, 64)])
-def test_partitioned_power_push_virtual(P, oracle, nparts, k):
+def test_partitioned_power_push_virtual(P, oracle, nparts, k, fused):
     """P parts of one block on one GPU (sequential, slices copied between
     them) against the oracle's power_push: per node |diff| <= lambda, and the
     exact all-part r_sum <= lambda."""
@@ -358,7 +359,7 @@ def test_partitioned_power_push_virtual(P, oracle, nparts, k):
     c = gcsr(g)
     lam = 1e-8
     src = P.sample_sources(np.diff(g.out_offsets()), k, 31)
-    res, rsd, rs, sweeps, parts = run_virtual_parts(g, nparts, src, 0.2, lam)
+    res, rsd, rs, sweeps, parts = run_virtual_parts(g, nparts, src, 0.2, lam, fused=fused)
     bounds = [(p.lo, p.hi) for p in parts]
     assert bounds[0][0] == 0 and bounds[-1][1] == g.n()
     assert all(bounds[i][1] == bounds[i + 1][0] for i in range(nparts - 1))
@@ -373,13 +374,14 @@ def test_partitioned_power_push_virtual(P, oracle, nparts, k):
         p.close()
 
 
-def test_partitioned_local_phase_only(P, oracle):
+@pytest.mark.parametrize("fused", [False, True])
+def test_partitioned_local_phase_only(P, oracle, fused):
     """lambda reached by the queue phase: no sweeps, outputs still exact."""
     from paper_2101_03652_b200.partition import run_virtual_parts
     g = dev(P, oracle.random_graph(400, 1, 6, 9))
     c = gcsr(g)
     res, rsd, rs, sweeps, parts = run_virtual_parts(g, 3, [5], 0.2, 1e-2,
-                                                    scan_threshold=10 ** 9)
+                                                    scan_threshold=10 ** 9, fused=fused)
     ref = oracle.power_push(c, 5, 0.2, 1e-2, scan_threshold=10 ** 9)
     assert sweeps == 0 and rs[0] <= 1e-2
     assert np.max(np.abs(res[0] - ref.estimates)) <= 1e-2

@@ -42,7 +42,8 @@ def virtual(a):
         outs, cs = P.power_push_batch(g, [s], ALPHA, LAM)
         single = time.perf_counter() - t0
         t0 = time.perf_counter()
-        res, rsd, rs, sweeps, parts = run_virtual_parts(g, a.parts, [s], ALPHA, LAM)
+        res, rsd, rs, sweeps, parts = run_virtual_parts(g, a.parts, [s], ALPHA, LAM,
+                                                        fused=a.fused)
         virt = time.perf_counter() - t0
         per = [p.stats()[1] for p in parts]
         recs.append({
@@ -60,7 +61,8 @@ def virtual(a):
             p.close()
         print(json.dumps(recs[-1]), flush=True)
     return {"config": f"configs[4] vertex-partitioned into {a.parts} parts, run as virtual parts "
-                      "on one GPU", "n": n, "m": g.m(), "generate_s": gen, "queries": recs}
+                      f"on one GPU ({'fused P2P-style y stores' if a.fused else 'y all-gather'} "
+                      "exchange)", "n": n, "m": g.m(), "generate_s": gen, "queries": recs}
 
 
 def dist_mode(a):
@@ -79,7 +81,7 @@ def dist_mode(a):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         part = GpuPart(g, world, rank, [s], ALPHA, LAM)
-        r = run_partitioned(part, comm_device=f"cuda:{local}")
+        r = run_partitioned(part, comm_device=f"cuda:{local}", fused=a.fused and world > 1)
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
         t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{local}")
@@ -103,6 +105,7 @@ def main():
     ap.add_argument("--scale", type=int, default=25)
     ap.add_argument("--ef", type=int, default=32)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--fused", action="store_true", help="fused exchange (y stores into peers)")
     a = ap.parse_args()
     rec = virtual(a) if a.mode == "virtual" else dist_mode(a)
     if rec is not None and a.out:
