@@ -398,8 +398,14 @@ __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& 
 // K contiguous values straight into registers (lanes = edge slots x columns),
 // so no value staging in shared memory and no per-tile hub split below WIDE_T.
 constexpr int WIDE_K = 4;
-constexpr uint32_t WIDE_T = 4096;
-constexpr uint32_t RMAX_W = 256;
+#ifndef PPRG_WIDE_T
+#define PPRG_WIDE_T 4096
+#endif
+#ifndef PPRG_RMAX_W
+#define PPRG_RMAX_W 256
+#endif
+constexpr uint32_t WIDE_T = PPRG_WIDE_T;
+constexpr uint32_t RMAX_W = PPRG_RMAX_W;
 
 // Sum of y over the in-edges [b, e) of one row for my columns, by one warp.
 // Lanes = ES edge slots x KC column lanes (x CPL contiguous columns). The ids
@@ -496,7 +502,10 @@ __device__ __forceinline__ uint32_t* wide_long_count(char* smem) {
 // Wide column blocks: warps take rows from a shared counter and sum each row
 // with warp_row_sum; rows longer than LONG_W in-edges are summed by all warps
 // of the block together (partials in shared memory) so no warp lags the tile.
-constexpr uint32_t LONG_W = 384;
+#ifndef PPRG_LONG_W
+#define PPRG_LONG_W 384
+#endif
+constexpr uint32_t LONG_W = PPRG_LONG_W;
 
 template <int K, int MODE>
 __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileDesc& d, char* smem,
