@@ -198,6 +198,19 @@ int pprg_run_traced(pprg_graph* g, int algo, uint32_t source, double alpha, doub
                     double* estimates_out, pprg_query_stats* qstats, pprg_checkpoint* points,
                     uint32_t capacity, uint32_t* count);
 
+/* One single-source query with a step observer (PushObserver, push.hpp:62-70,
+ * at step granularity): after every frontier level, global sweep or
+ * iteration, cb receives the full reserve / residue (host, n doubles each,
+ * valid during the call), r_sum and the cumulative edge pushes. param is
+ * lambda, or r_max for PPRG_ALGO_FIFO (with lambda_stop, <= 0 = none);
+ * epoch_num / scan_threshold as pprg_power_push (0 / -1 = defaults). */
+typedef void (*pprg_step_callback)(void* user, const double* reserve, const double* residue,
+                                   double r_sum, uint64_t pushes, uint32_t step);
+int pprg_run_observed(pprg_graph* g, int algo, uint32_t source, double alpha, double param,
+                      double lambda_stop, uint32_t epoch_num, int64_t scan_threshold,
+                      double* reserve_out, double* residue_out, pprg_query_stats* qstats,
+                      pprg_step_callback cb, void* user);
+
 /* ground_truth(g, s, alpha) metrics.hpp:41, metrics.cpp:44-55: the answer at
  * lambda = 1e-17 (r_sum <= 1e-17 on exit), for k sources; graphs with
  * n <= 2000 are cross-checked against an independent engine (l1 <= 1e-12,
@@ -205,6 +218,14 @@ int pprg_run_traced(pprg_graph* g, int algo, uint32_t source, double alpha, doub
 int pprg_ground_truth(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
                       double* estimates_out, uint32_t flags, pprg_query_stats* qstats,
                       pprg_call_stats* cstats);
+
+/* refine(g, s, alpha, r_max, state) push.hpp:118-119, push.cpp:208-222, on k
+ * caller states (reserve / residue, k x n query-major, updated in place):
+ * every active node in id order, drained until no residue exceeds
+ * deg_eff * r_max; qstats pushes = the refine's pushes, r_sum = exact. */
+int pprg_refine(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha, double r_max,
+                double* reserve_inout, double* residue_inout, uint32_t flags,
+                pprg_query_stats* qstats, pprg_call_stats* cstats);
 
 /* ---- SpeedPPR (speedppr.hpp, walk_index.hpp) ------------------------------- */
 /* compute_walk_budget(n, eps, mu) speedppr.hpp:16-17 */

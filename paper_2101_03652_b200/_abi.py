@@ -102,6 +102,8 @@ def load_library(path: str = lib_path):
     L.pprg_power_push.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
                                   C.c_int64, vp, vp, C.c_uint32, vp, vp, vp]
     L.pprg_walk_budget.argtypes = [C.c_uint64, C.c_double, C.c_double, u64p]
+    L.pprg_refine.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_double, vp, vp, C.c_uint32, vp,
+                              vp]
     L.pprg_ground_truth.argtypes = [vp, vp, C.c_uint32, C.c_double, vp, C.c_uint32, vp, vp]
     L.pprg_block_columns.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint32)]
     L.pprg_index_build.argtypes = [vp, C.c_double, C.c_uint64, C.POINTER(vp)]
@@ -415,6 +417,23 @@ def fifo_forward_push(g: Graph, s: int, alpha: float, r_max: float,
                                        lambda_stop if lambda_stop is not None else -1.0, rp, dp,
                                        flags, q, C.byref(cs)))
     return _vectors(src, res, rsd, q, alpha)[0]
+
+
+def refine(g: Graph, s: int, alpha: float, r_max: float, state: PPRVector) -> PPRVector:
+    """refine (push.hpp:118-119, push.cpp:208-222) of a push state given as a
+    PPRVector (estimates = reserve, residues); returns the refined state."""
+    load_library()
+    if not (r_max > 0.0):
+        raise InvalidArgument("refine: r_max must be positive")
+    src = _sources([s])
+    res = np.ascontiguousarray(state.estimates, np.float64).copy().reshape(1, -1)
+    rsd = np.ascontiguousarray(state.residues, np.float64).copy().reshape(1, -1)
+    q = (QStats * 1)()
+    _check(_lib.pprg_refine(g.handle, _ptr(src), 1, alpha, r_max, res.ctypes.data, rsd.ctypes.data,
+                            0, q, None))
+    out = _vectors(src, res, rsd, q, alpha)[0]
+    out.pushes = state.pushes + q[0].pushes
+    return out
 
 
 GROUND_TRUTH_LAMBDA = 1e-17  # kGroundTruthLambda, metrics.hpp:10

@@ -55,6 +55,42 @@ void notify(PushObserver* obs, const PPRVector& v, std::uint32_t iterations) {
   obs->on_iteration(st, iterations);
 }
 
+// With an observer: run the query observed (pprg_run_observed); after every
+// frontier level / global sweep / iteration the library hands over the full
+// reserve and residue, mirrored into a PushState for on_push / on_iteration
+// (step granularity, never per push).
+struct ObsCtx {
+  PushObserver* obs;
+  PushState* st;
+};
+
+void step_cb(void* user, const double* reserve, const double* residue, double r_sum,
+             std::uint64_t pushes, std::uint32_t step) {
+  auto* c = static_cast<ObsCtx*>(user);
+  const std::size_t n = c->st->reserve.size();
+  std::copy(reserve, reserve + n, c->st->reserve.begin());
+  std::copy(residue, residue + n, c->st->residue.begin());
+  c->st->r_sum = r_sum;
+  c->st->edge_push_count = pushes;
+  c->obs->on_push(*c->st);
+  c->obs->on_iteration(*c->st, step);
+}
+
+bool observed(const Graph& g, int algo, NodeId s, double alpha, double param, double lambda_stop,
+              std::uint32_t epochs, std::int64_t scan, PushObserver* obs, PPRVector& v,
+              pprg_query_stats* qout = nullptr) {
+  if (!obs) return false;
+  PushState st(g.n(), s);
+  ObsCtx ctx{obs, &st};
+  pprg_query_stats q{};
+  check(pprg_run_observed(g.device_handle(), algo, s, alpha, param, lambda_stop, epochs, scan,
+                          v.estimates.data(), v.residues.data(), &q, step_cb, &ctx));
+  v.achieved_r_sum = q.achieved_r_sum;
+  v.pushes = q.pushes;
+  if (qout) *qout = q;
+  return true;
+}
+
 void write_u64(std::ofstream& o, std::uint64_t v) {
   char b[8];
   for (int i = 0; i < 8; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
@@ -157,6 +193,7 @@ PPRVector power_iteration(const Graph& g, NodeId s, double alpha, double lambda,
                           PushObserver* observer) {
   PPRVector v = make_vector(g.n(), s, alpha);
   pprg_query_stats q{};
+  if (observed(g, PPRG_ALGO_POWITR, s, alpha, lambda, 0.0, 0, -1, observer, v)) return v;
   check(pprg_power_iteration(g.device_handle(), &s, 1, alpha, lambda, v.estimates.data(),
                              v.residues.data(), 0, &q, nullptr));
   v.achieved_r_sum = q.achieved_r_sum;
@@ -169,6 +206,7 @@ PPRVector sim_forward_push(const Graph& g, NodeId s, double alpha, double lambda
                            PushObserver* observer) {
   PPRVector v = make_vector(g.n(), s, alpha);
   pprg_query_stats q{};
+  if (observed(g, PPRG_ALGO_SIMFWDPUSH, s, alpha, lambda, 0.0, 0, -1, observer, v)) return v;
   check(pprg_sim_forward_push(g.device_handle(), &s, 1, alpha, lambda, v.estimates.data(),
                               v.residues.data(), 0, &q, nullptr));
   v.achieved_r_sum = q.achieved_r_sum;
@@ -181,6 +219,9 @@ PPRVector fifo_forward_push(const Graph& g, NodeId s, double alpha, double r_max
                             std::optional<double> lambda_stop, PushObserver* observer) {
   PPRVector v = make_vector(g.n(), s, alpha);
   pprg_query_stats q{};
+  if (observed(g, PPRG_ALGO_FIFO, s, alpha, r_max, lambda_stop ? *lambda_stop : -1.0, 0, -1,
+               observer, v))
+    return v;
   check(pprg_fifo_forward_push(g.device_handle(), &s, 1, alpha, r_max,
                                lambda_stop ? *lambda_stop : -1.0, v.estimates.data(),
                                v.residues.data(), 0, &q, nullptr));
@@ -194,6 +235,21 @@ PPRVector power_push(const Graph& g, NodeId s, double alpha, double lambda,
                      const QueryConfig& cfg, PushObserver* observer, PowerPushTrace* trace) {
   PPRVector v = make_vector(g.n(), s, alpha);
   pprg_query_stats q{};
+  if (observer) {
+    if (!(lambda > 0.0 && lambda <= 1.0))
+      throw std::invalid_argument("power_push: lambda must be in (0,1]");  // push.cpp:154-155
+    observed(g, PPRG_ALGO_POWERPUSH, s, alpha, lambda, 0.0, cfg.epoch_num,
+             cfg.scan_threshold ? static_cast<int64_t>(*cfg.scan_threshold) : -1, observer, v, &q);
+    if (trace) {  // push.cpp:168-180
+      trace->used_scan_phase = q.used_scan_phase != 0;
+      trace->epoch_r_max.clear();
+      const double m_eff = static_cast<double>(g.effective_edge_count());
+      if (trace->used_scan_phase)
+        for (std::uint32_t e = 1; e <= cfg.epoch_num; ++e)
+          trace->epoch_r_max.push_back(std::pow(lambda, static_cast<double>(e) / cfg.epoch_num) / m_eff);
+    }
+    return v;
+  }
   std::vector<double> eps(cfg.epoch_num);
   check(pprg_power_push(g.device_handle(), &s, 1, alpha, lambda, cfg.epoch_num,
                         cfg.scan_threshold ? static_cast<int64_t>(*cfg.scan_threshold) : -1,
@@ -334,6 +390,55 @@ PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
   v.pushes = q.pushes;
   v.walks = q.walks;
   return v;
+}
+
+// ---- push state (push.cpp:9-15, 70-79, 201-222) -----------------------------------
+void PushState::recompute_r_sum() {
+  double total = 0.0;
+  for (double r : residue) total += r;
+  if (std::abs(total - r_sum) > 1e-6)
+    throw std::logic_error("push: r_sum drifted more than 1e-6 from the residues");
+  r_sum = total;
+}
+
+PushState power_push_state(const Graph& g, NodeId s, double alpha, double lambda,
+                           const QueryConfig& cfg, PushObserver* observer, PowerPushTrace* trace) {
+  PPRVector v = power_push(g, s, alpha, lambda, cfg, observer, trace);
+  PushState st(g.n(), s);
+  st.reserve = std::move(v.estimates);
+  st.residue = std::move(v.residues);
+  st.r_sum = v.achieved_r_sum;
+  st.edge_push_count = v.pushes;
+  return st;
+}
+
+void refine(const Graph& g, NodeId s, double alpha, double r_max, PushState& state,
+            PushObserver* observer) {
+  if (!(r_max > 0.0)) throw std::invalid_argument("refine: r_max must be positive");
+  if (state.reserve.size() != g.n() || state.residue.size() != g.n())
+    throw std::invalid_argument("refine: state size does not match the graph");
+  pprg_query_stats q{};
+  check(pprg_refine(g.device_handle(), &s, 1, alpha, r_max, state.reserve.data(),
+                    state.residue.data(), 0, &q, nullptr));
+  state.queue.clear();
+  std::fill(state.in_queue.begin(), state.in_queue.end(), 0);
+  state.r_sum = q.achieved_r_sum;
+  state.edge_push_count += q.pushes;
+  if (observer) {
+    observer->on_push(state);
+    observer->on_iteration(state, q.local_levels);
+  }
+}
+
+PPRVector finish_state(PushState&& state, NodeId source, double alpha) {
+  PPRVector out;
+  out.estimates = std::move(state.reserve);
+  out.residues = std::move(state.residue);
+  out.source = source;
+  out.alpha = alpha;
+  out.achieved_r_sum = state.r_sum;
+  out.pushes = state.edge_push_count;
+  return out;
 }
 
 // ---- metrics.hpp (metrics.cpp:11-55) ---------------------------------------------

@@ -306,6 +306,41 @@ int pprg_run_traced(pprg_graph* g, int algo, uint32_t source, double alpha, doub
   });
 }
 
+int pprg_run_observed(pprg_graph* g, int algo, uint32_t source, double alpha, double param,
+                      double lambda_stop, uint32_t epoch_num, int64_t scan_threshold,
+                      double* reserve_out, double* residue_out, pprg_query_stats* q,
+                      pprg_step_callback cb, void* user) {
+  return guard([&] {
+    require(g && g->g && cb, "null argument");
+    require(algo >= PPRG_ALGO_POWITR && algo <= PPRG_ALGO_POWERPUSH, "unknown algorithm");
+    check_alpha(alpha);
+    pprg::Graph& G = *g->g;
+    if (algo == PPRG_ALGO_FIFO)
+      require(param > 0.0, "fifo_forward_push: r_max must be positive");  // push.cpp:142
+    else if (algo == PPRG_ALGO_POWERPUSH)
+      require(param > 0.0 && param <= 1.0, "power_push: lambda must be in (0,1]");
+    pprg::StepSink sink;
+    sink.cb = cb;
+    sink.user = user;
+    struct Reset {
+      ~Reset() { pprg::g_obs = nullptr; }
+    } reset;
+    pprg::g_obs = &sink;
+    std::vector<pprg::ColumnStats> cs(1);
+    pprg::CallStats call;
+    pprg::Outputs out{reserve_out, residue_out, false};
+    const pprg::Engine eng = algo == PPRG_ALGO_POWITR       ? pprg::Engine::PowItr
+                             : algo == PPRG_ALGO_SIMFWDPUSH ? pprg::Engine::SimFwdPush
+                             : algo == PPRG_ALGO_FIFO       ? pprg::Engine::Fifo
+                                                            : pprg::Engine::PowerPush;
+    pprg::run_push_engine(G, eng, &source, 1, alpha, eng == pprg::Engine::Fifo ? 0.0 : param,
+                          epoch_num ? epoch_num : 8, scan_threshold,
+                          eng == pprg::Engine::Fifo ? param : 0.0,
+                          lambda_stop > 0.0 ? lambda_stop : 0.0, out, cs.data(), &call);
+    fill_stats(cs, call, 1, q, nullptr);
+  });
+}
+
 int pprg_ground_truth(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha,
                       double* estimates_out, uint32_t flags, pprg_query_stats* q,
                       pprg_call_stats* c) {
@@ -501,6 +536,22 @@ void pprg_part_destroy(pprg_part* p) {
   if (!p) return;
   pprg::part_destroy(p->s);
   delete p;
+}
+
+int pprg_refine(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha, double r_max,
+                double* reserve_inout, double* residue_inout, uint32_t flags,
+                pprg_query_stats* q, pprg_call_stats* c) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    require(k == 0 || (sources && reserve_inout && residue_inout), "null argument");
+    check_alpha(alpha);
+    std::vector<pprg::ColumnStats> cs(k);
+    pprg::CallStats call;
+    if (k)
+      pprg::refine_state(*g->g, sources, k, alpha, r_max, reserve_inout, residue_inout,
+                         (flags & PPRG_OUT_DEVICE) != 0, cs.data(), &call);
+    fill_stats(cs, call, k, q, c);
+  });
 }
 
 int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out) {

@@ -127,7 +127,10 @@ struct PushView {
   const uint32_t* d_src = nullptr;
   std::vector<uint32_t> src;
 };
-uint32_t block_width(uint64_t n, uint32_t k);  // padded columns per block for k queries
+uint32_t block_width(uint64_t n, uint32_t k);
+void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, double r_max,
+                  double* reserve, double* residue, bool on_device, ColumnStats* cols,
+                  CallStats* call);  // padded columns per block for k queries
 void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double alpha,
                          double lambda, double r_max, ColumnStats* cols, CallStats* call,
                          PushView* view);
@@ -146,6 +149,20 @@ struct TraceSink {
   uint64_t dev_t0 = 0;     // %globaltimer at the call start
 };
 extern thread_local TraceSink* g_trace;
+
+// Step observer of an observed single-source call (the reference's
+// PushObserver, push.hpp:62-70, at step granularity: after every frontier
+// level, global sweep or iteration the full reserve / residue are copied to
+// the host and handed to `cb`).
+typedef void (*StepCallback)(void* user, const double* reserve, const double* residue,
+                             double r_sum, uint64_t pushes, uint32_t step);
+struct StepSink {
+  StepCallback cb = nullptr;
+  void* user = nullptr;
+  uint32_t step = 0;
+  std::vector<double> hr, hq;
+};
+extern thread_local StepSink* g_obs;
 uint64_t host_now_ns();
 uint64_t device_now_ns(Graph& g);
 

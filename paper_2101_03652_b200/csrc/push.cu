@@ -45,6 +45,7 @@ constexpr int SWEEP_ELEMS = NT * 8;     // edges x columns per tile (8 per threa
 enum SweepMode : int { M_POWERPUSH = 0, M_POWITR = 1, M_SIMFWD = 2, M_FINAL = 3 };
 
 thread_local TraceSink* g_trace = nullptr;
+thread_local StepSink* g_obs = nullptr;
 
 uint64_t host_now_ns() {
   return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -67,6 +68,7 @@ struct SweepCtl {
   double out_D[KMAX];
   unsigned out_sweeps[KMAX];
   int out_done[KMAX];
+  int out_epoch[KMAX];
   unsigned long long out_pushes[KMAX];
   unsigned total_sweeps;
 };
@@ -781,6 +783,7 @@ __global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant_
     ctl->out_D[tid] = cs[tid].D;
     ctl->out_sweeps[tid] = cs[tid].sweeps;
     ctl->out_done[tid] = cs[tid].done;
+    ctl->out_epoch[tid] = cs[tid].epoch;
     ctl->out_pushes[tid] = cs[tid].pushes;
   }
 }
@@ -1028,6 +1031,28 @@ __global__ void k_unpack(const double* a, uint64_t n, int K, int k_live, double 
        i += (uint64_t)gridDim.x * blockDim.x) {
     const int c = (int)(i % K);
     if (c < k_live) out[(uint64_t)c * n + i / K] = scale * a[i];
+  }
+}
+
+// query-major [c*n + u] -> interleaved [u*K + c] (padding columns 0)
+__global__ void k_pack(const double* in, uint64_t n, int K, int k_live, double scale, double* a) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * K;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % K);
+    a[i] = c < k_live ? scale * in[(uint64_t)c * n + i / K] : 0.0;
+  }
+}
+
+// refine outputs: reserve += alpha * (mass pushed here), residue = res
+__global__ void k_refine_out(const double* x, const double* res, uint64_t n, int K, int k_live,
+                             double alpha, double* reserve, double* residue) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n * K;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % K);
+    if (c >= k_live) continue;
+    const uint64_t o = (uint64_t)c * n + i / K;
+    if (x[i] != 0.0) reserve[o] += alpha * x[i];
+    residue[o] = res[i];
   }
 }
 
@@ -1364,6 +1389,25 @@ SweepParams base_params(Block& b) {
   return P;
 }
 
+// Observed calls: column 0's reserve / residue (device, interleaved with the
+// block's K) to the host sink.
+void emit_step(Block& b, const double* reserve_src, double reserve_scale, const double* residue_src,
+               double r_sum, uint64_t pushes) {
+  if (!g_obs) return;
+  Graph& g = b.g;
+  const uint64_t n = g.n, nk = n * (uint64_t)b.K;
+  cudaStream_t st = g.stream;
+  DevBuf<double> tmp(2 * n);
+  k_unpack<<<grid_for(nk), 256, 0, st>>>(reserve_src, n, b.K, 1, reserve_scale, tmp.get());
+  k_unpack<<<grid_for(nk), 256, 0, st>>>(residue_src, n, b.K, 1, 1.0, tmp.get() + n);
+  g_obs->hr.resize(n);
+  g_obs->hq.resize(n);
+  PPRG_CUDA(cudaMemcpyAsync(g_obs->hr.data(), tmp.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaMemcpyAsync(g_obs->hq.data(), tmp.get() + n, 8 * n, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  g_obs->cb(g_obs->user, g_obs->hr.data(), g_obs->hq.data(), r_sum, pushes, ++g_obs->step);
+}
+
 // Frontier levels (drain_queue, push.cpp:34-59) for every column in
 // `state == 0`. The initial frontier is seed_source (push.cpp:61-66) or, for
 // refine, every active node in id order (push.cpp:212-218). A level is
@@ -1505,6 +1549,7 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
       std::fprintf(stderr, "level: entries %llu heavy %u node_pushes %llu edge_pushes %llu appended %llu\n",
                    (unsigned long long)total, nheavy, nn, np, app);
     }
+    const bool observed_col0 = g_obs && (live & 1ull);
     for (uint32_t c = 0; c < b.k; ++c) {
       if (!((live >> c) & 1ull)) continue;
       b.r_sum[c] -= hdr[c];
@@ -1518,6 +1563,7 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
         state[c] = 1;
       }
     }
+    if (observed_col0) emit_step(b, w.x.get(), b.alpha, w.res.get(), b.r_sum[0], b.pushes[0]);
     std::swap(cur, nxt);
   }
   for (uint32_t c = 0; c < b.k; ++c)
@@ -1590,11 +1636,68 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   SweepTrace trace;
   trace.attach(P);
   EventTimer tm(st);
-  tm.start();
-  dispatch_sweeps<M_POWERPUSH>(g, b.K, P, true);
-  tm.stop();
   SweepCtl hc;
-  PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
+  if (g_obs) {
+    // observed: one sweep per launch, the explicit state handed out after each
+    std::vector<ColInit> stv(P.init, P.init + b.K);
+    std::memset(&hc, 0, sizeof hc);
+    DevBuf<double> snap(2 * g.n);
+    tm.start();
+    for (uint32_t sweep = 0;; ++sweep) {
+      bool all = true;
+      for (int c = 0; c < b.K; ++c) all &= stv[c].done != 0;
+      if (all) break;
+      if (sweep >= 200000) fail(EINTERNAL, "power push: sweep limit reached");
+      SweepParams Q = P;
+      Q.max_sweeps = 1;
+      for (int c = 0; c < b.K; ++c) Q.init[c] = stv[c];
+      PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+      dispatch_sweeps<M_POWERPUSH>(g, b.K, Q, true);
+      SweepCtl one;
+      PPRG_CUDA(cudaMemcpyAsync(&one, w.ctl.get(), sizeof one, cudaMemcpyDeviceToHost, st));
+      PPRG_CUDA(cudaStreamSynchronize(st));
+      hc.alg_bytes += one.alg_bytes;
+      hc.total_sweeps = sweep + 1;
+      for (int c = 0; c < b.K; ++c)
+        stv[c] = ColInit{one.out_rsum[c], one.out_D[c], one.out_epoch[c], one.out_done[c],
+                         one.out_sweeps[c], one.out_pushes[c]};
+      // explicit residues of the pull form (the final pass, outputs only)
+      SweepParams F = base_params(b);
+      F.x = w.x.get();
+      F.y[0] = F.y[1] = w.y0.get();
+      F.push_res = w.res.get();
+      F.out_reserve = snap.get();
+      F.out_residue = snap.get() + g.n;
+      for (int c = 0; c < b.K; ++c) {
+        F.final_pull[c] = 1;
+        F.init[c].r_sum = stv[c].r_sum;
+        F.init[c].D = stv[c].D;
+      }
+      PPRG_CUDA(cudaMemsetAsync(snap.get(), 0, 16 * g.n, st));
+      PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+      dispatch_sweeps<M_FINAL>(g, b.K, F, true);
+      g_obs->hr.resize(g.n);
+      g_obs->hq.resize(g.n);
+      PPRG_CUDA(cudaMemcpyAsync(g_obs->hr.data(), snap.get(), 8 * g.n, cudaMemcpyDeviceToHost, st));
+      PPRG_CUDA(cudaMemcpyAsync(g_obs->hq.data(), snap.get() + g.n, 8 * g.n, cudaMemcpyDeviceToHost, st));
+      PPRG_CUDA(cudaStreamSynchronize(st));
+      g_obs->cb(g_obs->user, g_obs->hr.data(), g_obs->hq.data(), stv[0].r_sum,
+                b.pushes[0] + stv[0].pushes, ++g_obs->step);
+    }
+    tm.stop();
+    for (int c = 0; c < b.K; ++c) {
+      hc.out_rsum[c] = stv[c].r_sum;
+      hc.out_D[c] = stv[c].D;
+      hc.out_done[c] = stv[c].done;
+      hc.out_sweeps[c] = stv[c].sweeps;
+      hc.out_pushes[c] = stv[c].pushes;
+    }
+  } else {
+    tm.start();
+    dispatch_sweeps<M_POWERPUSH>(g, b.K, P, true);
+    tm.stop();
+    PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
+  }
   call->sweep_ms += tm.ms();
   trace.fold(st, hc.total_sweeps, b.pushes[0], 0);
   call->alg_bytes += hc.alg_bytes;
@@ -1732,6 +1835,70 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
 
 }  // namespace
 
+// refine (push.cpp:208-222) from caller state: reserve / residue (k x n,
+// query-major, host or device) in, refined state out in place. The push form
+// keeps x = reserve / alpha; every active node in id order seeds the frontier
+// and the levels drain until no node is above deg_eff * r_max.
+void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, double r_max,
+                  double* reserve, double* residue, bool on_device, ColumnStats* cols,
+                  CallStats* call) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (!(r_max > 0.0)) fail(EINVAL_, "refine: r_max must be positive");  // push.cpp:210
+  for (uint32_t c = 0; c < k; ++c)
+    if (sources[c] >= g.n) fail(EINVAL_, "source out of range");
+  const uint64_t n = g.n;
+  for (uint32_t b0 = 0; b0 < k; b0 += KMAX) {
+    const uint32_t kb = k - b0 < (uint32_t)KMAX ? k - b0 : (uint32_t)KMAX;
+    Block b = make_block(g, sources + b0, kb, alpha, false);
+    cudaStream_t st = g.stream;
+    const uint64_t nk = n * (uint64_t)b.K;
+    double* hr = reserve + (uint64_t)b0 * n;
+    double* hq = residue + (uint64_t)b0 * n;
+    // device copies of the caller's state (or the caller's device buffers)
+    DevBuf<double> tr(on_device ? 0 : n * kb), tq(on_device ? 0 : n * kb);
+    double* dr = on_device ? hr : tr.get();
+    double* dq = on_device ? hq : tq.get();
+    if (!on_device) {
+      PPRG_CUDA(cudaMemcpyAsync(dr, hr, 8 * n * kb, cudaMemcpyHostToDevice, st));
+      PPRG_CUDA(cudaMemcpyAsync(dq, hq, 8 * n * kb, cudaMemcpyHostToDevice, st));
+    }
+    // x counts only the mass pushed here, so untouched reserves come back bit-identical
+    PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, st));
+    k_pack<<<grid_for(nk), 256, 0, st>>>(dq, n, b.K, kb, 1.0, b.w.res.get());
+    PPRG_CUDA(cudaGetLastError());
+    std::vector<int> all(KMAX, 1);
+    std::fill(b.r_sum.begin(), b.r_sum.end(), 0.0);
+    {  // r_sum of the incoming state (no drift check: it is the caller's)
+      PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
+      k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), n, b.K, b.w.dcols.get() + KMAX);
+      PPRG_CUDA(cudaMemcpyAsync(b.r_sum.data(), b.w.dcols.get() + KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
+      PPRG_CUDA(cudaStreamSynchronize(st));
+    }
+    std::vector<int> state(KMAX, 2);
+    for (uint32_t c = 0; c < kb; ++c) state[c] = 0;
+    EventTimer tl(st);
+    tl.start();
+    drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);
+    exact_rsum(b, all);  // push.cpp:221
+    tl.stop();
+    call->local_ms += tl.ms();
+    k_refine_out<<<grid_for(nk), 256, 0, st>>>(b.w.x.get(), b.w.res.get(), n, b.K, kb, alpha, dr, dq);
+    PPRG_CUDA(cudaGetLastError());
+    if (!on_device) {
+      PPRG_CUDA(cudaMemcpyAsync(hr, dr, 8 * n * kb, cudaMemcpyDeviceToHost, st));
+      PPRG_CUDA(cudaMemcpyAsync(hq, dq, 8 * n * kb, cudaMemcpyDeviceToHost, st));
+    }
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t c = 0; c < kb; ++c) {
+      cols[b0 + c].r_sum = b.r_sum[c];
+      cols[b0 + c].pushes = b.pushes[c];
+      cols[b0 + c].local_levels = b.levels[c];
+    }
+    call->kernel_launches += 3;
+  }
+}
+
 // Columns per block: wider blocks amortise the in-edge stream over more
 // queries; the per-block state (x, y, residues: n*K doubles each) is capped
 // at 1.6 GB per array, so K shrinks as n grows. PPRG_COLUMNS overrides.
@@ -1797,12 +1964,55 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       SweepTrace trace;
       trace.attach(P);
       EventTimer tm(st);
-      tm.start();
-      if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, P, true);
-      else dispatch_sweeps<M_SIMFWD>(g, b.K, P, true);
-      tm.stop();
       SweepCtl hc;
-      PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
+      if (g_obs) {
+        // observed: one iteration per launch (push.hpp:62-70 on_iteration)
+        std::vector<ColInit> stv(P.init, P.init + b.K);
+        std::memset(&hc, 0, sizeof hc);
+        double* rb[2] = {w.r0.get(), w.r1.get()};
+        double* yb[2] = {w.y0.get(), w.y1.get()};
+        int cur = 0;
+        tm.start();
+        for (uint32_t it = 0;; ++it) {
+          bool all = true;
+          for (int c = 0; c < b.K; ++c) all &= stv[c].done != 0;
+          if (all) break;
+          SweepParams Q = P;
+          Q.max_sweeps = 1;
+          Q.r[0] = rb[cur];
+          Q.r[1] = rb[cur ^ 1];
+          Q.y[0] = yb[cur];
+          Q.y[1] = yb[cur ^ 1];
+          for (int c = 0; c < b.K; ++c) Q.init[c] = stv[c];
+          PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+          if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, Q, true);
+          else dispatch_sweeps<M_SIMFWD>(g, b.K, Q, true);
+          SweepCtl one;
+          PPRG_CUDA(cudaMemcpyAsync(&one, w.ctl.get(), sizeof one, cudaMemcpyDeviceToHost, st));
+          PPRG_CUDA(cudaStreamSynchronize(st));
+          hc.alg_bytes += one.alg_bytes;
+          hc.total_sweeps = it + 1;
+          for (int c = 0; c < b.K; ++c)
+            stv[c] = ColInit{one.out_rsum[c], one.out_D[c], 0, one.out_done[c], one.out_sweeps[c],
+                             one.out_pushes[c]};
+          cur ^= 1;
+          emit_step(b, w.x.get(), 1.0, rb[cur], stv[0].r_sum,
+                    eng == Engine::PowItr ? (uint64_t)stv[0].sweeps * g.m_eff() : stv[0].pushes);
+        }
+        tm.stop();
+        for (int c = 0; c < b.K; ++c) {
+          hc.out_rsum[c] = stv[c].r_sum;
+          hc.out_done[c] = stv[c].done;
+          hc.out_sweeps[c] = stv[c].sweeps;
+          hc.out_pushes[c] = stv[c].pushes;
+        }
+      } else {
+        tm.start();
+        if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, P, true);
+        else dispatch_sweeps<M_SIMFWD>(g, b.K, P, true);
+        tm.stop();
+        PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
+      }
       call->sweep_ms += tm.ms();
       trace.fold(st, hc.total_sweeps, 0, eng == Engine::PowItr ? g.m_eff() : 0);
       call->alg_bytes += hc.alg_bytes;

@@ -2,6 +2,7 @@
 // test_graph.cpp, test_walks.cpp, test_speedppr.cpp under /root/reference/proj),
 // restated against the C++ drop-in (paper_2101_03652_b200/cpp): same API calls,
 // same expectations, running on the GPU. Exit status = number of failures.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <fstream>
@@ -160,6 +161,106 @@ int main() {
     write_ppr_csv("/tmp/pprg_dropin_vals.csv", vals);
     CHECK(read_ppr_csv("/tmp/pprg_dropin_vals.csv") == vals);
     std::remove("/tmp/pprg_dropin_vals.csv");
+  }
+  {  // observers at step granularity (test_push_engines.cpp:22-46, 283-339; test_metrics.cpp:36-56)
+    struct Probe : PushObserver {
+      std::uint64_t calls = 0;
+      double worst = 0.0;
+      std::vector<double> last_reserve;
+      double last_r_sum = 2.0;
+      bool monotone = true;
+      void on_push(const PushState& st) override {
+        ++calls;
+        double t = 0.0;
+        for (double x : st.reserve) t += x;
+        for (double x : st.residue) t += x;
+        worst = std::max(worst, std::fabs(t - 1.0));
+        if (!last_reserve.empty())
+          for (std::size_t v = 0; v < st.reserve.size(); ++v)
+            if (st.reserve[v] < last_reserve[v]) monotone = false;
+        if (st.r_sum > last_r_sum + 1e-15) monotone = false;
+        last_reserve = st.reserve;
+        last_r_sum = st.r_sum;
+      }
+    };
+    const std::vector<std::pair<std::uint64_t, std::uint64_t>> e = {
+        {0, 1}, {1, 2}, {2, 0}, {2, 3}, {3, 4}, {4, 0}, {4, 5}, {5, 6}, {6, 2}, {6, 7}, {7, 8}, {3, 9}};
+    const Graph gd = build_graph_from_edges(e);  // node 8, 9 are dead ends
+    std::uint64_t total = 0;
+    double worst = 0.0;
+    {
+      Probe p;
+      fifo_forward_push(gd, 1, 0.2, 1e-9, std::nullopt, &p);
+      CHECK(p.monotone);
+      total += p.calls;
+      worst = std::max(worst, p.worst);
+    }
+    {
+      Probe p;
+      power_push(gd, 1, 0.2, 1e-10, QueryConfig{}, &p);
+      CHECK(p.monotone);
+      total += p.calls;
+      worst = std::max(worst, p.worst);
+    }
+    {
+      Probe p;
+      PushState st = power_push_state(gd, 1, 0.2, 1e-4, QueryConfig{});
+      refine(gd, 1, 0.2, 1e-9, st, &p);
+      for (NodeId v = 0; v < gd.n(); ++v)
+        CHECK(st.residue[v] <= static_cast<double>(gd.out_degree(v) ? gd.out_degree(v) : 1) * 1e-9);
+      total += p.calls;
+      worst = std::max(worst, p.worst);
+    }
+    {
+      Probe p;
+      power_iteration(gd, 1, 0.2, 1e-13, &p);
+      sim_forward_push(gd, 1, 0.2, 1e-13, &p);
+      total += p.calls;
+      worst = std::max(worst, p.worst);
+    }
+    CHECK(total >= 100);
+    CHECK(worst <= 1e-9);
+
+    struct Trace : PushObserver {
+      std::vector<double> errors;
+      const double* truth = nullptr;
+      void on_iteration(const PushState& st, std::uint32_t) override {
+        double err = 0.0;
+        for (std::size_t v = 0; v < st.reserve.size(); ++v) err += std::fabs(st.reserve[v] - truth[v]);
+        errors.push_back(err);
+      }
+    } tr;
+    const double pi0[5] = {0.29366106080206994, 0.27166882276843485, 0.23285899094437276,
+                           0.1474773609314361, 0.054333764553686985};
+    tr.truth = pi0;
+    power_iteration(g, 0, 0.2, 1e-9, &tr);
+    CHECK(!tr.errors.empty());
+    for (std::size_t j = 1; j <= tr.errors.size(); ++j)
+      CHECK(std::fabs(tr.errors[j - 1] - std::pow(0.8, j)) < 1e-10);
+  }
+  {  // refine: already-inactive state is a fixed point (test_push_engines.cpp:342-350)
+    PushState st = power_push_state(g, 0, 0.2, 1e-6, QueryConfig{});
+    const std::uint64_t pushes_before = st.edge_push_count;
+    const auto reserve_before = st.reserve;
+    refine(g, 0, 0.2, 1.0, st);
+    CHECK(st.edge_push_count == pushes_before);
+    CHECK(st.reserve == reserve_before);
+  }
+  {  // refine enforces the per-node residue bound in O(m) pushes (test_push_engines.cpp:352-367)
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> e;
+    for (std::uint64_t v = 0; v < 300; ++v)
+      for (std::uint64_t j = 1; j <= 1 + v % 5; ++j) e.push_back({v, (v * 7 + j * 13) % 300});
+    const Graph gr = build_graph_from_edges(e);
+    const double r_max = 1e-7 / static_cast<double>(gr.m());
+    const double lambda = static_cast<double>(gr.m()) * r_max;
+    PushState st = power_push_state(gr, 4, 0.2, lambda, QueryConfig{});
+    const std::uint64_t before = st.edge_push_count;
+    refine(gr, 4, 0.2, r_max, st);
+    for (NodeId v = 0; v < gr.n(); ++v)
+      CHECK(st.residue[v] <= static_cast<double>(gr.out_degree(v)) * r_max);
+    CHECK(static_cast<double>(st.edge_push_count - before) <= lambda / (0.2 * r_max) * 1.01);
+    const PPRVector fin = finish_state(std::move(st), 4, 0.2);
+    CHECK(fin.achieved_r_sum <= lambda);
   }
   return failures;
 }

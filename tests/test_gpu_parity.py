@@ -469,3 +469,23 @@ def test_traced_progress_series(P, oracle, algo):
     assert np.max(np.abs(got.estimates - ref.estimates)) <= 1e-8
     cp = harness.cadence_filter(pts, 4 * g.m())
     assert all(b.pushes - a.pushes >= 0 for a, b in zip(cp, cp[1:]))
+
+
+# ---- refine on a caller state (push.cpp:208-222) ------------------------------------
+def test_refine_from_caller_state(P, oracle):
+    g = oracle.random_graph(500, 1, 5, 61)
+    d = dev(P, g)
+    m = int(g.offsets[-1])
+    r_max = 1e-7 / m
+    lam = m * r_max
+    st = P.power_push(d, 4, 0.2, lam)
+    out = P.refine(d, 4, 0.2, r_max, st)
+    deg = np.diff(g.offsets).astype(np.float64)
+    assert np.all(out.residues <= np.maximum(deg, 1) * r_max)
+    assert out.pushes - st.pushes <= lam / (0.2 * r_max) * 1.01
+    assert abs(out.estimates.sum() + out.residues.sum() - 1.0) < 1e-9
+    ref = oracle.power_push_refine(g, 4, 0.2, lam, r_max)
+    assert np.max(np.abs(out.estimates - ref.estimates)) <= lam
+    # an already-inactive state is a fixed point, bit for bit
+    same = P.refine(d, 4, 0.2, 1.0, st)
+    assert np.array_equal(same.estimates, st.estimates) and same.pushes == st.pushes
