@@ -87,6 +87,11 @@ int pprg_graph_generate_rmat(int scale, uint64_t edge_factor, double a, double b
                              uint64_t* edge_count_out, pprg_graph** out);
 int pprg_graph_generate_chung_lu(uint64_t n, uint64_t draws, double beta, uint64_t seed, int device,
                                  uint64_t* edges_out, uint64_t* edge_count_out, pprg_graph** out);
+/* load_graph_cache / save_graph_cache graph.hpp:102-106, graph.cpp:115-143:
+ * the PPRG file streams through pinned staging straight into / out of device
+ * memory (same format, checks and messages as the reference). */
+int pprg_graph_load_cache(const char* path, int device, pprg_graph** out);
+int pprg_graph_save_cache(pprg_graph* g, const char* path);
 /* n(), m(), dead_ends().size() — graph.hpp:20-21,33 */
 int pprg_graph_info(const pprg_graph* g, uint64_t* n, uint64_t* m, uint64_t* dead_ends);
 /* out_offsets()/out_neighbors()/dead_ends() — graph.hpp:31-33 (device -> host) */
@@ -238,6 +243,11 @@ int pprg_index_build(pprg_graph* g, double alpha, uint64_t seed, pprg_index** ou
 int pprg_index_from_host(pprg_graph* g, double alpha, uint64_t seed, const uint32_t* endpoints,
                          pprg_index** out);
 int pprg_index_export(const pprg_index* idx, uint32_t* endpoints);
+/* load_index / save_index walk_index.hpp:52-56, walk_index.cpp:57-104, device-
+ * direct; load also runs check_compatible(g) (walk_index.cpp:36-42). Files
+ * carry rng-id PPRG_RNG_PHILOX4X32_10; other ids are "unknown generator id". */
+int pprg_index_load(pprg_graph* g, const char* path, pprg_index** out);
+int pprg_index_save(const pprg_index* idx, const char* path);
 void pprg_index_destroy(pprg_index* idx);
 /* speedppr_query(g, s, cfg, index) speedppr.hpp:37-38, speedppr.cpp:74-111;
  * mu <= 0 means 1/n; idx may be NULL. */

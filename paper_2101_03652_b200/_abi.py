@@ -102,6 +102,10 @@ def load_library(path: str = lib_path):
     L.pprg_power_push.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_double, C.c_uint32,
                                   C.c_int64, vp, vp, C.c_uint32, vp, vp, vp]
     L.pprg_walk_budget.argtypes = [C.c_uint64, C.c_double, C.c_double, u64p]
+    L.pprg_graph_load_cache.argtypes = [C.c_char_p, C.c_int, C.POINTER(vp)]
+    L.pprg_graph_save_cache.argtypes = [vp, C.c_char_p]
+    L.pprg_index_load.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
+    L.pprg_index_save.argtypes = [vp, C.c_char_p]
     L.pprg_refine.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_double, vp, vp, C.c_uint32, vp,
                               vp]
     L.pprg_ground_truth.argtypes = [vp, vp, C.c_uint32, C.c_double, vp, C.c_uint32, vp, vp]

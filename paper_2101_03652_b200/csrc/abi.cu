@@ -139,6 +139,27 @@ int pprg_graph_build_from_edges(const uint64_t* pairs, uint64_t count, int devic
   });
 }
 
+int pprg_graph_load_cache(const char* path, int device, pprg_graph** out) {
+  return guard([&] {
+    require(path && out, "null argument");
+    auto h = new pprg_graph;
+    try {
+      h->g = pprg::graph_load_cache(path, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int pprg_graph_save_cache(pprg_graph* g, const char* path) {
+  return guard([&] {
+    require(g && g->g && path, "null argument");
+    pprg::graph_save_cache(*g->g, path);
+  });
+}
+
 int pprg_graph_generate_rmat(int scale, uint64_t edge_factor, double a, double b, double c,
                              uint64_t seed, int device, uint64_t* edges_out,
                              uint64_t* edge_count_out, pprg_graph** out) {
@@ -586,6 +607,28 @@ int pprg_index_build(pprg_graph* g, double alpha, uint64_t seed, pprg_index** ou
       throw;
     }
     *out = h;
+  });
+}
+
+int pprg_index_load(pprg_graph* g, const char* path, pprg_index** out) {
+  return guard([&] {
+    require(g && g->g && path && out, "null argument");
+    auto h = new pprg_index;
+    h->owner = g;
+    try {
+      h->w = pprg::index_load(*g->g, path);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int pprg_index_save(const pprg_index* idx, const char* path) {
+  return guard([&] {
+    require(idx && idx->w && idx->owner && path, "null argument");
+    pprg::index_save(*idx->owner->g, *idx->w, path);
   });
 }
 

@@ -16,6 +16,9 @@
 #include <string>
 #include <vector>
 
+#include <cstring>
+
+#include "fileio.h"
 #include "internal.h"
 
 namespace pprg {
@@ -555,6 +558,57 @@ std::unique_ptr<Graph> graph_from_csr(const uint64_t* h_off, const uint32_t* h_n
     PPRG_CUDA(cudaMemcpyAsync(g->nbr.get(), h_nbr, 4 * g->m, cudaMemcpyHostToDevice, g->stream));
   g->finish_build();
   return g;
+}
+
+// PPRG cache (graph.cpp:115-149) straight into device memory; same checks and
+// messages as load_graph_cache, then the usual device-side validation.
+std::unique_ptr<Graph> graph_load_cache(const std::string& path, int device) {
+  FileCloser fc;
+  fc.f = std::fopen(path.c_str(), "rb");
+  if (!fc.f) fail(EDATA, "cannot open graph cache: " + path);
+  char magic[4];
+  if (std::fread(magic, 1, 4, fc.f) != 4 || std::memcmp(magic, "PPRG", 4) != 0)
+    fail(EDATA, path + ": not a graph cache (bad magic)");
+  unsigned char ver = 0;
+  if (std::fread(&ver, 1, 1, fc.f) != 1 || ver != 1)
+    fail(EDATA, path + ": unsupported graph cache version");
+  uint64_t nm[2];
+  if (std::fread(nm, 8, 2, fc.f) != 2) fail(EDATA, path + ": truncated graph cache");
+  const uint64_t n = nm[0], m = nm[1];
+  const uint64_t body = 21ull + 8ull * (n + 1) + 4ull * m;
+  if (n >= (1ull << 40) || m >= (1ull << 40) || file_size(fc.f) < body)
+    fail(EDATA, path + ": truncated graph cache");
+  if (n > 0xffffffffull) fail(EINVAL_, "graph: n exceeds the NodeId range");
+  DeviceGuard dg(device);
+  auto g = std::make_unique<Graph>();
+  g->device = device;
+  g->stream = make_stream(device, &g->sm_count);
+  g->n = n;
+  g->m = m;
+  g->off.alloc(n + 1);
+  g->nbr.alloc(m ? m : 1);
+  {
+    Staging stg(g->stream);
+    if (!stg.read(fc.f, g->off.get(), 8 * (n + 1)) || !stg.read(fc.f, g->nbr.get(), 4 * m))
+      fail(EDATA, path + ": truncated graph cache");
+  }
+  g->finish_build();
+  return g;
+}
+
+void graph_save_cache(Graph& g, const std::string& path) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  FileCloser fc;
+  fc.f = std::fopen(path.c_str(), "wb");
+  if (!fc.f) fail(EDATA, "cannot open for writing: " + path);
+  const unsigned char ver = 1;
+  const uint64_t nm[2] = {g.n, g.m};
+  bool ok = std::fwrite("PPRG", 1, 4, fc.f) == 4 && std::fwrite(&ver, 1, 1, fc.f) == 1 &&
+            std::fwrite(nm, 8, 2, fc.f) == 2;
+  Staging stg(g.stream);
+  ok = ok && stg.write(fc.f, g.off.get(), 8 * (g.n + 1)) && stg.write(fc.f, g.nbr.get(), 4 * g.m);
+  if (!ok || std::fflush(fc.f) != 0) fail(EDATA, "write failed: " + path);
 }
 
 std::unique_ptr<Graph> graph_from_edges(const uint64_t* h_pairs, uint64_t count, int device) {

@@ -7,6 +7,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -204,7 +205,11 @@ struct WalkIndex {
   DevBuf<uint32_t> endpoints;  // [m], slice v = [off[v], off[v+1])
 };
 
+std::unique_ptr<Graph> graph_load_cache(const std::string& path, int device);
+void graph_save_cache(Graph& g, const std::string& path);
 std::unique_ptr<WalkIndex> index_build(Graph& g, double alpha, uint64_t seed);
+std::unique_ptr<WalkIndex> index_load(Graph& g, const std::string& path);
+void index_save(Graph& g, const WalkIndex& w, const std::string& path);
 std::unique_ptr<WalkIndex> index_from_host(Graph& g, double alpha, uint64_t seed,
                                            const uint32_t* h_endpoints);
 void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t k, double alpha,

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <vector>
 
+#include "fileio.h"
 #include "internal.h"
 
 namespace pprg {
@@ -229,6 +230,74 @@ std::unique_ptr<WalkIndex> index_from_host(Graph& g, double alpha, uint64_t seed
   PPRG_CUDA(cudaStreamSynchronize(g.stream));
   if (hb) fail(EDATA, "walk index: endpoint id out of range");  // walk_index.cpp:32-33
   return w;
+}
+
+namespace {
+__global__ void k_cmp_u64(const uint64_t* a, const uint64_t* b, uint64_t n, unsigned* diff) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    if (a[i] != b[i]) atomicOr(diff, 1u);
+}
+}  // namespace
+
+// PPRW (walk_index.cpp:57-104) straight into device memory, checked against
+// the graph like WalkIndex's constructor + check_compatible (walk_index.cpp:19-42).
+std::unique_ptr<WalkIndex> index_load(Graph& g, const std::string& path) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  FileCloser fc;
+  fc.f = std::fopen(path.c_str(), "rb");
+  if (!fc.f) fail(EDATA, "cannot open walk index: " + path);
+  char magic[4];
+  if (std::fread(magic, 1, 4, fc.f) != 4 || std::memcmp(magic, "PPRW", 4) != 0)
+    fail(EDATA, path + ": not a walk index (bad magic)");
+  unsigned char vr[2] = {0, 0};
+  if (std::fread(vr, 1, 2, fc.f) != 2 || vr[0] != 1) fail(EDATA, path + ": unsupported walk index version");
+  if (vr[1] != 2) fail(EDATA, path + ": unknown generator id");  // rng-id 2 = Philox4x32-10
+  double alpha = 0;
+  uint64_t snm[3];
+  if (std::fread(&alpha, 8, 1, fc.f) != 1 || std::fread(snm, 8, 3, fc.f) != 3)
+    fail(EDATA, path + ": truncated walk index");
+  const uint64_t n = snm[1], m = snm[2];
+  if (n != g.n || m != g.m) fail(EDATA, "walk index does not match the graph shape");
+  if (file_size(fc.f) < 38ull + 8ull * (n + 1) + 4ull * m) fail(EDATA, path + ": truncated walk index");
+  auto w = std::make_unique<WalkIndex>();
+  w->device = g.device;
+  w->alpha = alpha;
+  w->seed = snm[0];
+  w->m = m;
+  w->endpoints.alloc(m ? m : 1);
+  DevBuf<uint64_t> off(n + 1);
+  DevBuf<unsigned> flags(2);
+  PPRG_CUDA(cudaMemsetAsync(flags.get(), 0, 8, g.stream));
+  {
+    Staging stg(g.stream);
+    if (!stg.read(fc.f, off.get(), 8 * (n + 1)) || !stg.read(fc.f, w->endpoints.get(), 4 * m))
+      fail(EDATA, path + ": truncated walk index");
+  }
+  k_cmp_u64<<<gridn(n + 1), 256, 0, g.stream>>>(off.get(), g.off.get(), n + 1, flags.get());
+  if (m) k_check_index<<<gridn(m), 256, 0, g.stream>>>(w->endpoints.get(), m, n, flags.get() + 1);
+  unsigned hf[2] = {0, 0};
+  PPRG_CUDA(cudaMemcpyAsync(hf, flags.get(), 8, cudaMemcpyDeviceToHost, g.stream));
+  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+  if (hf[0]) fail(EDATA, "walk index slice length differs from out-degree");
+  if (hf[1]) fail(EDATA, "walk index: endpoint id out of range");
+  return w;
+}
+
+void index_save(Graph& g, const WalkIndex& w, const std::string& path) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  FileCloser fc;
+  fc.f = std::fopen(path.c_str(), "wb");
+  if (!fc.f) fail(EDATA, "cannot open for writing: " + path);
+  const unsigned char vr[2] = {1, 2};
+  const uint64_t snm[3] = {w.seed, g.n, g.m};
+  bool ok = std::fwrite("PPRW", 1, 4, fc.f) == 4 && std::fwrite(vr, 1, 2, fc.f) == 2 &&
+            std::fwrite(&w.alpha, 8, 1, fc.f) == 1 && std::fwrite(snm, 8, 3, fc.f) == 3;
+  Staging stg(g.stream);
+  ok = ok && stg.write(fc.f, g.off.get(), 8 * (g.n + 1)) && stg.write(fc.f, w.endpoints.get(), 4 * g.m);
+  if (!ok || std::fflush(fc.f) != 0) fail(EDATA, "write failed: " + path);
 }
 
 void walk_terminals(Graph& g, const uint32_t* h_start, const uint32_t* h_k, const uint32_t* h_v,

@@ -18,13 +18,19 @@ _G_MAGIC, _W_MAGIC, _VERSION = b"PPRG", b"PPRW", 1
 
 
 def save_graph_cache(g: Graph, path: str) -> None:
-    off, nbr = g.out_offsets(), g.out_neighbors()
+    """graph.cpp:115-125, written from device memory (pprg_graph_save_cache)."""
+    from ._abi import _check, load_library
+    _check(load_library().pprg_graph_save_cache(g.handle, path.encode()))
+
+
+def write_graph_cache(path: str, offsets, neighbors) -> None:
+    """The same PPRG bytes from host arrays (tests, tools)."""
     with open(path, "wb") as f:
         f.write(_G_MAGIC)
         f.write(bytes([_VERSION]))
-        f.write(np.array([g.n(), g.m()], "<u8").tobytes())
-        f.write(off.astype("<u8").tobytes())
-        f.write(nbr.astype("<u4").tobytes())
+        f.write(np.array([len(offsets) - 1, len(neighbors)], "<u8").tobytes())
+        f.write(np.asarray(offsets).astype("<u8").tobytes())
+        f.write(np.asarray(neighbors).astype("<u4").tobytes())
 
 
 def is_graph_cache(path: str) -> bool:
@@ -59,11 +65,27 @@ def read_graph_cache(path: str):
 
 
 def load_graph_cache(path: str, device=None) -> Graph:
+    """graph.cpp:127-143, streamed straight into device memory (pprg_graph_load_cache)."""
+    import ctypes as C
+    from ._abi import _check, _default_device, load_library
+    dev = _default_device() if device is None else device
+    h = C.c_void_p()
+    _check(load_library().pprg_graph_load_cache(path.encode(), dev, C.byref(h)))
+    return Graph(device=dev, _handle=h)
+
+
+def load_graph_cache_host(path: str, device=None) -> Graph:
     off, nbr = read_graph_cache(path)
     return Graph(off, nbr, device=device)
 
 
 def save_index(index: WalkIndex, path: str) -> None:
+    """walk_index.cpp:61-81 from device memory (pprg_index_save)."""
+    from ._abi import _check, load_library
+    _check(load_library().pprg_index_save(index._h, path.encode()))
+
+
+def write_index_host(index: WalkIndex, path: str) -> None:
     g = index.graph
     with open(path, "wb") as f:
         f.write(_W_MAGIC)
@@ -100,6 +122,23 @@ def read_index(path: str):
 
 
 def load_index(path: str, g: Graph) -> WalkIndex:
+    """walk_index.cpp:83-104 + check_compatible, streamed into device memory."""
+    import ctypes as C
+    from ._abi import _check, load_library
+    L = load_library()
+    h = C.c_void_p()
+    _check(L.pprg_index_load(g.handle, path.encode(), C.byref(h)))
+    alpha, seed = _index_header(path)
+    return WalkIndex(g, alpha, seed, h)
+
+
+def _index_header(path: str):
+    with open(path, "rb") as f:
+        hdr = f.read(22)
+    return float(np.frombuffer(hdr[6:14], "<f8")[0]), int(np.frombuffer(hdr[14:22], "<u8")[0])
+
+
+def load_index_host(path: str, g: Graph) -> WalkIndex:
     alpha, seed, off, ep = read_index(path)
     if off.size != g.n() + 1 or ep.size != g.m() or not np.array_equal(off, g.out_offsets()):
         raise DataError("walk index does not match the graph shape")

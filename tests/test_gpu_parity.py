@@ -489,3 +489,80 @@ def test_refine_from_caller_state(P, oracle):
     # an already-inactive state is a fixed point, bit for bit
     same = P.refine(d, 4, 0.2, 1.0, st)
     assert np.array_equal(same.estimates, st.estimates) and same.pushes == st.pushes
+
+
+# ---- device-direct PPRG / PPRW files (graph.cpp:115-143, walk_index.cpp:57-104) -------
+def test_graph_cache_roundtrip_device_direct(P, oracle, tmp_path):
+    from paper_2101_03652_b200 import formats
+    g = oracle.random_graph(3000, 0, 7, 12)
+    d = dev(P, g)
+    ours, host = str(tmp_path / "a.pprg"), str(tmp_path / "b.pprg")
+    formats.save_graph_cache(d, ours)
+    formats.write_graph_cache(host, g.offsets, g.neighbors)
+    assert open(ours, "rb").read() == open(host, "rb").read()
+    back = formats.load_graph_cache(ours)
+    assert np.array_equal(back.out_offsets(), g.offsets)
+    assert np.array_equal(back.out_neighbors(), g.neighbors)
+    assert np.array_equal(back.dead_ends(), d.dead_ends())
+
+
+def test_graph_cache_interop_with_reference(P, ref, oracle, tmp_path):
+    from paper_2101_03652_b200 import formats
+    g = oracle.random_graph(800, 0, 5, 3)
+    p1, p2 = str(tmp_path / "ours.pprg"), str(tmp_path / "ref.pprg")
+    formats.save_graph_cache(dev(P, g), p1)
+    rg = ref.load_graph_cache(p1)                # reference reads our file
+    assert np.array_equal(rg.csr().offsets, g.offsets)
+    rg.save(p2)                                  # and we read the reference's
+    back = formats.load_graph_cache(p2)
+    assert np.array_equal(back.out_neighbors(), g.neighbors)
+
+
+def test_graph_cache_errors(P, tmp_path):
+    from paper_2101_03652_b200 import formats
+    bad = tmp_path / "bad.pprg"
+    bad.write_bytes(b"XXXX\x01")
+    with pytest.raises(P.DataError, match="not a graph cache"):
+        formats.load_graph_cache(str(bad))
+    bad.write_bytes(b"PPRG\x02")
+    with pytest.raises(P.DataError, match="unsupported graph cache version"):
+        formats.load_graph_cache(str(bad))
+    bad.write_bytes(b"PPRG\x01" + np.array([5, 13], "<u8").tobytes() + b"\x00" * 10)
+    with pytest.raises(P.DataError, match="truncated graph cache"):
+        formats.load_graph_cache(str(bad))
+    with pytest.raises(P.DataError, match="cannot open graph cache"):
+        formats.load_graph_cache(str(tmp_path / "missing.pprg"))
+    # a corrupt body is caught by the device validation (graph.cpp:24-34)
+    off = np.array([0, 2, 1, 3], "<u8")
+    bad.write_bytes(b"PPRG\x01" + np.array([3, 3], "<u8").tobytes() + off.tobytes() +
+                    np.zeros(3, "<u4").tobytes())
+    with pytest.raises(P.DataError, match="non-decreasing"):
+        formats.load_graph_cache(str(bad))
+
+
+def test_index_file_roundtrip_device_direct(P, oracle, tmp_path):
+    from paper_2101_03652_b200 import formats
+    g = oracle.random_graph(2000, 0, 6, 5)
+    d = dev(P, g)
+    idx = P.build_index(d, 0.2, 77)
+    ours, host = str(tmp_path / "a.pprw"), str(tmp_path / "b.pprw")
+    formats.save_index(idx, ours)
+    formats.write_index_host(idx, host)
+    assert open(ours, "rb").read() == open(host, "rb").read()
+    back = formats.load_index(ours, d)
+    assert np.array_equal(back.endpoints(), idx.endpoints())
+    assert back.alpha() == 0.2 and back.seed() == 77
+    # another graph's shape, a foreign generator id, out-of-range endpoints
+    other = dev(P, oracle.random_graph(2000, 0, 6, 6))
+    with pytest.raises(P.DataError, match="does not match the graph shape|slice length differs"):
+        formats.load_index(ours, other)
+    raw = bytearray(open(ours, "rb").read())
+    raw[5] = 1
+    open(host, "wb").write(bytes(raw))
+    with pytest.raises(P.DataError, match="unknown generator id"):
+        formats.load_index(host, d)
+    raw[5] = 2
+    raw[-4:] = np.array([10 ** 6], "<u4").tobytes()
+    open(host, "wb").write(bytes(raw))
+    with pytest.raises(P.DataError, match="endpoint id out of range"):
+        formats.load_index(host, d)
