@@ -254,6 +254,16 @@ void pprg_index_destroy(pprg_index* idx);
 int pprg_speedppr(pprg_graph* g, const pprg_index* idx, const uint32_t* sources, uint32_t k,
                   double alpha, double epsilon, double mu, uint64_t seed, double* estimates_out,
                   uint32_t flags, pprg_query_stats* qstats, pprg_call_stats* cstats);
+/* monte_carlo_phase(g, s, alpha, state, W, [index,] rng) speedppr.hpp:24-30,
+ * speedppr.cpp:23-72, on a caller push state of one source (host reserve /
+ * residue, n doubles each): every v with residue r > 0 runs ceil(r*W) walks
+ * (clamped to deg_eff within the reference's slack, PPRG_EINTERNAL beyond it),
+ * each adding r/ceil(r*W) at its terminal; index prefixes are used where v has
+ * out-edges. Walks are Philox streams keyed by seed (the reference's Rng
+ * stream cannot be reproduced in parallel). */
+int pprg_monte_carlo(pprg_graph* g, const pprg_index* idx, uint32_t source, double alpha,
+                     uint64_t walk_budget, uint64_t seed, const double* reserve,
+                     const double* residue, double* estimates_out, uint64_t* walks_out);
 /* random_walk(g, start, source, alpha, rng) walk_index.hpp:12 for a batch of
  * (start_i, k_i, v_i) walk ids under one tag (test hook for the walk stream). */
 int pprg_walk_terminals(pprg_graph* g, const uint32_t* starts, const uint32_t* ks,

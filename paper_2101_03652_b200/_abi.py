@@ -106,6 +106,8 @@ def load_library(path: str = lib_path):
     L.pprg_graph_save_cache.argtypes = [vp, C.c_char_p]
     L.pprg_index_load.argtypes = [vp, C.c_char_p, C.POINTER(vp)]
     L.pprg_index_save.argtypes = [vp, C.c_char_p]
+    L.pprg_monte_carlo.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_uint64, C.c_uint64, vp, vp,
+                                   vp, u64p]
     L.pprg_refine.argtypes = [vp, vp, C.c_uint32, C.c_double, C.c_double, vp, vp, C.c_uint32, vp,
                               vp]
     L.pprg_ground_truth.argtypes = [vp, vp, C.c_uint32, C.c_double, vp, C.c_uint32, vp, vp]
@@ -438,6 +440,21 @@ def refine(g: Graph, s: int, alpha: float, r_max: float, state: PPRVector) -> PP
     out = _vectors(src, res, rsd, q, alpha)[0]
     out.pushes = state.pushes + q[0].pushes
     return out
+
+
+def monte_carlo_phase(g: Graph, s: int, alpha: float, state: PPRVector, walk_budget: int,
+                      seed: int, index: Optional["WalkIndex"] = None) -> PPRVector:
+    """monte_carlo_phase (speedppr.hpp:24-30, speedppr.cpp:23-72) on a refined
+    push state (estimates = reserve, residues); Philox walks keyed by seed."""
+    load_library()
+    res = np.ascontiguousarray(state.estimates, np.float64)
+    rsd = np.ascontiguousarray(state.residues, np.float64)
+    out = np.empty(g.n(), np.float64)
+    walks = C.c_uint64()
+    _check(_lib.pprg_monte_carlo(g.handle, index._h if index is not None else None, int(s), alpha,
+                                 int(walk_budget), int(seed), res.ctypes.data, rsd.ctypes.data,
+                                 out.ctypes.data, C.byref(walks)))
+    return PPRVector(out, np.zeros(g.n()), int(s), alpha, 0.0, state.pushes, int(walks.value))
 
 
 GROUND_TRUTH_LAMBDA = 1e-17  # kGroundTruthLambda, metrics.hpp:10

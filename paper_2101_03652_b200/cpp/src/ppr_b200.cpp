@@ -16,6 +16,7 @@
 #include "ppr/metrics.hpp"
 #include "ppr/push.hpp"
 #include "ppr/speedppr.hpp"
+#include "ppr/synthetic.hpp"
 #include "ppr/walk_index.hpp"
 
 namespace ppr {
@@ -372,6 +373,41 @@ std::uint64_t compute_walk_budget(std::uint64_t n, double epsilon, double mu) {
   return out;
 }
 
+namespace {
+PPRVector mc_phase(const Graph& g, NodeId s, double alpha, PushState&& st, std::uint64_t W,
+                   const WalkIndex* index, Rng& rng) {
+  if (st.reserve.size() != g.n() || st.residue.size() != g.n())
+    throw std::invalid_argument("monte carlo: state size does not match the graph");
+  if (index) {
+    index->check_compatible(g);
+    if (index->alpha() != alpha) throw std::runtime_error("walk index was built for a different alpha");
+  }
+  PPRVector out;
+  out.estimates.assign(g.n(), 0.0);
+  out.residues.assign(g.n(), 0.0);
+  std::uint64_t walks = 0;
+  check(pprg_monte_carlo(g.device_handle(), index ? index->device_handle() : nullptr, s, alpha, W,
+                         rng.next(), st.reserve.data(), st.residue.data(), out.estimates.data(),
+                         &walks));
+  out.source = s;
+  out.alpha = alpha;
+  out.achieved_r_sum = 0.0;  // speedppr.cpp:47
+  out.pushes = st.edge_push_count;
+  out.walks = walks;
+  return out;
+}
+}  // namespace
+
+PPRVector monte_carlo_phase(const Graph& g, NodeId s, double alpha, PushState&& state,
+                            std::uint64_t walk_budget, Rng& rng) {
+  return mc_phase(g, s, alpha, std::move(state), walk_budget, nullptr, rng);
+}
+
+PPRVector monte_carlo_phase(const Graph& g, NodeId s, double alpha, PushState&& state,
+                            std::uint64_t walk_budget, const WalkIndex& index, Rng& rng) {
+  return mc_phase(g, s, alpha, std::move(state), walk_budget, &index, rng);
+}
+
 PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
                          const WalkIndex* index) {  // speedppr.cpp:74-111
   cfg.validate();
@@ -390,6 +426,19 @@ PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
   v.pushes = q.pushes;
   v.walks = q.walks;
   return v;
+}
+
+// ---- synthetic.hpp ------------------------------------------------------------------
+Graph random_graph(NodeId n, std::uint32_t min_out, std::uint32_t max_out, std::uint64_t seed) {
+  if (n == 0) throw std::invalid_argument("random_graph: need at least one node");
+  if (min_out > max_out) throw std::invalid_argument("random_graph: min_out > max_out");
+  Rng rng(seed);
+  std::vector<std::uint64_t> off(static_cast<std::size_t>(n) + 1, 0);
+  for (NodeId v = 0; v < n; ++v)  // all degrees first, then all targets (one stream)
+    off[v + 1] = off[v] + min_out + rng.below(static_cast<std::uint64_t>(max_out - min_out) + 1);
+  std::vector<NodeId> nbr(off[n]);
+  for (auto& t : nbr) t = static_cast<NodeId>(rng.below(n));
+  return Graph(std::move(off), std::move(nbr));
 }
 
 // ---- push state (push.cpp:9-15, 70-79, 201-222) -----------------------------------

@@ -691,6 +691,23 @@ int pprg_speedppr(pprg_graph* g, const pprg_index* idx, const uint32_t* sources,
   });
 }
 
+int pprg_monte_carlo(pprg_graph* g, const pprg_index* idx, uint32_t source, double alpha,
+                     uint64_t walk_budget, uint64_t seed, const double* reserve,
+                     const double* residue, double* estimates_out, uint64_t* walks_out) {
+  return guard([&] {
+    require(g && g->g && reserve && residue && estimates_out && walks_out, "null argument");
+    check_alpha(alpha);
+    require(walk_budget >= 1, "monte carlo: walk budget must be positive");
+    if (idx) {  // walk_index.cpp:36-42, speedppr.cpp:62-64
+      if (idx->owner != g && (idx->w->m != g->g->m || idx->owner->g->n != g->g->n))
+        pprg::fail(pprg::EDATA, "walk index does not match the graph shape");
+      if (idx->w->alpha != alpha) pprg::fail(pprg::EDATA, "walk index was built for a different alpha");
+    }
+    pprg::monte_carlo(*g->g, idx ? idx->w.get() : nullptr, source, alpha, walk_budget, seed,
+                      reserve, residue, estimates_out, walks_out);
+  });
+}
+
 int pprg_walk_terminals(pprg_graph* g, const uint32_t* starts, const uint32_t* ks,
                         const uint32_t* vs, uint64_t count, uint32_t source, uint32_t tag,
                         double alpha, uint64_t seed, uint32_t* out) {

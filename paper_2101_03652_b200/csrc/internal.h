@@ -209,6 +209,8 @@ std::unique_ptr<Graph> graph_load_cache(const std::string& path, int device);
 void graph_save_cache(Graph& g, const std::string& path);
 std::unique_ptr<WalkIndex> index_build(Graph& g, double alpha, uint64_t seed);
 std::unique_ptr<WalkIndex> index_load(Graph& g, const std::string& path);
+void monte_carlo(Graph& g, const WalkIndex* idx, uint32_t s, double alpha, uint64_t W, uint64_t seed,
+                 const double* h_reserve, const double* h_residue, double* h_est, uint64_t* walks);
 void index_save(Graph& g, const WalkIndex& w, const std::string& path);
 std::unique_ptr<WalkIndex> index_from_host(Graph& g, double alpha, uint64_t seed,
                                            const uint32_t* h_endpoints);

@@ -40,7 +40,11 @@ constexpr int EMAX = 64;   // max epochs
 #endif
 constexpr int NT = PPRG_NT;
 #define PPRG_MAX_PEERS 15             // threads per block for the sweep kernels
-constexpr int SWEEP_ELEMS = NT * 8;     // edges x columns per tile (8 per thread)
+#ifndef PPRG_TILE_U
+#define PPRG_TILE_U 8
+#endif
+constexpr int TILE_U = PPRG_TILE_U;     // narrow path: gathers per thread per tile
+constexpr int SWEEP_ELEMS = NT * TILE_U;  // edges x columns per narrow tile
 
 enum SweepMode : int { M_POWERPUSH = 0, M_POWITR = 1, M_SIMFWD = 2, M_FINAL = 3 };
 
@@ -315,7 +319,7 @@ __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& 
   }
   {
     const uint32_t total = d.ne * K;
-    constexpr int U = 8;
+    constexpr int U = TILE_U;
     for (uint32_t f0 = 0; f0 < total; f0 += U * NT) {
       uint32_t id[U];
 #pragma unroll
@@ -616,7 +620,11 @@ template <int K, int MODE>
 #ifndef PPRG_MINB
 #define PPRG_MINB 8
 #endif
-__global__ void __launch_bounds__(NT, PPRG_MINB) k_sweeps(const __grid_constant__ SweepParams P) {
+#ifndef PPRG_MINB_NARROW
+#define PPRG_MINB_NARROW PPRG_MINB
+#endif
+__global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
+    k_sweeps(const __grid_constant__ SweepParams P) {
   using TC = Tile<K>;
   extern __shared__ __align__(16) char smem_dyn[];
   __shared__ ColSh cs[K];

@@ -300,6 +300,55 @@ void index_save(Graph& g, const WalkIndex& w, const std::string& path) {
   if (!ok || std::fflush(fc.f) != 0) fail(EDATA, "write failed: " + path);
 }
 
+// monte_carlo_phase (speedppr.cpp:23-72) on a caller push state (host
+// reserve / residue of one source): W_v walks per node with residue, index
+// prefixes where v has out-edges, fresh Philox walks otherwise.
+void monte_carlo(Graph& g, const WalkIndex* idx, uint32_t s, double alpha, uint64_t W, uint64_t seed,
+                 const double* h_reserve, const double* h_residue, double* h_est, uint64_t* walks) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  if (s >= g.n) fail(EINVAL_, "monte carlo: source out of range");
+  const uint64_t n = g.n;
+  cudaStream_t st = g.stream;
+  DevBuf<double> res(n), est(n);
+  DevBuf<unsigned long long> cnt(n), colw(65);
+  DevBuf<uint64_t> big(n);
+  DevBuf<unsigned> bad(1);
+  DevBuf<uint32_t> dsrc(1);
+  PPRG_CUDA(cudaMemcpyAsync(res.get(), h_residue, 8 * n, cudaMemcpyHostToDevice, st));
+  PPRG_CUDA(cudaMemcpyAsync(est.get(), h_reserve, 8 * n, cudaMemcpyHostToDevice, st));
+  PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
+  PPRG_CUDA(cudaMemsetAsync(colw.get(), 0, 8 * 65, st));
+  k_mc_counts<<<std::min<unsigned>(gridn(n), g.sm_count * 8), 256, 0, st>>>(
+      res.get(), g.deg.get(), n, 1, 1, (double)W, cnt.get(), bad.get(), colw.get());
+  unsigned hb = 0;
+  PPRG_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  if (hb) fail(EINTERNAL, "monte carlo: residue exceeds degree/W, state not refined");
+  McParams P;
+  std::memset(&P, 0, sizeof P);
+  P.off = g.off.get();
+  P.nbr = g.nbr.get();
+  P.deg = g.deg.get();
+  P.res = res.get();
+  P.cnt = cnt.get();
+  P.index = idx ? idx->endpoints.get() : nullptr;
+  P.nk = n;
+  P.K = 1;
+  P.alpha = alpha;
+  P.seed = seed;
+  P.est = est.get();
+  P.src[0] = s;
+  k_mc_entries<<<gridn(n), 256, 0, st>>>(P, big.get(), colw.get() + 64);
+  k_mc_big<<<g.sm_count * 8, 256, 0, st>>>(P, big.get(), colw.get() + 64);
+  PPRG_CUDA(cudaGetLastError());
+  unsigned long long hw = 0;
+  PPRG_CUDA(cudaMemcpyAsync(h_est, est.get(), 8 * n, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaMemcpyAsync(&hw, colw.get(), 8, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  *walks = hw;
+}
+
 void walk_terminals(Graph& g, const uint32_t* h_start, const uint32_t* h_k, const uint32_t* h_v,
                     uint64_t count, uint32_t source, uint32_t tag, double alpha, uint64_t seed,
                     uint32_t* h_out) {

@@ -15,6 +15,7 @@
 #include "ppr/metrics.hpp"
 #include "ppr/push.hpp"
 #include "ppr/speedppr.hpp"
+#include "ppr/synthetic.hpp"
 #include "ppr/walk_index.hpp"
 
 using namespace ppr;
@@ -261,6 +262,71 @@ int main() {
     CHECK(static_cast<double>(st.edge_push_count - before) <= lambda / (0.2 * r_max) * 1.01);
     const PPRVector fin = finish_state(std::move(st), 4, 0.2);
     CHECK(fin.achieved_r_sum <= lambda);
+  }
+  {  // monte carlo phase (test_speedppr.cpp:35-107), on the GPU
+    auto total = [](const std::vector<double>& xs) {
+      double t = 0.0;
+      for (double x : xs) t += x;
+      return t;
+    };
+    {
+      PushState st(5, 0);
+      st.residue.assign(5, 0.0);
+      st.reserve = {0.4, 0.3, 0.2, 0.1, 0.0};
+      st.r_sum = 0.0;
+      Rng rng(1);
+      const PPRVector out = monte_carlo_phase(g, 0, 0.2, std::move(st), 100, rng);
+      CHECK((out.estimates == std::vector<double>{0.4, 0.3, 0.2, 0.1, 0.0}));
+      CHECK(out.walks == 0);
+    }
+    {
+      const std::uint64_t W = 151;
+      PushState st(5, 0);
+      st.residue.assign(5, 0.0);
+      st.residue[1] = 3.0 / W;
+      st.r_sum = 3.0 / W;
+      Rng rng(2);
+      const PPRVector out = monte_carlo_phase(g, 0, 0.2, std::move(st), W, rng);
+      CHECK(out.walks == 3);
+      CHECK(std::fabs(total(out.estimates) - 3.0 / W) <= 1e-12 * 3.0 / W + 1e-18);
+      for (double x : out.estimates) CHECK(std::fabs(x * W - std::round(x * W)) < 1e-9);
+    }
+    for (std::uint64_t seed : {3, 4, 5}) {
+      const Graph gr = random_graph(40, 0, 4, seed);
+      const NodeId s = static_cast<NodeId>(seed % gr.n());
+      const std::uint64_t W = 4 * gr.effective_edge_count();
+      QueryConfig cfg;
+      PushState st = power_push_state(gr, s, 0.2, static_cast<double>(gr.effective_edge_count()) / W, cfg);
+      refine(gr, s, 0.2, 1.0 / static_cast<double>(W), st);
+      Rng rng(seed);
+      const PPRVector out = monte_carlo_phase(gr, s, 0.2, std::move(st), W, rng);
+      CHECK(std::fabs(total(out.estimates) - 1.0) < 1e-9);
+      CHECK(out.achieved_r_sum == 0.0);
+    }
+    {
+      PushState st(5, 0);  // residue[0] = 1 >> d/W
+      Rng rng(1);
+      CHECK_THROWS_AS(monte_carlo_phase(g, 0, 0.2, std::move(st), 100, rng), std::logic_error);
+    }
+    {
+      const Graph gr = random_graph(30, 0, 4, 13);
+      const WalkIndex idx = build_index(gr, 0.2, 21);
+      PushState st(gr.n(), 5);
+      Rng rng(7);
+      CHECK_THROWS_AS(monte_carlo_phase(gr, 5, 0.15, PushState(gr.n(), 5), 100, idx, rng),
+                      std::runtime_error);
+      // stored prefixes: a residue of k/W on a node with out-edges consumes its first k terminals
+      const std::uint64_t W = 1000;
+      NodeId v = 0;
+      while (gr.out_degree(v) < 3) ++v;
+      st.residue.assign(gr.n(), 0.0);
+      st.residue[v] = 3.0 / W;
+      st.reserve.assign(gr.n(), 0.0);
+      const PPRVector out = monte_carlo_phase(gr, 5, 0.2, std::move(st), W, idx, rng);
+      std::vector<double> expect(gr.n(), 0.0);
+      for (int k = 0; k < 3; ++k) expect[idx.endpoints_of(v)[k]] += (3.0 / W) / 3.0;
+      for (NodeId t = 0; t < gr.n(); ++t) CHECK(std::fabs(out.estimates[t] - expect[t]) < 1e-15);
+    }
   }
   return failures;
 }

@@ -566,3 +566,21 @@ def test_index_file_roundtrip_device_direct(P, oracle, tmp_path):
     open(host, "wb").write(bytes(raw))
     with pytest.raises(P.DataError, match="endpoint id out of range"):
         formats.load_index(host, d)
+
+
+def test_monte_carlo_expectation(P, oracle):
+    """E[MC(state)] = reserve + sum_v residue(v) pi(v, .) (test_speedppr.cpp:84-107)."""
+    g = oracle.random_graph(9, 1, 3, 11)
+    d = dev(P, g)
+    W = 60
+    m_eff = int(g.offsets[-1]) + int(np.sum(np.diff(g.offsets) == 0))
+    st = P.refine(d, 2, 0.2, 1.0 / W, P.power_push(d, 2, 0.2, m_eff / W))
+    expected = st.estimates.copy()
+    for v in range(g.n):
+        if st.residues[v] > 0:
+            expected += st.residues[v] * oracle.exact_ppr(g, v, 0.2)
+    runs = np.stack([P.monte_carlo_phase(d, 2, 0.2, st, W, 1000 + r).estimates
+                     for r in range(3000)])
+    se = runs.std(axis=0, ddof=1) / np.sqrt(len(runs))
+    assert np.all(np.abs(runs.mean(axis=0) - expected) <= 4 * se + 1e-12)
+    assert np.all(np.abs(runs.sum(axis=1) - 1.0) < 1e-9)
