@@ -3,6 +3,7 @@
 // as the reference's exception types (invalid_argument / runtime_error /
 // logic_error).
 #include <algorithm>
+#include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -427,6 +428,45 @@ PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
   v.walks = q.walks;
   return v;
 }
+
+// ---- edge lists (graph.cpp:66-113) ---------------------------------------------------
+namespace {
+Graph read_edge_file(const std::string& path, bool undirected) {
+  std::ifstream in(path);
+  if (!in) throw std::runtime_error("cannot open graph file: " + path);
+  std::vector<std::pair<std::uint64_t, std::uint64_t>> edges;
+  std::string line;
+  for (std::uint64_t no = 1; std::getline(in, line); ++no) {
+    const char* p = line.data();
+    const char* const end = p + line.size();
+    auto blank = [&] {
+      while (p < end && (*p == ' ' || *p == '\t' || *p == '\r')) ++p;
+    };
+    auto bad = [&](const char* what) {
+      throw std::runtime_error(path + ":" + std::to_string(no) + ": " + what);
+    };
+    blank();
+    if (p == end || *p == '#') continue;
+    std::uint64_t a = 0, b = 0;
+    auto r = std::from_chars(p, end, a);
+    if (r.ec != std::errc()) bad("expected non-negative integer source id");
+    p = r.ptr;
+    blank();
+    r = std::from_chars(p, end, b);
+    if (r.ec != std::errc()) bad("expected non-negative integer target id");
+    p = r.ptr;
+    blank();
+    if (p != end) bad("trailing content after edge pair");
+    edges.emplace_back(a, b);
+    if (undirected) edges.emplace_back(b, a);
+  }
+  if (edges.empty()) throw std::runtime_error(path + ": graph is empty after cleaning");
+  return build_graph_from_edges(edges);
+}
+}  // namespace
+
+Graph load_edge_list(const std::string& path) { return read_edge_file(path, false); }
+Graph undirected_to_directed(const std::string& path) { return read_edge_file(path, true); }
 
 // ---- synthetic.hpp ------------------------------------------------------------------
 Graph random_graph(NodeId n, std::uint32_t min_out, std::uint32_t max_out, std::uint64_t seed) {

@@ -328,5 +328,28 @@ int main() {
       for (NodeId t = 0; t < gr.n(); ++t) CHECK(std::fabs(out.estimates[t] - expect[t]) < 1e-15);
     }
   }
+  {  // edge list parsing (test_graph.cpp "edge list parsing", "undirected loading doubles every edge")
+    const std::string path = "/tmp/pprg_dropin_edges.txt";
+    {
+      std::ofstream out(path);
+      out << "# comment\n\n0 1\n  1\t2\r\n2 0\n";
+    }
+    const Graph a = load_edge_list(path);
+    CHECK(a.n() == 3 && a.m() == 3);
+    const Graph u = undirected_to_directed(path);
+    CHECK(u.m() == 6);
+    {
+      std::ofstream out(path);
+      out << "0 1\n1 2 3\n";
+    }
+    bool threw = false;
+    try {
+      load_edge_list(path);
+    } catch (const std::runtime_error& e) {
+      threw = std::string(e.what()).find(":2: trailing content after edge pair") != std::string::npos;
+    }
+    CHECK(threw);
+    std::remove(path.c_str());
+  }
   return failures;
 }
