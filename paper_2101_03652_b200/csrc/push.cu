@@ -1287,6 +1287,42 @@ uint64_t device_now_ns(Graph& g) {
 
 namespace {
 
+// Small device->host read-backs on the query path go through a kernel that
+// stores into mapped pinned memory instead of a copy-engine transfer, so they
+// never queue behind the multi-GB output copies of the previous block on the
+// copy engine (those overlap the next block's compute).
+__global__ void k_copy_bytes(unsigned char* dst, const unsigned char* src, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+struct MappedStage {
+  unsigned char* h = nullptr;
+  unsigned char* d = nullptr;
+  size_t cap = 0;
+  ~MappedStage() {
+    if (h) cudaFreeHost(h);
+  }
+};
+
+void d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (!bytes) return;
+  static thread_local MappedStage ms;
+  if (bytes > ms.cap) {
+    if (ms.h) PPRG_CUDA(cudaFreeHost(ms.h));
+    ms.cap = bytes < 65536 ? 65536 : bytes;
+    PPRG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ms.h), ms.cap,
+                            cudaHostAllocMapped | cudaHostAllocPortable));
+    PPRG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ms.d), ms.h, 0));
+  }
+  const unsigned blocks = (unsigned)((bytes + 255) / 256 < 64 ? (bytes + 255) / 256 : 64);
+  k_copy_bytes<<<blocks, 256, 0, st>>>(ms.d, static_cast<const unsigned char*>(src), bytes);
+  PPRG_CUDA(cudaGetLastError());
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(dst, ms.h, bytes);
+}
+
 struct EventTimer {
   cudaEvent_t a{}, b{};
   cudaStream_t st;
@@ -1472,14 +1508,14 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     PPRG_CUDA(cudaMemsetAsync(w.counters.get(), 0, 8 * NC, st));
     k_scan_active<<<grid_for(nk), 256, 0, st>>>(w.res.get(), g.deg.get(), n, K, w.dcols.get() + KMAX,
                                                 live0, w.stamp.get(), next_tag(), cur, n, col_cnt);
-    PPRG_CUDA(cudaMemcpyAsync(hc.data(), w.counters.get(), 8 * NC, cudaMemcpyDeviceToHost, st));
+    d2h_small(hc.data(), w.counters.get(), 8 * NC, st);
     PPRG_CUDA(cudaStreamSynchronize(st));
     for (int c = 0; c < K; ++c) qsize[c] = hc[1 + c];
     call->kernel_launches += 1;
   } else {
     std::vector<uint32_t> hdeg(K);
     for (int c = 0; c < K; ++c)
-      PPRG_CUDA(cudaMemcpyAsync(&hdeg[c], g.deg.get() + b.src[c], 4, cudaMemcpyDeviceToHost, st));
+      d2h_small(&hdeg[c], g.deg.get() + b.src[c], 4, st);
     PPRG_CUDA(cudaStreamSynchronize(st));
     for (uint32_t c = 0; c < b.k; ++c)  // seed_source, push.cpp:61-66
       if (state[c] == 0 && 1.0 > (double)(hdeg[c] ? hdeg[c] : 1) * r_max) {
@@ -1529,13 +1565,11 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     PPRG_CUDA(cudaGetLastError());
     call->kernel_launches += 1;
     unsigned nheavy = 0;
-    PPRG_CUDA(cudaMemcpyAsync(&nheavy, w.heavy_cnt.get(), 4, cudaMemcpyDeviceToHost, st));
+    d2h_small(&nheavy, w.heavy_cnt.get(), 4, st);
     PPRG_CUDA(cudaStreamSynchronize(st));
     if (nheavy) {
       std::vector<HeavyEntry> hv(nheavy);
-      PPRG_CUDA(cudaMemcpyAsync(hv.data(), w.heavy.get(), sizeof(HeavyEntry) * nheavy,
-                                cudaMemcpyDeviceToHost, st));
-      PPRG_CUDA(cudaStreamSynchronize(st));
+      d2h_small(hv.data(), w.heavy.get(), sizeof(HeavyEntry) * nheavy, st);
       std::vector<unsigned long long> pre(nheavy + 1, 0);
       for (unsigned h = 0; h < nheavy; ++h) pre[h + 1] = pre[h] + hv[h].deg;
       w.heavy_prefix.ensure(nheavy + 1);
@@ -1547,9 +1581,9 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
       PPRG_CUDA(cudaGetLastError());
       call->kernel_launches += 1;
     }
-    PPRG_CUDA(cudaMemcpyAsync(hc.data(), w.counters.get(), 8 * NC, cudaMemcpyDeviceToHost, st));
-    PPRG_CUDA(cudaMemcpyAsync(hdr.data(), col_dr, 8 * KMAX, cudaMemcpyDeviceToHost, st));
-    PPRG_CUDA(cudaMemcpyAsync(hstop.data(), d_stop, 4 * KMAX, cudaMemcpyDeviceToHost, st));
+    d2h_small(hc.data(), w.counters.get(), 8 * NC, st);
+    d2h_small(hdr.data(), col_dr, 8 * KMAX, st);
+    d2h_small(hstop.data(), d_stop, 4 * KMAX, st);
     PPRG_CUDA(cudaStreamSynchronize(st));
     if (std::getenv("PPRG_DEBUG_LOCAL")) {
       unsigned long long nn = 0, np = 0, app = 0;
@@ -1586,7 +1620,7 @@ void exact_rsum(Block& b, const std::vector<int>& which) {
   PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
   k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), g.n, b.K, b.w.dcols.get() + KMAX);
   std::vector<double> exact(KMAX);
-  PPRG_CUDA(cudaMemcpyAsync(exact.data(), b.w.dcols.get() + KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
+  d2h_small(exact.data(), b.w.dcols.get() + KMAX, 8 * KMAX, st);
   PPRG_CUDA(cudaStreamSynchronize(st));
   for (uint32_t c = 0; c < b.k; ++c) {
     if (!which[c]) continue;
@@ -1611,7 +1645,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   PPRG_CUDA(cudaMemsetAsync(w.dcols.get() + 2 * KMAX, 0, 8 * KMAX, st));
   k_init_pull<<<grid_reduce(nk), 256, 0, st>>>(w.x.get(), g.deg.get(), g.inv_deg.get(), g.n, b.K,
                                             b.alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
-  PPRG_CUDA(cudaMemcpyAsync(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
+  d2h_small(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, st);
   PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
   PPRG_CUDA(cudaStreamSynchronize(st));
   SweepParams P = base_params(b);
@@ -1662,7 +1696,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
       PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
       dispatch_sweeps<M_POWERPUSH>(g, b.K, Q, true);
       SweepCtl one;
-      PPRG_CUDA(cudaMemcpyAsync(&one, w.ctl.get(), sizeof one, cudaMemcpyDeviceToHost, st));
+      d2h_small(&one, w.ctl.get(), sizeof one, st);
       PPRG_CUDA(cudaStreamSynchronize(st));
       hc.alg_bytes += one.alg_bytes;
       hc.total_sweeps = sweep + 1;
@@ -1704,7 +1738,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
     tm.start();
     dispatch_sweeps<M_POWERPUSH>(g, b.K, P, true);
     tm.stop();
-    PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
+    d2h_small(&hc, w.ctl.get(), sizeof hc, st);
   }
   call->sweep_ms += tm.ms();
   trace.fold(st, hc.total_sweeps, b.pushes[0], 0);
@@ -1793,14 +1827,25 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
   tf.stop();
   call->kernel_launches += 1;
   SweepCtl fc;
-  PPRG_CUDA(cudaMemcpyAsync(&fc, w.ctl.get(), sizeof fc, cudaMemcpyDeviceToHost, st));
+  d2h_small(&fc, w.ctl.get(), sizeof fc, st);
   if (!direct && (out.reserve || out.residue)) {
     PPRG_CUDA(cudaEventRecord(w.ev_ready[slot], st));
     PPRG_CUDA(cudaStreamWaitEvent(w.copy_st, w.ev_ready[slot], 0));
-    if (out.reserve)
-      PPRG_CUDA(cudaMemcpyAsync(out.reserve, Q.out_reserve, 8 * n * k, cudaMemcpyDeviceToHost, w.copy_st));
-    if (out.residue)
-      PPRG_CUDA(cudaMemcpyAsync(out.residue, Q.out_residue, 8 * n * k, cudaMemcpyDeviceToHost, w.copy_st));
+    // chunked, so the compute stream's small read-backs (per level / phase)
+    // never queue behind a whole multi-GB output copy on the copy engine
+    static const size_t chunk = [] {
+      const char* e = std::getenv("PPRG_D2H_CHUNK_MB");
+      return (size_t)(e ? std::atof(e) : 32.0) << 20;
+    }();
+    auto d2h = [&](double* dst, const double* src, size_t bytes) {
+      for (size_t o = 0; o < bytes; o += chunk)
+        PPRG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dst) + o,
+                                  reinterpret_cast<const char*>(src) + o,
+                                  bytes - o < chunk ? bytes - o : chunk, cudaMemcpyDeviceToHost,
+                                  w.copy_st));
+    };
+    if (out.reserve) d2h(out.reserve, Q.out_reserve, 8 * n * k);
+    if (out.residue) d2h(out.residue, Q.out_residue, 8 * n * k);
     PPRG_CUDA(cudaEventRecord(w.ev_done[slot], w.copy_st));
   }
   PPRG_CUDA(cudaStreamSynchronize(st));
@@ -1880,7 +1925,7 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
     {  // r_sum of the incoming state (no drift check: it is the caller's)
       PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
       k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), n, b.K, b.w.dcols.get() + KMAX);
-      PPRG_CUDA(cudaMemcpyAsync(b.r_sum.data(), b.w.dcols.get() + KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
+      d2h_small(b.r_sum.data(), b.w.dcols.get() + KMAX, 8 * KMAX, st);
       PPRG_CUDA(cudaStreamSynchronize(st));
     }
     std::vector<int> state(KMAX, 2);
@@ -1954,7 +1999,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       k_seed<<<1, KMAX, 0, st>>>(w.r0.get(), w.d_src.get(), b.K, 1.0);
       k_init_pull<<<grid_reduce(nk), 256, 0, st>>>(w.r0.get(), g.deg.get(), g.inv_deg.get(), n, b.K,
                                                 alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
-      PPRG_CUDA(cudaMemcpyAsync(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, cudaMemcpyDeviceToHost, st));
+      d2h_small(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, st);
       PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
       PPRG_CUDA(cudaStreamSynchronize(st));
       SweepParams P = base_params(b);
@@ -1996,7 +2041,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
           if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, Q, true);
           else dispatch_sweeps<M_SIMFWD>(g, b.K, Q, true);
           SweepCtl one;
-          PPRG_CUDA(cudaMemcpyAsync(&one, w.ctl.get(), sizeof one, cudaMemcpyDeviceToHost, st));
+          d2h_small(&one, w.ctl.get(), sizeof one, st);
           PPRG_CUDA(cudaStreamSynchronize(st));
           hc.alg_bytes += one.alg_bytes;
           hc.total_sweeps = it + 1;
@@ -2019,7 +2064,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
         if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, P, true);
         else dispatch_sweeps<M_SIMFWD>(g, b.K, P, true);
         tm.stop();
-        PPRG_CUDA(cudaMemcpyAsync(&hc, w.ctl.get(), sizeof hc, cudaMemcpyDeviceToHost, st));
+        d2h_small(&hc, w.ctl.get(), sizeof hc, st);
       }
       call->sweep_ms += tm.ms();
       trace.fold(st, hc.total_sweeps, 0, eng == Engine::PowItr ? g.m_eff() : 0);
@@ -2456,7 +2501,7 @@ void part_finish(PartSession* s, double* reserve, double* residue, bool on_devic
   dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
   tf.stop();
   SweepCtl fc;
-  PPRG_CUDA(cudaMemcpyAsync(&fc, b.w.ctl.get(), sizeof fc, cudaMemcpyDeviceToHost, st));
+  d2h_small(&fc, b.w.ctl.get(), sizeof fc, st);
   if (!on_device && w) {
     for (uint32_t c = 0; c < k; ++c) {
       if (reserve)
