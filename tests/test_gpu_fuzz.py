@@ -1,0 +1,92 @@
+"""Seeded randomized parity sweep: graph shapes the reference's tests do not
+hit one by one (hub rows longer than a tile, many dead ends, self-loops and
+duplicate edges, isolated nodes, tiny and single-node graphs) x every
+high-precision engine x column-block widths, against the CPU oracle."""
+import numpy as np
+import pytest
+
+from oracle.pyoracle import CSR
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2101_03652_b200 as P
+    P.load_library()
+    return P
+
+
+def hub_graph(n, hubs, hub_deg, rng):
+    """Random graph plus `hubs` nodes with in-degree hub_deg (rows split into
+    several tile pieces) and a few self-loops / duplicate edges."""
+    src = rng.integers(0, n, size=6 * n)
+    dst = rng.integers(0, n, size=6 * n)
+    hs = rng.choice(n, size=hubs, replace=False)
+    extra_src = rng.integers(0, n, size=hubs * hub_deg)
+    extra_dst = np.repeat(hs, hub_deg)
+    loops = rng.integers(0, n, size=20)
+    s = np.concatenate([src, extra_src, loops, src[:50]])
+    d = np.concatenate([dst, extra_dst, loops, dst[:50]])
+    keep = rng.random(len(s)) > 0.1          # leaves dead ends behind
+    s, d = s[keep], d[keep]
+    order = np.argsort(s, kind="stable")
+    s, d = s[order], d[order]
+    off = np.zeros(n + 1, np.uint64)
+    np.add.at(off, s + 1, 1)
+    return CSR(np.cumsum(off).astype(np.uint64), d.astype(np.uint32))
+
+
+CASES = [(1, 0, 0, 0), (7, 0, 0, 1), (300, 1, 3000, 2), (2000, 3, 9000, 3), (5000, 2, 20000, 4)]
+
+
+@pytest.mark.parametrize("n,hubs,hub_deg,seed", CASES)
+@pytest.mark.parametrize("k", [1, 3, 16, 64])
+def test_power_push_fuzz(P, oracle, n, hubs, hub_deg, seed, k):
+    rng = np.random.default_rng(seed)
+    g = hub_graph(n, hubs, hub_deg, rng) if n > 1 else CSR(np.array([0, 1], np.uint64),
+                                                           np.array([0], np.uint32))
+    d = P.Graph(g.offsets, g.neighbors)
+    src = rng.integers(0, g.n, size=k)
+    lam = 1e-9
+    outs, _ = P.power_push_batch(d, src, 0.2, lam)
+    for q in range(0, k, max(1, k // 3)):
+        ref = oracle.power_push(g, int(src[q]), 0.2, lam)
+        o = outs[q]
+        assert o.achieved_r_sum <= lam
+        assert np.max(np.abs(o.estimates - ref.estimates)) <= lam
+        assert abs(o.estimates.sum() + o.residues.sum() - 1.0) < 1e-9
+        assert np.all(o.residues >= 0.0)
+
+
+@pytest.mark.parametrize("n,hubs,hub_deg,seed", CASES[1:])
+def test_power_iteration_fuzz(P, oracle, n, hubs, hub_deg, seed):
+    rng = np.random.default_rng(seed + 100)
+    g = hub_graph(n, hubs, hub_deg, rng)
+    d = P.Graph(g.offsets, g.neighbors)
+    src = rng.integers(0, g.n, size=5)
+    outs, _ = P.power_iteration_batch(d, src, 0.2, 1e-10)
+    for q, s in enumerate(src):
+        ref = oracle.power_iteration(g, int(s), 0.2, 1e-10)
+        assert np.max(np.abs(outs[q].estimates - ref.estimates)) <= 1e-12
+        assert outs[q].sweeps == ref.iterations
+
+
+@pytest.mark.parametrize("n,hubs,hub_deg,seed", CASES[1:])
+def test_fifo_and_ground_truth_fuzz(P, oracle, n, hubs, hub_deg, seed):
+    rng = np.random.default_rng(seed + 200)
+    g = hub_graph(n, hubs, hub_deg, rng)
+    d = P.Graph(g.offsets, g.neighbors)
+    s = int(rng.integers(0, g.n))
+    m_eff = int(g.offsets[-1]) + int(np.sum(np.diff(g.offsets) == 0))
+    lam = 1e-8
+    f = P.fifo_forward_push(d, s, 0.2, lam / m_eff)
+    deg = np.maximum(np.diff(g.offsets).astype(np.float64), 1)
+    assert np.all(f.residues <= deg * lam / m_eff)
+    truth = P.ground_truth(d, s, 0.2)
+    assert truth.achieved_r_sum <= 1e-17
+    assert np.all(truth.estimates - f.estimates >= -1e-15)  # FIFO under-estimates
+    # l1 = r_sum up to the rounding accumulated over millions of fp64 pushes
+    assert np.abs(truth.estimates - f.estimates).sum() <= f.achieved_r_sum + 1e-12
+    if g.n <= 2000:
+        assert np.abs(truth.estimates - oracle.exact_ppr(g, s, 0.2)).sum() <= 1e-12
