@@ -424,7 +424,8 @@ constexpr uint32_t RMAX_W = PPRG_RMAX_W;
 #endif
 template <int K>
 __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double* yg, uint64_t b,
-                                             uint64_t e, double (&s)[(K < 32 ? 1 : K / 32)]) {
+                                             uint64_t e, double (&s)[(K < 32 ? 1 : K / 32)],
+                                             bool have_first = false, uint32_t first_id = 0) {
   constexpr int KC = K < 32 ? K : 32;
   constexpr int CPL = K / KC;
   constexpr int ES = 32 / KC;
@@ -436,7 +437,7 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double*
   for (int q = 0; q < CPL; ++q) acc[q][0] = acc[q][1] = 0.0;
   for (uint64_t p0 = b; p0 < e; p0 += 32) {
     const uint64_t pl = p0 + lane;
-    const uint32_t myid = pl < e ? ld_stream(P.in_nbr + pl) : 0u;
+    const uint32_t myid = (have_first && p0 == b) ? first_id : (pl < e ? ld_stream(P.in_nbr + pl) : 0u);
     const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
     for (int j0 = 0; j0 < cnt; j0 += G * ES) {
       double v[G][CPL];
@@ -544,23 +545,38 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
   __syncthreads();
   if (dn_slot) *dn = P.desc[*dn_slot < P.ntiles ? *dn_slot : 0];  // next tile's descriptor
   // ---- short rows: one warp per row, dynamic -----------------------------
-  for (;;) {
+  // Rows are taken one ahead: the next row's first 32 in-edge ids are loaded
+  // before this row's gathers, so their latency hides behind the gathers.
+  auto grab = [&]() -> uint32_t {
     uint32_t r = 0;
     if (lane == 0) r = atomicAdd(rowctr, 1u);
-    r = __shfl_sync(0xffffffffu, r, 0);
-    if (r >= nr) break;
+    return __shfl_sync(0xffffffffu, r, 0);
+  };
+  auto first_ids = [&](uint32_t r) -> uint32_t {
+    if (r >= nr) return 0u;
     const uint64_t b = soff[r], e = soff[r + 1];
-    if (e - b > LONG_W) continue;
-    const uint32_t u = snode[r];
-    double xo[CPL], rc[CPL], s[CPL];
+    return (e - b <= LONG_W && b + lane < e) ? ld_stream(P.in_nbr + b + lane) : 0u;
+  };
+  uint32_t r = grab();
+  uint32_t ids = first_ids(r);
+  while (r < nr) {
+    const uint64_t b = soff[r], e = soff[r + 1];
+    const uint32_t rn = grab();
+    const uint32_t ids_n = first_ids(rn);
+    if (e - b <= LONG_W) {
+      const uint32_t u = snode[r];
+      double xo[CPL], rc[CPL], s[CPL];
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {  // issued early; lands during the edge loop
-      const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
-      xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
-      rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
+      for (int q = 0; q < CPL; ++q) {  // issued early; lands during the edge loop
+        const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
+        xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
+        rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
+      }
+      warp_row_sum<K>(P, yg, b, e, s, true, ids);
+      if (es0) decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
     }
-    warp_row_sum<K>(P, yg, b, e, s);
-    if (es0) decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
+    r = rn;
+    ids = ids_n;
   }
   // ---- long rows: all warps split the edges ---------------------------------
   const uint32_t nl = slong[RMAX_W];
