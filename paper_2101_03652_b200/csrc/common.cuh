@@ -219,6 +219,38 @@ __device__ __forceinline__ unsigned ld_acquire32(const unsigned* p) {
 // = (barrier generation + 1) * gridDim.x. Requires a cooperative launch (all
 // blocks co-resident). The gpu-scope fence also invalidates the SM's L1, so
 // every sweep starts from values at least as new as the previous sweep's.
+// Two-level grid barrier: blocks arrive on one of up to 32 group counters
+// (separate 128-byte lines), the last of each group on the top counter, and
+// the very last block publishes the generation that everyone polls. The
+// serialised atomics per barrier drop from gridDim.x to ~gridDim.x/32 + 32.
+struct GridBarrier {
+  unsigned long long grp[32][16];
+  unsigned long long top[16];
+  unsigned long long flag[16];
+};
+
+__device__ __forceinline__ void grid_barrier2(GridBarrier* gb, unsigned long long gen) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned ng = gridDim.x < 32 ? gridDim.x : 32;
+    const unsigned g = blockIdx.x % ng;
+    const unsigned long long gsize = gridDim.x / ng + (g < gridDim.x % ng ? 1 : 0);
+    __threadfence();
+    const unsigned long long old = atomicAdd(&gb->grp[g][0], 1ull);
+    if (old + 1 == gsize * gen) {
+      __threadfence();
+      const unsigned long long o2 = atomicAdd(&gb->top[0], 1ull);
+      if (o2 + 1 == (unsigned long long)ng * gen) {
+        __threadfence();
+        atomicExch(&gb->flag[0], gen);
+      }
+    }
+    while (ld_acquire(&gb->flag[0]) < gen) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void grid_barrier(unsigned long long* counter,
                                              unsigned long long target) {
   __syncthreads();

@@ -59,6 +59,7 @@ uint64_t host_now_ns() {
 
 struct SweepCtl {
   unsigned long long barrier;
+  GridBarrier gbar;
   unsigned ticket[3];
   unsigned pad_;
   double pushed[3][KMAX];              // powerpush: pushed mass; powitr: sum of next
@@ -757,7 +758,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
       __syncthreads();
       break;
     }
-    grid_barrier(&ctl->barrier, (++gen) * gridDim.x);
+    grid_barrier2(&ctl->gbar, ++gen);
     // every block derives the identical next state from the reduced buffers
     if (tid < K) {
       const int cc = tid;
