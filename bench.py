@@ -328,6 +328,7 @@ def main():
                          "peak_kind": peak_kind, "kernel": "k_sweeps<K,POWERPUSH>",
                          "alg_bytes_per_step": alg / args.steps,
                          "alg_bytes_per_launch": alg / max(sweep_launches, 1),
+                         "achieved_whole_step_GBps": alg / args.steps / (ms / args.steps / 1e3) / 1e9,
                          "sweep_ms_per_step": sweep_ms / args.steps,
                          "sweeps_per_block": sweeps[-1]},
             "clocks": clk.summary()}
