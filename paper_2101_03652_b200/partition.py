@@ -273,7 +273,7 @@ def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None,
     y = part.y_view()
 
     def exchange():  # all-gather-v of the y row slices; the final pass needs it too
-        if fused:
+        if fused or world == 1:
             return
         for p, (lo, hi) in enumerate(bounds):
             if hi > lo:
