@@ -803,6 +803,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
     }
     __syncthreads();
   }
+  if (MODE == M_POWERPUSH && P.npeers) __threadfence_system();  // peer y stores performed
   if (blockIdx.x == 0 && tid < K) {
     ctl->out_rsum[tid] = cs[tid].r_sum;
     ctl->out_D[tid] = cs[tid].D;
@@ -2231,6 +2232,7 @@ __global__ void k_part_y(const double* x, const double* inv_deg, uint64_t lo, ui
     y[i] = v;
     for (int p = 0; p < peers.n; ++p) peers.y[p][i] = v;
   }
+  if (peers.n) __threadfence_system();
 }
 
 __global__ void k_pack_counters(const SweepCtl* ctl, int K, double* out) {
