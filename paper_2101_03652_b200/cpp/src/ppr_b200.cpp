@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
 #include <fstream>
 #include <stdexcept>
 #include <string>
@@ -17,6 +18,7 @@
 #include "ppr/metrics.hpp"
 #include "ppr/push.hpp"
 #include "ppr/speedppr.hpp"
+#include "ppr/sweep.hpp"
 #include "ppr/synthetic.hpp"
 #include "ppr/walk_index.hpp"
 
@@ -606,6 +608,121 @@ std::vector<double> read_ppr_csv(const std::string& path) {
     ++expected;
   }
   return values;
+}
+
+// ---- sweep.hpp (sweep.cpp:16-147) ----------------------------------------------------
+bool is_high_precision_algo(const std::string& name) {
+  return name == kAlgoPowItr || name == kAlgoFifoFwdPush || name == kAlgoSimFwdPush ||
+         name == kAlgoPowerPush;
+}
+bool is_known_algo(const std::string& name) {
+  return is_high_precision_algo(name) || name == kAlgoSpeedPPR;
+}
+
+CheckpointRecorder::CheckpointRecorder(std::uint64_t cadence)
+    : cadence_(cadence ? cadence : 1), next_mark_(cadence_),
+      started_(std::chrono::steady_clock::now()) {}
+
+void CheckpointRecorder::on_push(const PushState& st) {
+  if (st.edge_push_count < next_mark_) return;
+  const auto ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now() - started_)
+                      .count();
+  checkpoints_.push_back({st.edge_push_count, st.r_sum, static_cast<std::uint64_t>(ns)});
+  while (next_mark_ <= st.edge_push_count) next_mark_ += cadence_;
+}
+
+namespace {
+PPRVector run_high_precision(const Graph& g, NodeId s, const std::string& algo, double alpha,
+                             double lambda, PushObserver* obs) {
+  if (algo == kAlgoPowItr) return power_iteration(g, s, alpha, lambda, obs);
+  if (algo == kAlgoSimFwdPush) return sim_forward_push(g, s, alpha, lambda, obs);
+  if (algo == kAlgoFifoFwdPush)
+    return fifo_forward_push(g, s, alpha, lambda / static_cast<double>(g.effective_edge_count()),
+                             std::nullopt, obs);
+  QueryConfig cfg;
+  cfg.alpha = alpha;
+  return power_push(g, s, alpha, lambda, cfg, obs);
+}
+std::uint64_t since_ns(std::chrono::steady_clock::time_point t0) {
+  return static_cast<std::uint64_t>(
+      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
+          .count());
+}
+}  // namespace
+
+SweepResult run_sweep(const Graph& g, const std::vector<NodeId>& sources, const SweepPlan& plan) {
+  for (const auto& a : plan.algorithms)
+    if (!is_known_algo(a)) throw std::invalid_argument("unknown algorithm: " + a);
+  const std::uint64_t cadence = plan.checkpoint_every ? plan.checkpoint_every : 4 * g.m();
+  const double mu = plan.mu ? *plan.mu : default_mu(g.n());
+  SweepResult result;
+  for (NodeId s : sources) {
+    const PPRVector truth = ground_truth(g, s, plan.alpha);
+    for (const auto& algo : plan.algorithms) {
+      if (is_high_precision_algo(algo)) {
+        for (double lambda : plan.lambdas) {
+          CheckpointRecorder rec(cadence);
+          const auto t0 = std::chrono::steady_clock::now();
+          const PPRVector got = run_high_precision(g, s, algo, plan.alpha, lambda, &rec);
+          const std::uint64_t wall = since_ns(t0);
+          const ErrorReport rep = compare_to_truth(got.estimates, truth.estimates, mu, 0.0);
+          SweepCell cell;
+          cell.row = {s, algo, lambda, wall, got.pushes, got.walks, rep.l1, rep.max_rel_above_mu};
+          cell.checkpoints = rec.checkpoints();
+          result.cells.push_back(std::move(cell));
+        }
+      } else {
+        for (double eps : plan.epsilons)
+          for (std::uint64_t seed : plan.seeds) {
+            QueryConfig cfg;
+            cfg.alpha = plan.alpha;
+            cfg.epsilon = eps;
+            cfg.mu = plan.mu;
+            cfg.seed = seed;
+            const auto t0 = std::chrono::steady_clock::now();
+            const PPRVector got = speedppr_query(g, s, cfg);
+            const std::uint64_t wall = since_ns(t0);
+            const ErrorReport rep = compare_to_truth(got.estimates, truth.estimates, mu, eps);
+            SweepCell cell;
+            cell.row = {s, algo, eps, wall, got.pushes, got.walks, rep.l1, rep.max_rel_above_mu};
+            result.cells.push_back(std::move(cell));
+          }
+      }
+    }
+  }
+  return result;
+}
+
+void write_sweep_csv(const SweepResult& result, const std::string& directory,
+                     const std::string& graph_name) {
+  namespace fs = std::filesystem;
+  fs::create_directories(directory);
+  const fs::path dir(directory);
+  std::ofstream summary(dir / (graph_name + "_sweep.csv"), std::ios::trunc);
+  if (!summary) throw std::runtime_error("cannot write sweep summary");
+  summary << "source,algo,param,wall_time_ns,edge_pushes,walks,l1_error,max_rel_error\n";
+  for (const auto& cell : result.cells) {
+    const auto& r = cell.row;
+    summary << r.source << ',' << r.algo << ',' << format_double(r.param) << ',' << r.wall_time_ns
+            << ',' << r.edge_pushes << ',' << r.walks << ',' << format_double(r.l1_error) << ','
+            << format_double(r.max_rel_error) << '\n';
+    if (!cell.checkpoints.empty()) {
+      char param[32];
+      std::snprintf(param, sizeof(param), "%g", r.param);
+      std::ofstream series(dir / (graph_name + "_" + r.algo + "_" + param + ".csv"), std::ios::trunc);
+      series << "pushes,r_sum,time_ns\n";
+      for (const auto& c : cell.checkpoints)
+        series << c.pushes << ',' << format_double(c.r_sum) << ',' << c.time_ns << '\n';
+    }
+  }
+}
+
+std::vector<NodeId> sample_sources(const Graph& g, std::uint64_t count, std::uint64_t seed) {
+  Rng rng(seed);
+  std::vector<NodeId> out(count);
+  for (auto& s : out) s = static_cast<NodeId>(rng.below(g.n()));
+  return out;
 }
 
 }  // namespace ppr

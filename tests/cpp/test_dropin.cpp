@@ -16,6 +16,7 @@
 #include "ppr/push.hpp"
 #include "ppr/speedppr.hpp"
 #include "ppr/synthetic.hpp"
+#include "ppr/sweep.hpp"
 #include "ppr/walk_index.hpp"
 
 using namespace ppr;
@@ -350,6 +351,35 @@ int main() {
     }
     CHECK(threw);
     std::remove(path.c_str());
+  }
+  {  // sweep harness (test_metrics.cpp sweep cases)
+    SweepPlan plan;
+    plan.algorithms = {kAlgoPowerPush, kAlgoPowItr, kAlgoSpeedPPR};
+    plan.lambdas = {1e-4, 1e-8};
+    plan.epsilons = {0.5};
+    const SweepResult r = run_sweep(g, {0}, plan);
+    CHECK(r.cells.size() == 5);
+    CHECK(r.cells[0].row.edge_pushes <= r.cells[1].row.edge_pushes);  // pushes grow as lambda shrinks
+    for (const auto& c : r.cells)
+      if (c.row.algo != kAlgoSpeedPPR) CHECK(c.row.l1_error <= c.row.param + 1e-12);
+    CHECK(!r.cells[1].checkpoints.empty());
+    bool threw = false;
+    try {
+      SweepPlan bad;
+      bad.algorithms = {"nosuch"};
+      run_sweep(g, {0}, bad);
+    } catch (const std::invalid_argument&) {
+      threw = true;
+    }
+    CHECK(threw);
+    write_sweep_csv(r, "/tmp/pprg_dropin_sweep", "five");
+    std::ifstream in("/tmp/pprg_dropin_sweep/five_sweep.csv");
+    std::string header;
+    std::getline(in, header);
+    CHECK(header == "source,algo,param,wall_time_ns,edge_pushes,walks,l1_error,max_rel_error");
+    const auto src = sample_sources(g, 10, 3);
+    CHECK(src.size() == 10);
+    for (NodeId v : src) CHECK(v < g.n());
   }
   return failures;
 }
