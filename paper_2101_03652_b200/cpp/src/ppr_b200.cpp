@@ -14,6 +14,7 @@
 
 #include "../../../include/pprg.h"
 #include "ppr/csv.hpp"
+#include "ppr/exact_ppr.hpp"
 #include "ppr/graph.hpp"
 #include "ppr/metrics.hpp"
 #include "ppr/push.hpp"
@@ -573,6 +574,38 @@ PPRVector ground_truth(const Graph& g, NodeId s, double alpha) {
   v.achieved_r_sum = qs.achieved_r_sum;
   v.pushes = qs.pushes;
   return v;
+}
+
+// ---- exact_ppr.hpp (exact_ppr.cpp:45-90 guards and checks) -------------------------
+DensePPR exact_ppr(const Graph& g, NodeId s, double alpha) {
+  const NodeId n = g.n();
+  if (n > kDenseSolveMaxNodes)
+    throw std::invalid_argument("exact_ppr: graph exceeds the dense solve guard");
+  if (!(alpha > 0.0 && alpha < 1.0)) throw std::invalid_argument("exact_ppr: alpha must be in (0,1)");
+  if (s >= n) throw std::invalid_argument("exact_ppr: source out of range");
+  std::vector<double> x(n, 0.0);
+  pprg_query_stats qs{};
+  check(pprg_ground_truth(g.device_handle(), &s, 1, alpha, x.data(), 0, &qs, nullptr));
+  double sum = 0.0;
+  for (double& v : x) {
+    if (v < 0.0) {
+      if (v < -1e-12) throw std::logic_error("exact_ppr: negative probability");
+      v = 0.0;
+    }
+    sum += v;
+  }
+  if (std::abs(sum - 1.0) > 1e-10) throw std::logic_error("exact_ppr: result does not sum to 1");
+  std::vector<double> resid(x);  // pi - alpha e_s - (1-alpha) pi P
+  resid[s] -= alpha;
+  for (NodeId v = 0; v < n; ++v) {
+    const auto out = effective_out(g, v, s);
+    const double share = (1.0 - alpha) * x[v] / static_cast<double>(out.degree());
+    for (NodeId u : out) resid[u] -= share;
+  }
+  double l1 = 0.0;
+  for (double r : resid) l1 += std::abs(r);
+  if (l1 > 1e-10) throw std::logic_error("exact_ppr: residual check failed");
+  return DensePPR{std::move(x)};
 }
 
 // ---- csv.hpp (csv.cpp:9-43) --------------------------------------------------------

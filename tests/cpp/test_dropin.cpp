@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "ppr/csv.hpp"
+#include "ppr/exact_ppr.hpp"
 #include "ppr/graph.hpp"
 #include "ppr/metrics.hpp"
 #include "ppr/push.hpp"
@@ -380,6 +381,18 @@ int main() {
     const auto src = sample_sources(g, 10, 3);
     CHECK(src.size() == 10);
     for (NodeId v : src) CHECK(v < g.n());
+  }
+  {  // exact_ppr (test_oracle.cpp: five-node frozen solve, two-cycle closed form, guards)
+    const double pi0[5] = {0.29366106080206994, 0.27166882276843485, 0.23285899094437276,
+                           0.1474773609314361, 0.054333764553686985};
+    const DensePPR d = exact_ppr(g, 0, 0.2);
+    for (int v = 0; v < 5; ++v) CHECK(std::fabs(d.pi[v] - pi0[v]) < 1e-12);
+    const Graph two = build_graph_from_edges({{0, 1}, {1, 0}});
+    const DensePPR t = exact_ppr(two, 0, 0.2);
+    CHECK(std::fabs(t.pi[0] - 5.0 / 9.0) < 1e-12 && std::fabs(t.pi[1] - 4.0 / 9.0) < 1e-12);
+    CHECK_THROWS_AS(exact_ppr(g, 9, 0.2), std::invalid_argument);
+    CHECK_THROWS_AS(exact_ppr(g, 0, 0.0), std::invalid_argument);
+    CHECK_THROWS_AS(exact_ppr(random_graph(2001, 1, 2, 1), 0, 0.2), std::invalid_argument);
   }
   return failures;
 }
