@@ -27,22 +27,28 @@ class WalkIndex {
     return {endpoints_.data() + offsets_[v], static_cast<std::size_t>(offsets_[v + 1] - offsets_[v])};
   }
   void check_compatible(const Graph& g) const;
+  // Device copy bound to g (uploaded on first use with a graph when the index
+  // came from a file without one).
+  pprg_index* device_handle(const Graph& g) const;
   pprg_index* device_handle() const { return dev_.get(); }
 
  private:
   friend WalkIndex build_index(const Graph&, double, std::uint64_t);
   friend WalkIndex load_index(const std::string&, const Graph&);
+  friend WalkIndex load_index(const std::string&);
   double alpha_ = 0;
   std::uint64_t seed_ = 0;
   std::vector<std::uint64_t> offsets_;
   std::vector<NodeId> endpoints_;
-  std::shared_ptr<pprg_index> dev_;
+  mutable std::shared_ptr<pprg_index> dev_;
+  mutable const void* dev_graph_ = nullptr;
 };
 
 WalkIndex build_index(const Graph& g, double alpha, std::uint64_t seed);
 void save_index(const WalkIndex& index, const std::string& path);
-// The reference's load_index(path) needs no graph; ours binds the device copy
-// to the graph it will serve.
+// load_index(path) (walk_index.cpp:83-104) keeps the index on the host until
+// it first serves a graph; the two-argument form binds it immediately.
+WalkIndex load_index(const std::string& path);
 WalkIndex load_index(const std::string& path, const Graph& g);
 
 }  // namespace ppr

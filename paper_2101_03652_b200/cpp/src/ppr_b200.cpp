@@ -304,6 +304,7 @@ WalkIndex build_index(const Graph& g, double alpha, std::uint64_t seed) {
   check(pprg_index_build(g.device_handle(), alpha, seed, &h));
   WalkIndex w;
   w.dev_.reset(h, pprg_index_destroy);
+  w.dev_graph_ = g.device_handle();
   w.alpha_ = alpha;
   w.seed_ = seed;
   w.offsets_ = g.out_offsets();
@@ -336,7 +337,7 @@ void save_index(const WalkIndex& index, const std::string& path) {  // walk_inde
   if (!out) throw std::runtime_error("write failed: " + path);
 }
 
-WalkIndex load_index(const std::string& path, const Graph& g) {  // walk_index.cpp:83-104
+WalkIndex load_index(const std::string& path) {  // walk_index.cpp:83-104
   std::ifstream in(path, std::ios::binary);
   if (!in) throw std::runtime_error("cannot open walk index: " + path);
   char magic[4];
@@ -356,11 +357,43 @@ WalkIndex load_index(const std::string& path, const Graph& g) {  // walk_index.c
   w.endpoints_.resize(m);
   for (auto& e : w.endpoints_) e = read_u32(in);
   if (!in) throw std::runtime_error(path + ": truncated walk index");
-  w.check_compatible(g);
-  pprg_index* h = nullptr;
-  check(pprg_index_from_host(g.device_handle(), alpha, seed, w.endpoints_.data(), &h));
-  w.dev_.reset(h, pprg_index_destroy);
+  // WalkIndex constructor checks (walk_index.cpp:19-34)
+  if (w.offsets_.empty() || w.offsets_.front() != 0 || w.offsets_.back() != m)
+    throw std::runtime_error("walk index: inconsistent offsets");
+  for (std::size_t i = 0; i + 1 < w.offsets_.size(); ++i)
+    if (w.offsets_[i + 1] < w.offsets_[i])
+      throw std::runtime_error("walk index: offsets must be non-decreasing");
+  for (NodeId e : w.endpoints_)
+    if (e >= n) throw std::runtime_error("walk index: endpoint id out of range");
   return w;
+}
+
+WalkIndex load_index(const std::string& path, const Graph& g) {
+  WalkIndex w = load_index(path);
+  (void)w.device_handle(g);
+  return w;
+}
+
+pprg_index* WalkIndex::device_handle(const Graph& g) const {
+  if (dev_ && dev_graph_ == g.device_handle()) return dev_.get();
+  check_compatible(g);
+  pprg_index* h = nullptr;
+  check(pprg_index_from_host(g.device_handle(), alpha_, seed_, endpoints_.data(), &h));
+  dev_.reset(h, pprg_index_destroy);
+  dev_graph_ = g.device_handle();
+  return h;
+}
+
+void push_once(PushState& st, NodeId v, const Graph& g, NodeId s, double alpha) {
+  const double r = st.residue[v];
+  if (r <= 0.0) return;
+  st.reserve[v] += alpha * r;
+  st.residue[v] = 0.0;  // zeroed before the spread: a self-loop keeps its share
+  const auto out = effective_out(g, v, s);
+  const double share = (1.0 - alpha) * r / static_cast<double>(out.degree());
+  for (NodeId u : out) st.residue[u] += share;
+  st.r_sum -= alpha * r;
+  st.edge_push_count += out.degree();
 }
 
 double walk_budget_real(std::uint64_t n, double epsilon, double mu) {  // speedppr.cpp:8-14
@@ -390,7 +423,7 @@ PPRVector mc_phase(const Graph& g, NodeId s, double alpha, PushState&& st, std::
   out.estimates.assign(g.n(), 0.0);
   out.residues.assign(g.n(), 0.0);
   std::uint64_t walks = 0;
-  check(pprg_monte_carlo(g.device_handle(), index ? index->device_handle() : nullptr, s, alpha, W,
+  check(pprg_monte_carlo(g.device_handle(), index ? index->device_handle(g) : nullptr, s, alpha, W,
                          rng.next(), st.reserve.data(), st.residue.data(), out.estimates.data(),
                          &walks));
   out.source = s;
@@ -424,7 +457,7 @@ PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
   }
   PPRVector v = make_vector(g.n(), s, cfg.alpha);
   pprg_query_stats q{};
-  check(pprg_speedppr(g.device_handle(), index ? index->device_handle() : nullptr, &s, 1,
+  check(pprg_speedppr(g.device_handle(), index ? index->device_handle(g) : nullptr, &s, 1,
                       cfg.alpha, *cfg.epsilon, cfg.mu ? *cfg.mu : -1.0, cfg.seed,
                       v.estimates.data(), 0, &q, nullptr));
   v.pushes = q.pushes;
