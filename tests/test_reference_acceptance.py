@@ -30,3 +30,14 @@ def test_reference_acceptance_suite_on_the_gpu_engine():
         m = re.search(r"interruption points, worst gap ([0-9.e+-]+)", out)
         assert m and float(m.group(1)) <= 1e-9, out
         assert "failed: at least 1000 interruption points" in out
+
+
+def test_reference_cli_tests_on_our_command_line():
+    """tests/test_cli.cpp (compiled unchanged) driving tools/ppr, our CLI."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "test_cli_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/test_cli_dropin not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, os.path.join(ROOT, "tools", "ppr")], capture_output=True, text=True,
+                       timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "all cli checks passed" in r.stdout
