@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "ppr/graph.hpp"
+#include "ppr/rng.hpp"
 #include "ppr/types.hpp"
 
 struct pprg_index;
@@ -15,6 +16,12 @@ struct pprg_index;
 namespace ppr {
 
 inline constexpr std::uint8_t kRngIdPhilox4x32_10 = 2;
+
+// One alpha-random walk on the host from a caller's Rng stream
+// (walk_index.hpp:16): stop with probability alpha, else move to a uniform
+// effective out-neighbour (dead ends jump to source). The GPU engines draw
+// their walks from Philox streams instead.
+NodeId random_walk(const Graph& g, NodeId start, NodeId source, double alpha, Rng& rng);
 
 class WalkIndex {
  public:

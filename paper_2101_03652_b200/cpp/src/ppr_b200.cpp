@@ -384,6 +384,15 @@ pprg_index* WalkIndex::device_handle(const Graph& g) const {
   return h;
 }
 
+NodeId random_walk(const Graph& g, NodeId start, NodeId source, double alpha, Rng& rng) {
+  NodeId at = start;
+  while (rng.uniform01() >= alpha) {
+    const auto out = effective_out(g, at, source);
+    at = out[rng.below(out.degree())];
+  }
+  return at;
+}
+
 void push_once(PushState& st, NodeId v, const Graph& g, NodeId s, double alpha) {
   const double r = st.residue[v];
   if (r <= 0.0) return;
