@@ -1,0 +1,794 @@
+// Device side of the global sweeps: the persistent k_sweeps<K, MODE> kernel
+// (PowerPush epochs, PowItr / SimFwdPush iterations, the final residue pass)
+// and its tile / row machinery. Included by push.cu only (one translation unit).
+#pragma once
+#include <cub/cub.cuh>
+
+#include <cstdint>
+
+#include "internal.h"
+
+namespace pprg {
+
+constexpr int KMAX = 64;
+constexpr int EMAX = 64;   // max epochs
+#ifndef PPRG_NT
+#define PPRG_NT 128
+#endif
+constexpr int NT = PPRG_NT;
+#define PPRG_MAX_PEERS 15             // threads per block for the sweep kernels
+#ifndef PPRG_TILE_U
+#define PPRG_TILE_U 8
+#endif
+constexpr int TILE_U = PPRG_TILE_U;     // narrow path: gathers per thread per tile
+constexpr int SWEEP_ELEMS = NT * TILE_U;  // edges x columns per narrow tile
+
+enum SweepMode : int { M_POWERPUSH = 0, M_POWITR = 1, M_SIMFWD = 2, M_FINAL = 3 };
+
+thread_local TraceSink* g_trace = nullptr;
+thread_local StepSink* g_obs = nullptr;
+
+uint64_t host_now_ns() {
+  return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+struct SweepCtl {
+  unsigned long long barrier;
+  GridBarrier gbar;
+  unsigned ticket[3];
+  unsigned pad_;
+  double pushed[3][KMAX];              // powerpush: pushed mass; powitr: sum of next
+  unsigned long long npush[3][KMAX];   // edge pushes (sum deg_eff)
+  unsigned long long nnode[3][KMAX];   // node pushes
+  double dsum[3][KMAX];                // (1-alpha) * sum_dead x   (or next)
+  unsigned long long et[3][KMAX];      // sum of out-degrees over pushed rows (E_t)
+  unsigned long long alg_bytes;
+  // final state (block 0)
+  double out_rsum[KMAX];
+  double out_D[KMAX];
+  unsigned out_sweeps[KMAX];
+  int out_done[KMAX];
+  int out_epoch[KMAX];
+  unsigned long long out_pushes[KMAX];
+  unsigned total_sweeps;
+};
+
+struct SweepParams {
+  uint64_t n, m;
+  const uint64_t* in_off;      // compacted transpose rows (in-degree > 0)
+  const uint32_t* crow;        // node id of each compacted row
+  const uint32_t* cdeg;        // out-degree of each compacted row's node
+  const double* cinv;          // 1 / effective out-degree of each compacted row's node
+  const uint64_t* in_off_full; // transpose offsets per node
+  const uint32_t* in_nbr;
+  const uint32_t* deg;
+  const double* inv_deg;
+  const uint32_t* tile_lo;
+  const TileDesc* desc;        // row-aligned tile plan
+  double* hub_acc;             // [ntiles][K] per-piece partial sums of hub rows
+  unsigned* hub_cnt;           // [nhubs] arrived pieces
+  uint64_t ntiles;
+  uint32_t T;
+  int k_live;  // real columns (<= K)
+  int E;
+  double alpha;
+  double lambda;               // powitr termination
+  double* x;                   // powerpush state / powitr reserve
+  double* y[2];                // gather operand (powitr double-buffers)
+  double* r[2];                // powitr residues (double-buffered)
+  const double* push_res;      // finalize: push-form residues (columns without scan phase)
+  double* carry_head;
+  double* carry_tail;
+  unsigned* split_cnt;
+
+  SweepCtl* ctl;
+  double* out_reserve;         // finalize outputs, query-major [c*n + u]
+  double* out_residue;
+  double* res_inter;           // finalize: explicit residues back into [u*K + c] (SpeedPPR)
+  uint32_t max_sweeps;
+  double* peer_y[PPRG_MAX_PEERS];  // fused exchange: other parts' y buffers (P2P / same device)
+  int npeers;
+  TracePoint* trace;            // per-sweep progress of column 0 (traced calls), or null
+  uint32_t trace_cap;
+  uint64_t own_lo, own_hi;      // node range this launch owns (vertex partition; else [0, n))
+  unsigned long long handoff_np;  // refine epoch: hand off to the frontier below this many edge pushes
+  uint32_t src[KMAX];
+  int final_pull[KMAX];        // finalize: 1 = residue from pull form
+  double thr[EMAX];            // epoch r_max (lambda is per call, so shared by columns)
+  double lam[EMAX];            // epoch lambda
+  ColInit init[KMAX];
+};
+
+struct ColSh {
+  double r_sum, D;
+  int epoch, done;
+  unsigned sweeps;
+  unsigned long long pushes;
+};
+
+// Tile geometry: a row-aligned tile holds at most T = SWEEP_ELEMS/K in-edges
+// and at most RMAX rows (host-built plan, Graph::tile_plan). Its gathered
+// values vals[e*K + c] and its row data live in shared memory.
+template <int K>
+struct Tile {
+  static constexpr int T = SWEEP_ELEMS / K;
+  static constexpr int RMAX = T < 256 ? T : 256;
+  static constexpr int LONG = K == 1 ? 32 : 16;  // rows longer than this: warp per row
+  // vals[SWEEP_ELEMS] f64 | sinv[RMAX] f64 | hub[NT/32 * K] f64 | soff[RMAX+1] i32 | snode, sdeg, slong [RMAX] u32
+  static constexpr size_t bytes = 8ull * (SWEEP_ELEMS + RMAX + (NT / 32) * K) +
+                                  4ull * (RMAX + 1) + 12ull * RMAX + 16;
+};
+
+struct Acc {  // per-thread sweep counters for the thread's column
+  double push = 0, d = 0;
+  unsigned long long np = 0, nn = 0, et = 0;
+};
+
+struct BlockAcc {  // shared, per column
+  double* push;
+  double* d;
+  unsigned long long* np;
+  unsigned long long* nn;
+  unsigned long long* et;
+};
+
+// The per-(row, column) decision: push form of push.cpp:182-193 in pull
+// representation, the PowItr update of push.cpp:90-99, or the final explicit
+// residue. `acc` is the sum over in-neighbours v of y_v.
+template <int K, int MODE>
+__device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, const double* thr_cur,
+                                       uint32_t u, int c, double acc, double xo, double rc,
+                                       uint32_t dg, double inv, const double* yg, double* rnxt,
+                                       double* ynxt, Acc& a) {
+  const uint64_t ix = (uint64_t)u * K + c;
+  const bool is_src = u == P.src[c];
+  const double alpha = P.alpha, oma = 1.0 - P.alpha;
+  if constexpr (MODE == M_POWERPUSH) {
+    if (cs[c].done) return;
+    const double inflow = acc + (is_src ? 1.0 + cs[c].D : 0.0);
+    const double r = inflow - xo;
+    if (r > (dg ? (double)dg : 1.0) * thr_cur[c]) {
+      st_state(P.x + ix, inflow);
+      if (dg) {
+        const double yv = oma * inflow * inv;
+        P.y[0][ix] = yv;
+        for (int p = 0; p < P.npeers; ++p) P.peer_y[p][ix] = yv;  // fused exchange
+      }
+      a.push += r;
+      a.np += dg ? dg : 1;
+      a.nn += 1;
+      a.et += dg;
+      xo = inflow;
+    }
+    if (!dg) a.d += oma * xo;
+  } else if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) {
+    if (cs[c].done) {
+      rnxt[ix] = rc;
+      ynxt[ix] = __ldcg(yg + ix);
+      return;
+    }
+    const double nxt = acc + (is_src ? cs[c].D : 0.0);
+    P.x[ix] = xo + alpha * rc;  // reserve += alpha * r
+    rnxt[ix] = nxt;
+    ynxt[ix] = oma * nxt * inv;
+    a.push += nxt;  // sum of next = the exact r_sum (push.cpp:101-103)
+    if (MODE == M_POWITR || rc != 0.0) {
+      a.np += dg ? dg : 1;
+      a.nn += 1;
+      a.et += dg;
+    }
+    if (!dg) a.d += oma * nxt;
+  } else {  // M_FINAL
+    double res;
+    if (P.final_pull[c]) {
+      const double inflow = acc + (is_src ? 1.0 + cs[c].D : 0.0);
+      res = inflow - xo;
+      if (res < 0.0) res = 0.0;  // rounding of the implicit form only
+    } else {
+      res = P.push_res[ix];
+    }
+    if (P.res_inter) P.res_inter[ix] = res;
+    if (c < P.k_live) {
+      if (P.out_reserve) P.out_reserve[(uint64_t)c * P.n + u] = alpha * xo;
+      if (P.out_residue) P.out_residue[(uint64_t)c * P.n + u] = res;
+    }
+    a.push += res;
+  }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void decide_at(const SweepParams& P, const ColSh* cs,
+                                          const double* thr_cur, uint32_t u, int c, double acc,
+                                          uint32_t dg, double inv, const double* yg,
+                                          const double* rcur, double* rnxt, double* ynxt, Acc& a) {
+  const uint64_t ix = (uint64_t)u * K + c;
+  decide<K, MODE>(P, cs, thr_cur, u, c, acc, __ldcg(P.x + ix),
+                  (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0, dg, inv, yg,
+                  rnxt, ynxt, a);
+}
+
+// One piece of a hub row (more in-edges than a tile holds): the block sums its
+// edges per column, adds the piece total into the row's accumulator, and the
+// last piece to arrive decides the row (release-ordered counter; the partials
+// are read back from L2). Only hub pieces pay this protocol.
+template <int K, int MODE>
+__device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, uint64_t j,
+                                       double* hubsh, int* flag, const ColSh* cs, const double* thr_cur,
+                                       const double* yg, const double* rcur, double* rnxt,
+                                       double* ynxt, Acc& a) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = tid % K;
+  const uint64_t total = (uint64_t)d.ne * K;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  uint64_t f = tid;
+  for (; f + 3 * NT < total; f += 4 * NT) {
+    const uint32_t i0 = __ldg(P.in_nbr + d.e0 + f / K);
+    const uint32_t i1 = __ldg(P.in_nbr + d.e0 + (f + NT) / K);
+    const uint32_t i2 = __ldg(P.in_nbr + d.e0 + (f + 2 * NT) / K);
+    const uint32_t i3 = __ldg(P.in_nbr + d.e0 + (f + 3 * NT) / K);
+    s0 += yg[(uint64_t)i0 * K + c];
+    s1 += yg[(uint64_t)i1 * K + c];
+    s2 += yg[(uint64_t)i2 * K + c];
+    s3 += yg[(uint64_t)i3 * K + c];
+  }
+  for (; f < total; f += NT) s0 += yg[(uint64_t)__ldg(P.in_nbr + d.e0 + f / K) * K + c];
+  double s = (s0 + s1) + (s2 + s3);
+#pragma unroll
+  for (int o = 16; o >= K && o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  for (int i = tid; i < (NT / 32) * K; i += NT) hubsh[i] = 0.0;
+  __syncthreads();
+  if (lane < K) hubsh[warp * K + c] = s;  // the lanes holding this warp's per-column sums
+  __syncthreads();
+  if (tid < K) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += hubsh[w * K + tid];
+    P.hub_acc[j * K + tid] = t;  // this piece's partial (slot = its tile)
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
+    *flag = old == d.npieces - 1;
+    if (*flag) P.hub_cnt[d.hub] = 0;
+  }
+  __syncthreads();
+  if (*flag && tid < K) {
+    // the last piece sums the partials in piece order: deterministic
+    const double* part = P.hub_acc + (j - d.piece) * K + tid;
+    double acc = 0.0;
+    for (uint32_t p = 0; p < d.npieces; ++p) acc += __ldcg(part + (uint64_t)p * K);
+    const uint32_t u = __ldg(P.crow + d.r0);
+    decide_at<K, MODE>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
+                       rcur, rnxt, ynxt, a);
+  }
+}
+
+// One row-aligned tile: gather y of every in-edge into shared memory (all
+// loads of the tile issued together), then one thread per (row, column) sums
+// its row and decides; rows longer than LONG are summed by a whole warp.
+template <int K, int MODE>
+__device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& d, char* smem,
+                                          const ColSh* cs, const double* thr_cur, const double* yg,
+                                          const double* rcur, double* rnxt, double* ynxt, Acc& a,
+                                          const BlockAcc& ba, uint32_t* nlong,
+                                          const unsigned long long* dn_slot, TileDesc* dn) {
+  using TC = Tile<K>;
+  constexpr int RMAX = TC::RMAX;
+  double* vals = reinterpret_cast<double*>(smem);
+  double* sinv = vals + SWEEP_ELEMS;
+  int32_t* soff = reinterpret_cast<int32_t*>(sinv + RMAX + (NT / 32) * K);
+  uint32_t* snode = reinterpret_cast<uint32_t*>(soff + RMAX + 1);
+  uint32_t* sdeg = snode + RMAX;
+  uint32_t* slong = sdeg + RMAX;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c = tid % K;
+  const uint32_t nr = d.nr;
+  // ---- stage rows and gather (one memory latency) -------------------------
+  for (uint32_t t = tid; t <= nr; t += NT) soff[t] = (int32_t)(__ldg(P.in_off + d.r0 + t) - d.e0);
+  for (uint32_t t = tid; t < nr; t += NT) {
+    snode[t] = __ldg(P.crow + d.r0 + t);
+    sdeg[t] = __ldg(P.cdeg + d.r0 + t);
+    sinv[t] = __ldg(P.cinv + d.r0 + t);
+    const uint64_t len = __ldg(P.in_off + d.r0 + t + 1) - __ldg(P.in_off + d.r0 + t);
+    if (len > (uint64_t)TC::LONG) slong[atomicAdd(nlong, 1u)] = t;
+  }
+  {
+    const uint32_t total = d.ne * K;
+    constexpr int U = TILE_U;
+    for (uint32_t f0 = 0; f0 < total; f0 += U * NT) {
+      uint32_t id[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t f = f0 + tid + i * NT;
+        id[i] = f < total ? __ldg(P.in_nbr + d.e0 + f / K) : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < U; ++i) {
+        const uint32_t f = f0 + tid + i * NT;
+        if (f < total) vals[f] = yg[(uint64_t)id[i] * K + (f % K)];
+      }
+    }
+  }
+  __syncthreads();
+  if (dn_slot) *dn = P.desc[*dn_slot < P.ntiles ? *dn_slot : 0];  // next tile's descriptor
+  // ---- short rows: one thread per (row, column) ------------------------------
+  for (uint32_t fi = tid; fi < nr * K; fi += NT) {
+    const uint32_t r = fi / K;
+    const int32_t b = soff[r], e = soff[r + 1];
+    if (e - b > TC::LONG) continue;
+    const uint32_t u = snode[r];
+    const uint64_t ix = (uint64_t)u * K + c;
+    const double xo = __ldcg(P.x + ix);  // issued before the sum: lands meanwhile
+    const double rc = (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0;
+    double s0 = 0.0, s1 = 0.0;
+    int32_t q = b;
+    for (; q + 1 < e; q += 2) {
+      s0 += vals[q * K + c];
+      s1 += vals[(q + 1) * K + c];
+    }
+    if (q < e) s0 += vals[q * K + c];
+    decide<K, MODE>(P, cs, thr_cur, u, c, s0 + s1, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a);
+  }
+  // ---- long rows: one warp per row -----------------------------------------
+  {
+    constexpr int KC = K < 32 ? K : 32;
+    constexpr int CPL = K / KC;
+    constexpr int ES = 32 / KC;  // edge slots per warp
+    const int es = lane / KC, kc = lane % KC;
+    const uint32_t nl = *nlong;
+    for (uint32_t li = warp; li < nl; li += NT / 32) {
+      const uint32_t r = slong[li];
+      const int32_t b = soff[r], e = soff[r + 1];
+      double s[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) s[q] = 0.0;
+      for (int32_t p = b + es; p < e; p += ES)
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) s[q] += vals[p * K + kc + q * KC];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q)
+#pragma unroll
+        for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+      if (es == 0) {
+        if constexpr (CPL == 1) {
+          decide_at<K, MODE>(P, cs, thr_cur, snode[r], kc, s[0], sdeg[r], sinv[r], yg, rcur, rnxt,
+                             ynxt, a);
+        } else {  // K = 64: lane kc decides columns kc and kc+32; counters via shared atomics
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) {
+            Acc b2;
+            const int cc = kc + q * KC;
+            decide_at<K, MODE>(P, cs, thr_cur, snode[r], cc, s[q], sdeg[r], sinv[r], yg, rcur,
+                               rnxt, ynxt, b2);
+            if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
+            if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
+            if (b2.np) atomicAdd(&ba.np[cc], b2.np);
+            if (b2.nn) atomicAdd(&ba.nn[cc], b2.nn);
+            if (b2.et) atomicAdd(&ba.et[cc], b2.et);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *nlong = 0;
+}
+
+// Wide column blocks (K >= WIDE_K): tiles of up to WIDE_T in-edges and
+// RMAX_W rows; warps take rows from a shared counter and gather each in-edge's
+// K contiguous values straight into registers (lanes = edge slots x columns),
+// so no value staging in shared memory and no per-tile hub split below WIDE_T.
+constexpr int WIDE_K = 4;
+#ifndef PPRG_WIDE_T
+#define PPRG_WIDE_T 4096
+#endif
+#ifndef PPRG_RMAX_W
+#define PPRG_RMAX_W 256
+#endif
+constexpr uint32_t WIDE_T = PPRG_WIDE_T;
+constexpr uint32_t RMAX_W = PPRG_RMAX_W;
+
+// Sum of y over the in-edges [b, e) of one row for my columns, by one warp.
+// Lanes = ES edge slots x KC column lanes (x CPL contiguous columns). The ids
+// of 32 consecutive edges are loaded once, coalesced, and broadcast by shuffle;
+// the gathers are then issued G at a time into registers before any add, so
+// each warp keeps G row-loads in flight (tail slots re-load the last edge and
+// are masked out of the sum).
+#ifndef PPRG_G
+#define PPRG_G 8
+#endif
+template <int K>
+__device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double* yg, uint64_t b,
+                                             uint64_t e, double (&s)[(K < 32 ? 1 : K / 32)],
+                                             bool have_first = false, uint32_t first_id = 0) {
+  constexpr int KC = K < 32 ? K : 32;
+  constexpr int CPL = K / KC;
+  constexpr int ES = 32 / KC;
+  constexpr int G = PPRG_G;
+  const int lane = threadIdx.x & 31, es = lane / KC, kc = lane % KC;
+  const double* ybase = yg + kc * CPL;
+  double acc[CPL][2];
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (uint64_t p0 = b; p0 < e; p0 += 32) {
+    const uint64_t pl = p0 + lane;
+    const uint32_t myid = (have_first && p0 == b) ? first_id : (pl < e ? ld_stream(P.in_nbr + pl) : 0u);
+    const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
+    for (int j0 = 0; j0 < cnt; j0 += G * ES) {
+      double v[G][CPL];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const int j = j0 + g * ES + es;
+        const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
+        const double* src = ybase + (uint64_t)id * K;
+        if constexpr (CPL == 2) {
+          const double2 v2 = ld_gather2(src);
+          v[g][0] = v2.x;
+          v[g][1] = v2.y;
+        } else {
+          v[g][0] = ld_gather(src);
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const bool ok = j0 + g * ES + es < cnt;
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) acc[q][g & 1] += ok ? v[g][q] : 0.0;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) {
+    s[q] = acc[q][0] + acc[q][1];
+#pragma unroll
+    for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
+  }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* cs,
+                                            const double* thr_cur, uint32_t u, const double* s,
+                                            const double* xo, const double* rc, uint32_t dg,
+                                            double inv, const double* yg, double* rnxt,
+                                            double* ynxt, Acc& a, const BlockAcc& ba) {
+  constexpr int KC = K < 32 ? K : 32;
+  constexpr int CPL = K / KC;
+  const int kc = (threadIdx.x & 31) % KC;
+  if constexpr (CPL == 1) {
+    decide<K, MODE>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], dg, inv, yg, rnxt, ynxt, a);
+  } else {  // K = 64: lane kc owns columns 2kc, 2kc+1; counters via shared atomics
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      Acc b2;
+      const int cc = kc * CPL + q;
+      decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
+      if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
+      if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
+      if (b2.np) atomicAdd(&ba.np[cc], b2.np);
+      if (b2.nn) atomicAdd(&ba.nn[cc], b2.nn);
+      if (b2.et) atomicAdd(&ba.et[cc], b2.et);
+    }
+  }
+}
+
+// Long-row counter slot of the wide layout (zeroed at kernel start).
+template <int K>
+__device__ __forceinline__ uint32_t* wide_long_count(char* smem) {
+  uint64_t* soff = reinterpret_cast<uint64_t*>(smem);
+  double* sinv = reinterpret_cast<double*>(soff + RMAX_W + 1);
+  double* spart = sinv + RMAX_W;
+  uint32_t* snode = reinterpret_cast<uint32_t*>(spart + (NT / 32) * K);
+  return snode + 3 * RMAX_W;
+}
+
+// Wide column blocks: warps take rows from a shared counter and sum each row
+// with warp_row_sum; rows longer than LONG_W in-edges are summed by all warps
+// of the block together (partials in shared memory) so no warp lags the tile.
+#ifndef PPRG_LONG_W
+#define PPRG_LONG_W 384
+#endif
+constexpr uint32_t LONG_W = PPRG_LONG_W;
+
+template <int K, int MODE>
+__device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileDesc& d, char* smem,
+                                               const ColSh* cs, const double* thr_cur,
+                                               const double* yg, const double* rcur, double* rnxt,
+                                               double* ynxt, Acc& a, const BlockAcc& ba,
+                                               uint32_t* rowctr,
+                                               const unsigned long long* dn_slot, TileDesc* dn) {
+  constexpr int KC = K < 32 ? K : 32;
+  constexpr int CPL = K / KC;
+  constexpr int NW = NT / 32;
+  uint64_t* soff = reinterpret_cast<uint64_t*>(smem);
+  double* sinv = reinterpret_cast<double*>(soff + RMAX_W + 1);
+  double* spart = sinv + RMAX_W;                       // [NW][K] long-row partials
+  uint32_t* snode = reinterpret_cast<uint32_t*>(spart + NW * K);
+  uint32_t* sdeg = snode + RMAX_W;
+  uint32_t* slong = sdeg + RMAX_W;                     // [RMAX_W] long rows; slong[RMAX_W] = count
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int es0 = lane < KC;  // lanes holding the reduced sums
+  const int kc = lane % KC;
+  const uint32_t nr = d.nr;
+  for (uint32_t t = tid; t <= nr; t += NT) soff[t] = __ldg(P.in_off + d.r0 + t);
+  for (uint32_t t = tid; t < nr; t += NT) {
+    snode[t] = __ldg(P.crow + d.r0 + t);
+    sdeg[t] = __ldg(P.cdeg + d.r0 + t);
+    sinv[t] = __ldg(P.cinv + d.r0 + t);
+    const uint64_t len = __ldg(P.in_off + d.r0 + t + 1) - __ldg(P.in_off + d.r0 + t);
+    if (len > LONG_W) slong[atomicAdd(&slong[RMAX_W], 1u)] = t;
+  }
+  __syncthreads();
+  if (dn_slot) *dn = P.desc[*dn_slot < P.ntiles ? *dn_slot : 0];  // next tile's descriptor
+  // ---- short rows: one warp per row, dynamic -----------------------------
+  // Rows are taken one ahead: the next row's first 32 in-edge ids are loaded
+  // before this row's gathers, so their latency hides behind the gathers.
+  auto grab = [&]() -> uint32_t {
+    uint32_t r = 0;
+    if (lane == 0) r = atomicAdd(rowctr, 1u);
+    return __shfl_sync(0xffffffffu, r, 0);
+  };
+  auto first_ids = [&](uint32_t r) -> uint32_t {
+    if (r >= nr) return 0u;
+    const uint64_t b = soff[r], e = soff[r + 1];
+    return (e - b <= LONG_W && b + lane < e) ? ld_stream(P.in_nbr + b + lane) : 0u;
+  };
+  uint32_t r = grab();
+  uint32_t ids = first_ids(r);
+  while (r < nr) {
+    const uint64_t b = soff[r], e = soff[r + 1];
+    const uint32_t rn = grab();
+    const uint32_t ids_n = first_ids(rn);
+    if (e - b <= LONG_W) {
+      const uint32_t u = snode[r];
+      double xo[CPL], rc[CPL], s[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {  // issued early; lands during the edge loop
+        const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
+        xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
+        rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
+      }
+      warp_row_sum<K>(P, yg, b, e, s, true, ids);
+      if (es0) decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
+    }
+    r = rn;
+    ids = ids_n;
+  }
+  // ---- long rows: all warps split the edges ---------------------------------
+  const uint32_t nl = slong[RMAX_W];
+  for (uint32_t li = 0; li < nl; ++li) {
+    const uint32_t r = slong[li];
+    const uint64_t b = soff[r], e = soff[r + 1];
+    const uint64_t chunk = ((e - b) + NW - 1) / NW;
+    const uint64_t wb = b + warp * chunk, we = wb + chunk < e ? wb + chunk : e;
+    double s[CPL];
+    warp_row_sum<K>(P, yg, wb < e ? wb : e, we, s);
+    if (es0)
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) spart[warp * K + kc * CPL + q] = s[q];
+    __syncthreads();
+    if (warp == 0 && es0) {
+      const uint32_t u = snode[r];
+      double xo[CPL], rc[CPL];
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) {
+        const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
+        xo[q] = __ldcg(P.x + ix);
+        rc[q] = (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0;
+        double t = 0.0;
+        for (int w = 0; w < NW; ++w) t += spart[w * K + kc * CPL + q];
+        s[q] = t;
+      }
+      decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    *rowctr = 0;
+    slong[RMAX_W] = 0;
+  }
+}
+
+// Sources with in-degree 0 are not rows of the compacted transpose; their
+// only inflow is the unit start mass plus the dead-end mass D (block 0).
+template <int K, int MODE>
+__device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* cs,
+                                            const double* thr_cur, const double* yg,
+                                            const double* rcur, double* rnxt, double* ynxt,
+                                            Acc& a) {
+  const int tid = threadIdx.x;
+  if (blockIdx.x != 0 || tid >= K) return;
+  const uint32_t u = P.src[tid];
+  if (u < P.own_lo || u >= P.own_hi) return;  // another partition's row
+  if (__ldg(P.in_off_full + u + 1) != __ldg(P.in_off_full + u)) return;
+  const uint64_t ix = (uint64_t)u * K + tid;
+  decide<K, MODE>(P, cs, thr_cur, u, tid, 0.0, __ldcg(P.x + ix),
+                  (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0, __ldg(P.deg + u),
+                  __ldg(P.inv_deg + u), yg, rnxt, ynxt, a);
+}
+
+template <int K, int MODE>
+#ifndef PPRG_MINB
+#define PPRG_MINB 8
+#endif
+#ifndef PPRG_MINB_NARROW
+#define PPRG_MINB_NARROW PPRG_MINB
+#endif
+__global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
+    k_sweeps(const __grid_constant__ SweepParams P) {
+  using TC = Tile<K>;
+  extern __shared__ __align__(16) char smem_dyn[];
+  __shared__ ColSh cs[K];
+  __shared__ double thr_cur[K];
+  __shared__ double sh_push[K], sh_d[K];
+  __shared__ unsigned long long sh_np[K], sh_nn[K], sh_et[K];
+  __shared__ unsigned long long sh_tile[3];
+  __shared__ int sh_any;
+  __shared__ double sh_hub[(NT / 32) * K];
+  __shared__ int sh_flag;
+  __shared__ uint32_t sh_nlong;
+  const int tid = threadIdx.x;
+  SweepCtl* ctl = P.ctl;
+  if (tid < K) {
+    cs[tid].r_sum = P.init[tid].r_sum;
+    cs[tid].D = P.init[tid].D;
+    cs[tid].epoch = P.init[tid].epoch;
+    cs[tid].done = P.init[tid].done;
+    cs[tid].sweeps = P.init[tid].sweeps;
+    cs[tid].pushes = P.init[tid].pushes;
+  }
+  __syncthreads();
+  const BlockAcc ba{sh_push, sh_d, sh_np, sh_nn, sh_et};
+  unsigned long long gen = 0;
+  const int c = tid % K;
+  for (uint32_t sweep = 0;; ++sweep) {
+    const int buf = sweep % 3;
+    if (tid == 0) {
+      int any = 0;
+      for (int cc = 0; cc < K; ++cc) any |= !cs[cc].done;
+      sh_any = any && (MODE == M_FINAL ? sweep == 0 : sweep < P.max_sweeps);
+      if (sh_any) sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
+      sh_nlong = 0;
+      if constexpr (K >= WIDE_K) *wide_long_count<K>(smem_dyn) = 0;
+    }
+    if (tid < K) {
+      thr_cur[tid] = (MODE == M_POWERPUSH && !cs[tid].done) ? P.thr[cs[tid].epoch] : 0.0;
+      sh_push[tid] = 0.0;
+      sh_d[tid] = 0.0;
+      sh_np[tid] = 0;
+      sh_nn[tid] = 0;
+      sh_et[tid] = 0;
+    }
+    __syncthreads();
+    if (!sh_any) break;
+    if (blockIdx.x == 0 && tid == 0 && MODE != M_FINAL) {
+      const int nb = (sweep + 1) % 3;  // last read two barriers ago; safe to clear
+      ctl->ticket[nb] = 0;
+      for (int cc = 0; cc < K; ++cc) {
+        ctl->pushed[nb][cc] = 0;
+        ctl->npush[nb][cc] = 0;
+        ctl->nnode[nb][cc] = 0;
+        ctl->dsum[nb][cc] = 0;
+        ctl->et[nb][cc] = 0;
+      }
+    }
+    const double* yg = P.y[MODE == M_POWERPUSH || MODE == M_FINAL ? 0 : (sweep & 1)];
+    const double* rcur = P.r[sweep & 1];
+    double* rnxt = P.r[(sweep + 1) & 1];
+    double* ynxt = P.y[(sweep + 1) & 1];
+    Acc a;
+    // Tiles in ticket (= id) order; the next ticket is fetched one tile ahead
+    // and the next descriptor is loaded inside the current tile.
+    unsigned long long j = sh_tile[0];
+    TileDesc d = P.desc[j < P.ntiles ? j : 0];
+    for (uint32_t it = 0;; ++it) {
+      if (j >= P.ntiles) break;
+      if (tid == 0) sh_tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
+      TileDesc dn = d;
+      if (d.npieces > 1) {
+        hub_piece<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+        dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
+        __syncthreads();
+      } else if constexpr (K >= WIDE_K) {
+        tile_rows_wide<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba,
+                                &sh_nlong, &sh_tile[(it + 1) & 1], &dn);
+      } else {
+        tile_rows<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba, &sh_nlong,
+                           &sh_tile[(it + 1) & 1], &dn);
+      }
+      j = sh_tile[(it + 1) & 1];
+      d = dn;
+    }
+    source_rows<K, MODE>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+    // block-level flush of this sweep's accumulators: reduce over the lanes of
+    // the same column first (shuffles), then one shared atomic per warp/column
+    {
+      const int lane = tid & 31;
+#pragma unroll
+      for (int o = 16; o >= K && o > 0; o >>= 1) {
+        a.push += __shfl_xor_sync(0xffffffffu, a.push, o);
+        a.d += __shfl_xor_sync(0xffffffffu, a.d, o);
+        a.np += __shfl_xor_sync(0xffffffffu, a.np, o);
+        a.nn += __shfl_xor_sync(0xffffffffu, a.nn, o);
+        a.et += __shfl_xor_sync(0xffffffffu, a.et, o);
+      }
+      if (lane < (K < 32 ? K : 32)) {
+        if (a.push != 0.0) atomicAdd(&sh_push[c], a.push);
+        if (a.d != 0.0) atomicAdd(&sh_d[c], a.d);
+        if (a.np) atomicAdd(&sh_np[c], a.np);
+        if (a.nn) atomicAdd(&sh_nn[c], a.nn);
+        if (a.et) atomicAdd(&sh_et[c], a.et);
+      }
+    }
+    __syncthreads();
+    if (tid < K) {
+      if (sh_push[tid] != 0.0) atomicAdd(&ctl->pushed[buf][tid], sh_push[tid]);
+      if (sh_d[tid] != 0.0) atomicAdd(&ctl->dsum[buf][tid], sh_d[tid]);
+      if (sh_np[tid]) atomicAdd(&ctl->npush[buf][tid], sh_np[tid]);
+      if (sh_nn[tid]) atomicAdd(&ctl->nnode[buf][tid], sh_nn[tid]);
+      if (sh_et[tid]) atomicAdd(&ctl->et[buf][tid], sh_et[tid]);
+    }
+    if (MODE == M_FINAL) {
+      __syncthreads();
+      break;
+    }
+    grid_barrier2(&ctl->gbar, ++gen);
+    // every block derives the identical next state from the reduced buffers
+    if (tid < K) {
+      const int cc = tid;
+      if (!cs[cc].done) {
+        const double pushed = __ldcg(&ctl->pushed[buf][cc]);
+        const unsigned long long np = __ldcg(&ctl->npush[buf][cc]);
+        cs[cc].sweeps += 1;
+        cs[cc].pushes += np;
+        cs[cc].D = __ldcg(&ctl->dsum[buf][cc]);
+        if (P.trace && cc == 0 && blockIdx.x == 0 && sweep < P.trace_cap) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          const double rs = MODE == M_POWERPUSH ? cs[cc].r_sum - P.alpha * pushed : pushed;
+          P.trace[sweep] = TracePoint{cs[cc].pushes, rs, t};
+        }
+        if (MODE == M_POWERPUSH) {
+          cs[cc].r_sum -= P.alpha * pushed;
+          if (np == 0) cs[cc].epoch += 1;  // fixpoint: nothing active at this threshold
+          else if (cs[cc].epoch == P.E - 1 && np < P.handoff_np) cs[cc].epoch += 1;  // refine tail
+          while (cs[cc].epoch < P.E && !(cs[cc].r_sum > P.lam[cs[cc].epoch])) cs[cc].epoch += 1;
+          if (cs[cc].epoch >= P.E) cs[cc].done = 1;
+        } else {
+          cs[cc].r_sum = pushed;
+          if (!(cs[cc].r_sum > P.lambda)) cs[cc].done = 1;
+        }
+      }
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      // B = 8(n+1) + 8 k n + 4 E_t + 24 P_t over the live columns;
+      // E_t (rows pushed in any column) is taken as the largest per-column sum.
+      unsigned long long live = 0, pt = 0, et = 0;
+      for (int cc = 0; cc < P.k_live; ++cc) {
+        pt += __ldcg(&ctl->nnode[buf][cc]);
+        const unsigned long long e = __ldcg(&ctl->et[buf][cc]);
+        et = e > et ? e : et;
+        live += 1;
+      }
+      if (MODE != M_POWERPUSH) et = P.m;
+      ctl->alg_bytes += 8ull * (P.n + 1) + 8ull * live * P.n + 4ull * et +
+                        (MODE == M_POWERPUSH ? 24ull * pt : 24ull * live * P.n);
+      ctl->total_sweeps = sweep + 1;
+    }
+    __syncthreads();
+  }
+  if (MODE == M_POWERPUSH && P.npeers) __threadfence_system();  // peer y stores performed
+  if (blockIdx.x == 0 && tid < K) {
+    ctl->out_rsum[tid] = cs[tid].r_sum;
+    ctl->out_D[tid] = cs[tid].D;
+    ctl->out_sweeps[tid] = cs[tid].sweeps;
+    ctl->out_done[tid] = cs[tid].done;
+    ctl->out_epoch[tid] = cs[tid].epoch;
+    ctl->out_pushes[tid] = cs[tid].pushes;
+  }
+}
+
+}  // namespace pprg
