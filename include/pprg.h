@@ -273,6 +273,10 @@ int pprg_walk_terminals(pprg_graph* g, const uint32_t* starts, const uint32_t* k
 /* ---- device buffers for device-resident outputs (bench / zero-copy) ------- */
 int pprg_device_alloc(int device, uint64_t bytes, void** out);
 int pprg_device_free(int device, void* p);
+/* Page-locked host buffers for result vectors: device-to-host copies into
+ * them run at full link speed and overlap the next block's compute. */
+int pprg_host_alloc(uint64_t bytes, void** out);
+int pprg_host_free(void* p);
 
 #ifdef __cplusplus
 }

@@ -20,7 +20,7 @@ from ._abi import (PPRVector, QueryConfig, Graph, WalkIndex, CallStats, PowerPus
                    build_graph_from_edges, generate_rmat, generate_chung_lu, power_iteration,
                    sim_forward_push, fifo_forward_push, power_push, power_push_batch,
                    power_iteration_batch, speedppr_query, speedppr_batch, build_index,
-                   compute_walk_budget, walk_terminals, ground_truth, ground_truth_batch, refine, monte_carlo_phase,
+                   compute_walk_budget, walk_terminals, ground_truth, ground_truth_batch, refine, monte_carlo_phase, pinned_empty,
                    GROUND_TRUTH_LAMBDA, default_lambda, default_mu,
                    default_scan_threshold, load_library, lib_path, PPRGError, InvalidArgument,
                    DataError, LogicError, KINDEX_TAG, RNG_ID_PHILOX)

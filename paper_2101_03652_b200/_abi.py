@@ -122,6 +122,8 @@ def load_library(path: str = lib_path):
     L.pprg_walk_terminals.argtypes = [vp, vp, vp, vp, C.c_uint64, C.c_uint32, C.c_uint32,
                                       C.c_double, C.c_uint64, vp]
     L.pprg_device_count.argtypes = [C.POINTER(C.c_int)]
+    L.pprg_host_alloc.argtypes = [C.c_uint64, C.POINTER(vp)]
+    L.pprg_host_free.argtypes = [vp]
     L.pprg_device_alloc.argtypes = [C.c_int, C.c_uint64, C.POINTER(vp)]
     L.pprg_device_free.argtypes = [C.c_int, vp]
     _lib = L
@@ -354,9 +356,57 @@ def _sources(sources) -> np.ndarray:
     return np.ascontiguousarray(np.atleast_1d(np.asarray(sources, dtype=np.uint32)))
 
 
-def _outs(g: Graph, k: int, keep: bool, device_out):
+class _Pinned:
+    """Owner of a page-locked host allocation (pprg_host_alloc)."""
+
+    def __init__(self, nbytes: int):
+        self.p = vp()
+        _check(load_library().pprg_host_alloc(max(nbytes, 1), C.byref(self.p)))
+
+    def __del__(self):
+        try:
+            if self.p:
+                _lib.pprg_host_free(self.p)
+                self.p = vp()
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, dtype=np.float64) -> np.ndarray:
+    """A numpy array in page-locked host memory (freed with the array)."""
+    dt = np.dtype(dtype)
+    n = int(np.prod(shape))
+    owner = _Pinned(n * dt.itemsize)
+    buf = (C.c_char * max(n * dt.itemsize, 1)).from_address(owner.p.value)
+    arr = np.frombuffer(buf, dtype=dt, count=n).reshape(shape)
+    arr_owner = _PinnedArray(arr, owner)
+    return arr_owner.view
+
+
+class _PinnedArray:
+    def __init__(self, arr, owner):
+        self.view = arr.view(_PinnedNd)
+        self.view._owner = owner
+
+
+class _PinnedNd(np.ndarray):
+    """ndarray subclass that keeps its page-locked allocation alive."""
+
+    def __array_finalize__(self, obj):
+        self._owner = getattr(obj, "_owner", None)
+
+
+def _outs(g: Graph, k: int, keep: bool, device_out, host_out=None):
     if device_out is not None:
         return None, None, device_out[0], device_out[1], OUT_DEVICE
+    if host_out is not None:  # caller's arrays, e.g. pinned_empty((k, n)) reused across calls
+        res, rsd = host_out
+        for a in (res, rsd):
+            if a is not None and (a.dtype != np.float64 or a.shape != (k, g.n())
+                                  or not a.flags.c_contiguous):
+                raise InvalidArgument("host_out arrays must be C-contiguous float64 (k, n)")
+        return (res, rsd, res.ctypes.data if res is not None else None,
+                rsd.ctypes.data if rsd is not None else None, 0)
     if not keep:
         return None, None, None, None, 0
     res = np.empty((k, g.n()), np.float64)
@@ -375,12 +425,15 @@ def _vectors(src, res, rsd, q, alpha):
 
 
 def power_push_batch(g: Graph, sources, alpha: float, lam: float, epoch_num: int = 8,
-                     scan_threshold: Optional[int] = None, keep: bool = True, device_out=None):
+                     scan_threshold: Optional[int] = None, keep: bool = True, device_out=None,
+                     host_out=None):
     """k independent power_push queries as one column block per <= 64 sources.
+    host_out = (reserve, residue) caller arrays (k, n) — page-locked ones from
+    pinned_empty() make the result copies overlap the next block's compute.
     Returns (list[PPRVector], CallStats)."""
     load_library()
     src = _sources(sources)
-    res, rsd, rp, dp, flags = _outs(g, len(src), keep, device_out)
+    res, rsd, rp, dp, flags = _outs(g, len(src), keep, device_out, host_out)
     q = (QStats * max(len(src), 1))()
     cs = CStats()
     _check(_lib.pprg_power_push(g.handle, _ptr(src), len(src), alpha, lam, epoch_num,

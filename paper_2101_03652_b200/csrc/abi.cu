@@ -724,6 +724,17 @@ int pprg_device_alloc(int device, uint64_t bytes, void** out) {
   });
 }
 
+int pprg_host_alloc(uint64_t bytes, void** out) {
+  return guard([&] {
+    require(out != nullptr, "null argument");
+    PPRG_CUDA(cudaHostAlloc(out, bytes ? bytes : 1, cudaHostAllocPortable));
+  });
+}
+
+int pprg_host_free(void* p) {
+  return guard([&] { PPRG_CUDA(cudaFreeHost(p)); });
+}
+
 int pprg_device_free(int device, void* p) {
   return guard([&] {
     pprg::DeviceGuard dg(device);
