@@ -271,8 +271,11 @@ struct MappedStage {
   }
 };
 
+thread_local uint64_t t_readback_kernels = 0;  // counted into CallStats::kernel_launches
+
 void d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   if (!bytes) return;
+  ++t_readback_kernels;
   static thread_local MappedStage ms;
   if (bytes > ms.cap) {
     if (ms.h) PPRG_CUDA(cudaFreeHost(ms.h));
@@ -866,6 +869,7 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
   for (uint32_t c = 0; c < k; ++c)
     if (sources[c] >= g.n) fail(EINVAL_, "source out of range");
   const uint64_t n = g.n;
+  const uint64_t rb0 = t_readback_kernels;
   for (uint32_t b0 = 0; b0 < k; b0 += KMAX) {
     const uint32_t kb = k - b0 < (uint32_t)KMAX ? k - b0 : (uint32_t)KMAX;
     Block b = make_block(g, sources + b0, kb, alpha, false);
@@ -915,6 +919,7 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
     }
     call->kernel_launches += 3;
   }
+  call->kernel_launches += (uint32_t)(t_readback_kernels - rb0);
 }
 
 // Columns per block: wider blocks amortise the in-edge stream over more
@@ -940,6 +945,12 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
   std::lock_guard<std::mutex> lk(g.mu);
   for (uint32_t c = 0; c < k; ++c)
     if (sources[c] >= g.n) fail(EINVAL_, "source out of range");
+  const uint64_t rb0 = t_readback_kernels;
+  struct CountReadbacks {
+    CallStats* call;
+    uint64_t rb0;
+    ~CountReadbacks() { call->kernel_launches += (uint32_t)(t_readback_kernels - rb0); }
+  } count_rb{call, rb0};
   const bool pull = eng != Engine::Fifo;
   if (pull) g.ensure_transpose();
   const uint32_t bmax = block_columns(g.n, k);
@@ -1097,6 +1108,7 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
                          double lambda, double r_max, ColumnStats* cols, CallStats* call,
                          PushView* view) {
   g.ensure_transpose();
+  const uint64_t rb0 = t_readback_kernels;
   Block b = make_block(g, sources, k, alpha, true);
   // PowerPush to lambda, then refine (push.cpp:208-222) as a final sweep
   // epoch at r_max run to its fixpoint, so the refine is pull sweeps over the
@@ -1121,6 +1133,7 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
     cols[c].local_levels = b.levels[c];
     cols[c].used_scan_phase = b.scan[c];
   }
+  call->kernel_launches += (uint32_t)(t_readback_kernels - rb0);
   view->K = b.K;
   view->k = k;
   view->x = b.w.x.get();
