@@ -290,18 +290,23 @@ def main():
     pin_src = torch.from_numpy(mine.astype(np.int64)).pin_memory()
     e2e_steps = args.e2e_steps or args.steps
 
+    import ctypes
+    L = P.load_library()
+    L.pprg_graph_sync.argtypes = [ctypes.c_void_p]
+
     def step_e2e():
+        # PPRG_ASYNC_HOST: a step returns once computed; its last result copies
+        # land while the next step computes (pprg_graph_sync below waits for all)
         src = pin_src.numpy().astype(np.uint32)
-        import ctypes
-        L = P.load_library()
         q = (P._abi.QStats * k)()
         c = P._abi.CStats()
         P._abi._check(L.pprg_power_push(g.handle, src.ctypes.data, k, CFG["alpha"], CFG["lam"],
-                                        8, -1, pin_res.data_ptr(), pin_rsd.data_ptr(), 0, q,
+                                        8, -1, pin_res.data_ptr(), pin_rsd.data_ptr(), 2, q,
                                         ctypes.byref(c), None))
         return c
 
     step_e2e()
+    P._abi._check(L.pprg_graph_sync(g.handle))
     barrier(world)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -309,6 +314,7 @@ def main():
     for _ in range(e2e_steps):
         c = step_e2e()
         e2e_launches += c.kernel_launches
+    P._abi._check(L.pprg_graph_sync(g.handle))  # every step's results are on the host
     torch.cuda.synchronize()
     e2e_ms = (time.perf_counter() - t0) * 1000.0
     e2e_ms = max_over_ranks(world, e2e_ms)

@@ -35,6 +35,9 @@ extern "C" {
 #define PPRG_ENCCL 5
 
 #define PPRG_OUT_DEVICE 1u /* output pointers are device pointers on the graph's GPU */
+#define PPRG_ASYNC_HOST 2u /* host outputs: return once computed; the last block's copies
+                              may still be landing -- pprg_graph_sync(g) waits for them.
+                              Lets consecutive calls overlap copies with compute. */
 
 #define PPRG_RNG_PHILOX4X32_10 2u /* PPRW rng-id byte for our walk index (reference uses 1 = mt19937_64, rng.hpp:10) */
 
@@ -269,6 +272,9 @@ int pprg_monte_carlo(pprg_graph* g, const pprg_index* idx, uint32_t source, doub
 int pprg_walk_terminals(pprg_graph* g, const uint32_t* starts, const uint32_t* ks,
                         const uint32_t* vs, uint64_t count, uint32_t source, uint32_t tag,
                         double alpha, uint64_t seed, uint32_t* out);
+
+/* Wait until every host-output copy issued by earlier calls on g has landed. */
+int pprg_graph_sync(pprg_graph* g);
 
 /* ---- device buffers for device-resident outputs (bench / zero-copy) ------- */
 int pprg_device_alloc(int device, uint64_t bytes, void** out);

@@ -123,6 +123,7 @@ def load_library(path: str = lib_path):
                                       C.c_double, C.c_uint64, vp]
     L.pprg_device_count.argtypes = [C.POINTER(C.c_int)]
     L.pprg_host_alloc.argtypes = [C.c_uint64, C.POINTER(vp)]
+    L.pprg_graph_sync.argtypes = [vp]
     L.pprg_host_free.argtypes = [vp]
     L.pprg_device_alloc.argtypes = [C.c_int, C.c_uint64, C.POINTER(vp)]
     L.pprg_device_free.argtypes = [C.c_int, vp]

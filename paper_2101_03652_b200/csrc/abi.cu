@@ -90,7 +90,8 @@ int push_engine(pprg_graph* g, pprg::Engine eng, const uint32_t* sources, uint32
     check_alpha(alpha);
     std::vector<pprg::ColumnStats> cs(k);
     pprg::CallStats call;
-    pprg::Outputs out{reserve_out, residue_out, (flags & PPRG_OUT_DEVICE) != 0};
+    pprg::Outputs out{reserve_out, residue_out, (flags & PPRG_OUT_DEVICE) != 0,
+                      (flags & PPRG_ASYNC_HOST) != 0};
     if (k)
       pprg::run_push_engine(*g->g, eng, sources, k, alpha, lambda, epoch_num, scan_threshold,
                             r_max, lambda_stop, out, cs.data(), &call);
@@ -714,6 +715,13 @@ int pprg_walk_terminals(pprg_graph* g, const uint32_t* starts, const uint32_t* k
   return guard([&] {
     require(g && g->g && out, "null argument");
     pprg::walk_terminals(*g->g, starts, ks, vs, count, source, tag, alpha, seed, out);
+  });
+}
+
+int pprg_graph_sync(pprg_graph* g) {
+  return guard([&] {
+    require(g && g->g, "null graph");
+    pprg::graph_sync(*g->g);
   });
 }
 

@@ -109,7 +109,9 @@ struct Outputs {  // host or device pointers (k x n, query-major); any may be nu
   double* reserve = nullptr;
   double* residue = nullptr;
   bool on_device = false;
+  bool async_host = false;  // return before the last host copies land (graph_sync waits)
 };
+void graph_sync(Graph& g);  // wait for every pending host-output copy of g
 
 enum class Engine { PowerPush, PowItr, SimFwdPush, Fifo };
 

@@ -137,6 +137,12 @@ static void sync_host_copies(const Graph& g) {
     if (kv.second && kv.second->copy_st) PPRG_CUDA(cudaStreamSynchronize(kv.second->copy_st));
 }
 
+void graph_sync(Graph& g) {
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  sync_host_copies(g);
+}
+
 void release_workspaces(const Graph* g) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
   g_ws.erase(g);
@@ -1089,7 +1095,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
     }
     tdev.stop();
     call->device_ms += tdev.ms();
-    if (b0 + kb >= k) sync_host_copies(g);
+    if (b0 + kb >= k && !out.async_host) sync_host_copies(g);
     if (eng == Engine::PowerPush || eng == Engine::Fifo)
       for (uint32_t c = 0; c < kb; ++c) {
         cs[c].r_sum = b.r_sum[c];

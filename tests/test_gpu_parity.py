@@ -584,3 +584,22 @@ def test_monte_carlo_expectation(P, oracle):
     se = runs.std(axis=0, ddof=1) / np.sqrt(len(runs))
     assert np.all(np.abs(runs.mean(axis=0) - expected) <= 4 * se + 1e-12)
     assert np.all(np.abs(runs.sum(axis=1) - 1.0) < 1e-9)
+
+
+def test_async_host_outputs(P, oracle):
+    """PPRG_ASYNC_HOST: results are complete after pprg_graph_sync."""
+    import ctypes
+    g = P.generate_rmat(14, 8, 2)
+    src = P.sample_sources(np.diff(g.out_offsets()), 130, 2).astype(np.uint32)
+    k, n = len(src), g.n()
+    res, rsd = P.pinned_empty((k, n)), P.pinned_empty((k, n))
+    res[:] = -1.0
+    L = P.load_library()
+    q = (P._abi.QStats * k)()
+    P._abi._check(L.pprg_power_push(g.handle, src.ctypes.data, k, 0.2, 1e-8, 8, -1,
+                                    res.ctypes.data, rsd.ctypes.data, 2, q, None, None))
+    P._abi._check(L.pprg_graph_sync(g.handle))
+    ref, _ = P.power_push_batch(g, src, 0.2, 1e-8)
+    assert np.all(res >= 0.0)
+    for i in (0, 64, 129):
+        assert np.max(np.abs(res[i] - ref[i].estimates)) <= 2e-8
