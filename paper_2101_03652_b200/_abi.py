@@ -623,7 +623,7 @@ def build_index(g: Graph, alpha: float, seed: int) -> WalkIndex:
 
 
 def speedppr_batch(g: Graph, sources, cfg: QueryConfig, index: Optional[WalkIndex] = None,
-                   keep=True, device_out=None):
+                   keep=True, device_out=None, host_out=None):
     load_library()
     cfg.validate()
     if cfg.epsilon is None:
@@ -639,6 +639,11 @@ def speedppr_batch(g: Graph, sources, cfg: QueryConfig, index: Optional[WalkInde
     flags = 0
     if device_out is not None:
         ep, flags = device_out, OUT_DEVICE
+    elif host_out is not None:  # e.g. pinned_empty((k, n)), reused across calls
+        est = host_out
+        if est.dtype != np.float64 or est.shape != (k, g.n()) or not est.flags.c_contiguous:
+            raise InvalidArgument("host_out must be a C-contiguous float64 (k, n) array")
+        ep = est.ctypes.data
     elif keep:
         est = np.empty((k, g.n()), np.float64)
         ep = est.ctypes.data
@@ -647,7 +652,7 @@ def speedppr_batch(g: Graph, sources, cfg: QueryConfig, index: Optional[WalkInde
     _check(_lib.pprg_speedppr(g.handle, index._h if index is not None else None, _ptr(src), k,
                               cfg.alpha, cfg.epsilon, cfg.mu if cfg.mu is not None else -1.0,
                               cfg.seed, ep, flags, q, C.byref(cs)))
-    zeros = np.zeros((k, g.n())) if keep else None
+    zeros = np.zeros((k, g.n())) if (keep or host_out is not None) else None
     return _vectors(src, est, zeros, q, cfg.alpha), CallStats.of(cs)
 
 

@@ -112,6 +112,10 @@ struct Outputs {  // host or device pointers (k x n, query-major); any may be nu
   bool async_host = false;  // return before the last host copies land (graph_sync waits)
 };
 void graph_sync(Graph& g);  // wait for every pending host-output copy of g
+// Small device->host read-back through mapped pinned memory (no copy engine),
+// synchronous on st; counted in t_readback_kernels.
+void d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t st);
+extern thread_local uint64_t t_readback_kernels;
 
 enum class Engine { PowerPush, PowItr, SimFwdPush, Fifo };
 

@@ -277,6 +277,8 @@ struct MappedStage {
   }
 };
 
+}  // namespace
+
 thread_local uint64_t t_readback_kernels = 0;  // counted into CallStats::kernel_launches
 
 void d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
@@ -296,6 +298,8 @@ void d2h_small(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   PPRG_CUDA(cudaStreamSynchronize(st));
   std::memcpy(dst, ms.h, bytes);
 }
+
+namespace {
 
 struct EventTimer {
   cudaEvent_t a{}, b{};

@@ -366,6 +366,39 @@ void walk_terminals(Graph& g, const uint32_t* h_start, const uint32_t* h_k, cons
   PPRG_CUDA(cudaStreamSynchronize(g.stream));
 }
 
+namespace {
+// Per-call Monte Carlo buffers and the two-slot output staging of speedppr().
+struct McState {
+  DevBuf<unsigned long long> cnt, colw;
+  DevBuf<uint64_t> big;
+  DevBuf<double> est, stage[2];
+  DevBuf<unsigned> bad;
+  uint64_t nk = 0;
+  unsigned slot = 0;
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t ready[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+  explicit McState(cudaStream_t st) {
+    colw.alloc(65);
+    bad.alloc(1);
+    PPRG_CUDA(cudaStreamCreateWithFlags(&copy_st, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      PPRG_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+      PPRG_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+      PPRG_CUDA(cudaEventRecord(done[i], copy_st));
+    }
+    (void)st;
+  }
+  ~McState() {
+    cudaStreamSynchronize(copy_st);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(ready[i]);
+      cudaEventDestroy(done[i]);
+    }
+    cudaStreamDestroy(copy_st);
+  }
+};
+}  // namespace
+
 void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t k, double alpha,
               double epsilon, double mu, uint64_t seed, double* est_out, bool out_on_device,
               ColumnStats* cols, CallStats* call) {
@@ -385,6 +418,7 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
   PPRG_CUDA(cudaEventCreate(&e0));
   PPRG_CUDA(cudaEventCreate(&e1));
   PPRG_CUDA(cudaEventRecord(e0, st));
+  McState mc(st);
   for (uint32_t b0 = 0; b0 < k; b0 += 64) {
     const uint32_t kb = k - b0 < 64u ? k - b0 : 64u;
     ColumnStats* cs = cols + b0;
@@ -418,51 +452,65 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
     speedppr_push_stage(g, sources + b0, kb, alpha, lambda, r_max, cs, call, &pv);
     const int K = pv.K;
     const uint64_t nk = n * (uint64_t)K;
-    DevBuf<unsigned long long> cnt(nk), colw(64 + 1);
-    DevBuf<uint64_t> big(nk);
-    DevBuf<double> est(nk), outb(out_on_device ? 0 : n * kb);
-    DevBuf<unsigned> bad(1);
-    unsigned long long* nbig = colw.get() + 64;
-    PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
-    PPRG_CUDA(cudaMemsetAsync(colw.get(), 0, 8 * 65, st));
-    k_mc_counts<<<std::min<unsigned>(gridn(nk), g.sm_count * 8), 256, 0, st>>>(pv.res, g.deg.get(), n, K, kb, (double)W, cnt.get(),
-                                          bad.get(), colw.get());
-    k_est_init<<<gridn(nk), 256, 0, st>>>(pv.x, nk, alpha, est.get());
+    // buffers live across blocks: a cudaFree per block would synchronise the
+    // device and serialise the previous block's output copy with this block
+    if (!mc.cnt.get() || mc.nk < nk) {
+      mc.nk = nk;
+      mc.cnt.alloc(nk);
+      mc.big.alloc(nk);
+      mc.est.alloc(nk);
+    }
+    unsigned long long* nbig = mc.colw.get() + 64;
+    PPRG_CUDA(cudaMemsetAsync(mc.bad.get(), 0, 4, st));
+    PPRG_CUDA(cudaMemsetAsync(mc.colw.get(), 0, 8 * 65, st));
+    k_mc_counts<<<std::min<unsigned>(gridn(nk), g.sm_count * 8), 256, 0, st>>>(
+        pv.res, g.deg.get(), n, K, kb, (double)W, mc.cnt.get(), mc.bad.get(), mc.colw.get());
+    k_est_init<<<gridn(nk), 256, 0, st>>>(pv.x, nk, alpha, mc.est.get());
     McParams P;
     std::memset(&P, 0, sizeof P);
     P.off = g.off.get();
     P.nbr = g.nbr.get();
     P.deg = g.deg.get();
     P.res = pv.res;
-    P.cnt = cnt.get();
+    P.cnt = mc.cnt.get();
     P.index = idx ? idx->endpoints.get() : nullptr;
     P.nk = nk;
     P.K = K;
     P.alpha = alpha;
     P.seed = seed;
-    P.est = est.get();
+    P.est = mc.est.get();
     for (int c = 0; c < K; ++c) P.src[c] = pv.src[c];
     // Entries run thread-per-(v, c); entries over 32 walks are queued and run
     // warp-per-entry by a fixed-size grid that reads the queue length on device.
-    k_mc_entries<<<gridn(nk), 256, 0, st>>>(P, big.get(), nbig);
-    k_mc_big<<<g.sm_count * 8, 256, 0, st>>>(P, big.get(), nbig);
+    k_mc_entries<<<gridn(nk), 256, 0, st>>>(P, mc.big.get(), nbig);
+    k_mc_big<<<g.sm_count * 8, 256, 0, st>>>(P, mc.big.get(), nbig);
     PPRG_CUDA(cudaGetLastError());
-    double* dst = est_out ? (out_on_device ? est_out + (uint64_t)b0 * n : outb.get()) : nullptr;
-    if (dst) k_unpack_est<<<gridn(nk), 256, 0, st>>>(est.get(), n, K, kb, dst);
-    if (est_out && !out_on_device)
-      PPRG_CUDA(cudaMemcpyAsync(est_out + (uint64_t)b0 * n, outb.get(), 8 * n * kb, kind, st));
+    if (est_out && out_on_device) {
+      k_unpack_est<<<gridn(nk), 256, 0, st>>>(mc.est.get(), n, K, kb, est_out + (uint64_t)b0 * n);
+    } else if (est_out) {
+      // staged: the copy of this block overlaps the next block's compute
+      const int slot = mc.slot++ & 1;
+      PPRG_CUDA(cudaStreamWaitEvent(st, mc.done[slot], 0));
+      mc.stage[slot].ensure(n * 64);
+      k_unpack_est<<<gridn(nk), 256, 0, st>>>(mc.est.get(), n, K, kb, mc.stage[slot].get());
+      PPRG_CUDA(cudaEventRecord(mc.ready[slot], st));
+      PPRG_CUDA(cudaStreamWaitEvent(mc.copy_st, mc.ready[slot], 0));
+      PPRG_CUDA(cudaMemcpyAsync(est_out + (uint64_t)b0 * n, mc.stage[slot].get(), 8 * n * kb,
+                                cudaMemcpyDeviceToHost, mc.copy_st));
+      PPRG_CUDA(cudaEventRecord(mc.done[slot], mc.copy_st));
+    }
     unsigned long long hw[65];
     unsigned hb = 0;
-    PPRG_CUDA(cudaMemcpyAsync(hw, colw.get(), 8 * 65, cudaMemcpyDeviceToHost, st));
-    PPRG_CUDA(cudaMemcpyAsync(&hb, bad.get(), 4, cudaMemcpyDeviceToHost, st));
-    PPRG_CUDA(cudaStreamSynchronize(st));
+    d2h_small(hw, mc.colw.get(), 8 * 65, st);
+    d2h_small(&hb, mc.bad.get(), 4, st);
     if (hb) fail(EINTERNAL, "monte carlo: residue exceeds degree/W, state not refined");
-    call->kernel_launches += 5;
+    call->kernel_launches += 7;
     for (uint32_t c = 0; c < kb; ++c) cs[c].walks = hw[c];
     for (uint32_t c = 0; c < kb; ++c) cs[c].r_sum = 0;  // speedppr.cpp:47
   }
   PPRG_CUDA(cudaEventRecord(e1, st));
   PPRG_CUDA(cudaEventSynchronize(e1));
+  PPRG_CUDA(cudaStreamSynchronize(mc.copy_st));  // every block's estimates are on the host
   float ms = 0;
   PPRG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
   call->device_ms += ms;
