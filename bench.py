@@ -322,6 +322,9 @@ def main():
 
     peak, peak_kind = peaks()
     achieved = alg / (sweep_ms / 1000.0) / 1e9 if sweep_ms > 0 else 0.0
+    traffic = traffic_for("config3")
+    launch_s = sweep_ms / max(sweep_launches, 1) / 1000.0
+    dram_rate = traffic / launch_s / 1e9 if (traffic and launch_s > 0) else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -330,11 +333,15 @@ def main():
                     "d2h_bytes_per_step": 16 * k * n},
             "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic_for("config3"),
+                         "frac": achieved / peak, "traffic": traffic,
                          "peak_kind": peak_kind, "kernel": "k_sweeps<K,POWERPUSH>",
                          "alg_bytes_per_step": alg / args.steps,
                          "alg_bytes_per_launch": alg / max(sweep_launches, 1),
                          "achieved_whole_step_GBps": alg / args.steps / (ms / args.steps / 1e3) / 1e9,
+                         # ncu DRAM bytes per launch over the live launch time: the rate the
+                         # kernel actually moves (gather misses included), vs the same peak
+                         "dram_traffic_GBps": dram_rate,
+                         "dram_traffic_frac": dram_rate / peak if dram_rate else None,
                          "sweep_ms_per_step": sweep_ms / args.steps,
                          "sweeps_per_block": sweeps[-1]},
             "clocks": clk.summary()}
