@@ -448,6 +448,56 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double*
   }
 }
 
+// A hub piece in the wide layout: each warp sums a contiguous quarter of the
+// piece's in-edges with warp_row_sum (one 8K-byte row per load instruction,
+// G loads in flight), the warps' per-column partials meet in shared memory,
+// and the piece protocol of hub_piece follows (partial slot, release-ordered
+// counter, last piece decides from the partials in piece order). Measured on
+// configs[2]: sweep kernel -4% against the column-per-thread hub_piece.
+template <int K, int MODE>
+__device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc& d, uint64_t j,
+                                            double* hubsh, int* flag, const ColSh* cs,
+                                            const double* thr_cur, const double* yg,
+                                            const double* rcur, double* rnxt, double* ynxt,
+                                            Acc& a) {
+  constexpr int KC = K < 32 ? K : 32;
+  constexpr int CPL = K / KC;
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t chunk = ((uint64_t)d.ne + NW - 1) / NW;
+  const uint64_t b = d.e0 + (uint64_t)warp * chunk;
+  const uint64_t e0 = d.e0 + d.ne;
+  const uint64_t e = b + chunk < e0 ? b + chunk : e0;
+  double s[CPL];
+  warp_row_sum<K>(P, yg, b < e ? b : e, e, s);
+  if (lane < KC)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) hubsh[warp * K + (lane % KC) * CPL + q] = s[q];
+  __syncthreads();
+  if (tid < K) {
+    double t = 0.0;
+    for (int w = 0; w < NW; ++w) t += hubsh[w * K + tid];
+    P.hub_acc[j * K + tid] = t;  // this piece's partial (slot = its tile)
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned old;
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
+    *flag = old == d.npieces - 1;
+    if (*flag) P.hub_cnt[d.hub] = 0;
+  }
+  __syncthreads();
+  if (*flag && tid < K) {
+    const double* part = P.hub_acc + (j - d.piece) * K + tid;
+    double acc = 0.0;
+    for (uint32_t p = 0; p < d.npieces; ++p) acc += __ldcg(part + (uint64_t)p * K);
+    const uint32_t u = __ldg(P.crow + d.r0);
+    decide_at<K, MODE>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
+                       rcur, rnxt, ynxt, a);
+  }
+}
+
 template <int K, int MODE>
 __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* cs,
                                             const double* thr_cur, uint32_t u, const double* s,
@@ -689,7 +739,10 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
       if (tid == 0) sh_tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
       TileDesc dn = d;
       if (d.npieces > 1) {
-        hub_piece<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+        if constexpr (K >= WIDE_K)
+          hub_piece_wide<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+        else
+          hub_piece<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
         dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
         __syncthreads();
       } else if constexpr (K >= WIDE_K) {

@@ -135,6 +135,128 @@ __global__ void pull_warp_k4(const uint64_t* __restrict__ ioff, const uint32_t* 
     if (sub == 0) next[4 * (uint64_t)u + c] = acc;
   }
 }
+
+// ---- K = 64 interleaved columns: the bench's block shape --------------------
+// One warp per destination row, lanes = 32 x 16 B of one in-edge's 512-byte y
+// row; in-edge ids loaded 32 at a time (coalesced) and broadcast by shuffle,
+// G row gathers issued before any add. Writes the 64 sums (x row). `mask`
+// folds source ids into a small table (L2-resident variant) when nonzero.
+template <int G>
+__global__ void __launch_bounds__(128, 8) pull_k64(const uint64_t* __restrict__ ioff, const uint32_t* __restrict__ inb,
+                         const double* __restrict__ y, double* next, uint32_t n, uint32_t mask) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  const double* yb = y + 2 * lane;
+  for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
+    const uint64_t b = ioff[u], e = ioff[u + 1];
+    double a0 = 0.0, a1 = 0.0;
+    for (uint64_t p0 = b; p0 < e; p0 += 32) {
+      uint32_t myid = p0 + lane < e ? inb[p0 + lane] : 0u;
+      if (mask) myid &= mask;
+      const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
+      for (int j0 = 0; j0 < cnt; j0 += G) {
+        double2 v[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int j = j0 + g;
+          const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
+          v[g] = *reinterpret_cast<const double2*>(yb + (uint64_t)id * 64);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const bool ok = j0 + g < cnt;
+          a0 += ok ? v[g].x : 0.0;
+          a1 += ok ? v[g].y : 0.0;
+        }
+      }
+    }
+    *reinterpret_cast<double2*>(next + (uint64_t)u * 64 + 2 * lane) = make_double2(a0, a1);
+  }
+}
+// Same, rows taken from a global atomic counter in chunks of 32 (dynamic balance).
+template <int G>
+__global__ void __launch_bounds__(128, 8) pull_k64_dyn(const uint64_t* __restrict__ ioff, const uint32_t* __restrict__ inb,
+                         const double* __restrict__ y, double* next, uint32_t n, unsigned* ctr) {
+  const int lane = threadIdx.x & 31;
+  const double* yb = y + 2 * lane;
+  for (;;) {
+    uint32_t base = 0;
+    if (lane == 0) base = atomicAdd(ctr, 8u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= n) break;
+    for (uint32_t u = base; u < base + 8 && u < n; ++u) {
+      const uint64_t b = ioff[u], e = ioff[u + 1];
+      double a0 = 0.0, a1 = 0.0;
+      for (uint64_t p0 = b; p0 < e; p0 += 32) {
+        const uint32_t myid = p0 + lane < e ? inb[p0 + lane] : 0u;
+        const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
+        for (int j0 = 0; j0 < cnt; j0 += G) {
+          double2 v[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int j = j0 + g;
+            const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
+            v[g] = *reinterpret_cast<const double2*>(yb + (uint64_t)id * 64);
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const bool ok = j0 + g < cnt;
+            a0 += ok ? v[g].x : 0.0;
+            a1 += ok ? v[g].y : 0.0;
+          }
+        }
+      }
+      *reinterpret_cast<double2*>(next + (uint64_t)u * 64 + 2 * lane) = make_double2(a0, a1);
+    }
+  }
+}
+
+// Edge-balanced variant: rows longer than PL in-edges are cut into pieces of PL
+// edges (host-built list), pieces of split rows add their partial sums with
+// fp64 RED; warps take pieces in grid-stride order.
+struct Piece { uint32_t row; uint32_t len; uint64_t b; uint32_t split; uint32_t pad; };
+template <int G>
+__global__ void __launch_bounds__(128, 8) pull_k64_pieces(const Piece* __restrict__ pc, uint64_t npc,
+                         const uint32_t* __restrict__ inb, const double* __restrict__ y, double* next, uint32_t mask,
+                         double* ystate = nullptr) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (gridDim.x * blockDim.x) >> 5;
+  const double* yb = y + 2 * lane;
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < npc; w += warps) {
+    const Piece P = pc[w];
+    const uint64_t b = P.b, e = P.b + P.len;
+    double a0 = 0.0, a1 = 0.0;
+    for (uint64_t p0 = b; p0 < e; p0 += 32) {
+      uint32_t myid = p0 + lane < e ? inb[p0 + lane] : 0u;
+      if (mask) myid &= mask;
+      const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
+      for (int j0 = 0; j0 < cnt; j0 += G) {
+        double2 v[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int j = j0 + g;
+          const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
+          v[g] = *reinterpret_cast<const double2*>(yb + (uint64_t)id * 64);
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const bool ok = j0 + g < cnt;
+          a0 += ok ? v[g].x : 0.0;
+          a1 += ok ? v[g].y : 0.0;
+        }
+      }
+    }
+    double* dst = next + (uint64_t)P.row * 64 + 2 * lane;
+    if (P.split) { atomicAdd(dst, a0); atomicAdd(dst + 1, a1); }
+    else if (ystate) {  // PowerPush state traffic: read x row, push -> write x and y rows
+      const double2 xo = __ldcg(reinterpret_cast<const double2*>(dst));
+      if (a0 + 1.0 != xo.x || a1 + 1.0 != xo.y) {  // always: an upper bound (80% push in practice)
+        *reinterpret_cast<double2*>(dst) = make_double2(a0, a1);
+        *reinterpret_cast<double2*>(ystate + (uint64_t)P.row * 64 + 2 * lane) = make_double2(0.8 * a0, 0.8 * a1);
+      }
+    } else *reinterpret_cast<double2*>(dst) = make_double2(a0, a1);
+  }
+}
 // raw rates
 __global__ void rand_red(const uint32_t* __restrict__ idx, uint64_t cnt, double* vec) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x)
@@ -209,11 +331,60 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(cur, h.data(), 8ull * 4 * n, cudaMemcpyHostToDevice));
   }
   const int G = sms * 8;  // 8 x 256 threads per SM resident
+  float t;
   auto rep = [&](const char* name, float us, double bytes, double ops) {
     printf("%-16s %9.1f us  %7.1f GB/s(alg)  %7.1f Gops/s\n", name, us, bytes / us / 1e3, ops / us / 1e3);
   };
+
+  if (argc > 3 && atoi(argv[3]) == 64) {  // K = 64 ceiling probe
+    double *y64, *x64; unsigned* ctr;
+    CK(cudaMalloc(&y64, 8ull * 64 * n)); CK(cudaMalloc(&x64, 8ull * 64 * n)); CK(cudaMalloc(&ctr, 4));
+    CK(cudaMemset(y64, 0, 8ull * 64 * n));
+    const double b64 = 4.0 * m + 512.0 * m + 512.0 * n;  // ids + gathered rows + x rows written
+    for (int blocks : {sms * 8, sms * 16, sms * 32}) {
+      t = timeit([&] { pull_k64<8><<<blocks, 128>>>(io, inbp, y64, x64, n, 0); }, 5);
+      printf("pull_k64_G8 grid=%d", blocks); rep("", t, b64, (double)m);
+    }
+    t = timeit([&] { pull_k64<4><<<sms * 8, 128>>>(io, inbp, y64, x64, n, 0); }, 5); rep("pull_k64_G4", t, b64, (double)m);
+    t = timeit([&] { pull_k64<16><<<sms * 8, 128>>>(io, inbp, y64, x64, n, 0); }, 5); rep("pull_k64_G16", t, b64, (double)m);
+    t = timeit([&] { cudaMemsetAsync(ctr, 0, 4); pull_k64_dyn<8><<<sms * 8, 128>>>(io, inbp, y64, x64, n, ctr); }, 5);
+    rep("pull_k64_dyn_G8", t, b64, (double)m);
+    // source ids folded into 2^17 rows (64 MB of y): the gathers hit L2
+    t = timeit([&] { pull_k64<8><<<sms * 8, 128>>>(io, inbp, y64, x64, n, (1u << 17) - 1); }, 5);
+    rep("pull_k64_L2res", t, b64, (double)m);
+    t = timeit([&] { pull_k64<8><<<sms * 8, 128>>>(io, inbp, y64, x64, n, (1u << 14) - 1); }, 5);
+    rep("pull_k64_L2small", t, b64, (double)m);
+
+    for (uint32_t PL : {128u, 512u, 2048u}) {
+      std::vector<uint64_t> h(n + 1);
+      CK(cudaMemcpy(h.data(), io, 8ull * (n + 1), cudaMemcpyDeviceToHost));
+      std::vector<Piece> pcs;
+      for (uint32_t u = 0; u < n; ++u) {
+        const uint64_t len = h[u + 1] - h[u];
+        if (!len) continue;
+        const uint32_t split = len > PL;
+        for (uint64_t q = 0; q < len; q += PL)
+          pcs.push_back(Piece{u, (uint32_t)(len - q < PL ? len - q : PL), h[u] + q, split, 0});
+      }
+      Piece* dpc; CK(cudaMalloc(&dpc, sizeof(Piece) * pcs.size()));
+      CK(cudaMemcpy(dpc, pcs.data(), sizeof(Piece) * pcs.size(), cudaMemcpyHostToDevice));
+      for (int blocks : {sms * 8, sms * 32}) {
+        t = timeit([&] { pull_k64_pieces<8><<<blocks, 128>>>(dpc, pcs.size(), inbp, y64, x64, 0); }, 5);
+        printf("pieces PL=%u grid=%d npc=%zu", PL, blocks, pcs.size()); rep("", t, b64, (double)m);
+      }
+      {  // + the PowerPush per-row state traffic (x row read, x and y rows written); y2 = y64 copy target
+        double* y2; CK(cudaMalloc(&y2, 8ull * 64 * n)); CK(cudaMemset(x64, 0, 8ull * 64 * n));
+        t = timeit([&] { pull_k64_pieces<8><<<sms * 32, 128>>>(dpc, pcs.size(), inbp, y64, x64, 0, y2); }, 5);
+        printf("pieces PL=%u +state", PL); rep("", t, b64, (double)m);
+        cudaFree(y2);
+      }
+      t = timeit([&] { pull_k64_pieces<8><<<sms * 32, 128>>>(dpc, pcs.size(), inbp, y64, x64, (1u << 17) - 1); }, 5);
+      printf("pieces PL=%u L2res", PL); rep("", t, b64, (double)m);
+      cudaFree(dpc);
+    }
+    return 0;
+  }
   const double b1 = 8.0 * (n + 1) + 4.0 * m + 32.0 * n;
-  float t;
   t = timeit([&] { cudaMemsetAsync(next, 0, 8ull * n); push_warp<<<G, 256>>>(o, nbp, cur, next, n, 0); }, 10);
   rep("push_warp_k1", t, b1, (double)m);
   t = timeit([&] { cudaMemsetAsync(next, 0, 8ull * n); push_thread<<<G, 256>>>(o, nbp, cur, next, n, 0); }, 10);
