@@ -51,12 +51,27 @@ def log(*a):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, device: int):
         self.device, self.rows, self.proc = device, [], None
+        self.t0, self.t1 = 0.0, float("inf")
+
+    def mark_start(self):  # samples before this (nvidia-smi start-up, warm-up) are dropped
+        self.t0 = time.time()
+
+    def mark_stop(self):
+        self.t1 = time.time()
+
+    @staticmethod
+    def _t(stamp: str) -> float:
+        import datetime
+        try:
+            return datetime.datetime.strptime(stamp, "%Y/%m/%d %H:%M:%S.%f").timestamp()
+        except ValueError:
+            return -1.0
 
     def __enter__(self):
         try:
@@ -83,14 +98,16 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        # rows carry nvidia-smi's own timestamp (host local time): keep the timed region's
+        rows = [r[1:] for r in self.rows if r and self.t0 <= self._t(r[0]) <= self.t1 + 0.25]
+        sm = [float(r[0]) for r in rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
+        reasons = sorted({names[i] for r in rows for i in range(4)
                           if len(r) > 3 + i and r[3 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows)}
 
 
 def peaks():
@@ -103,6 +120,14 @@ def peaks():
 
 def traffic_for(workload: str):
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(workload)
+    return None
+
+
+def ceiling_for(workload: str):
+    p = os.path.join(ROOT, "profiles", "ceilings.json")
     if os.path.exists(p):
         with open(p) as f:
             return json.load(f).get(workload)
@@ -256,6 +281,8 @@ def main():
         return P.power_push_batch(g, mine, CFG["alpha"], CFG["lam"],
                                   device_out=(dev_res.data_ptr(), dev_rsd.data_ptr()))
 
+    clk = ClockSampler(local)
+    clk.__enter__()  # nvidia-smi starts before the warm-up; only timed-region samples count
     for _ in range(args.warmup):
         step_device()
     barrier(world)
@@ -264,7 +291,8 @@ def main():
     sweep_ms = dev_ms = 0.0
     alg = launches = sweep_launches = 0
     sweeps = []
-    with ClockSampler(local) as clk:
+    with clk:
+        clk.mark_start()
         start.record()
         for _ in range(args.steps):
             outs, cs = step_device()
@@ -276,6 +304,7 @@ def main():
             sweeps.append(cs.max_sweeps)
         stop.record()
         torch.cuda.synchronize()
+        clk.mark_stop()
     barrier(world)
     ms = start.elapsed_time(stop)
     ms = max_over_ranks(world, ms)
@@ -325,6 +354,17 @@ def main():
     traffic = traffic_for("config3")
     launch_s = sweep_ms / max(sweep_launches, 1) / 1000.0
     dram_rate = traffic / launch_s / 1e9 if (traffic and launch_s > 0) else None
+    # measured ms per sweep (a launch runs one block's sweeps) against the
+    # gather-pattern ceiling microbenchmark (profiles/ceilings.json)
+    ceil = ceiling_for("config3")
+    ms_sweep = launch_s * 1000.0 / max(sweeps[-1], 1)
+    gather_ceiling = None
+    if ceil:
+        gather_ceiling = {"ms_per_sweep": ms_sweep,
+                          "ceiling_ms_per_sweep": ceil["gather_state_ms_per_sweep"],
+                          "frac": ceil["gather_state_ms_per_sweep"] / ms_sweep,
+                          "l2_resident_ms_per_sweep": ceil["l2_resident_gather_ms_per_sweep"],
+                          "source": "profiles/ceilings.json"}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -343,7 +383,12 @@ def main():
                          "dram_traffic_GBps": dram_rate,
                          "dram_traffic_frac": dram_rate / peak if dram_rate else None,
                          "sweep_ms_per_step": sweep_ms / args.steps,
-                         "sweeps_per_block": sweeps[-1]},
+                         "device_ms_per_step": dev_ms / args.steps,
+                         "sweeps_per_block": sweeps[-1],
+                         # the sweep is bound by its y-row gathers (L2 sectors + gather
+                         # misses), which the algorithmic bytes do not count: fraction of
+                         # a minimal kernel with the same gathers and state traffic
+                         "gather_ceiling": gather_ceiling},
             "clocks": clk.summary()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
