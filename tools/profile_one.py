@@ -21,6 +21,7 @@ ap.add_argument("--seed", type=int, default=3)
 ap.add_argument("--queries", type=int, default=4)
 ap.add_argument("--engine", default="powerpush", choices=["powerpush", "powitr", "speedppr"])
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--epochs", type=int, default=8)
 a = ap.parse_args()
 g = P.generate_rmat(a.scale, a.ef, a.seed)
 src = P.sample_sources(np.diff(g.out_offsets()), a.queries, a.seed)
@@ -29,7 +30,7 @@ print(f"n={g.n()} m={g.m()} dead={len(g.dead_ends())}")
 
 def run():
     if a.engine == "powerpush":
-        return P.power_push_batch(g, src, 0.2, 1e-8, keep=False)
+        return P.power_push_batch(g, src, 0.2, 1e-8, epoch_num=a.epochs, keep=False)
     if a.engine == "powitr":
         return P.power_iteration_batch(g, src, 0.2, 1e-8, keep=False)
     return P.speedppr_batch(g, src, P.QueryConfig(epsilon=0.5, seed=4), keep=False)
