@@ -273,8 +273,24 @@ __global__ void k_refine_out(const double* x, const double* res, uint64_t n, int
   }
 }
 
-inline uint32_t tile_edges(int K) { return K >= WIDE_K ? WIDE_T : (uint32_t)(SWEEP_ELEMS / K); }
-inline uint32_t tile_rmax(int K) {
+// One-column sweeps run as warp tasks (sweep_k1_warps) on graphs with at least
+// PPRG_K1W_MIN_M in-edges (default 4M); smaller graphs, where a sweep is a few
+// microseconds of latency chains, keep the block-tile path (tile_rows).
+inline bool k1w_on(const Graph& g, int K) {
+  if (K != 1 || !PPRG_K1W) return false;
+  static const uint64_t min_m = [] {
+    const char* e = std::getenv("PPRG_K1W_MIN_M");
+    return e ? std::strtoull(e, nullptr, 10) : 4000000ull;
+  }();
+  return g.m >= min_m;
+}
+inline uint32_t tile_edges(int K, bool w) {
+  if (w) return K1W_T;
+  return K >= WIDE_K ? WIDE_T : (uint32_t)(SWEEP_ELEMS / K);
+}
+inline uint32_t tile_hub(int K, bool w) { return w ? K1W_H : tile_edges(K, w); }
+inline uint32_t tile_rmax(int K, bool w) {
+  if (w) return K1W_R;
   if (K >= WIDE_K) return RMAX_W;
   const int T = SWEEP_ELEMS / K;
   return T < 256 ? T : 256;

@@ -470,9 +470,10 @@ const uint32_t* Graph::split_rows(uint32_t T, uint64_t* count) {
 // Greedy row-aligned packing in id order (so sweeps stay id-ordered): rows are
 // added to the current tile while it keeps <= T in-edges and <= R rows; a row
 // with more than T in-edges becomes ceil(deg/T) hub pieces of its own.
-const Graph::Plan& Graph::tile_plan(uint32_t T, uint32_t R) {
+const Graph::Plan& Graph::tile_plan(uint32_t T, uint32_t R, uint32_t H) {
   ensure_transpose();
-  const uint64_t key = ((uint64_t)T << 32) | R;
+  if (H < T) H = T;
+  const uint64_t key = ((uint64_t)T << 40) | ((uint64_t)H << 16) | R;
   auto it = plans.find(key);
   if (it != plans.end()) return it->second;
   std::vector<uint64_t> h_off(n_rows + 1);
@@ -488,15 +489,20 @@ const Graph::Plan& Graph::tile_plan(uint32_t T, uint32_t R) {
   };
   for (uint64_t r = 0; r < n_rows; ++r) {
     const uint64_t d = h_off[r + 1] - h_off[r];
-    if (d > T) {
+    if (d > H) {
       close();
-      const uint32_t np = (uint32_t)((d + T - 1) / T);
+      const uint32_t np = (uint32_t)((d + H - 1) / H);
       for (uint32_t p = 0; p < np; ++p) {
-        const uint64_t e0 = h_off[r] + (uint64_t)p * T;
-        const uint64_t ne = std::min<uint64_t>(T, h_off[r + 1] - e0);
+        const uint64_t e0 = h_off[r] + (uint64_t)p * H;
+        const uint64_t ne = std::min<uint64_t>(H, h_off[r + 1] - e0);
         tl.push_back(TileDesc{e0, (uint32_t)ne, (uint32_t)r, 1, nhubs, p, np});
       }
       ++nhubs;
+      continue;
+    }
+    if (d > T) {  // a long row, whole, in a tile of its own
+      close();
+      tl.push_back(TileDesc{h_off[r], (uint32_t)d, (uint32_t)r, 1, 0, 0, 1});
       continue;
     }
     if (cur.nr && (cur.ne + d > T || cur.nr >= R)) close();

@@ -61,7 +61,10 @@ struct Graph {
     uint64_t ntiles = 0, nhubs = 0;
   };
   std::map<uint64_t, Plan> plans;  // key: (T << 32) | RMAX
-  const Plan& tile_plan(uint32_t max_edges, uint32_t max_rows);
+  // rows packed while a tile holds <= max_edges in-edges and <= max_rows rows; a
+  // row longer than max_edges is a tile of its own, and a row longer than
+  // hub_edges (default max_edges) is cut into pieces of hub_edges edges
+  const Plan& tile_plan(uint32_t max_edges, uint32_t max_rows, uint32_t hub_edges = 0);
   uint64_t m_eff() const { return m + n_dead; }
 };
 

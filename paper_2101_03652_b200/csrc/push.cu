@@ -170,11 +170,12 @@ void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
 
   const size_t wide_bytes = 8ull * (RMAX_W + 1) + 8ull * RMAX_W + 8ull * (NT / 32) * K +
                             4ull * (3 * RMAX_W + 1) + 16;
-  const size_t smem = K >= WIDE_K ? wide_bytes : Tile<K>::bytes;
+  const size_t smem = K >= WIDE_K ? wide_bytes : P.k1w ? k1w_bytes : Tile<K>::bytes;
   auto kern = k_sweeps<K, MODE>;
   static bool attr_set = false;
   if (!attr_set) {
-    PPRG_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const size_t most = K >= WIDE_K ? wide_bytes : std::max(k1w_bytes, Tile<K>::bytes);
+    PPRG_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)most));
     attr_set = true;
   }
   if (cooperative) {
@@ -190,7 +191,9 @@ void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
       const char* e = std::getenv("PPRG_TILES_PER_BLOCK");
       return e ? std::atof(e) : -1.0;
     }();
-    const double tpb = tpb_env >= 0 ? tpb_env : (K < WIDE_K ? 2.0 : 0.0);
+    // (one-column warp tasks: ~2 per warp, i.e. 8 per block)
+    const double tpb = tpb_env >= 0 ? tpb_env
+                                    : P.k1w ? 2.0 * (NT / 32) : (K < WIDE_K ? 2.0 : 0.0);
     if (tpb > 0 && P.ntiles > 0) {
       const double want = (double)P.ntiles / tpb;
       const unsigned lo = (unsigned)g.sm_count;
@@ -371,7 +374,7 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   const TileDesc* dsc = nullptr;
   uint64_t nhubs = 0;
   if (need_pull) {
-    const Graph::Plan& pl = g.tile_plan(tile_edges(K), tile_rmax(K));
+    const Graph::Plan& pl = g.tile_plan(tile_edges(K, k1w_on(g, K)), tile_rmax(K, k1w_on(g, K)), tile_hub(K, k1w_on(g, K)));
     dsc = pl.tiles.get();
     ntiles = pl.ntiles;
     nhubs = pl.nhubs;
@@ -417,6 +420,7 @@ SweepParams base_params(Block& b) {
   P.desc = b.desc;
   P.ntiles = b.ntiles;
   P.T = SWEEP_ELEMS / b.K;
+  P.k1w = k1w_on(g, b.K);
   P.carry_head = b.w.carry_h.get();
   P.carry_tail = b.w.carry_t.get();
   P.split_cnt = b.w.split_cnt.get();
@@ -1320,7 +1324,7 @@ PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t
   Block& b = *s->b;
   const int K = b.K;
   // ---- the cut: row-start tiles, balanced on in-edges ------------------------
-  const Graph::Plan& pl = g.tile_plan(tile_edges(K), tile_rmax(K));
+  const Graph::Plan& pl = g.tile_plan(tile_edges(K, k1w_on(g, K)), tile_rmax(K, k1w_on(g, K)), tile_hub(K, k1w_on(g, K)));
   const std::vector<TileDesc>& tl = pl.host;
   uint64_t total = 0;
   for (const TileDesc& t : tl) total += t.ne;

@@ -72,6 +72,7 @@ struct SweepParams {
   uint64_t ntiles;
   uint32_t T;
   int k_live;  // real columns (<= K)
+  int k1w;     // K = 1: warp tasks (sweep_k1_warps) instead of block tiles
   int E;
   double alpha;
   double lambda;               // powitr termination
@@ -377,6 +378,173 @@ __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& 
   if (tid == 0) *nlong = 0;
 }
 
+// One-column sweeps (K = 1) by independent warps (PPRG_K1W). The tile plan is
+// cut into warp tasks: <= 256 in-edges and <= 64 whole rows, or one whole row
+// of <= K1W_H in-edges, or one K1W_H-edge piece of a longer row. Warps take
+// tasks in id order, CH at a time from the sweep's ticket (fetched one chunk
+// ahead), with no block barrier anywhere; the next task's descriptor is
+// loaded one ahead. Per 256-edge round a task's in-edge ids (8 per lane,
+// coalesced) and gathers are issued before its row data (2 rows per lane:
+// offset, node, degree, x) is needed; per 32-edge window the row starts are
+// OR-reduced into a bit mask, each lane's row key is a popcount of it, and a
+// segmented shuffle reduction leaves every row segment's sum in its first
+// lane, which adds it into the warp's row accumulator in shared memory.
+// Pieces meet through the hub protocol of hub_piece (partial slot,
+// release-ordered counter, the last piece sums the partials in piece order).
+#ifndef PPRG_K1W
+#define PPRG_K1W 1
+#endif
+#ifndef PPRG_K1W_H
+#define PPRG_K1W_H 1024
+#endif
+#ifndef PPRG_K1W_CH
+#define PPRG_K1W_CH 2
+#endif
+constexpr uint32_t K1W_T = 256;         // packed-task edges (32 lanes x 8 gathers per round)
+constexpr uint32_t K1W_R = 64;          // packed-task rows (2 per lane)
+constexpr uint32_t K1W_H = PPRG_K1W_H;  // longest whole-row task; longer rows are pieces
+constexpr uint32_t K1W_CH = PPRG_K1W_CH;
+constexpr size_t k1w_bytes = 8ull * (NT / 32) * K1W_R;
+
+__device__ __forceinline__ uint32_t le_mask(int j) { return 0xFFFFFFFFu >> (31 - j); }
+
+template <int MODE>
+__device__ __forceinline__ void sweep_k1_warps(const SweepParams& P, const ColSh* cs,
+                                               const double* thr_cur, const double* yg,
+                                               const double* rcur, double* rnxt, double* ynxt,
+                                               Acc& a, double* sacc_all, unsigned* ticket) {
+  constexpr int G = K1W_T / 32;
+  constexpr bool RC = MODE == M_POWITR || MODE == M_SIMFWD;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* sacc = sacc_all + warp * K1W_R;
+  const uint64_t nt = P.ntiles;
+  auto grab = [&]() -> uint64_t {
+    unsigned b = 0;
+    if (lane == 0) b = atomicAdd(ticket, K1W_CH);
+    return __shfl_sync(0xffffffffu, b, 0);
+  };
+  uint64_t base = grab();
+  uint64_t nbase = base < nt ? grab() : nt;
+  TileDesc d{};
+  if (base < nt) d = P.desc[base];
+  while (base < nt) {
+    for (uint32_t ci = 0; ci < K1W_CH; ++ci) {
+      const uint64_t t = base + ci;
+      if (t >= nt) break;
+      const uint64_t tn = (ci + 1 < K1W_CH && t + 1 < nt) ? t + 1 : nbase;
+      TileDesc dn = d;
+      if (tn < nt) dn = P.desc[tn];  // next task, one ahead
+      if (d.npieces > 1) {  // one piece of a row longer than K1W_H
+        double sum = 0.0;
+        for (uint32_t rb = 0; rb < d.ne; rb += K1W_T) {
+          uint32_t id[G];
+          double v[G];
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const uint32_t pe = rb + 32 * g + lane;
+            id[g] = pe < d.ne ? ld_stream(P.in_nbr + d.e0 + pe) : 0u;
+          }
+#pragma unroll
+          for (int g = 0; g < G; ++g) v[g] = rb + 32 * g + lane < d.ne ? ld_gather(yg + id[g]) : 0.0;
+          sum += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+        int last = 0;
+        if (lane == 0) {
+          P.hub_acc[t] = sum;
+          unsigned old;
+          asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+                       : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
+          last = old == d.npieces - 1;
+          if (last) P.hub_cnt[d.hub] = 0;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {  // the partials in piece order (lane-strided, then a fixed tree)
+          const double* part = P.hub_acc + (t - d.piece);
+          double acc = 0.0;
+          for (uint32_t p = lane; p < d.npieces; p += 32) acc += __ldcg(part + p);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+          if (lane == 0) {
+            const uint32_t u = __ldg(P.crow + d.r0);
+            decide<1, MODE>(P, cs, thr_cur, u, 0, acc, __ldcg(P.x + u),
+                            RC ? __ldcg(rcur + u) : 0.0, __ldg(P.cdeg + d.r0),
+                            __ldg(P.cinv + d.r0), yg, rnxt, ynxt, a);
+          }
+        }
+        d = dn;
+        continue;
+      }
+      // rows: lane holds rows lane and lane + 32 of the task
+      uint32_t st0 = 0xFFFFFFFFu, st1 = 0xFFFFFFFFu, u0 = 0, u1 = 0, dg0 = 0, dg1 = 0;
+      double inv0 = 0.0, inv1 = 0.0, xo0 = 0.0, xo1 = 0.0, rc0 = 0.0, rc1 = 0.0;
+      if ((uint32_t)lane < d.nr) {
+        const uint64_t r = d.r0 + lane;
+        st0 = (uint32_t)(__ldg(P.in_off + r) - d.e0);
+        u0 = __ldg(P.crow + r);
+        dg0 = __ldg(P.cdeg + r);
+        inv0 = __ldg(P.cinv + r);
+        xo0 = __ldcg(P.x + u0);
+        if constexpr (RC) rc0 = __ldcg(rcur + u0);
+      }
+      if ((uint32_t)lane + 32 < d.nr) {
+        const uint64_t r = d.r0 + lane + 32;
+        st1 = (uint32_t)(__ldg(P.in_off + r) - d.e0);
+        u1 = __ldg(P.crow + r);
+        dg1 = __ldg(P.cdeg + r);
+        inv1 = __ldg(P.cinv + r);
+        xo1 = __ldcg(P.x + u1);
+        if constexpr (RC) rc1 = __ldcg(rcur + u1);
+      }
+      sacc[lane] = 0.0;
+      sacc[lane + 32] = 0.0;
+      __syncwarp();
+      int before = 0;  // rows started before the window
+      for (uint32_t rb = 0; rb < d.ne; rb += K1W_T) {
+        uint32_t id[G];
+        double v[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint32_t pe = rb + 32 * g + lane;
+          id[g] = pe < d.ne ? ld_stream(P.in_nbr + d.e0 + pe) : 0u;
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) v[g] = rb + 32 * g + lane < d.ne ? ld_gather(yg + id[g]) : 0.0;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint32_t w0 = rb + 32 * g;
+          if (w0 >= d.ne) break;  // warp-uniform
+          uint32_t bit = 0;
+          if (st0 - w0 < 32u) bit |= 1u << (st0 - w0);
+          if (st1 - w0 < 32u) bit |= 1u << (st1 - w0);
+          const uint32_t M = __reduce_or_sync(0xffffffffu, bit);
+          const int key = before - 1 + __popc(M & le_mask(lane));
+          double x = v[g];
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double xn = __shfl_down_sync(0xffffffffu, x, o);
+            // lane + o is in my segment iff no row starts in (lane, lane + o]
+            if (lane + o < 32 && !(M & le_mask(lane + o) & ~le_mask(lane))) x += xn;
+          }
+          if (w0 + lane < d.ne && (lane == 0 || ((M >> lane) & 1u))) sacc[key] += x;
+          __syncwarp();
+          before += __popc(M);
+        }
+      }
+      if ((uint32_t)lane < d.nr)
+        decide<1, MODE>(P, cs, thr_cur, u0, 0, sacc[lane], xo0, rc0, dg0, inv0, yg, rnxt, ynxt, a);
+      if ((uint32_t)lane + 32 < d.nr)
+        decide<1, MODE>(P, cs, thr_cur, u1, 0, sacc[lane + 32], xo1, rc1, dg1, inv1, yg, rnxt,
+                        ynxt, a);
+      __syncwarp();
+      d = dn;
+    }
+    base = nbase;
+    nbase = base < nt ? grab() : nt;
+  }
+}
+
 // Wide column blocks (K >= WIDE_K): tiles of up to WIDE_T in-edges and
 // RMAX_W rows; warps take rows from a shared counter and gather each in-edge's
 // K contiguous values straight into registers (lanes = edge slots x columns),
@@ -667,7 +835,10 @@ template <int K, int MODE>
 #ifndef PPRG_MINB_NARROW
 #define PPRG_MINB_NARROW PPRG_MINB
 #endif
-__global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
+#ifndef PPRG_MINB_K1
+#define PPRG_MINB_K1 6
+#endif
+__global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K1 : PPRG_MINB_NARROW))
     k_sweeps(const __grid_constant__ SweepParams P) {
   using TC = Tile<K>;
   extern __shared__ __align__(16) char smem_dyn[];
@@ -700,7 +871,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
       int any = 0;
       for (int cc = 0; cc < K; ++cc) any |= !cs[cc].done;
       sh_any = any && (MODE == M_FINAL ? sweep == 0 : sweep < P.max_sweeps);
-      if (sh_any) sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
+      if (sh_any && !P.k1w) sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
       sh_nlong = 0;
       if constexpr (K >= WIDE_K) *wide_long_count<K>(smem_dyn) = 0;
     }
@@ -732,6 +903,10 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
     Acc a;
     // Tiles in ticket (= id) order; the next ticket is fetched one tile ahead
     // and the next descriptor is loaded inside the current tile.
+    if (K == 1 && PPRG_K1W && P.k1w) {
+      sweep_k1_warps<MODE>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a,
+                           reinterpret_cast<double*>(smem_dyn), &ctl->ticket[buf]);
+    } else {
     unsigned long long j = sh_tile[0];
     TileDesc d = P.desc[j < P.ntiles ? j : 0];
     for (uint32_t it = 0;; ++it) {
@@ -754,6 +929,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : PPRG_MINB_NARROW))
       }
       j = sh_tile[(it + 1) & 1];
       d = dn;
+    }
     }
     source_rows<K, MODE>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
     // block-level flush of this sweep's accumulators: reduce over the lanes of

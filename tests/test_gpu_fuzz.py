@@ -37,7 +37,8 @@ def hub_graph(n, hubs, hub_deg, rng):
     return CSR(np.cumsum(off).astype(np.uint64), d.astype(np.uint32))
 
 
-CASES = [(1, 0, 0, 0), (7, 0, 0, 1), (300, 1, 3000, 2), (2000, 3, 9000, 3), (5000, 2, 20000, 4)]
+CASES = [(1, 0, 0, 0), (7, 0, 0, 1), (300, 1, 3000, 2), (2000, 3, 9000, 3), (5000, 2, 20000, 4),
+         (3000, 4, 700, 5)]  # the last: rows of 256-1024 in-edges (whole-row warp tasks)
 
 
 @pytest.mark.parametrize("n,hubs,hub_deg,seed", CASES)
