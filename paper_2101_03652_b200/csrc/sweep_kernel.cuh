@@ -559,6 +559,19 @@ constexpr int WIDE_K = 4;
 constexpr uint32_t WIDE_T = PPRG_WIDE_T;
 constexpr uint32_t RMAX_W = PPRG_RMAX_W;
 
+// Column lanes of the wide layout: each lane loads CPL = K / KC contiguous
+// columns of an in-edge's row. K = 64: 32 lanes x 16 B; K = 32 (PPRG_VEC2):
+// 16 lanes x 16 B, two in-edges per warp load instruction (5.5% faster per
+// sweep than 32 lanes x 8 B on configs[2]; for K = 4..16 the same split was
+// 12-40% slower, so they keep one column per lane).
+#ifndef PPRG_VEC2
+#define PPRG_VEC2 1
+#endif
+template <int K>
+__host__ __device__ constexpr int wide_kc() {
+  return K >= 64 ? 32 : (PPRG_VEC2 && K == 32) ? 16 : (K < 32 ? K : 32);
+}
+
 // Sum of y over the in-edges [b, e) of one row for my columns, by one warp.
 // Lanes = ES edge slots x KC column lanes (x CPL contiguous columns). The ids
 // of 32 consecutive edges are loaded once, coalesced, and broadcast by shuffle;
@@ -570,9 +583,9 @@ constexpr uint32_t RMAX_W = PPRG_RMAX_W;
 #endif
 template <int K>
 __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double* yg, uint64_t b,
-                                             uint64_t e, double (&s)[(K < 32 ? 1 : K / 32)],
+                                             uint64_t e, double (&s)[K / wide_kc<K>()],
                                              bool have_first = false, uint32_t first_id = 0) {
-  constexpr int KC = K < 32 ? K : 32;
+  constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   constexpr int ES = 32 / KC;
   constexpr int G = PPRG_G;
@@ -628,7 +641,7 @@ __device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc
                                             const double* thr_cur, const double* yg,
                                             const double* rcur, double* rnxt, double* ynxt,
                                             Acc& a) {
-  constexpr int KC = K < 32 ? K : 32;
+  constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -672,7 +685,7 @@ __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* c
                                             const double* xo, const double* rc, uint32_t dg,
                                             double inv, const double* yg, double* rnxt,
                                             double* ynxt, Acc& a, const BlockAcc& ba) {
-  constexpr int KC = K < 32 ? K : 32;
+  constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   const int kc = (threadIdx.x & 31) % KC;
   if constexpr (CPL == 1) {
@@ -717,7 +730,7 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
                                                double* ynxt, Acc& a, const BlockAcc& ba,
                                                uint32_t* rowctr,
                                                const unsigned long long* dn_slot, TileDesc* dn) {
-  constexpr int KC = K < 32 ? K : 32;
+  constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   constexpr int NW = NT / 32;
   uint64_t* soff = reinterpret_cast<uint64_t*>(smem);

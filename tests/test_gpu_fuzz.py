@@ -42,7 +42,7 @@ CASES = [(1, 0, 0, 0), (7, 0, 0, 1), (300, 1, 3000, 2), (2000, 3, 9000, 3), (500
 
 
 @pytest.mark.parametrize("n,hubs,hub_deg,seed", CASES)
-@pytest.mark.parametrize("k", [1, 3, 16, 64])
+@pytest.mark.parametrize("k", [1, 3, 16, 32, 64])
 def test_power_push_fuzz(P, oracle, n, hubs, hub_deg, seed, k):
     rng = np.random.default_rng(seed)
     g = hub_graph(n, hubs, hub_deg, rng) if n > 1 else CSR(np.array([0, 1], np.uint64),

@@ -182,7 +182,7 @@ def test_power_push_random_graphs_vs_oracle(P, oracle, lam):
             check_hp(P.power_push(d, s, 0.2, lam), oracle.power_push(g, s, 0.2, lam), lam)
 
 
-@pytest.mark.parametrize("k", [3, 8, 64])
+@pytest.mark.parametrize("k", [3, 8, 32, 64])
 def test_power_push_column_block(P, oracle, k):
     g = oracle.random_graph(1500, 0, 6, 11)
     d = dev(P, g)
