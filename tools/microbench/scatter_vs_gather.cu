@@ -257,6 +257,44 @@ __global__ void __launch_bounds__(128, 8) pull_k64_pieces(const Piece* __restric
     } else *reinterpret_cast<double2*>(dst) = make_double2(a0, a1);
   }
 }
+
+// 128-column rows (1 KB): lanes load 32 B each (two 16-byte loads)
+template <int G>
+__global__ void __launch_bounds__(128, 8) pull_k128_pieces(const Piece* __restrict__ pc, uint64_t npc,
+                         const uint32_t* __restrict__ inb, const double* __restrict__ y, double* next) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t warps = (gridDim.x * blockDim.x) >> 5;
+  const double* yb = y + 4 * lane;
+  for (uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5; w < npc; w += warps) {
+    const Piece P = pc[w];
+    const uint64_t b = P.b, e = P.b + P.len;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (uint64_t p0 = b; p0 < e; p0 += 32) {
+      const uint32_t myid = p0 + lane < e ? inb[p0 + lane] : 0u;
+      const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
+      for (int j0 = 0; j0 < cnt; j0 += G) {
+        double2 v[G][2];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int j = j0 + g;
+          const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
+          const double2* src = reinterpret_cast<const double2*>(yb + (uint64_t)id * 128);
+          v[g][0] = src[0];
+          v[g][1] = src[1];
+        }
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const bool ok = j0 + g < cnt;
+          a0 += ok ? v[g][0].x : 0.0; a1 += ok ? v[g][0].y : 0.0;
+          a2 += ok ? v[g][1].x : 0.0; a3 += ok ? v[g][1].y : 0.0;
+        }
+      }
+    }
+    double* dst = next + (uint64_t)P.row * 128 + 4 * lane;
+    if (P.split) { atomicAdd(dst, a0); atomicAdd(dst + 1, a1); atomicAdd(dst + 2, a2); atomicAdd(dst + 3, a3); }
+    else { reinterpret_cast<double2*>(dst)[0] = make_double2(a0, a1); reinterpret_cast<double2*>(dst)[1] = make_double2(a2, a3); }
+  }
+}
 // raw rates
 __global__ void rand_red(const uint32_t* __restrict__ idx, uint64_t cnt, double* vec) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cnt; i += (uint64_t)gridDim.x * blockDim.x)
@@ -377,6 +415,17 @@ int main(int argc, char** argv) {
         t = timeit([&] { pull_k64_pieces<8><<<sms * 32, 128>>>(dpc, pcs.size(), inbp, y64, x64, 0, y2); }, 5);
         printf("pieces PL=%u +state", PL); rep("", t, b64, (double)m);
         cudaFree(y2);
+      }
+      if (PL == 128) {  // 128 columns: per-query cost vs 64
+        double *y128, *x128;
+        CK(cudaMalloc(&y128, 8ull * 128 * n)); CK(cudaMalloc(&x128, 8ull * 128 * n));
+        CK(cudaMemset(y128, 0, 8ull * 128 * n));
+        for (int G2 : {4, 8}) {
+          t = G2 == 4 ? timeit([&] { pull_k128_pieces<4><<<sms * 32, 128>>>(dpc, pcs.size(), inbp, y128, x128); }, 5)
+                      : timeit([&] { pull_k128_pieces<8><<<sms * 32, 128>>>(dpc, pcs.size(), inbp, y128, x128); }, 5);
+          printf("pieces PL=128 K=128 G=%d (per 64 columns: %.1f us)", G2, t / 2); rep("", t, 2 * b64, (double)m);
+        }
+        cudaFree(y128); cudaFree(x128);
       }
       t = timeit([&] { pull_k64_pieces<8><<<sms * 32, 128>>>(dpc, pcs.size(), inbp, y64, x64, (1u << 17) - 1); }, 5);
       printf("pieces PL=%u L2res", PL); rep("", t, b64, (double)m);
