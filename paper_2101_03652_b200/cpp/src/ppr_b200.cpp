@@ -24,6 +24,47 @@
 #include "ppr/walk_index.hpp"
 
 namespace ppr {
+
+// ---- push.hpp host containers -------------------------------------------------
+FifoQueue::FifoQueue(std::size_t n) : slots_(n + 1) {}
+bool FifoQueue::empty() const { return first_ == last_; }
+std::size_t FifoQueue::size() const {
+  return last_ >= first_ ? last_ - first_ : slots_.size() - (first_ - last_);
+}
+void FifoQueue::push(NodeId v) {
+  slots_[last_] = v;
+  if (++last_ == slots_.size()) last_ = 0;
+}
+NodeId FifoQueue::pop() {
+  const NodeId v = slots_[first_];
+  if (++first_ == slots_.size()) first_ = 0;
+  return v;
+}
+void FifoQueue::clear() { first_ = last_ = 0; }
+
+PushState::PushState(NodeId n, NodeId s)
+    : reserve(n, 0.0), residue(n, 0.0), r_sum(1.0), in_queue(n, 0), queue(n) {
+  residue[s] = 1.0;
+}
+
+// ---- types.hpp (reference types.hpp:17-53) -----------------------------------
+double default_lambda(EdgeId m) { return std::min(1.0 / static_cast<double>(m), 1e-8); }
+double default_mu(NodeId n) { return 1.0 / static_cast<double>(n); }
+std::uint64_t default_scan_threshold(NodeId n) { return n / 4; }
+
+void QueryConfig::validate() const {
+  auto bad = [](const char* what) { throw std::invalid_argument(what); };
+  if (!(alpha >= 0.0 && alpha < 1.0)) bad("alpha must be in [0,1)");
+  if (lambda && !(*lambda > 0.0 && *lambda <= 1.0)) bad("lambda must be in (0,1]");
+  if (epsilon && !(*epsilon > 0.0)) bad("epsilon must be positive");
+  if (mu && !(*mu > 0.0 && *mu <= 1.0)) bad("mu must be in (0,1]");
+  if (epoch_num == 0) bad("epoch_num must be positive");
+}
+double QueryConfig::lambda_for(EdgeId m) const { return lambda.value_or(default_lambda(m)); }
+double QueryConfig::mu_for(NodeId n) const { return mu.value_or(default_mu(n)); }
+std::uint64_t QueryConfig::scan_threshold_for(NodeId n) const {
+  return scan_threshold.value_or(default_scan_threshold(n));
+}
 namespace {
 
 void check(int rc) {
