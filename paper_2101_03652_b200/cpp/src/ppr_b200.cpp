@@ -25,6 +25,21 @@
 
 namespace ppr {
 
+// ---- rng.hpp ----------------------------------------------------------------
+std::uint64_t Rng::below(std::uint64_t bound) {
+  using u128 = unsigned __int128;
+  u128 prod = static_cast<u128>(next()) * bound;
+  auto low = static_cast<std::uint64_t>(prod);
+  if (low < bound) {
+    const std::uint64_t reject_below = (0 - bound) % bound;  // 2^64 mod bound
+    while (low < reject_below) {
+      prod = static_cast<u128>(next()) * bound;
+      low = static_cast<std::uint64_t>(prod);
+    }
+  }
+  return static_cast<std::uint64_t>(prod >> 64);
+}
+
 // ---- push.hpp host containers -------------------------------------------------
 FifoQueue::FifoQueue(std::size_t n) : slots_(n + 1) {}
 bool FifoQueue::empty() const { return first_ == last_; }
