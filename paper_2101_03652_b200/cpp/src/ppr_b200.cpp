@@ -181,20 +181,20 @@ std::uint32_t read_u32(std::ifstream& in) {
 
 // ---- graph.hpp ---------------------------------------------------------------
 Graph::Graph(std::vector<std::uint64_t> out_offsets, std::vector<NodeId> out_neighbors)
-    : out_offsets_(std::move(out_offsets)), out_neighbors_(std::move(out_neighbors)) {
-  if (out_offsets_.empty()) throw std::runtime_error("graph: offsets array must have length n+1");
-  n_ = static_cast<NodeId>(out_offsets_.size() - 1);
-  m_ = out_neighbors_.size();
-  if (out_offsets_.back() != m_) throw std::runtime_error("graph: offsets must end at m");
+    : off_(std::move(out_offsets)), nbr_(std::move(out_neighbors)) {
+  if (off_.empty()) throw std::runtime_error("graph: offsets array must have length n+1");
+  n_ = static_cast<NodeId>(off_.size() - 1);
+  m_ = nbr_.size();
+  if (off_.back() != m_) throw std::runtime_error("graph: offsets must end at m");
   pprg_graph* h = nullptr;
-  check(pprg_graph_create(out_offsets_.data(), out_neighbors_.data(), n_, device_from_env(), &h));
+  check(pprg_graph_create(off_.data(), nbr_.data(), n_, device_from_env(), &h));
   dev_.reset(h, pprg_graph_destroy);
   for (NodeId v = 0; v < n_; ++v)
-    if (out_degree(v) == 0) dead_ends_.push_back(v);
+    if (is_dead_end(v)) dead_.push_back(v);
 }
 
 void Graph::validate() const {  // the device validated at construction (graph.cpp:24-34)
-  if (out_offsets_[0] != 0) throw std::runtime_error("graph: offsets must start at 0");
+  if (off_[0] != 0) throw std::runtime_error("graph: offsets must start at 0");
 }
 
 Graph build_graph_from_edges(const std::vector<std::pair<std::uint64_t, std::uint64_t>>& edges) {
