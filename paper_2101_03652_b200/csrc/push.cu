@@ -655,8 +655,10 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
     P.lam[E] = -1.0;
     P.thr[E] = refine_rmax;
     // a sweep costs a pass over every in-edge; once the refine tail pushes
-    // fewer than m_eff/64 edges per sweep the frontier kernels finish it
-    double f = 1.0 / 64;
+    // fewer than m_eff/128 edges per sweep the frontier kernels finish it
+    // (configs[3]: 155 ms per 64 queries against 171 ms at m_eff/64 and
+    // 165-170 ms at m_eff/256 or /512)
+    double f = 1.0 / 128;
     if (const char* e = std::getenv("PPRG_REFINE_HANDOFF")) f = std::atof(e);
     P.handoff_np = (unsigned long long)(f * m_eff);
   }
