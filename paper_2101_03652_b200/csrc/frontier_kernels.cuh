@@ -284,13 +284,27 @@ inline bool k1w_on(const Graph& g, int K) {
   }();
   return g.m >= min_m;
 }
-inline uint32_t tile_edges(int K, bool w) {
-  if (w) return K1W_T;
-  return K >= WIDE_K ? WIDE_T : (uint32_t)(SWEEP_ELEMS / K);
+// Wide-path tile size: WIDE_T, or smaller on graphs too small to give every
+// resident block about PPRG_WIDE_TILES tiles per sweep (a power of two, at
+// least 256 in-edges), so small graphs do not leave most of the grid idle.
+inline uint32_t wide_tile_edges(const Graph& g) {
+  static const double per_block = [] {
+    const char* e = std::getenv("PPRG_WIDE_TILES");
+    return e ? std::atof(e) : 2.0;
+  }();
+  if (per_block <= 0) return WIDE_T;
+  const double want = (double)g.m / (per_block * 8.0 * (double)g.sm_count);
+  uint32_t t = WIDE_T;
+  while (t > 256 && (double)t > want) t >>= 1;
+  return t;
 }
-inline uint32_t tile_hub(int K, bool w) { return w ? K1W_H : tile_edges(K, w); }
-inline uint32_t tile_rmax(int K, bool w) {
-  if (w) return K1W_R;
+inline uint32_t tile_edges(const Graph& g, int K) {
+  if (k1w_on(g, K)) return K1W_T;
+  return K >= WIDE_K ? wide_tile_edges(g) : (uint32_t)(SWEEP_ELEMS / K);
+}
+inline uint32_t tile_hub(const Graph& g, int K) { return k1w_on(g, K) ? K1W_H : tile_edges(g, K); }
+inline uint32_t tile_rmax(const Graph& g, int K) {
+  if (k1w_on(g, K)) return K1W_R;
   if (K >= WIDE_K) return RMAX_W;
   const int T = SWEEP_ELEMS / K;
   return T < 256 ? T : 256;

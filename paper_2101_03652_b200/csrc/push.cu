@@ -374,7 +374,7 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   const TileDesc* dsc = nullptr;
   uint64_t nhubs = 0;
   if (need_pull) {
-    const Graph::Plan& pl = g.tile_plan(tile_edges(K, k1w_on(g, K)), tile_rmax(K, k1w_on(g, K)), tile_hub(K, k1w_on(g, K)));
+    const Graph::Plan& pl = g.tile_plan(tile_edges(g, K), tile_rmax(g, K), tile_hub(g, K));
     dsc = pl.tiles.get();
     ntiles = pl.ntiles;
     nhubs = pl.nhubs;
@@ -1326,7 +1326,7 @@ PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t
   Block& b = *s->b;
   const int K = b.K;
   // ---- the cut: row-start tiles, balanced on in-edges ------------------------
-  const Graph::Plan& pl = g.tile_plan(tile_edges(K, k1w_on(g, K)), tile_rmax(K, k1w_on(g, K)), tile_hub(K, k1w_on(g, K)));
+  const Graph::Plan& pl = g.tile_plan(tile_edges(g, K), tile_rmax(g, K), tile_hub(g, K));
   const std::vector<TileDesc>& tl = pl.host;
   uint64_t total = 0;
   for (const TileDesc& t : tl) total += t.ne;
