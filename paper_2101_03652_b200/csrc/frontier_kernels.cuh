@@ -78,7 +78,7 @@ __device__ __forceinline__ void relax_scatter(const FrontierParams& P, uint32_t 
 // (queue size <= limit before the pop, push.cpp:38), claim r (the pop,
 // push.cpp:40-43), x += r, then scatter (1-a) r / deg_eff to the effective
 // out-neighbours with fp64 atomics, 4 independent atomics per lane in flight.
-// Entries with more than HEAVY_DEG out-edges are queued for k_frontier_heavy,
+// Entries with more than HEAVY_DEG out-edges are queued for k_frontier_heavy_chunks,
 // so a hub never serialises one warp. Per-column counters accumulate in
 // shared memory and are flushed once per block.
 __global__ void __launch_bounds__(256) k_frontier(const __grid_constant__ FrontierParams P,
@@ -147,31 +147,34 @@ __global__ void __launch_bounds__(256) k_frontier(const __grid_constant__ Fronti
   }
 }
 
-// The scatter of heavy entries, one thread per out-edge over all of them.
-__global__ void __launch_bounds__(256) k_frontier_heavy(const __grid_constant__ FrontierParams P,
-                                                        const HeavyEntry* heavy,
-                                                        const unsigned long long* prefix,
-                                                        unsigned nheavy, unsigned long long total) {
-  for (unsigned long long e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-       e - threadIdx.x < total; e += (uint64_t)gridDim.x * blockDim.x) {
-    const bool ok = e < total;
-    uint32_t t = 0;
-    int c = 0;
-    double share = 0.0;
-    if (ok) {
-      unsigned lo = 0, hi = nheavy;  // last h with prefix[h] <= e
-      while (lo + 1 < hi) {
-        const unsigned mid = (lo + hi) >> 1;
-        if (prefix[mid] <= e) lo = mid; else hi = mid;
-      }
-      const HeavyEntry h = heavy[lo];
-      c = (int)h.c;
-      share = h.share;
-      t = __ldg(P.nbr + h.begin + (e - prefix[lo]));
+// The scatter of heavy entries by chunks of HEAVY_CHUNK out-edges of one entry
+// (host-built list: no per-edge search for the owning entry), a block per
+// chunk, four neighbour ids per thread loaded before the first atomic. Every
+// lane of a chunk shares the entry's column, so appends group the whole warp.
+constexpr uint32_t HEAVY_CHUNK = 1024;
+struct HeavyChunk {
+  uint32_t h;      // heavy entry
+  uint32_t first;  // first out-edge of the chunk, relative to the entry
+};
+
+__global__ void __launch_bounds__(256) k_frontier_heavy_chunks(const __grid_constant__ FrontierParams P,
+                                                               const HeavyEntry* heavy,
+                                                               const HeavyChunk* chunks,
+                                                               unsigned nchunks) {
+  for (unsigned ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const HeavyChunk k = chunks[ch];
+    const HeavyEntry e = heavy[k.h];
+    const uint32_t end = e.deg - k.first < HEAVY_CHUNK ? e.deg : k.first + HEAVY_CHUNK;
+    const uint32_t q0 = k.first + threadIdx.x;
+    uint32_t t[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t q = q0 + 256u * i;
+      t[i] = q < end ? __ldg(P.nbr + e.begin + q) : 0xFFFFFFFFu;
     }
-    // all lanes of a ballot group must share the column: group by column
-    const unsigned same = __match_any_sync(0xffffffffu, ok ? c : -1);
-    if (ok) relax_scatter(P, t, c, share, true, same);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      relax_scatter(P, t[i], (int)e.c, e.share, t[i] != 0xFFFFFFFFu, 0xffffffffu);
   }
 }
 

@@ -70,7 +70,7 @@ struct Workspace {
   DevBuf<HeavyEntry> heavy;
   DevBuf<unsigned> heavy_cnt;
   DevBuf<unsigned> col_stop;
-  DevBuf<unsigned long long> heavy_prefix;
+  DevBuf<unsigned long long> heavy_chunks;
   unsigned level_tag = 0;
   uint64_t ntiles_alloc = 0;
 };
@@ -566,14 +566,17 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     if (nheavy) {
       std::vector<HeavyEntry> hv(nheavy);
       d2h_small(hv.data(), w.heavy.get(), sizeof(HeavyEntry) * nheavy, st);
-      std::vector<unsigned long long> pre(nheavy + 1, 0);
-      for (unsigned h = 0; h < nheavy; ++h) pre[h + 1] = pre[h] + hv[h].deg;
-      w.heavy_prefix.ensure(nheavy + 1);
-      PPRG_CUDA(cudaMemcpyAsync(w.heavy_prefix.get(), pre.data(), 8 * (nheavy + 1),
+      // chunks of HEAVY_CHUNK out-edges per heavy entry (the kernel's work list)
+      std::vector<HeavyChunk> chunks;
+      for (unsigned h = 0; h < nheavy; ++h)
+        for (uint32_t f = 0; f < hv[h].deg; f += HEAVY_CHUNK) chunks.push_back(HeavyChunk{h, f});
+      const unsigned nch = (unsigned)chunks.size();
+      w.heavy_chunks.ensure((sizeof(HeavyChunk) * nch + 7) / 8);
+      PPRG_CUDA(cudaMemcpyAsync(w.heavy_chunks.get(), chunks.data(), sizeof(HeavyChunk) * nch,
                                 cudaMemcpyHostToDevice, st));
-      k_frontier_heavy<<<grid_for(pre[nheavy]), 256, 0, st>>>(F, w.heavy.get(),
-                                                              w.heavy_prefix.get(), nheavy,
-                                                              pre[nheavy]);
+      const unsigned cap = (unsigned)g.sm_count * 8;
+      k_frontier_heavy_chunks<<<nch < cap ? nch : cap, 256, 0, st>>>(
+          F, w.heavy.get(), reinterpret_cast<const HeavyChunk*>(w.heavy_chunks.get()), nch);
       PPRG_CUDA(cudaGetLastError());
       call->kernel_launches += 1;
     }
