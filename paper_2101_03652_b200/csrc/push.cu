@@ -557,7 +557,19 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     F.level_tag = next_tag();
     // live columns are contiguous in pre[] but their segments sit at c*n: the
     // kernel maps (c, pos) -> cur[c*n + pos]
-    k_frontier<<<grid_for(total * 32), 256, 0, st>>>(F, w.heavy.get(), w.heavy_cnt.get());
+    {
+      // grid-stride over the entries with at most PPRG_FRONTIER_BPS blocks per SM
+      // (0 = one warp per entry): fewer short-lived blocks and block barriers.
+      // 24 measured best: configs[2] local phase 8.5 -> 6.8 ms per 64-source
+      // block, configs[3] frontier 40.9 -> 35.7 ms per 64 queries.
+      static const int bps = [] {
+        const char* e = std::getenv("PPRG_FRONTIER_BPS");
+        return e ? std::atoi(e) : 24;
+      }();
+      unsigned grid = grid_for(total * 32);
+      if (bps > 0 && grid > (unsigned)(bps * g.sm_count)) grid = (unsigned)(bps * g.sm_count);
+      k_frontier<<<grid, 256, 0, st>>>(F, w.heavy.get(), w.heavy_cnt.get());
+    }
     PPRG_CUDA(cudaGetLastError());
     call->kernel_launches += 1;
     unsigned nheavy = 0;
