@@ -138,7 +138,16 @@ __global__ void k_mc_entries(const __grid_constant__ McParams P, uint64_t* big,
     const uint32_t v = (uint32_t)(i / P.K);
     const int c = (int)(i % P.K);
     const double contribution = P.res[i] / (double)wc;  // speedppr.cpp:41
-    for (uint32_t kk = 0; kk < (uint32_t)wc; ++kk)
+    // four walks' terminals resolved before their adds (independent loads in flight)
+    uint32_t kk = 0;
+    for (; kk + 4 <= (uint32_t)wc; kk += 4) {
+      uint32_t t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = mc_terminal(P, v, c, kk + j);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) atomicAdd(P.est + (uint64_t)t[j] * P.K + c, contribution);
+    }
+    for (; kk < (uint32_t)wc; ++kk)
       atomicAdd(P.est + (uint64_t)mc_terminal(P, v, c, kk) * P.K + c, contribution);
   }
 }
