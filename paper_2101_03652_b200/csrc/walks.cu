@@ -164,7 +164,15 @@ __global__ void k_mc_big(const __grid_constant__ McParams P, const uint64_t* big
     const int c = (int)(i % P.K);
     const unsigned long long wc = P.cnt[i];
     const double contribution = P.res[i] / (double)wc;
-    for (unsigned long long kk = lane; kk < wc; kk += 32)
+    unsigned long long kk = lane;
+    for (; kk + 96 < wc; kk += 128) {  // four walks per lane resolved before their adds
+      uint32_t t[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = mc_terminal(P, v, c, (uint32_t)(kk + 32 * j));
+#pragma unroll
+      for (int j = 0; j < 4; ++j) atomicAdd(P.est + (uint64_t)t[j] * P.K + c, contribution);
+    }
+    for (; kk < wc; kk += 32)
       atomicAdd(P.est + (uint64_t)mc_terminal(P, v, c, (uint32_t)kk) * P.K + c, contribution);
   }
 }
