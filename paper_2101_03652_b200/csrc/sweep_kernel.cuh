@@ -133,7 +133,15 @@ struct BlockAcc {  // shared, per column
   unsigned long long* np;
   unsigned long long* nn;
   unsigned long long* et;
+  // two-columns-per-lane decisions (K = 32, 64): node pushes and edge pushes
+  // packed into one 64-bit add (nn << 40 | np; per block and sweep np < 2^40 and
+  // nn < 2^24, since n <= 6.2M at these widths), and dead-end pushes counted
+  // separately (et = np - dead) - one 64-bit shared atomic (a CAS loop on
+  // sm_100) per push instead of three
+  unsigned long long* pk;
+  unsigned* nd;
 };
+constexpr int PK_SHIFT = 40;
 
 // The per-(row, column) decision: push form of push.cpp:182-193 in pull
 // representation, the PowItr update of push.cpp:90-99, or the final explicit
@@ -698,9 +706,10 @@ __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* c
       decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
       if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
       if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
-      if (b2.np) atomicAdd(&ba.np[cc], b2.np);
-      if (b2.nn) atomicAdd(&ba.nn[cc], b2.nn);
-      if (b2.et) atomicAdd(&ba.et[cc], b2.et);
+      if (b2.nn) {
+        atomicAdd(&ba.pk[cc], (b2.nn << PK_SHIFT) | b2.np);
+        if (!b2.et) atomicAdd(&ba.nd[cc], 1u);  // a dead end's push (np 1, no out-edges)
+      }
     }
   }
 }
@@ -875,7 +884,9 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
     cs[tid].pushes = P.init[tid].pushes;
   }
   __syncthreads();
-  const BlockAcc ba{sh_push, sh_d, sh_np, sh_nn, sh_et};
+  __shared__ unsigned long long sh_pk[K];
+  __shared__ unsigned sh_nd[K];
+  const BlockAcc ba{sh_push, sh_d, sh_np, sh_nn, sh_et, sh_pk, sh_nd};
   unsigned long long gen = 0;
   const int c = tid % K;
   for (uint32_t sweep = 0;; ++sweep) {
@@ -895,6 +906,8 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
       sh_np[tid] = 0;
       sh_nn[tid] = 0;
       sh_et[tid] = 0;
+      sh_pk[tid] = 0;
+      sh_nd[tid] = 0;
     }
     __syncthreads();
     if (!sh_any) break;
@@ -966,6 +979,12 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
       }
     }
     __syncthreads();
+    if (tid < K && sh_pk[tid]) {  // unpack the two-columns-per-lane counters
+      const unsigned long long np = sh_pk[tid] & ((1ull << PK_SHIFT) - 1);
+      sh_np[tid] += np;
+      sh_nn[tid] += sh_pk[tid] >> PK_SHIFT;
+      sh_et[tid] += np - sh_nd[tid];
+    }
     if (tid < K) {
       if (sh_push[tid] != 0.0) atomicAdd(&ctl->pushed[buf][tid], sh_push[tid]);
       if (sh_d[tid] != 0.0) atomicAdd(&ctl->dsum[buf][tid], sh_d[tid]);
