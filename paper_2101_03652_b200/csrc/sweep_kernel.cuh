@@ -142,6 +142,9 @@ struct BlockAcc {  // shared, per column
   unsigned* nd;
 };
 constexpr int PK_SHIFT = 40;
+#ifndef PPRG_PUSH_REG
+#define PPRG_PUSH_REG 1
+#endif
 
 // The per-(row, column) decision: push form of push.cpp:182-193 in pull
 // representation, the PowItr update of push.cpp:90-99, or the final explicit
@@ -692,7 +695,8 @@ __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* c
                                             const double* thr_cur, uint32_t u, const double* s,
                                             const double* xo, const double* rc, uint32_t dg,
                                             double inv, const double* yg, double* rnxt,
-                                            double* ynxt, Acc& a, const BlockAcc& ba) {
+                                            double* ynxt, Acc& a, const BlockAcc& ba,
+                                            double* pacc = nullptr) {
   constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   const int kc = (threadIdx.x & 31) % KC;
@@ -704,7 +708,8 @@ __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* c
       Acc b2;
       const int cc = kc * CPL + q;
       decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
-      if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
+      if (PPRG_PUSH_REG && pacc) pacc[q] += b2.push;  // flushed once per tile
+      else if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
       if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
       if (b2.nn) {
         atomicAdd(&ba.pk[cc], (b2.nn << PK_SHIFT) | b2.np);
@@ -751,6 +756,9 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int es0 = lane < KC;  // lanes holding the reduced sums
   const int kc = lane % KC;
+  double pacc[CPL];  // pushed mass of my columns in this tile (PPRG_PUSH_REG)
+#pragma unroll
+  for (int q = 0; q < CPL; ++q) pacc[q] = 0.0;
   const uint32_t nr = d.nr;
   for (uint32_t t = tid; t <= nr; t += NT) soff[t] = __ldg(P.in_off + d.r0 + t);
   for (uint32_t t = tid; t < nr; t += NT) {
@@ -791,7 +799,7 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
         rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
       }
       warp_row_sum<K>(P, yg, b, e, s, true, ids);
-      if (es0) decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
+      if (es0) decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
     }
     r = rn;
     ids = ids_n;
@@ -821,10 +829,14 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
         for (int w = 0; w < NW; ++w) t += spart[w * K + kc * CPL + q];
         s[q] = t;
       }
-      decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba);
+      decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
     }
     __syncthreads();
   }
+  if (PPRG_PUSH_REG && es0)
+#pragma unroll
+    for (int q = 0; q < CPL; ++q)
+      if (pacc[q] != 0.0) atomicAdd(&ba.push[kc * CPL + q], pacc[q]);
   __syncthreads();
   if (tid == 0) {
     *rowctr = 0;
