@@ -229,24 +229,38 @@ struct GridBarrier {
   unsigned long long flag[16];
 };
 
+// The barrier's release (before arriving) and acquire (after the flag) fences:
+// acq_rel at gpu scope is what the arrival/flag chain needs (PPRG_BAR_SC=1:
+// the sequentially consistent __threadfence instead).
+#ifndef PPRG_BAR_SC
+#define PPRG_BAR_SC 0
+#endif
+__device__ __forceinline__ void bar_fence() {
+#if PPRG_BAR_SC
+  __threadfence();
+#else
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
+}
+
 __device__ __forceinline__ void grid_barrier2(GridBarrier* gb, unsigned long long gen) {
   __syncthreads();
   if (threadIdx.x == 0) {
     const unsigned ng = gridDim.x < 32 ? gridDim.x : 32;
     const unsigned g = blockIdx.x % ng;
     const unsigned long long gsize = gridDim.x / ng + (g < gridDim.x % ng ? 1 : 0);
-    __threadfence();
+    bar_fence();
     const unsigned long long old = atomicAdd(&gb->grp[g][0], 1ull);
     if (old + 1 == gsize * gen) {
-      __threadfence();
+      bar_fence();
       const unsigned long long o2 = atomicAdd(&gb->top[0], 1ull);
       if (o2 + 1 == (unsigned long long)ng * gen) {
-        __threadfence();
+        bar_fence();
         atomicExch(&gb->flag[0], gen);
       }
     }
     while (ld_acquire(&gb->flag[0]) < gen) __nanosleep(20);
-    __threadfence();
+    bar_fence();
   }
   __syncthreads();
 }

@@ -106,6 +106,8 @@ struct ColSh {
   double r_sum, D;
   int epoch, done;
   unsigned sweeps;
+  uint32_t src;  // the column's source (a shared copy: P.src[c] with a per-lane c
+                 // would be a divergent, serialised constant-bank load)
   unsigned long long pushes;
 };
 
@@ -155,7 +157,7 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
                                        uint32_t dg, double inv, const double* yg, double* rnxt,
                                        double* ynxt, Acc& a) {
   const uint64_t ix = (uint64_t)u * K + c;
-  const bool is_src = u == P.src[c];
+  const bool is_src = u == cs[c].src;
   const double alpha = P.alpha, oma = 1.0 - P.alpha;
   if constexpr (MODE == M_POWERPUSH) {
     if (cs[c].done) return;
@@ -894,6 +896,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
     cs[tid].done = P.init[tid].done;
     cs[tid].sweeps = P.init[tid].sweeps;
     cs[tid].pushes = P.init[tid].pushes;
+    cs[tid].src = P.src[tid];
   }
   __syncthreads();
   __shared__ unsigned long long sh_pk[K];
