@@ -132,7 +132,8 @@ int pprg_power_push(pprg_graph* g, const uint32_t* sources, uint32_t k, double a
  * GPU. Part p of nparts owns the pull-sweep rows [node_lo, node_hi), cut at
  * row-aligned tiles so every part holds ~m/nparts in-edges (every part
  * computes the same cut). The caller moves data between parts:
- *   begin -> all-reduce(partial_sums, 2*64 doubles) -> start
+ *   begin -> (nparts > 1) broadcast part 0's x, resum -> all-reduce(partial_sums,
+ *   2*64 doubles) -> start
  *   while need_sweeps: all-gather y row slices [lo*C, hi*C) (C = columns)
  *                      -> sweep -> all-reduce(counters, 5*C doubles, device)
  *                      -> advance(summed counters, host) until done
@@ -165,6 +166,14 @@ int pprg_part_begin(pprg_graph* g, uint32_t nparts, uint32_t part, const uint32_
 int pprg_part_start(pprg_part* p, const double* summed, int* need_sweeps);
 /* device pointers: y [n * columns] (interleaved u*columns + c) and counters [5 * columns] */
 int pprg_part_buffers(pprg_part* p, double** y, uint32_t* columns, double** counters);
+/* The local queue phase (push.cpp:163-166) is level-synchronous with fp64
+ * atomics, so two parts running it need not stop in the same state. A
+ * multi-part query therefore adopts ONE part's result: the caller copies
+ * part 0's x [n * columns] (device pointer from pprg_part_local_x) into every
+ * other part's x, then calls pprg_part_resum to recompute that part's
+ * partial_sums before the all-reduce that feeds pprg_part_start. */
+int pprg_part_local_x(pprg_part* p, double** x);
+int pprg_part_resum(pprg_part* p, double* partial_sums);
 /* one global sweep over this part's rows; local_counters (host, optional) gets a copy */
 int pprg_part_sweep(pprg_part* p, double* local_counters);
 int pprg_part_advance(pprg_part* p, const double* summed, int* done);

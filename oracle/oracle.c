@@ -4,6 +4,7 @@
 #include "oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -640,4 +641,126 @@ int og_speedppr_query(const uint64_t* off, const uint32_t* nbr, uint64_t n, uint
   *pushes = st.pushes;
   free(residue);
   return rc;
+}
+
+/* ========================================================================
+ * Synthetic R-MAT input (SURVEY 8(d) "Synthetic inputs"), restated on the
+ * host so the reference arm of bench.py never needs the GPU library to make
+ * its input. The definition is the product's (pprg_graph_generate_rmat,
+ * graph.cu k_rmat + sort_clean + build_from_sorted_keys) and is pinned to it
+ * bit-for-bit by tests/test_gpu_configs.py:
+ *   edge i descends `scale` levels; level l uses 32-bit word (l mod 4) of
+ *   Philox4x32-10(ctr = (i_lo, i_hi, 'RMAT', l/4), key = seed); p = w/2^32
+ *   selects quadrant a (0,0) / b (0,1) / c (1,0) / d (1,1) by p < a, < a+b,
+ *   < a+b+c. Edges are sorted by (u, v), duplicates and self-loops dropped,
+ *   surviving endpoint ids relabelled by rank (graph.cpp:40-51 semantics) and
+ *   the CSR built with each row in ascending neighbour order.
+ * ======================================================================== */
+typedef struct {
+  uint64_t lo, hi, seed;
+  int scale;
+  double a, ab, abc;
+  uint64_t* keys;
+} rmat_job;
+
+static void* rmat_worker(void* arg) {
+  const rmat_job* j = (const rmat_job*)arg;
+  const uint32_t key[2] = {(uint32_t)j->seed, (uint32_t)(j->seed >> 32)};
+  const int s = j->scale;
+  for (uint64_t i = j->lo; i < j->hi; ++i) {
+    uint32_t u = 0, v = 0, o[4] = {0, 0, 0, 0};
+    for (int l = 0; l < s; ++l) {
+      if ((l & 3) == 0) {
+        const uint32_t ctr[4] = {(uint32_t)i, (uint32_t)(i >> 32), 0x524D4154u, (uint32_t)(l >> 2)};
+        og_philox4x32_10(ctr, key, o);
+      }
+      const double p = (double)o[l & 3] * 0x1.0p-32;
+      const uint32_t bu = p >= j->ab, bv = (p >= j->a && p < j->ab) || p >= j->abc;
+      u = (u << 1) | bu;
+      v = (v << 1) | bv;
+    }
+    j->keys[i] = ((uint64_t)u << s) | v; /* compact (u, v) key: 2*scale bits */
+  }
+  return NULL;
+}
+
+/* LSD radix sort of `cnt` keys of `bits` bits, 16 bits per pass. */
+static void radix_sort_u64(uint64_t* keys, uint64_t* tmp, uint64_t cnt, int bits) {
+  uint64_t* hist = (uint64_t*)malloc(sizeof(uint64_t) << 16);
+  uint64_t* const first = keys;
+  for (int shift = 0; shift < bits; shift += 16) {
+    memset(hist, 0, sizeof(uint64_t) << 16);
+    for (uint64_t i = 0; i < cnt; ++i) ++hist[(keys[i] >> shift) & 0xFFFF];
+    uint64_t run = 0;
+    for (int d = 0; d < 65536; ++d) {
+      const uint64_t c = hist[d];
+      hist[d] = run;
+      run += c;
+    }
+    for (uint64_t i = 0; i < cnt; ++i) tmp[hist[(keys[i] >> shift) & 0xFFFF]++] = keys[i];
+    uint64_t* t = keys;
+    keys = tmp;
+    tmp = t;
+  }
+  if (keys != first) memcpy(first, keys, 8 * cnt); /* result in the caller's first buffer */
+  free(hist);
+}
+
+int og_generate_rmat(int scale, uint64_t edge_factor, double a, double b, double c, uint64_t seed,
+                     int threads, uint64_t* off_out, uint32_t* nbr_out, uint64_t* n_out,
+                     uint64_t* m_out) {
+  if (scale < 1 || scale > 31) return 1;
+  if (!(a >= 0 && b >= 0 && c >= 0 && a + b + c <= 1.0)) return 1;
+  const uint64_t draws = edge_factor << scale, id_space = 1ull << scale;
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  uint64_t* keys = (uint64_t*)malloc(8 * (draws ? draws : 1));
+  uint64_t* tmp = (uint64_t*)malloc(8 * (draws ? draws : 1));
+  if (!keys || !tmp) {
+    free(keys);
+    free(tmp);
+    return 2;
+  }
+  pthread_t tid[256];
+  rmat_job job[256];
+  for (int t = 0; t < threads; ++t) {
+    job[t] = (rmat_job){draws * t / threads, draws * (t + 1) / threads, seed, scale, a, a + b,
+                        a + b + c, keys};
+    pthread_create(&tid[t], NULL, rmat_worker, &job[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+  radix_sort_u64(keys, tmp, draws, 2 * scale);
+  const uint64_t vmask = id_space - 1;
+  uint64_t cnt = 0; /* unique, no self-loops, compacted in place */
+  for (uint64_t i = 0; i < draws; ++i) {
+    const uint64_t k = keys[i];
+    if ((i == 0 || keys[i - 1] != k) && (k >> scale) != (k & vmask)) tmp[cnt++] = k;
+  }
+  free(keys);
+  if (cnt == 0) {
+    free(tmp);
+    return 2; /* "graph is empty after cleaning" */
+  }
+  uint32_t* rank = (uint32_t*)calloc(id_space + 1, 4);
+  for (uint64_t i = 0; i < cnt; ++i) {
+    rank[tmp[i] >> scale] = 1;
+    rank[tmp[i] & vmask] = 1;
+  }
+  uint64_t n = 0;
+  for (uint64_t v = 0; v <= id_space; ++v) {
+    const uint32_t p = rank[v];
+    rank[v] = (uint32_t)n;
+    n += p;
+  }
+  memset(off_out, 0, 8 * (n + 1));
+  for (uint64_t i = 0; i < cnt; ++i) {
+    ++off_out[rank[tmp[i] >> scale] + 1];
+    nbr_out[i] = rank[tmp[i] & vmask];
+  }
+  for (uint64_t v = 0; v < n; ++v) off_out[v + 1] += off_out[v];
+  free(rank);
+  free(tmp);
+  *n_out = n;
+  *m_out = cnt;
+  return 0;
 }

@@ -55,6 +55,13 @@ uint64_t og_dead_ends(const uint64_t* off, uint64_t n, uint32_t* out /* may be N
 int og_random_graph(uint32_t n, uint32_t min_out, uint32_t max_out, uint64_t seed,
                     uint64_t* off_out, uint32_t* nbr_out, uint64_t* m_out);
 
+/* Synthetic R-MAT (the product's generator definition, restated on the host;
+ * see oracle.c). off_out needs 2^scale+1 entries, nbr_out edge_factor<<scale.
+ * Returns 1 on bad parameters, 2 on an empty graph or allocation failure. */
+int og_generate_rmat(int scale, uint64_t edge_factor, double a, double b, double c, uint64_t seed,
+                     int threads, uint64_t* off_out, uint32_t* nbr_out, uint64_t* n_out,
+                     uint64_t* m_out);
+
 /* ---- push engines: push.cpp ------------------------------------------- */
 typedef struct {
   double r_sum;

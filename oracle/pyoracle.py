@@ -108,6 +108,9 @@ class Oracle:
         L.og_philox_walk.restype = C.c_uint32
         L.og_philox_build_index.argtypes = [u64p, u32p, C.c_uint64, C.c_double, C.c_uint64, u32p]
         L.og_build_graph_from_edges.argtypes = [u64p, C.c_uint64, u64p, u32p, C.POINTER(C.c_uint64)]
+        L.og_generate_rmat.argtypes = [C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double,
+                                       C.c_uint64, C.c_int, vp, vp, C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64)]
         L.og_random_graph.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64, vp, vp,
                                       C.POINTER(C.c_uint64)]
         L.og_push_once.argtypes = [u64p, u32p, C.c_uint64, C.c_uint32, C.c_double, f64p, f64p,
@@ -165,6 +168,17 @@ class Oracle:
         n = C.c_uint64()
         _check(self.L.og_build_graph_from_edges(pairs.reshape(-1), cnt, off, nbr, C.byref(n)))
         return CSR(off[: n.value + 1].copy(), nbr)
+
+    def generate_rmat(self, scale, edge_factor, seed, a=0.57, b=0.19, c=0.19, threads=None) -> CSR:
+        """Host restatement of pprg_graph_generate_rmat (bit-exact; see oracle.c)."""
+        threads = threads or os.cpu_count() or 1
+        off = np.zeros((1 << scale) + 1, np.uint64)
+        nbr = np.empty(max(edge_factor << scale, 1), np.uint32)
+        n, m = C.c_uint64(), C.c_uint64()
+        _check(self.L.og_generate_rmat(scale, edge_factor, a, b, c, seed, threads, off.ctypes.data,
+                                       nbr.ctypes.data, C.byref(n), C.byref(m)),
+               "rmat generation")
+        return CSR(off[: n.value + 1].copy(), nbr[: m.value].copy())
 
     def random_graph(self, n, min_out, max_out, seed) -> CSR:
         m = C.c_uint64()

@@ -487,6 +487,20 @@ int pprg_part_buffers(pprg_part* p, double** y, uint32_t* columns, double** coun
   });
 }
 
+int pprg_part_local_x(pprg_part* p, double** x) {
+  return guard([&] {
+    require(p && x, "partition: null argument");
+    *x = pprg::part_x(p->s);
+  });
+}
+
+int pprg_part_resum(pprg_part* p, double* partial_sums) {
+  return guard([&] {
+    require(p && partial_sums, "partition: null argument");
+    pprg::part_resum(p->s, partial_sums);
+  });
+}
+
 int pprg_part_sweep(pprg_part* p, double* local_counters) {
   return guard([&] {
     require(p != nullptr, "partition: null argument");

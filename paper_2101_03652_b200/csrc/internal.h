@@ -202,6 +202,8 @@ void part_finish(PartSession* s, double* reserve, double* residue, bool on_devic
 void part_stats(const PartSession* s, ColumnStats* cols, CallStats* call);
 double* part_y(PartSession* s, uint32_t* K);
 double* part_counters(PartSession* s);
+double* part_x(PartSession* s);
+void part_resum(PartSession* s, double* partial_host);
 int part_device(const PartSession* s);
 void part_set_peers(PartSession* s, double* const* peer_y, uint32_t npeers);
 void part_destroy(PartSession* s);

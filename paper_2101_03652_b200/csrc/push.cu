@@ -1562,6 +1562,28 @@ double* part_y(PartSession* s, uint32_t* K) {
   return s->b->w.y0.get();
 }
 double* part_counters(PartSession* s) { return s->counters.get(); }
+double* part_x(PartSession* s) { return s->b->w.x.get(); }
+
+// After the caller overwrote x with another part's local-phase result (the
+// local phase is run once and its x broadcast, so every part starts from one
+// consistent push state), recompute this part's share of sum(x) and of the
+// dead-end sum.
+void part_resum(PartSession* s, double* partial_host) {
+  Graph& g = *s->g;
+  DeviceGuard dg(g.device);
+  std::lock_guard<std::mutex> lk(g.mu);
+  Block& b = *s->b;
+  const int K = b.K;
+  cudaStream_t st = g.stream;
+  PPRG_CUDA(cudaMemsetAsync(s->sums.get(), 0, 16 * KMAX, st));
+  if (s->hi > s->lo)
+    k_part_sums<<<grid_reduce((s->hi - s->lo) * K), 256, 0, st>>>(b.w.x.get(), g.deg.get(), s->lo,
+                                                               s->hi, K, s->sums.get());
+  PPRG_CUDA(cudaGetLastError());
+  PPRG_CUDA(cudaMemcpyAsync(partial_host, s->sums.get(), 16 * KMAX, cudaMemcpyDeviceToHost, st));
+  PPRG_CUDA(cudaStreamSynchronize(st));
+  s->call.kernel_launches += 1;
+}
 int part_device(const PartSession* s) { return s->g->device; }
 
 void part_destroy(PartSession* s) {

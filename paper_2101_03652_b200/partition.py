@@ -5,7 +5,8 @@ holds ~m/P in-edges). The engine's per-part primitives are the C-ABI
 pprg_part_* sessions (include/pprg.h); this module is the exchange between
 them, over NCCL on GPUs (or gloo for the CPU protocol tests):
 
-    begin  -> all_reduce(sum x, sum dead-end x)   -> start (identical epoch state)
+    begin  -> broadcast part 0's local-phase x, resum
+           -> all_reduce(sum x, sum dead-end x)   -> start (identical epoch state)
     sweep loop:  broadcast every part's y row slice (all-gather-v of y)
                  -> sweep own rows -> all_reduce(sweep counters) -> advance
     finish -> all_reduce(residue sums) = exact r_sum per source
@@ -58,6 +59,8 @@ def _bind(L):
     L.pprg_part_start.argtypes = [vp, vp, C.POINTER(C.c_int)]
     L.pprg_part_buffers.argtypes = [vp, C.POINTER(vp), C.POINTER(C.c_uint32), C.POINTER(vp)]
     L.pprg_part_sweep.argtypes = [vp, vp]
+    L.pprg_part_local_x.argtypes = [vp, C.POINTER(vp)]
+    L.pprg_part_resum.argtypes = [vp, vp]
     L.pprg_part_advance.argtypes = [vp, vp, C.POINTER(C.c_int)]
     L.pprg_part_finish.argtypes = [vp, vp, vp, C.c_uint32, vp]
     L.pprg_part_stats.argtypes = [vp, vp, vp]
@@ -151,6 +154,18 @@ class GpuPart:
         self.columns, self._y, self._cnt = cols.value, y.value, cnt.value
         return partial
 
+    def x_view(self):
+        """This part's local-phase state x [n * columns] (device)."""
+        x = C.c_void_p()
+        _check(_lib().pprg_part_local_x(self.h, C.byref(x)))
+        return _device_view(x.value, self.n * self.columns, self.g.device)
+
+    def resum(self) -> np.ndarray:
+        """Partial sums of this part after x was overwritten (adopted local phase)."""
+        partial = np.zeros(2 * KMAX, np.float64)
+        _check(_lib().pprg_part_resum(self.h, _p(partial)))
+        return partial
+
     def start(self, summed: np.ndarray) -> bool:
         need = C.c_int()
         s = np.ascontiguousarray(summed, np.float64)
@@ -240,6 +255,11 @@ def _open_peer_buffers(part, group, dev):
     return ptrs
 
 
+def ranks_of(group, world):
+    import torch.distributed as dist
+    return [dist.get_global_rank(group, p) if group is not None else p for p in range(world)]
+
+
 def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None,
                     fused: bool = False) -> PartitionResult:
     """Drive one part through the exchange protocol with torch.distributed.
@@ -260,6 +280,17 @@ def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None,
         return t.cpu().numpy()
 
     partial = part.begin()
+    if world > 1:
+        # one local phase for all parts: rank 0's x (the level-synchronous
+        # queue phase need not stop in the same state on every rank)
+        x = part.x_view()
+        if on_gpu:
+            dist.broadcast(x, src=ranks_of(group, world)[0], group=group)
+        else:
+            xc = x.cpu()
+            dist.broadcast(xc, src=ranks_of(group, world)[0], group=group)
+            x.copy_(xc)
+        partial = part.resum()
     peers = _open_peer_buffers(part, group, dev) if fused else []
     if fused:
         part.set_peers(peers)
@@ -268,7 +299,7 @@ def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None,
     allb = [torch.empty_like(mine) for _ in range(world)]
     dist.all_gather(allb, mine, group=group)
     bounds = [(int(b[0]), int(b[1])) for b in allb]
-    ranks = [dist.get_global_rank(group, p) if group is not None else p for p in range(world)]
+    ranks = ranks_of(group, world)
     Cw = part.columns
     y = part.y_view()
 
@@ -286,6 +317,8 @@ def run_partitioned(part, group=None, comm_device=None, finish_kwargs=None,
     while need:
         part.sweep()
         cnt = part.counters_view()
+        if not on_gpu and cnt.is_cuda:  # gloo: reduce a host copy
+            cnt = cnt.cpu()
         dist.all_reduce(cnt, group=group)
         need = not part.advance(cnt.cpu().numpy())
         exchange()
@@ -309,7 +342,12 @@ def run_virtual_parts(g: _abi.Graph, nparts: int, sources: Sequence[int], alpha:
     import torch
     parts = [GpuPart(g, nparts, p, sources, alpha, lam, epoch_num, scan_threshold)
              for p in range(nparts)]
-    partial = sum(p.begin() for p in parts)
+    for p in parts:
+        p.begin()
+    x0 = parts[0].x_view()
+    for p in parts[1:]:  # one local phase for all parts (see run_partitioned)
+        p.x_view().copy_(x0)
+    partial = sum(p.resum() for p in parts)
     if fused:
         for p in parts:
             p.set_peers([q.y_ptr() for q in parts if q is not p])

@@ -50,6 +50,17 @@ class NumpyPart:
     def begin(self):
         return np.zeros(128)
 
+    def x_view(self):  # the adopted local-phase state (zero here: no queue phase)
+        import torch
+        return torch.from_numpy(self.x.reshape(-1))
+
+    def resum(self):
+        out = np.zeros(128)
+        xs = self.x[self.lo:self.hi]
+        out[:self.k] = xs.sum(axis=0)
+        out[64:64 + self.k] = xs[self.deg[self.lo:self.hi] == 0].sum(axis=0)
+        return out
+
     def start(self, summed):
         return self.rule.init(summed[:64], summed[64:128])
 
