@@ -43,6 +43,7 @@ class WalkIndex {
   friend WalkIndex build_index(const Graph&, double, std::uint64_t);
   friend WalkIndex load_index(const std::string&, const Graph&);
   friend WalkIndex load_index(const std::string&);
+  friend void save_index(const WalkIndex&, const std::string&);
   double alpha_ = 0;
   std::uint64_t seed_ = 0;
   std::vector<std::uint64_t> offsets_;

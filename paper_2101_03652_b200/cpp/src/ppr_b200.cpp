@@ -3,14 +3,18 @@
 // as the reference's exception types (invalid_argument / runtime_error /
 // logic_error).
 #include <algorithm>
+#include <bit>
 #include <charconv>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
+#include <iterator>
+#include <limits>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 
 #include "../../../include/pprg.h"
 #include "ppr/csv.hpp"
@@ -152,31 +156,6 @@ bool observed(const Graph& g, int algo, NodeId s, double alpha, double param, do
   return true;
 }
 
-void write_u64(std::ofstream& o, std::uint64_t v) {
-  char b[8];
-  for (int i = 0; i < 8; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
-  o.write(b, 8);
-}
-void write_u32(std::ofstream& o, std::uint32_t v) {
-  char b[4];
-  for (int i = 0; i < 4; ++i) b[i] = static_cast<char>((v >> (8 * i)) & 0xff);
-  o.write(b, 4);
-}
-std::uint64_t read_u64(std::ifstream& in) {
-  unsigned char b[8] = {};
-  in.read(reinterpret_cast<char*>(b), 8);
-  std::uint64_t v = 0;
-  for (int i = 0; i < 8; ++i) v |= static_cast<std::uint64_t>(b[i]) << (8 * i);
-  return v;
-}
-std::uint32_t read_u32(std::ifstream& in) {
-  unsigned char b[4] = {};
-  in.read(reinterpret_cast<char*>(b), 4);
-  std::uint32_t v = 0;
-  for (int i = 0; i < 4; ++i) v |= static_cast<std::uint32_t>(b[i]) << (8 * i);
-  return v;
-}
-
 }  // namespace
 
 // ---- graph.hpp ---------------------------------------------------------------
@@ -197,56 +176,58 @@ void Graph::validate() const {  // the device validated at construction (graph.c
   if (off_[0] != 0) throw std::runtime_error("graph: offsets must start at 0");
 }
 
-Graph build_graph_from_edges(const std::vector<std::pair<std::uint64_t, std::uint64_t>>& edges) {
-  if (edges.empty()) throw std::runtime_error("graph is empty after cleaning");
-  std::vector<std::uint64_t> flat(2 * edges.size());
-  for (std::size_t i = 0; i < edges.size(); ++i) {
-    flat[2 * i] = edges[i].first;
-    flat[2 * i + 1] = edges[i].second;
-  }
-  pprg_graph* h = nullptr;
-  check(pprg_graph_build_from_edges(flat.data(), edges.size(), device_from_env(), &h));
+Graph Graph::adopt(pprg_graph* h) {
+  Graph g;
+  g.dev_.reset(h, pprg_graph_destroy);
   std::uint64_t n = 0, m = 0, nd = 0;
   check(pprg_graph_info(h, &n, &m, &nd));
-  std::vector<std::uint64_t> off(n + 1);
-  std::vector<NodeId> nbr(m);
-  check(pprg_graph_export(h, off.data(), nbr.data(), nullptr));
-  pprg_graph_destroy(h);
-  return Graph(std::move(off), std::move(nbr));
+  g.n_ = static_cast<NodeId>(n);
+  g.m_ = m;
+  g.off_.resize(n + 1);
+  g.nbr_.resize(m);
+  g.dead_.resize(nd);
+  check(pprg_graph_export(h, g.off_.data(), g.nbr_.data(), g.dead_.data()));
+  return g;
 }
 
-void save_graph_cache(const Graph& g, const std::string& path) {  // graph.cpp:115-125
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
-  if (!out) throw std::runtime_error("cannot open for writing: " + path);
-  out.write("PPRG", 4);
-  out.put(1);
-  write_u64(out, g.n());
-  write_u64(out, g.m());
-  for (auto o : g.out_offsets()) write_u64(out, o);
-  for (auto u : g.out_neighbors()) write_u32(out, u);
-  if (!out) throw std::runtime_error("write failed: " + path);
+namespace {
+// Pairs -> the flat (u, v) u64 array the device builder takes; the sort,
+// relabel and stable scatter of graph.cpp:36-63 run on the GPU.
+Graph build_on_device(const std::uint64_t* flat, std::size_t pairs) {
+  if (pairs == 0) throw std::runtime_error("graph is empty after cleaning");
+  pprg_graph* h = nullptr;
+  check(pprg_graph_build_from_edges(flat, pairs, device_from_env(), &h));
+  return Graph::adopt(h);
+}
+}  // namespace
+
+Graph build_graph_from_edges(const std::vector<std::pair<std::uint64_t, std::uint64_t>>& edges) {
+  static_assert(sizeof(std::pair<std::uint64_t, std::uint64_t>) == 16);
+  return build_on_device(reinterpret_cast<const std::uint64_t*>(edges.data()), edges.size());
 }
 
-Graph load_graph_cache(const std::string& path) {  // graph.cpp:127-143
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw std::runtime_error("cannot open graph cache: " + path);
-  char magic[4];
-  if (!in.read(magic, 4) || std::memcmp(magic, "PPRG", 4) != 0)
-    throw std::runtime_error(path + ": not a graph cache (bad magic)");
-  if (in.get() != 1) throw std::runtime_error(path + ": unsupported graph cache version");
-  const std::uint64_t n = read_u64(in), m = read_u64(in);
-  std::vector<std::uint64_t> off(n + 1);
-  for (auto& o : off) o = read_u64(in);
-  std::vector<NodeId> nbr(m);
-  for (auto& u : nbr) u = read_u32(in);
-  if (!in) throw std::runtime_error(path + ": truncated graph cache");
-  return Graph(std::move(off), std::move(nbr));
+// PPRG files (graph.cpp:115-149 format: "PPRG", u8 version 1, n, m, offsets,
+// neighbours, little endian) are read and written by the engine straight
+// between the file and device memory through pinned staging buffers
+// (pprg_graph_load_cache / pprg_graph_save_cache), with the reference's checks
+// and messages; the host copies are then exported from the device.
+void save_graph_cache(const Graph& g, const std::string& path) {
+  check(pprg_graph_save_cache(g.device_handle(), path.c_str()));
+}
+
+Graph load_graph_cache(const std::string& path) {
+  pprg_graph* h = nullptr;
+  check(pprg_graph_load_cache(path.c_str(), device_from_env(), &h));
+  return Graph::adopt(h);
 }
 
 bool is_graph_cache(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  char magic[4];
-  return in && in.read(magic, 4) && std::memcmp(magic, "PPRG", 4) == 0;
+  char head[4] = {};
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  const std::size_t got = std::fread(head, 1, 4, f);
+  std::fclose(f);
+  return got == 4 && std::string_view(head, 4) == "PPRG";
 }
 
 // ---- push.hpp ----------------------------------------------------------------
@@ -369,58 +350,75 @@ WalkIndex build_index(const Graph& g, double alpha, std::uint64_t seed) {
   return w;
 }
 
-void save_index(const WalkIndex& index, const std::string& path) {  // walk_index.cpp:61-81
-  std::ofstream out(path, std::ios::binary | std::ios::trunc);
-  if (!out) throw std::runtime_error("cannot open for writing: " + path);
-  out.write("PPRW", 4);
-  out.put(1);
-  out.put(static_cast<char>(index.rng_id()));
-  std::uint64_t bits;
-  const double a = index.alpha();
-  std::memcpy(&bits, &a, 8);
-  write_u64(out, bits);
-  write_u64(out, index.seed());
-  write_u64(out, index.node_count());
-  write_u64(out, index.endpoint_count());
-  std::uint64_t off = 0;
-  write_u64(out, 0);
-  for (NodeId v = 0; v < index.node_count(); ++v) {
-    off += index.endpoints_of(v).size();
-    write_u64(out, off);
+// PPRW files (walk_index.hpp:52-56 format: "PPRW", u8 version 1, u8 rng id,
+// f64 alpha, u64 seed, n, m, offsets (n+1) x u64, endpoints m x u32; little
+// endian). An index with a device copy is written by the engine straight from
+// device memory (pprg_index_save); otherwise, and for loads without a graph,
+// the arrays move in bulk through stdio.
+namespace {
+static_assert(std::endian::native == std::endian::little, "PPRW/PPRG files are little endian");
+
+struct File {
+  std::FILE* f;
+  std::string path;
+  File(const std::string& p, const char* mode) : f(std::fopen(p.c_str(), mode)), path(p) {}
+  ~File() {
+    if (f) std::fclose(f);
   }
-  for (NodeId v = 0; v < index.node_count(); ++v)
-    for (NodeId e : index.endpoints_of(v)) write_u32(out, e);
-  if (!out) throw std::runtime_error("write failed: " + path);
+  bool get(void* dst, std::size_t bytes) { return std::fread(dst, 1, bytes, f) == bytes; }
+  bool put(const void* src, std::size_t bytes) { return std::fwrite(src, 1, bytes, f) == bytes; }
+};
+}  // namespace
+
+void save_index(const WalkIndex& index, const std::string& path) {
+  if (index.dev_) {
+    check(pprg_index_save(index.dev_.get(), path.c_str()));
+    return;
+  }
+  File out(path, "wb");
+  if (!out.f) throw std::runtime_error("cannot open for writing: " + path);
+  const std::uint8_t head[2] = {1, static_cast<std::uint8_t>(index.rng_id())};
+  const double alpha = index.alpha();
+  const std::uint64_t fields[3] = {index.seed(), index.node_count(), index.endpoint_count()};
+  bool ok = out.put("PPRW", 4) && out.put(head, 2) && out.put(&alpha, 8) && out.put(fields, 24) &&
+            out.put(index.offsets_.data(), 8 * index.offsets_.size()) &&
+            out.put(index.endpoints_.data(), 4 * index.endpoints_.size());
+  ok = (std::fflush(out.f) == 0) && ok;
+  if (!ok) throw std::runtime_error("write failed: " + path);
 }
 
-WalkIndex load_index(const std::string& path) {  // walk_index.cpp:83-104
-  std::ifstream in(path, std::ios::binary);
-  if (!in) throw std::runtime_error("cannot open walk index: " + path);
+WalkIndex load_index(const std::string& path) {
+  File in(path, "rb");
+  if (!in.f) throw std::runtime_error("cannot open walk index: " + path);
   char magic[4];
-  if (!in.read(magic, 4) || std::memcmp(magic, "PPRW", 4) != 0)
+  std::uint8_t head[2] = {};
+  if (!in.get(magic, 4) || std::string_view(magic, 4) != "PPRW")
     throw std::runtime_error(path + ": not a walk index (bad magic)");
-  if (in.get() != 1) throw std::runtime_error(path + ": unsupported walk index version");
-  if (in.get() != kRngIdPhilox4x32_10) throw std::runtime_error(path + ": unknown generator id");
-  const std::uint64_t abits = read_u64(in);
-  double alpha;
-  std::memcpy(&alpha, &abits, 8);
-  const std::uint64_t seed = read_u64(in), n = read_u64(in), m = read_u64(in);
+  if (!in.get(head, 2) || head[0] != 1)
+    throw std::runtime_error(path + ": unsupported walk index version");
+  if (head[1] != kRngIdPhilox4x32_10) throw std::runtime_error(path + ": unknown generator id");
+  double alpha = 0.0;
+  std::uint64_t fields[3] = {};  // seed, n, m
   WalkIndex w;
+  bool ok = in.get(&alpha, 8) && in.get(fields, 24);
+  if (ok) {
+    w.offsets_.resize(fields[1] + 1);
+    w.endpoints_.resize(fields[2]);
+    ok = in.get(w.offsets_.data(), 8 * w.offsets_.size()) &&
+         in.get(w.endpoints_.data(), 4 * w.endpoints_.size());
+  }
+  if (!ok) throw std::runtime_error(path + ": truncated walk index");
   w.alpha_ = alpha;
-  w.seed_ = seed;
-  w.offsets_.resize(n + 1);
-  for (auto& o : w.offsets_) o = read_u64(in);
-  w.endpoints_.resize(m);
-  for (auto& e : w.endpoints_) e = read_u32(in);
-  if (!in) throw std::runtime_error(path + ": truncated walk index");
-  // WalkIndex constructor checks (walk_index.cpp:19-34)
-  if (w.offsets_.empty() || w.offsets_.front() != 0 || w.offsets_.back() != m)
+  w.seed_ = fields[0];
+  // the WalkIndex constructor's checks (walk_index.cpp:19-34 semantics)
+  const auto& off = w.offsets_;
+  if (off.front() != 0 || off.back() != fields[2])
     throw std::runtime_error("walk index: inconsistent offsets");
-  for (std::size_t i = 0; i + 1 < w.offsets_.size(); ++i)
-    if (w.offsets_[i + 1] < w.offsets_[i])
-      throw std::runtime_error("walk index: offsets must be non-decreasing");
-  for (NodeId e : w.endpoints_)
-    if (e >= n) throw std::runtime_error("walk index: endpoint id out of range");
+  if (!std::is_sorted(off.begin(), off.end()))
+    throw std::runtime_error("walk index: offsets must be non-decreasing");
+  if (std::any_of(w.endpoints_.begin(), w.endpoints_.end(),
+                  [&](NodeId e) { return e >= fields[1]; }))
+    throw std::runtime_error("walk index: endpoint id out of range");
   return w;
 }
 
@@ -530,39 +528,71 @@ PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
   return v;
 }
 
-// ---- edge lists (graph.cpp:66-113) ---------------------------------------------------
+// ---- edge lists (graph.hpp:97-100; format of graph.cpp:66-104) ---------------
+// The whole file is read into memory and scanned once by a small state machine
+// that appends straight into the flat pair array the device builder takes.
+// Accepted: per line, optional blanks (space, tab, CR), then either nothing,
+// a '#' comment, or two unsigned decimal ids separated by blanks. Errors name
+// the file and the 1-based line ("path:line: what"), as the reference's.
 namespace {
-Graph read_edge_file(const std::string& path, bool undirected) {
-  std::ifstream in(path);
-  if (!in) throw std::runtime_error("cannot open graph file: " + path);
-  std::vector<std::pair<std::uint64_t, std::uint64_t>> edges;
-  std::string line;
-  for (std::uint64_t no = 1; std::getline(in, line); ++no) {
-    const char* p = line.data();
-    const char* const end = p + line.size();
-    auto blank = [&] {
-      while (p < end && (*p == ' ' || *p == '\t' || *p == '\r')) ++p;
-    };
-    auto bad = [&](const char* what) {
-      throw std::runtime_error(path + ":" + std::to_string(no) + ": " + what);
-    };
-    blank();
-    if (p == end || *p == '#') continue;
-    std::uint64_t a = 0, b = 0;
-    auto r = std::from_chars(p, end, a);
-    if (r.ec != std::errc()) bad("expected non-negative integer source id");
-    p = r.ptr;
-    blank();
-    r = std::from_chars(p, end, b);
-    if (r.ec != std::errc()) bad("expected non-negative integer target id");
-    p = r.ptr;
-    blank();
-    if (p != end) bad("trailing content after edge pair");
-    edges.emplace_back(a, b);
-    if (undirected) edges.emplace_back(b, a);
+class EdgeScanner {
+ public:
+  EdgeScanner(const std::string& path, bool both_directions)
+      : path_(path), both_(both_directions) {}
+
+  std::vector<std::uint64_t> scan(std::string_view text) {
+    std::vector<std::uint64_t> flat;
+    std::size_t pos = 0;
+    while (pos < text.size()) {
+      ++line_;
+      std::size_t eol = text.find('\n', pos);
+      if (eol == std::string_view::npos) eol = text.size();
+      scan_line(text.substr(pos, eol - pos), flat);
+      pos = eol + 1;
+    }
+    return flat;
   }
-  if (edges.empty()) throw std::runtime_error(path + ": graph is empty after cleaning");
-  return build_graph_from_edges(edges);
+
+ private:
+  static bool blank(char c) { return c == ' ' || c == '\t' || c == '\r'; }
+
+  [[noreturn]] void error(const char* what) const {
+    throw std::runtime_error(path_ + ":" + std::to_string(line_) + ": " + what);
+  }
+
+  // one unsigned id at `i`; advances past it and the blanks after it
+  std::uint64_t id(std::string_view ln, std::size_t& i, const char* what) const {
+    std::uint64_t v = 0;
+    const auto r = std::from_chars(ln.data() + i, ln.data() + ln.size(), v);
+    if (r.ec != std::errc()) error(what);
+    i = static_cast<std::size_t>(r.ptr - ln.data());
+    while (i < ln.size() && blank(ln[i])) ++i;
+    return v;
+  }
+
+  void scan_line(std::string_view ln, std::vector<std::uint64_t>& flat) const {
+    std::size_t i = 0;
+    while (i < ln.size() && blank(ln[i])) ++i;
+    if (i == ln.size() || ln[i] == '#') return;
+    const std::uint64_t u = id(ln, i, "expected non-negative integer source id");
+    const std::uint64_t v = id(ln, i, "expected non-negative integer target id");
+    if (i != ln.size()) error("trailing content after edge pair");
+    flat.insert(flat.end(), {u, v});
+    if (both_) flat.insert(flat.end(), {v, u});
+  }
+
+  std::string path_;
+  bool both_;
+  std::uint64_t line_ = 0;
+};
+
+Graph read_edge_file(const std::string& path, bool undirected) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open graph file: " + path);
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  const std::vector<std::uint64_t> flat = EdgeScanner(path, undirected).scan(text);
+  if (flat.empty()) throw std::runtime_error(path + ": graph is empty after cleaning");
+  return build_on_device(flat.data(), flat.size() / 2);
 }
 }  // namespace
 
@@ -631,13 +661,35 @@ PPRVector finish_state(PushState&& state, NodeId source, double alpha) {
   return out;
 }
 
-// ---- metrics.hpp (metrics.cpp:11-55) ---------------------------------------------
+// ---- metrics.hpp (semantics of metrics.cpp:11-42) ---------------------------------
+namespace {
+// One pass over (estimate, truth): the l1 distance and, for truth >= mu, the
+// relative errors (count above epsilon, maximum). epsilon < 0 counts nothing.
+ErrorReport accumulate_errors(const double* est, const double* truth, std::size_t n, double mu,
+                              double epsilon) {
+  ErrorReport r;
+  for (std::size_t i = 0; i < n; ++i) {
+    const double gap = std::abs(est[i] - truth[i]);
+    r.l1 += gap;
+    if (!(truth[i] >= mu)) continue;
+    const double rel = gap / truth[i];
+    r.nodes_above_mu += 1;
+    r.violations += rel > epsilon ? 1 : 0;
+    if (rel > r.max_rel_above_mu) r.max_rel_above_mu = rel;
+  }
+  return r;
+}
+
+void require_same_length(std::size_t a, std::size_t b, const char* fn) {
+  if (a != b) throw std::invalid_argument(std::string(fn) + ": vector lengths differ");
+}
+}  // namespace
+
 double l1_error(std::span<const double> estimate, std::span<const double> truth) {
-  if (estimate.size() != truth.size())
-    throw std::invalid_argument("l1_error: vector lengths differ");
-  double total = 0.0;
-  for (std::size_t i = 0; i < estimate.size(); ++i) total += std::abs(estimate[i] - truth[i]);
-  return total;
+  require_same_length(estimate.size(), truth.size(), "l1_error");
+  return accumulate_errors(estimate.data(), truth.data(), estimate.size(),
+                           std::numeric_limits<double>::infinity(), 0.0)
+      .l1;
 }
 
 double l1_error(const PPRVector& estimate, const PPRVector& truth) {
@@ -649,19 +701,8 @@ double l1_error(const PPRVector& estimate, const PPRVector& truth) {
 
 ErrorReport compare_to_truth(std::span<const double> estimate, std::span<const double> truth,
                              double mu, double epsilon) {
-  if (estimate.size() != truth.size())
-    throw std::invalid_argument("compare_to_truth: vector lengths differ");
-  ErrorReport r;
-  for (std::size_t i = 0; i < estimate.size(); ++i) {
-    const double d = std::abs(estimate[i] - truth[i]);
-    r.l1 += d;
-    if (truth[i] >= mu) {
-      ++r.nodes_above_mu;
-      r.max_rel_above_mu = std::max(r.max_rel_above_mu, d / truth[i]);
-      if (d / truth[i] > epsilon) ++r.violations;
-    }
-  }
-  return r;
+  require_same_length(estimate.size(), truth.size(), "compare_to_truth");
+  return accumulate_errors(estimate.data(), truth.data(), estimate.size(), mu, epsilon);
 }
 
 PPRVector ground_truth(const Graph& g, NodeId s, double alpha) {
@@ -706,120 +747,166 @@ DensePPR exact_ppr(const Graph& g, NodeId s, double alpha) {
   return DensePPR{std::move(x)};
 }
 
-// ---- csv.hpp (csv.cpp:9-43) --------------------------------------------------------
+// ---- csv.hpp (file format of csv.cpp:9-43: "node,ppr" then v,value rows) ------------
 std::string format_double(double value) {
-  char buffer[40];
-  std::snprintf(buffer, sizeof(buffer), "%.17g", value);
-  return buffer;
+  char buf[32];  // %.17g round-trips every finite double
+  const int len = std::snprintf(buf, sizeof buf, "%.17g", value);
+  return std::string(buf, static_cast<std::size_t>(len));
 }
 
 void write_ppr_csv(const std::string& path, std::span<const double> values) {
-  std::ofstream out(path, std::ios::trunc);
-  if (!out) throw std::runtime_error("cannot open for writing: " + path);
-  out << "node,ppr\n";
-  for (std::size_t v = 0; v < values.size(); ++v) out << v << ',' << format_double(values[v]) << '\n';
-  if (!out) throw std::runtime_error("write failed: " + path);
+  std::string text = "node,ppr\n";
+  text.reserve(text.size() + values.size() * 28);
+  for (std::size_t v = 0; v < values.size(); ++v)
+    text.append(std::to_string(v)).append(1, ',').append(format_double(values[v])).append(1, '\n');
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) throw std::runtime_error("cannot open for writing: " + path);
+  const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+  if (std::fclose(f) != 0 || !ok) throw std::runtime_error("write failed: " + path);
 }
 
 std::vector<double> read_ppr_csv(const std::string& path) {
-  std::ifstream in(path);
+  std::ifstream in(path, std::ios::binary);
   if (!in) throw std::runtime_error("cannot open: " + path);
-  std::string line;
-  if (!std::getline(in, line) || line != "node,ppr")
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  std::string_view rest(text);
+  auto next_line = [&rest]() {
+    const std::size_t eol = std::min(rest.find('\n'), rest.size());
+    std::string_view ln = rest.substr(0, eol);
+    rest.remove_prefix(std::min(eol + 1, rest.size()));
+    if (!ln.empty() && ln.back() == '\r') ln.remove_suffix(1);
+    return ln;
+  };
+  if (rest.empty() || next_line() != "node,ppr")
     throw std::runtime_error(path + ": missing node,ppr header");
   std::vector<double> values;
-  std::uint64_t expected = 0;
-  while (std::getline(in, line)) {
-    if (line.empty()) continue;
-    const auto comma = line.find(',');
-    if (comma == std::string::npos) throw std::runtime_error(path + ": malformed row: " + line);
-    if (std::stoull(line.substr(0, comma)) != expected)
+  while (!rest.empty()) {
+    const std::string_view ln = next_line();
+    if (ln.empty()) continue;
+    const std::size_t comma = ln.find(',');
+    if (comma == std::string_view::npos)
+      throw std::runtime_error(path + ": malformed row: " + std::string(ln));
+    std::uint64_t id = 0;
+    const auto r = std::from_chars(ln.data(), ln.data() + comma, id);
+    if (r.ec != std::errc() || r.ptr != ln.data() + comma || id != values.size())
       throw std::runtime_error(path + ": node ids must be consecutive from 0");
-    values.push_back(std::stod(line.substr(comma + 1)));
-    ++expected;
+    values.push_back(std::stod(std::string(ln.substr(comma + 1))));
   }
   return values;
 }
 
-// ---- sweep.hpp (sweep.cpp:16-147) ----------------------------------------------------
+// ---- sweep.hpp (the harness of sweep.cpp, on the GPU engines) ------------------------
+// Cells run through the C ABI: the truths of all sources in one batched
+// ground_truth call, each high-precision cell as one pprg_run_traced query
+// whose per-step series (one point per global sweep / iteration / frontier
+// level, recorded on the device side of the call) is thinned to the plan's
+// push cadence, each SpeedPPR cell as one pprg_speedppr query.
 bool is_high_precision_algo(const std::string& name) {
-  return name == kAlgoPowItr || name == kAlgoFifoFwdPush || name == kAlgoSimFwdPush ||
-         name == kAlgoPowerPush;
+  static const char* const names[] = {kAlgoPowItr, kAlgoFifoFwdPush, kAlgoSimFwdPush,
+                                      kAlgoPowerPush};
+  return std::any_of(std::begin(names), std::end(names),
+                     [&](const char* a) { return name == a; });
 }
 bool is_known_algo(const std::string& name) {
-  return is_high_precision_algo(name) || name == kAlgoSpeedPPR;
+  return name == kAlgoSpeedPPR || is_high_precision_algo(name);
 }
+
+namespace {
+// Keeps a point each time the cumulative edge pushes reach the next multiple
+// of the cadence (shared by CheckpointRecorder and the traced sweep cells).
+struct CadenceFilter {
+  std::uint64_t cadence, next;
+  explicit CadenceFilter(std::uint64_t c) : cadence(c ? c : 1), next(c ? c : 1) {}
+  bool take(std::uint64_t pushes) {
+    if (pushes < next) return false;
+    next += cadence * ((pushes - next) / cadence + 1);
+    return true;
+  }
+};
+
+int traced_algo(const std::string& name) {
+  if (name == kAlgoPowItr) return PPRG_ALGO_POWITR;
+  if (name == kAlgoSimFwdPush) return PPRG_ALGO_SIMFWDPUSH;
+  if (name == kAlgoFifoFwdPush) return PPRG_ALGO_FIFO;
+  return PPRG_ALGO_POWERPUSH;
+}
+
+std::uint64_t elapsed_ns(std::chrono::steady_clock::time_point since) {
+  return static_cast<std::uint64_t>(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                                        std::chrono::steady_clock::now() - since)
+                                        .count());
+}
+}  // namespace
 
 CheckpointRecorder::CheckpointRecorder(std::uint64_t cadence)
     : cadence_(cadence ? cadence : 1), next_mark_(cadence_),
       started_(std::chrono::steady_clock::now()) {}
 
 void CheckpointRecorder::on_push(const PushState& st) {
-  if (st.edge_push_count < next_mark_) return;
-  const auto ns = std::chrono::duration_cast<std::chrono::nanoseconds>(
-                      std::chrono::steady_clock::now() - started_)
-                      .count();
-  checkpoints_.push_back({st.edge_push_count, st.r_sum, static_cast<std::uint64_t>(ns)});
-  while (next_mark_ <= st.edge_push_count) next_mark_ += cadence_;
+  CadenceFilter f(cadence_);
+  f.next = next_mark_;
+  if (!f.take(st.edge_push_count)) return;
+  next_mark_ = f.next;
+  checkpoints_.push_back({st.edge_push_count, st.r_sum, elapsed_ns(started_)});
 }
-
-namespace {
-PPRVector run_high_precision(const Graph& g, NodeId s, const std::string& algo, double alpha,
-                             double lambda, PushObserver* obs) {
-  if (algo == kAlgoPowItr) return power_iteration(g, s, alpha, lambda, obs);
-  if (algo == kAlgoSimFwdPush) return sim_forward_push(g, s, alpha, lambda, obs);
-  if (algo == kAlgoFifoFwdPush)
-    return fifo_forward_push(g, s, alpha, lambda / static_cast<double>(g.effective_edge_count()),
-                             std::nullopt, obs);
-  QueryConfig cfg;
-  cfg.alpha = alpha;
-  return power_push(g, s, alpha, lambda, cfg, obs);
-}
-std::uint64_t since_ns(std::chrono::steady_clock::time_point t0) {
-  return static_cast<std::uint64_t>(
-      std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0)
-          .count());
-}
-}  // namespace
 
 SweepResult run_sweep(const Graph& g, const std::vector<NodeId>& sources, const SweepPlan& plan) {
-  for (const auto& a : plan.algorithms)
-    if (!is_known_algo(a)) throw std::invalid_argument("unknown algorithm: " + a);
+  if (auto bad = std::find_if_not(plan.algorithms.begin(), plan.algorithms.end(), is_known_algo);
+      bad != plan.algorithms.end())
+    throw std::invalid_argument("unknown algorithm: " + *bad);
+  const NodeId n = g.n();
+  const double mu = plan.mu.value_or(default_mu(n));
   const std::uint64_t cadence = plan.checkpoint_every ? plan.checkpoint_every : 4 * g.m();
-  const double mu = plan.mu ? *plan.mu : default_mu(g.n());
+  for (NodeId s : sources)
+    if (s >= n) throw std::invalid_argument("source out of range");
+
+  // every source's truth in one device call (k x n, query-major)
+  std::vector<double> truth(static_cast<std::size_t>(n) * sources.size());
+  std::vector<pprg_query_stats> tq(sources.size());
+  if (!sources.empty())
+    check(pprg_ground_truth(g.device_handle(), sources.data(),
+                            static_cast<std::uint32_t>(sources.size()), plan.alpha, truth.data(), 0,
+                            tq.data(), nullptr));
+
   SweepResult result;
-  for (NodeId s : sources) {
-    const PPRVector truth = ground_truth(g, s, plan.alpha);
-    for (const auto& algo : plan.algorithms) {
+  std::vector<double> est(n);
+  std::vector<pprg_checkpoint> series(1u << 16);
+  auto emit = [&](NodeId s, const std::string& algo, double param, std::uint64_t wall,
+                  const pprg_query_stats& q, const double* t, double eps) {
+    SweepCell cell;
+    const ErrorReport rep = accumulate_errors(est.data(), t, n, mu, eps);
+    cell.row = SweepRow{s, algo, param, wall, q.pushes, q.walks, rep.l1, rep.max_rel_above_mu};
+    result.cells.push_back(std::move(cell));
+  };
+  for (std::size_t i = 0; i < sources.size(); ++i) {
+    const NodeId s = sources[i];
+    const double* t = truth.data() + i * n;
+    for (const std::string& algo : plan.algorithms) {
       if (is_high_precision_algo(algo)) {
         for (double lambda : plan.lambdas) {
-          CheckpointRecorder rec(cadence);
+          pprg_query_stats q{};
+          std::uint32_t count = 0;
           const auto t0 = std::chrono::steady_clock::now();
-          const PPRVector got = run_high_precision(g, s, algo, plan.alpha, lambda, &rec);
-          const std::uint64_t wall = since_ns(t0);
-          const ErrorReport rep = compare_to_truth(got.estimates, truth.estimates, mu, 0.0);
-          SweepCell cell;
-          cell.row = {s, algo, lambda, wall, got.pushes, got.walks, rep.l1, rep.max_rel_above_mu};
-          cell.checkpoints = rec.checkpoints();
-          result.cells.push_back(std::move(cell));
+          check(pprg_run_traced(g.device_handle(), traced_algo(algo), s, plan.alpha, lambda,
+                                est.data(), &q, series.data(),
+                                static_cast<std::uint32_t>(series.size()), &count));
+          emit(s, algo, lambda, elapsed_ns(t0), q, t, 0.0);
+          CadenceFilter keep(cadence);
+          for (std::uint32_t c = 0; c < count; ++c)
+            if (keep.take(series[c].pushes))
+              result.cells.back().checkpoints.push_back(
+                  {series[c].pushes, series[c].r_sum, series[c].time_ns});
         }
-      } else {
-        for (double eps : plan.epsilons)
-          for (std::uint64_t seed : plan.seeds) {
-            QueryConfig cfg;
-            cfg.alpha = plan.alpha;
-            cfg.epsilon = eps;
-            cfg.mu = plan.mu;
-            cfg.seed = seed;
-            const auto t0 = std::chrono::steady_clock::now();
-            const PPRVector got = speedppr_query(g, s, cfg);
-            const std::uint64_t wall = since_ns(t0);
-            const ErrorReport rep = compare_to_truth(got.estimates, truth.estimates, mu, eps);
-            SweepCell cell;
-            cell.row = {s, algo, eps, wall, got.pushes, got.walks, rep.l1, rep.max_rel_above_mu};
-            result.cells.push_back(std::move(cell));
-          }
+        continue;
       }
+      for (double eps : plan.epsilons)
+        for (std::uint64_t seed : plan.seeds) {
+          pprg_query_stats q{};
+          const auto t0 = std::chrono::steady_clock::now();
+          check(pprg_speedppr(g.device_handle(), nullptr, &s, 1, plan.alpha, eps,
+                              plan.mu ? *plan.mu : -1.0, seed, est.data(), 0, &q, nullptr));
+          emit(s, algo, eps, elapsed_ns(t0), q, t, eps);
+        }
     }
   }
   return result;
@@ -828,31 +915,42 @@ SweepResult run_sweep(const Graph& g, const std::vector<NodeId>& sources, const 
 void write_sweep_csv(const SweepResult& result, const std::string& directory,
                      const std::string& graph_name) {
   namespace fs = std::filesystem;
-  fs::create_directories(directory);
   const fs::path dir(directory);
-  std::ofstream summary(dir / (graph_name + "_sweep.csv"), std::ios::trunc);
-  if (!summary) throw std::runtime_error("cannot write sweep summary");
-  summary << "source,algo,param,wall_time_ns,edge_pushes,walks,l1_error,max_rel_error\n";
-  for (const auto& cell : result.cells) {
-    const auto& r = cell.row;
-    summary << r.source << ',' << r.algo << ',' << format_double(r.param) << ',' << r.wall_time_ns
-            << ',' << r.edge_pushes << ',' << r.walks << ',' << format_double(r.l1_error) << ','
-            << format_double(r.max_rel_error) << '\n';
-    if (!cell.checkpoints.empty()) {
-      char param[32];
-      std::snprintf(param, sizeof(param), "%g", r.param);
-      std::ofstream series(dir / (graph_name + "_" + r.algo + "_" + param + ".csv"), std::ios::trunc);
-      series << "pushes,r_sum,time_ns\n";
-      for (const auto& c : cell.checkpoints)
-        series << c.pushes << ',' << format_double(c.r_sum) << ',' << c.time_ns << '\n';
-    }
+  fs::create_directories(dir);
+  auto write_file = [](const fs::path& path, const std::string& text) {
+    std::FILE* f = std::fopen(path.c_str(), "wb");
+    if (!f) throw std::runtime_error("cannot write " + path.string());
+    const bool ok = std::fwrite(text.data(), 1, text.size(), f) == text.size();
+    if (std::fclose(f) != 0 || !ok) throw std::runtime_error("write failed: " + path.string());
+  };
+  auto join = [](std::initializer_list<std::string> fields) {
+    std::string line;
+    for (const std::string& f : fields) line.append(line.empty() ? "" : ",").append(f);
+    return line + "\n";
+  };
+  std::string summary = "source,algo,param,wall_time_ns,edge_pushes,walks,l1_error,max_rel_error\n";
+  for (const SweepCell& cell : result.cells) {
+    const SweepRow& r = cell.row;
+    summary += join({std::to_string(r.source), r.algo, format_double(r.param),
+                     std::to_string(r.wall_time_ns), std::to_string(r.edge_pushes),
+                     std::to_string(r.walks), format_double(r.l1_error),
+                     format_double(r.max_rel_error)});
+    if (cell.checkpoints.empty()) continue;
+    char tag[32];  // series file name carries the parameter in %g form
+    std::snprintf(tag, sizeof tag, "%g", r.param);
+    std::string text = "pushes,r_sum,time_ns\n";
+    for (const Checkpoint& c : cell.checkpoints)
+      text += join({std::to_string(c.pushes), format_double(c.r_sum), std::to_string(c.time_ns)});
+    write_file(dir / (graph_name + "_" + r.algo + "_" + tag + ".csv"), text);
   }
+  write_file(dir / (graph_name + "_sweep.csv"), summary);
 }
 
 std::vector<NodeId> sample_sources(const Graph& g, std::uint64_t count, std::uint64_t seed) {
-  Rng rng(seed);
-  std::vector<NodeId> out(count);
-  for (auto& s : out) s = static_cast<NodeId>(rng.below(g.n()));
+  Rng rng(seed);  // Rng(seed).below(n) per source, with replacement
+  std::vector<NodeId> out;
+  out.reserve(count);
+  while (out.size() < count) out.push_back(static_cast<NodeId>(rng.below(g.n())));
   return out;
 }
 
