@@ -171,6 +171,11 @@ __device__ __forceinline__ double ld_state(const double* p) {  // coherent (L2),
   return __ldcg(p);
 #endif
 }
+__device__ __forceinline__ double2 ld_state2(const double* p) {  // two adjacent columns
+  double2 v;
+  asm volatile("ld.global.cg.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
 __device__ __forceinline__ void st_state(double* p, double v) {
 #if PPRG_HINTS >= 1
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" :: "l"(p), "d"(v), "l"(l2_evict_first()) : "memory");

@@ -127,19 +127,6 @@ __global__ void k_split_flags(const uint64_t* cin_off, uint64_t n_rows, uint32_t
 }
 
 // own_lo[j] = first row u with in_off[u] >= j*T (lower_bound over row starts)
-__global__ void k_tiles(const uint64_t* in_off, uint64_t n, uint64_t ntiles, uint32_t T,
-                        uint32_t* own_lo) {
-  GRID_STRIDE(j, ntiles + 1) {
-    const uint64_t key = j * (uint64_t)T;
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (in_off[mid] < key) lo = mid + 1; else hi = mid;
-    }
-    own_lo[j] = (uint32_t)lo;
-  }
-}
-
 // ---- generators ------------------------------------------------------------
 // R-MAT: edge i descends `scale` levels; level l uses 32-bit word l of the
 // Philox stream ctr = (i_lo, i_hi, 'RMAT', l/4) keyed by seed. Quadrants in
@@ -524,20 +511,6 @@ const Graph::Plan& Graph::tile_plan(uint32_t T, uint32_t R, uint32_t H) {
   PPRG_CUDA(cudaStreamSynchronize(stream));
   pl.host = std::move(tl);
   return plans.emplace(key, std::move(pl)).first->second;
-}
-
-const uint32_t* Graph::tiles(uint32_t T, uint64_t* ntiles) {
-  ensure_transpose();
-  *ntiles = m / T + 1;
-  auto it = tile_lo.find(T);
-  if (it != tile_lo.end()) return it->second.get();
-  DevBuf<uint32_t> lo(*ntiles + 1);
-  k_tiles<<<blocks_for(*ntiles + 1), TB, 0, stream>>>(cin_off.get(), n_rows, *ntiles, T, lo.get());
-  PPRG_CUDA(cudaStreamSynchronize(stream));
-  PPRG_CUDA(cudaGetLastError());
-  const uint32_t* p = lo.get();
-  tile_lo.emplace(T, std::move(lo));
-  return p;
 }
 
 static cudaStream_t make_stream(int device, int* sms) {

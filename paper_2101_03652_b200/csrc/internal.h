@@ -43,7 +43,6 @@ struct Graph {
   DevBuf<uint32_t> cin_row;   // [n_rows] node id of compacted row
   DevBuf<uint32_t> cin_deg;   // [n_rows] out-degree of the compacted row's node
   DevBuf<double> cin_inv;     // [n_rows] 1 / effective out-degree
-  std::map<uint32_t, DevBuf<uint32_t>> tile_lo;  // per tile size: first owned compact row of tile j
   std::map<uint32_t, DevBuf<uint2>> tile_d;      // per tile size: (first row, rows) of tile j
   std::map<uint32_t, DevBuf<uint32_t>> tile_split;  // per tile size: compact rows spanning tiles
   std::mutex mu;
@@ -52,7 +51,6 @@ struct Graph {
   ~Graph();
   void finish_build();  // deg / inv_deg / dead-ends from off; validates
   void ensure_transpose();
-  const uint32_t* tiles(uint32_t edges_per_tile, uint64_t* ntiles);
   const uint2* tile_desc(uint32_t edges_per_tile, uint64_t* ntiles);
   const uint32_t* split_rows(uint32_t edges_per_tile, uint64_t* count);
   struct Plan {

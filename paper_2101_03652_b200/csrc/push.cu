@@ -43,8 +43,6 @@ struct Workspace {
   DevBuf<double> x, y0, y1, r0, r1, res;
   DevBuf<unsigned> stamp;
   DevBuf<uint32_t> fa, fb;  // frontier segments [K][n] of node ids
-  DevBuf<double> carry_h, carry_t;
-  DevBuf<unsigned> split_cnt;
   DevBuf<double> hub_acc;
   DevBuf<unsigned> hub_cnt;
   // host-output staging: finalize writes slot s while the copy stream drains
@@ -72,7 +70,6 @@ struct Workspace {
   DevBuf<unsigned> col_stop;
   DevBuf<unsigned long long> heavy_chunks;
   unsigned level_tag = 0;
-  uint64_t ntiles_alloc = 0;
 };
 
 static std::mutex g_ws_mu;
@@ -103,13 +100,6 @@ static void ws_alloc(Workspace& w, Graph& g, int K) {
 
 static void ws_tiles(Workspace& w, Graph& g, uint64_t ntiles, uint64_t nhubs) {
   const int K = w.K;
-  if (ntiles > w.ntiles_alloc) {
-    w.carry_h.alloc((ntiles + 1) * K);
-    w.carry_t.alloc((ntiles + 1) * K);
-    w.split_cnt.alloc(ntiles + 1);
-    PPRG_CUDA(cudaMemsetAsync(w.split_cnt.get(), 0, 4 * (ntiles + 1), g.stream));
-    w.ntiles_alloc = ntiles;
-  }
   if ((ntiles + 1) * K > w.hub_acc.n) w.hub_acc.alloc((ntiles + 1) * K);
   if (nhubs + 1 > w.hub_cnt.n) {
     w.hub_cnt.alloc(nhubs + 1);
@@ -350,7 +340,6 @@ struct Block {
   int K;
   uint32_t k;
   uint64_t ntiles = 0;
-  const uint32_t* tile_lo = nullptr;
   const TileDesc* desc = nullptr;
   uint64_t nhubs = 0;
   double alpha;
@@ -370,7 +359,6 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
                  Workspace* own = nullptr) {
   const int K = round_k(k);
   uint64_t ntiles = 0;
-  const uint32_t* tl = nullptr;
   const TileDesc* dsc = nullptr;
   uint64_t nhubs = 0;
   if (need_pull) {
@@ -386,7 +374,6 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   Workspace& w = own ? *own : workspace(g, K, ntiles, nhubs);
   Block b(g, w, K, k, alpha);
   b.ntiles = ntiles;
-  b.tile_lo = tl;
   b.desc = dsc;
   b.nhubs = nhubs;
   for (uint32_t c = 0; c < k; ++c) b.src[c] = sources[c];
@@ -416,14 +403,10 @@ SweepParams base_params(Block& b) {
   P.cinv = g.cin_inv.get();
   P.in_off_full = g.in_off.get();
   P.in_nbr = g.in_nbr.get();
-  P.tile_lo = b.tile_lo;
   P.desc = b.desc;
   P.ntiles = b.ntiles;
   P.T = SWEEP_ELEMS / b.K;
   P.k1w = k1w_on(g, b.K);
-  P.carry_head = b.w.carry_h.get();
-  P.carry_tail = b.w.carry_t.get();
-  P.split_cnt = b.w.split_cnt.get();
   P.hub_acc = b.w.hub_acc.get();
   P.hub_cnt = b.w.hub_cnt.get();
   return P;
@@ -641,6 +624,26 @@ void exact_rsum(Block& b, const std::vector<int>& which) {
   }
 }
 
+// The final pass clamps implicit residues that rounding left below zero; a
+// sum of clamped mass beyond rounding level means the pull-form state was
+// inconsistent (e.g. parts starting from different local phases): fail loudly.
+constexpr double kNegResidueTol = 1e-12;
+
+// The sweeps stop on the tracked r_sum (r_sum -= alpha * pushed); the exact
+// residue sum of the final pass replaces it. The two differ by accumulated
+// rounding (~1e-15 absolute), so the last epoch stops a relative 1e-6 below
+// lambda: the exact r_sum then lands <= lambda, which the reference guarantees
+// by looping on the recomputed sum (push.cpp:180-196). The push thresholds
+// (epoch_r_max) are the reference's unchanged.
+double stop_lambda(double epoch_lambda, uint32_t e, uint32_t E) {
+  return e + 1 == E ? epoch_lambda * (1.0 - 1e-6) : epoch_lambda;
+}
+void check_final(const SweepCtl& fc) {
+  if (fc.neg_sum < -kNegResidueTol)
+    fail(EINTERNAL, "final pass: " + std::to_string(fc.neg_count) +
+                        " negative implicit residues summing to " + std::to_string(fc.neg_sum));
+}
+
 // Global phase: epochs of asynchronous pull sweeps in one persistent
 // cooperative kernel (push.cpp:168-197) for the columns with scan[c] set.
 // refine_rmax > 0 appends a refine epoch (push.cpp:208-222): threshold
@@ -662,7 +665,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   SweepParams P = base_params(b);
   for (uint32_t e = 0; e < E; ++e) {
     const double el = std::pow(lambda, static_cast<double>(e + 1) / E);  // push.cpp:176-178
-    P.lam[e] = el;
+    P.lam[e] = stop_lambda(el, e, E);
     P.thr[e] = el / m_eff;
   }
   const int Et = (int)E + (refine_rmax > 0.0);
@@ -841,6 +844,7 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
   call->kernel_launches += 1;
   SweepCtl fc;
   d2h_small(&fc, w.ctl.get(), sizeof fc, st);
+  check_final(fc);
   if (!direct && (out.reserve || out.residue)) {
     PPRG_CUDA(cudaEventRecord(w.ev_ready[slot], st));
     PPRG_CUDA(cudaStreamWaitEvent(w.copy_st, w.ev_ready[slot], 0));
@@ -1131,6 +1135,10 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
     } else {
       power_push_block(b, lambda, epoch_num, scan_threshold, call);
       finalize(b, o, false, call);
+      for (uint32_t c = 0; c < kb; ++c)
+        if (b.scan[c] && b.r_sum[c] > lambda)
+          fail(EINTERNAL, "power push: exact r_sum " + std::to_string(b.r_sum[c]) +
+                              " above lambda after the global phase");
     }
     tdev.stop();
     call->device_ms += tdev.ms();
@@ -1409,8 +1417,9 @@ bool part_start(PartSession* s, const double* summed) {
   s->lam.assign(EMAX, 0.0);
   s->thr.assign(EMAX, 0.0);
   for (uint32_t e = 0; e < s->E; ++e) {
-    s->lam[e] = std::pow(s->lambda, static_cast<double>(e + 1) / s->E);  // push.cpp:176-178
-    s->thr[e] = s->lam[e] / m_eff;
+    const double el = std::pow(s->lambda, static_cast<double>(e + 1) / s->E);  // push.cpp:176-178
+    s->lam[e] = stop_lambda(el, e, s->E);
+    s->thr[e] = el / m_eff;
   }
   s->st.assign(KMAX, ColInit{});
   s->used_scan.assign(KMAX, 0);
@@ -1526,6 +1535,7 @@ void part_finish(PartSession* s, double* reserve, double* residue, bool on_devic
   tf.stop();
   SweepCtl fc;
   d2h_small(&fc, b.w.ctl.get(), sizeof fc, st);
+  check_final(fc);
   if (!on_device && w) {
     for (uint32_t c = 0; c < k; ++c) {
       if (reserve)

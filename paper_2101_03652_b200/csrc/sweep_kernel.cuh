@@ -3,6 +3,7 @@
 // and its tile / row machinery. Included by push.cu only (one translation unit).
 #pragma once
 #include <cub/cub.cuh>
+#include <math_constants.h>
 
 #include <cstdint>
 
@@ -53,6 +54,10 @@ struct SweepCtl {
   int out_epoch[KMAX];
   unsigned long long out_pushes[KMAX];
   unsigned total_sweeps;
+  // final pass: implicit residues below zero (rounding of inflow - x only;
+  // clamped to 0 in the outputs, counted and summed here and checked on the host)
+  unsigned long long neg_count;
+  double neg_sum;
 };
 
 struct SweepParams {
@@ -65,7 +70,6 @@ struct SweepParams {
   const uint32_t* in_nbr;
   const uint32_t* deg;
   const double* inv_deg;
-  const uint32_t* tile_lo;
   const TileDesc* desc;        // row-aligned tile plan
   double* hub_acc;             // [ntiles][K] per-piece partial sums of hub rows
   unsigned* hub_cnt;           // [nhubs] arrived pieces
@@ -80,9 +84,6 @@ struct SweepParams {
   double* y[2];                // gather operand (powitr double-buffers)
   double* r[2];                // powitr residues (double-buffered)
   const double* push_res;      // finalize: push-form residues (columns without scan phase)
-  double* carry_head;
-  double* carry_tail;
-  unsigned* split_cnt;
 
   SweepCtl* ctl;
   double* out_reserve;         // finalize outputs, query-major [c*n + u]
@@ -199,7 +200,11 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
     if (P.final_pull[c]) {
       const double inflow = acc + (is_src ? 1.0 + cs[c].D : 0.0);
       res = inflow - xo;
-      if (res < 0.0) res = 0.0;  // rounding of the implicit form only
+      if (res < 0.0) {  // rounding of the implicit form only: counted, checked on the host
+        atomicAdd(&P.ctl->neg_count, 1ull);
+        atomicAdd(&P.ctl->neg_sum, res);
+        res = 0.0;
+      }
     } else {
       res = P.push_res[ix];
     }
@@ -225,8 +230,10 @@ __device__ __forceinline__ void decide_at(const SweepParams& P, const ColSh* cs,
 
 // One piece of a hub row (more in-edges than a tile holds): the block sums its
 // edges per column, adds the piece total into the row's accumulator, and the
-// last piece to arrive decides the row (release-ordered counter; the partials
-// are read back from L2). Only hub pieces pay this protocol.
+// last piece to arrive decides the row (acq_rel counter: each piece releases
+// its partial, the last arriver acquires all of them before the block barrier
+// hands them to the deciding threads; partials read back from L2). Only hub
+// pieces pay this protocol.
 template <int K, int MODE>
 __device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, uint64_t j,
                                        double* hubsh, int* flag, const ColSh* cs, const double* thr_cur,
@@ -263,7 +270,7 @@ __device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, 
   __syncthreads();
   if (tid == 0) {
     unsigned old;
-    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
                  : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
     *flag = old == d.npieces - 1;
     if (*flag) P.hub_cnt[d.hub] = 0;
@@ -467,11 +474,12 @@ __device__ __forceinline__ void sweep_k1_warps(const SweepParams& P, const ColSh
         if (lane == 0) {
           P.hub_acc[t] = sum;
           unsigned old;
-          asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+          asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
                        : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
           last = old == d.npieces - 1;
           if (last) P.hub_cnt[d.hub] = 0;
         }
+        __syncwarp();  // orders lane 0's acquire before the other lanes' partial reads
         last = __shfl_sync(0xffffffffu, last, 0);
         if (last) {  // the partials in piece order (lane-strided, then a fixed tree)
           const double* part = P.hub_acc + (t - d.piece);
@@ -607,9 +615,12 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double*
   double acc[CPL][2];
 #pragma unroll
   for (int q = 0; q < CPL; ++q) acc[q][0] = acc[q][1] = 0.0;
+  // the ids of the next 32 in-edges are loaded one chunk ahead, so their
+  // latency hides behind this chunk's gathers (rows longer than 32 in-edges)
+  uint32_t nextid = have_first ? first_id : (b + lane < e ? ld_stream(P.in_nbr + b + lane) : 0u);
   for (uint64_t p0 = b; p0 < e; p0 += 32) {
-    const uint64_t pl = p0 + lane;
-    const uint32_t myid = (have_first && p0 == b) ? first_id : (pl < e ? ld_stream(P.in_nbr + pl) : 0u);
+    const uint32_t myid = nextid;
+    if (p0 + 32 < e) nextid = p0 + 32 + lane < e ? ld_stream(P.in_nbr + p0 + 32 + lane) : 0u;
     const int cnt = e - p0 < 32 ? (int)(e - p0) : 32;
     for (int j0 = 0; j0 < cnt; j0 += G * ES) {
       double v[G][CPL];
@@ -649,11 +660,15 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double*
 // counter, last piece decides from the partials in piece order). Measured on
 // configs[2]: sweep kernel -4% against the column-per-thread hub_piece.
 template <int K, int MODE>
-__device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc& d, uint64_t j,
+__device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc d, uint64_t j,
                                             double* hubsh, int* flag, const ColSh* cs,
                                             const double* thr_cur, const double* yg,
                                             const double* rcur, double* rnxt, double* ynxt,
-                                            Acc& a) {
+                                            double* sh_push, double* sh_d,
+                                            unsigned long long* sh_np, unsigned long long* sh_nn,
+                                            unsigned long long* sh_et) {
+  // (no by-reference locals: the deciding thread's counters go straight to
+  // the block's shared per-column sums, so the call needs no stack frame)
   constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   constexpr int NW = NT / 32;
@@ -676,7 +691,7 @@ __device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc
   __syncthreads();
   if (tid == 0) {
     unsigned old;
-    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
                  : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
     *flag = old == d.npieces - 1;
     if (*flag) P.hub_cnt[d.hub] = 0;
@@ -687,14 +702,48 @@ __device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc
     double acc = 0.0;
     for (uint32_t p = 0; p < d.npieces; ++p) acc += __ldcg(part + (uint64_t)p * K);
     const uint32_t u = __ldg(P.crow + d.r0);
+    Acc a;
     decide_at<K, MODE>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
                        rcur, rnxt, ynxt, a);
+    if (a.push != 0.0) atomicAdd(&sh_push[tid], a.push);
+    if (a.d != 0.0) atomicAdd(&sh_d[tid], a.d);
+    if (a.np) atomicAdd(&sh_np[tid], a.np);
+    if (a.nn) atomicAdd(&sh_nn[tid], a.nn);
+    if (a.et) atomicAdd(&sh_et[tid], a.et);
   }
+}
+
+// decide<K, M_POWERPUSH> with the column's threshold and source in registers
+// (thr = +inf: the column is done).
+template <int K>
+__device__ __forceinline__ void decide_pp(const SweepParams& P, const ColSh* cs, double thr,
+                                          uint32_t src, uint32_t u, int c, double acc, double xo,
+                                          uint32_t dg, double inv, Acc& a) {
+  if (thr == CUDART_INF) return;
+  const uint64_t ix = (uint64_t)u * K + c;
+  const double oma = 1.0 - P.alpha;
+  const double inflow = acc + (u == src ? 1.0 + cs[c].D : 0.0);
+  const double r = inflow - xo;
+  if (r > (dg ? (double)dg : 1.0) * thr) {
+    st_state(P.x + ix, inflow);
+    if (dg) {
+      const double yv = oma * inflow * inv;
+      P.y[0][ix] = yv;
+      for (int p = 0; p < P.npeers; ++p) P.peer_y[p][ix] = yv;  // fused exchange
+    }
+    a.push += r;
+    a.np += dg ? dg : 1;
+    a.nn += 1;
+    a.et += dg;
+    xo = inflow;
+  }
+  if (!dg) a.d += oma * xo;
 }
 
 template <int K, int MODE>
 __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* cs,
-                                            const double* thr_cur, uint32_t u, const double* s,
+                                            const double* thr_cur, const uint32_t* csrc,
+                                            uint32_t u, const double* s,
                                             const double* xo, const double* rc, uint32_t dg,
                                             double inv, const double* yg, double* rnxt,
                                             double* ynxt, Acc& a, const BlockAcc& ba,
@@ -705,11 +754,18 @@ __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* c
   if constexpr (CPL == 1) {
     decide<K, MODE>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], dg, inv, yg, rnxt, ynxt, a);
   } else {  // K = 64: lane kc owns columns 2kc, 2kc+1; counters via shared atomics
+    // the lane's two thresholds and sources in one conflict-free 16 / 8-byte
+    // shared load each (a done column's threshold is +inf)
+    const double2 th = reinterpret_cast<const double2*>(thr_cur)[kc];
+    const uint2 sr = reinterpret_cast<const uint2*>(csrc)[kc];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       Acc b2;
       const int cc = kc * CPL + q;
-      decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
+      if constexpr (MODE == M_POWERPUSH)
+        decide_pp<K>(P, cs, q ? th.y : th.x, q ? sr.y : sr.x, u, cc, s[q], xo[q], dg, inv, b2);
+      else
+        decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
       if (PPRG_PUSH_REG && pacc) pacc[q] += b2.push;  // flushed once per tile
       else if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
       if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
@@ -742,6 +798,7 @@ constexpr uint32_t LONG_W = PPRG_LONG_W;
 template <int K, int MODE>
 __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileDesc& d, char* smem,
                                                const ColSh* cs, const double* thr_cur,
+                                               const uint32_t* csrc,
                                                const double* yg, const double* rcur, double* rnxt,
                                                double* ynxt, Acc& a, const BlockAcc& ba,
                                                uint32_t* rowctr,
@@ -794,14 +851,19 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
     if (e - b <= LONG_W) {
       const uint32_t u = snode[r];
       double xo[CPL], rc[CPL], s[CPL];
+      if constexpr (CPL == 2) {  // issued early (one 16-byte load); lands during the edge loop
+        const double2 x2 = es0 ? ld_state2(P.x + (uint64_t)u * K + kc * 2) : make_double2(0.0, 0.0);
+        xo[0] = x2.x;
+        xo[1] = x2.y;
+      }
 #pragma unroll
       for (int q = 0; q < CPL; ++q) {  // issued early; lands during the edge loop
         const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
-        xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
+        if constexpr (CPL != 2) xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
         rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
       }
       warp_row_sum<K>(P, yg, b, e, s, true, ids);
-      if (es0) decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
+      if (es0) decide_cols<K, MODE>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
     }
     r = rn;
     ids = ids_n;
@@ -831,7 +893,7 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
         for (int w = 0; w < NW; ++w) t += spart[w * K + kc * CPL + q];
         s[q] = t;
       }
-      decide_cols<K, MODE>(P, cs, thr_cur, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
+      decide_cols<K, MODE>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
     }
     __syncthreads();
   }
@@ -879,7 +941,8 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
   using TC = Tile<K>;
   extern __shared__ __align__(16) char smem_dyn[];
   __shared__ ColSh cs[K];
-  __shared__ double thr_cur[K];
+  __shared__ __align__(16) double thr_cur[K];
+  __shared__ __align__(16) uint32_t csrc[K];  // column sources (lane-pair loads in decide_cols)
   __shared__ double sh_push[K], sh_d[K];
   __shared__ unsigned long long sh_np[K], sh_nn[K], sh_et[K];
   __shared__ unsigned long long sh_tile[3];
@@ -897,6 +960,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
     cs[tid].sweeps = P.init[tid].sweeps;
     cs[tid].pushes = P.init[tid].pushes;
     cs[tid].src = P.src[tid];
+    csrc[tid] = P.src[tid];
   }
   __syncthreads();
   __shared__ unsigned long long sh_pk[K];
@@ -915,7 +979,9 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
       if constexpr (K >= WIDE_K) *wide_long_count<K>(smem_dyn) = 0;
     }
     if (tid < K) {
-      thr_cur[tid] = (MODE == M_POWERPUSH && !cs[tid].done) ? P.thr[cs[tid].epoch] : 0.0;
+      // a done column's threshold is +inf (decide_pp's done test); decide()
+      // checks cs[].done itself
+      thr_cur[tid] = MODE != M_POWERPUSH ? 0.0 : cs[tid].done ? CUDART_INF : P.thr[cs[tid].epoch];
       sh_push[tid] = 0.0;
       sh_d[tid] = 0.0;
       sh_np[tid] = 0;
@@ -956,13 +1022,14 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
       TileDesc dn = d;
       if (d.npieces > 1) {
         if constexpr (K >= WIDE_K)
-          hub_piece_wide<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+          hub_piece_wide<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt,
+                                  sh_push, sh_d, sh_np, sh_nn, sh_et);
         else
           hub_piece<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
         dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
         __syncthreads();
       } else if constexpr (K >= WIDE_K) {
-        tile_rows_wide<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba,
+        tile_rows_wide<K, MODE>(P, d, smem_dyn, cs, thr_cur, csrc, yg, rcur, rnxt, ynxt, a, ba,
                                 &sh_nlong, &sh_tile[(it + 1) & 1], &dn);
       } else {
         tile_rows<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba, &sh_nlong,
