@@ -69,6 +69,7 @@ struct Workspace {
   DevBuf<unsigned> heavy_cnt;
   DevBuf<unsigned> col_stop;
   DevBuf<unsigned long long> heavy_chunks;
+  DevBuf<DrainCtl> drain_ctl;
   unsigned level_tag = 0;
 };
 
@@ -512,6 +513,65 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     if (state[c] != 0) continue;
     if (still_live(c, qsize[c])) live |= 1ull << c;
     else state[c] = 1;
+  }
+  // Unobserved calls: every level in one persistent launch (k_drain), one
+  // read-back per drain instead of several per level.
+  static const bool host_levels = std::getenv("PPRG_HOST_LEVELS") != nullptr;
+  if (live && !g_obs && !g_trace && !host_levels && !std::getenv("PPRG_DEBUG_LOCAL")) {
+    if (!w.drain_ctl.get()) w.drain_ctl.alloc(1);
+    if (w.level_tag >= 0x80000000u) {  // level L stamps level_tag + L + 1: keep it from wrapping
+      PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, st));
+      w.level_tag = 0;
+    }
+    DrainParams D;
+    std::memset(&D, 0, sizeof D);
+    D.off = g.off.get();
+    D.nbr = g.nbr.get();
+    D.deg = g.deg.get();
+    D.res = w.res.get();
+    D.x = w.x.get();
+    D.stamp = w.stamp.get();
+    D.seg[0] = cur;
+    D.seg[1] = nxt;
+    D.seg_cap = n;
+    D.heavy = w.heavy.get();
+    D.ctl = w.drain_ctl.get();
+    D.limit = limit == UINT64_MAX ? ~0ull : (unsigned long long)limit;
+    D.live0 = live;
+    D.lam_stop = lam_stop;
+    D.alpha = b.alpha;
+    D.tag0 = w.level_tag;
+    D.max_levels = 0xFFFFFFFFu - w.level_tag - 1;
+    D.K = K;
+    for (int c = 0; c < K; ++c) {
+      D.src[c] = b.src[c];
+      D.thr[c] = r_max;
+      D.r_sum0[c] = b.r_sum[c];
+      D.q0[c] = ((live >> c) & 1ull) ? qsize[c] : 0;
+    }
+    PPRG_CUDA(cudaMemsetAsync(D.ctl, 0, sizeof(DrainCtl), st));
+    static int per_sm = [] {
+      int v = 0;
+      PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_drain, DRAIN_NT, 0));
+      return v;
+    }();
+    if (per_sm < 1) fail(EINTERNAL, "drain kernel cannot be resident");
+    void* args[] = {(void*)&D};
+    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)k_drain, dim3((unsigned)(per_sm * g.sm_count)),
+                                          dim3(DRAIN_NT), args, 0, st));
+    PPRG_CUDA(cudaGetLastError());
+    call->kernel_launches += 1;
+    DrainCtl hd;
+    d2h_small(&hd, D.ctl, sizeof hd, st);
+    if (hd.out_live) fail(EINTERNAL, "drain: level limit reached");
+    w.level_tag += hd.levels_run;
+    for (uint32_t c = 0; c < b.k; ++c) {
+      if (!((live >> c) & 1ull)) continue;
+      b.r_sum[c] = hd.out_rsum[c];
+      b.pushes[c] += hd.out_np[c];
+      b.levels[c] += hd.out_levels[c];
+    }
+    live = 0;
   }
   while (live) {
     uint64_t total = 0;
