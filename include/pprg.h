@@ -38,6 +38,12 @@ extern "C" {
 #define PPRG_ASYNC_HOST 2u /* host outputs: return once computed; the last block's copies
                               may still be landing -- pprg_graph_sync(g) waits for them.
                               Lets consecutive calls overlap copies with compute. */
+#define PPRG_DETERMINISTIC 4u /* bitwise-reproducible results: identical inputs give identical
+                                 bits on every run (the reference's rerun guarantee, SPEC.md
+                                 "two runs with identical argv produce identical result files").
+                                 Deterministic sweeps run in waves with double-buffered y
+                                 (more sweeps), local phases pop before they scatter, and
+                                 every cross-thread sum is exact fixed point. Slower. */
 
 #define PPRG_RNG_PHILOX4X32_10 2u /* PPRW rng-id byte for our walk index (reference uses 1 = mt19937_64, rng.hpp:10) */
 
@@ -70,6 +76,10 @@ typedef struct {
 
 const char* pprg_last_error(void);
 int pprg_version(void);
+/* Process-wide default for PPRG_DETERMINISTIC (0 = off at load). Calls without
+ * a flags argument (pprg_run_traced, pprg_run_observed) follow it; calls with
+ * flags are deterministic when either the flag or the default is set. */
+int pprg_set_deterministic(int on);
 int pprg_device_count(int* count);
 
 /* ---- graphs (graph.hpp) -------------------------------------------------- */

@@ -23,7 +23,8 @@ from ._abi import (PPRVector, QueryConfig, Graph, WalkIndex, CallStats, PowerPus
                    compute_walk_budget, walk_terminals, ground_truth, ground_truth_batch, refine, monte_carlo_phase, pinned_empty,
                    GROUND_TRUTH_LAMBDA, default_lambda, default_mu,
                    default_scan_threshold, load_library, lib_path, PPRGError, InvalidArgument,
-                   DataError, LogicError, KINDEX_TAG, RNG_ID_PHILOX)
+                   DataError, LogicError, KINDEX_TAG, RNG_ID_PHILOX, set_deterministic,
+                   deterministic)
 from .formats import save_graph_cache, load_graph_cache, save_index, load_index, is_graph_cache
 from .sources import sample_sources
 

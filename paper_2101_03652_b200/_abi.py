@@ -127,8 +127,32 @@ def load_library(path: str = lib_path):
     L.pprg_host_free.argtypes = [vp]
     L.pprg_device_alloc.argtypes = [C.c_int, C.c_uint64, C.POINTER(vp)]
     L.pprg_device_free.argtypes = [C.c_int, vp]
+    if hasattr(L, "pprg_set_deterministic"):  # (older builds loaded through PPRG_LIB lack it)
+        L.pprg_set_deterministic.argtypes = [C.c_int]
     _lib = L
     return L
+
+
+def set_deterministic(on: bool = True) -> None:
+    """Process-wide PPRG_DETERMINISTIC (include/pprg.h): every later query returns
+    bitwise-identical results for identical inputs (the reference's rerun
+    guarantee), at the cost of more sweeps. Off by default."""
+    _check(load_library().pprg_set_deterministic(1 if on else 0))
+
+
+class deterministic:
+    """Context manager: deterministic queries inside the block."""
+
+    def __init__(self, on: bool = True):
+        self.on = on
+
+    def __enter__(self):
+        set_deterministic(self.on)
+        return self
+
+    def __exit__(self, *exc):
+        set_deterministic(False)
+        return False
 
 
 def _check(rc):

@@ -199,6 +199,9 @@ def main(argv: Optional[List[str]] = None) -> int:  # ppr_main.cpp:223-296
         return EXIT_OK if e.code in (0, None) else EXIT_USAGE
     run = {"clean": run_clean, "query": run_query, "build-index": run_build_index,
            "groundtruth": run_groundtruth, "bench": run_bench}[a.cmd]
+    if a.cmd != "bench":
+        # SPEC.md: identical argv -> identical result files for every subcommand
+        _abi.set_deterministic(True)
     try:
         return run(a)
     except (UsageError, _abi.InvalidArgument) as e:

@@ -86,6 +86,14 @@ std::uint64_t QueryConfig::scan_threshold_for(NodeId n) const {
 }
 namespace {
 
+// The reference is a deterministic library (SPEC.md: identical inputs give
+// identical results), so its drop-in runs the engine in PPRG_DETERMINISTIC
+// mode; PPRG_FAST=1 selects the faster nondeterministic sweeps instead.
+const int g_det_init = [] {
+  pprg_set_deterministic(std::getenv("PPRG_FAST") ? 0 : 1);
+  return 0;
+}();
+
 void check(int rc) {
   if (rc == PPRG_OK) return;
   const std::string msg = pprg_last_error();

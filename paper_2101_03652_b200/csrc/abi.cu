@@ -1,6 +1,7 @@
 // extern "C" boundary (include/pprg.h): argument checks with the reference's
 // error behaviour, exception -> status mapping, per-thread error message.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -28,9 +29,11 @@ void release_workspaces(const Graph* g);
 
 namespace {
 thread_local std::string t_err;
+std::atomic<int> g_det_default{0};
 
 template <typename F>
 int guard(F&& f) {
+  pprg::DetScope det(g_det_default.load() != 0);  // PPRG_DETERMINISTIC flags add to it
   try {
     f();
     return PPRG_OK;
@@ -85,6 +88,7 @@ int push_engine(pprg_graph* g, pprg::Engine eng, const uint32_t* sources, uint32
                 double lambda_stop, double* reserve_out, double* residue_out, uint32_t flags,
                 pprg_query_stats* q, pprg_call_stats* c) {
   return guard([&] {
+    if (flags & PPRG_DETERMINISTIC) pprg::t_det = true;
     require(g && g->g, "null graph");
     require(k == 0 || sources, "null sources");
     check_alpha(alpha);
@@ -104,6 +108,11 @@ extern "C" {
 
 const char* pprg_last_error(void) { return t_err.c_str(); }
 int pprg_version(void) { return 1; }
+
+int pprg_set_deterministic(int on) {
+  g_det_default.store(on ? 1 : 0);
+  return PPRG_OK;
+}
 
 int pprg_device_count(int* count) {
   return guard([&] { PPRG_CUDA(cudaGetDeviceCount(count)); });
@@ -367,6 +376,7 @@ int pprg_ground_truth(pprg_graph* g, const uint32_t* sources, uint32_t k, double
                       double* estimates_out, uint32_t flags, pprg_query_stats* q,
                       pprg_call_stats* c) {
   return guard([&] {
+    if (flags & PPRG_DETERMINISTIC) pprg::t_det = true;
     require(g && g->g, "null graph");
     require(k == 0 || (sources && estimates_out), "null argument");
     check_alpha(alpha);
@@ -578,6 +588,7 @@ int pprg_refine(pprg_graph* g, const uint32_t* sources, uint32_t k, double alpha
                 double* reserve_inout, double* residue_inout, uint32_t flags,
                 pprg_query_stats* q, pprg_call_stats* c) {
   return guard([&] {
+    if (flags & PPRG_DETERMINISTIC) pprg::t_det = true;
     require(g && g->g, "null graph");
     require(k == 0 || (sources && reserve_inout && residue_inout), "null argument");
     check_alpha(alpha);
@@ -686,6 +697,7 @@ int pprg_speedppr(pprg_graph* g, const pprg_index* idx, const uint32_t* sources,
                   double alpha, double epsilon, double mu, uint64_t seed, double* estimates_out,
                   uint32_t flags, pprg_query_stats* q, pprg_call_stats* c) {
   return guard([&] {
+    if (flags & PPRG_DETERMINISTIC) pprg::t_det = true;
     require(g && g->g, "null graph");
     require(k == 0 || sources, "null sources");
     // QueryConfig::validate + speedppr.cpp:76-83

@@ -6,39 +6,12 @@
 
 namespace pprg {
 // ---- local phase / refine / FIFO: frontier levels in push form ------------
-// Entry = linear index i = u*K + c. One warp per entry: claim r with
-// atomicExch (the FIFO pop, push.cpp:38-41), x += r, scatter (1-a) r / deg_eff
-// with fp64 RED, and append newly active (t, c) once per level (stamp).
-// Frontier of one level: per column c a FIFO segment
-// cur[c*seg_cap, c*seg_cap + q_c) of node ids, so an entry's position in its
-// segment is the number of pops of column c before it.
-struct FrontierParams {
-  const uint64_t* off;
-  const uint32_t* nbr;
-  const uint32_t* deg;
-  double* res;
-  double* x;
-  unsigned* stamp;
-  const uint32_t* cur;
-  uint32_t* next;
-  uint64_t seg_cap;
-  uint64_t total;                 // sum of q_c
-  unsigned long long* col_cnt;    // [K] appends per column this level (= next segment length)
-  double* col_dr;                 // [K] alpha * sum r pushed
-  unsigned long long* col_np;     // [K] edge pushes
-  unsigned long long* col_nn;     // [K] node pushes
-  unsigned* col_stop;             // [K] set when the queue outgrows `limit` (push.cpp:38)
-  unsigned long long* col_resv;   // [K] out-degrees reserved by this level's pops
-  unsigned long long limit;
-  unsigned long long col_live;    // bit c set: column c still in this phase
-  unsigned level_tag;
-  int K;
-  double alpha;
-  uint64_t pre[KMAX + 1];         // segment prefix: column c owns [pre[c], pre[c+1])
-  uint32_t src[KMAX];
-  double thr[KMAX];
-};
-
+// Entry = (node v, column c) of the interleaved state i = v*K + c. Frontier of
+// one level: per column c a FIFO segment seg[c*seg_cap, c*seg_cap + q_c) of
+// node ids, so an entry's position in its segment is the number of pops of
+// column c before it. One warp per entry: claim r (the FIFO pop,
+// push.cpp:38-41), x += r, scatter (1-a) r / deg_eff over the out-edges
+// (push.cpp:44-56) and append each newly active (t, c) once per level (stamp).
 struct HeavyEntry {  // a frontier node whose scatter is spread over the grid
   uint64_t begin;    // first out-edge
   uint32_t deg;
@@ -46,26 +19,38 @@ struct HeavyEntry {  // a frontier node whose scatter is spread over the grid
   double share;
 };
 constexpr uint32_t HEAVY_DEG = 2048;
+constexpr uint32_t HEAVY_CHUNK = 1024;
 
 // Where a level's scatter lands: residues, the enqueue test's thresholds and
-// stamps, and column c's next segment with its append counter.
+// stamps, and column c's next segment with its append counter. DET: residues
+// are fixed-point integers (value * sc[c]) in the same 8-byte slots, so their
+// sums are exact and independent of the order of the atomics.
+template <bool DET>
 struct ScatterCtx {
   double* res;
   const uint32_t* deg;
-  const double* thr;              // [K] enqueue threshold per unit of deg_eff
+  const double* thr;              // [K] enqueue threshold per unit of deg_eff (DET: * sc)
+  const double* sc;               // [K] DET: fixed-point scale 2^S_c
   unsigned* stamp;
   unsigned tag;
   uint32_t* next;
   uint64_t seg_cap;
   int K;
   unsigned long long* col_cnt;    // [K] appends (= next segment length)
+  unsigned long long* col_deg;    // [K] DET with a queue limit: sum of the appended deg_eff, else null
 };
 
 // Append t to column c's next segment once per level when it becomes active
 // (drain_queue's enqueue test, push.cpp:49-53); one atomic per ballot group.
-__device__ __forceinline__ void maybe_append(const ScatterCtx& C, bool app, uint32_t t, int c,
-                                             unsigned mask) {
-  const unsigned bal = __ballot_sync(mask, app);
+template <bool DET>
+__device__ __forceinline__ void maybe_append(const ScatterCtx<DET>& C, bool app, uint32_t t, int c,
+                                             uint32_t td, unsigned mask) {
+  // every lane of the warp is here; `mask` is this lane's group (one column)
+  const unsigned bal = __ballot_sync(0xffffffffu, app) & mask;
+  if (DET && C.col_deg && bal) {
+    const unsigned dsum = __reduce_add_sync(mask, app ? (td ? td : 1u) : 0u);
+    if ((threadIdx.x & 31) == __ffs(bal) - 1) atomicAdd(C.col_deg + c, (unsigned long long)dsum);
+  }
   if (app) {
     const int lane = threadIdx.x & 31, leader = __ffs(bal) - 1;
     unsigned long long basepos = 0;
@@ -75,120 +60,63 @@ __device__ __forceinline__ void maybe_append(const ScatterCtx& C, bool app, uint
   }
 }
 
-__device__ __forceinline__ void relax_scatter(const ScatterCtx& C, uint32_t t, int c, double share,
+// share added to (t, c), then the enqueue test on the new value. The degree
+// of t is loaded before the atomic (independent of it).
+template <bool DET>
+__device__ __forceinline__ void relax_scatter(const ScatterCtx<DET>& C, uint32_t t, int c, double share,
                                               bool ok, unsigned mask) {
   bool app = false;
+  uint32_t td = 0;
   if (ok) {
     const uint64_t ti = (uint64_t)t * C.K + c;
-    const double nv = atomicAdd(C.res + ti, share) + share;
-    const uint32_t td = __ldg(C.deg + t);
+    td = __ldg(C.deg + t);
+    double nv;
+    if constexpr (DET) {
+      const long long q = __double2ll_rn(share * C.sc[c]);
+      nv = (double)(long long)(atomicAdd(reinterpret_cast<unsigned long long*>(C.res + ti),
+                                         (unsigned long long)q) + (unsigned long long)q);
+    } else {
+      nv = atomicAdd(C.res + ti, share) + share;
+    }
     if (nv > (double)(td ? td : 1) * C.thr[c])
       app = atomicExch(C.stamp + ti, C.tag) != C.tag;
   }
-  maybe_append(C, app, t, c, mask);
+  maybe_append(C, app, t, c, td, mask);
 }
 
-// Per-block counters of a level (shared), flushed once per block.
-struct LevelAcc {
-  double* dr;
-  unsigned long long* np;
-  unsigned long long* nn;
-};
-
-// One frontier entry (v, c) at position pos of its column's segment of
-// length q, popped by one warp: check drain_queue's loop condition (queue
-// size <= limit before the pop, push.cpp:38), claim r (the pop,
-// push.cpp:40-43), x += r, then scatter (1-a) r / deg_eff to the effective
-// out-neighbours with fp64 atomics, 4 independent atomics per lane in flight.
-// Entries with more than HEAVY_DEG out-edges are queued for the chunked
-// heavy scatter, so a hub never serialises one warp.
-__device__ __forceinline__ void pop_entry(const ScatterCtx& C, const uint64_t* off,
-                                          const uint32_t* nbr, double* x, double alpha,
-                                          uint32_t src_c, unsigned long long limit,
-                                          unsigned* col_stop, unsigned long long* col_resv,
-                                          uint32_t v, int c, uint64_t pos, uint64_t q,
-                                          const LevelAcc& la, HeavyEntry* heavy,
-                                          unsigned* heavy_cnt) {
-  const int lane = threadIdx.x & 31;
-  const uint64_t i = (uint64_t)v * C.K + c;
-  const uint32_t d = C.deg[v];
-  double r = 0.0;
-  if (lane == 0) {
-    bool stop = *(volatile unsigned*)(col_stop + c) != 0;
-    if (!stop && limit != ~0ull) {
-      // appends of the pops before this one are bounded by their out-degrees,
-      // reserved at pop time, so concurrent warps see the queue growth at once
-      const unsigned long long reserved = atomicAdd(col_resv + c, (unsigned long long)(d ? d : 1));
-      if (q - pos + reserved > limit) {
-        stop = true;
-        col_stop[c] = 1;
-      }
-    }
-    if (!stop) r = __longlong_as_double((long long)atomicExch((unsigned long long*)(C.res + i), 0ull));
-  }
-  r = __shfl_sync(0xffffffffu, r, 0);
-  if (!(r > 0.0)) return;
-  const uint64_t de = d ? d : 1;
-  const double share = (1.0 - alpha) * r / (double)de;
-  const uint64_t b = off[v];
-  if (lane == 0) {
-    x[i] += r;
-    atomicAdd(&la.dr[c], alpha * r);
-    atomicAdd(&la.np[c], (unsigned long long)de);
-    atomicAdd(&la.nn[c], 1ull);
-    if (de > HEAVY_DEG) heavy[atomicAdd(heavy_cnt, 1u)] = HeavyEntry{b, d, (uint32_t)c, share};
-  }
-  if (de > HEAVY_DEG) return;
-  for (uint64_t q0 = 0; q0 < de; q0 += 128) {
+// Scatter `share` over the de out-edges starting at b of an entry by its
+// group of GL lanes (every lane of the warp calls this; de = 0 for lanes
+// without an entry), four neighbour ids per lane in flight. Dead ends scatter
+// to the column's source.
+template <int GL>
+__device__ __forceinline__ unsigned group_mask() {
+  if constexpr (GL == 32) return 0xffffffffu;
+  else return ((1u << GL) - 1u) << ((threadIdx.x & 31) / GL * GL);
+}
+template <bool DET, int GL>
+__device__ __forceinline__ void group_scatter(const ScatterCtx<DET>& C, const uint32_t* nbr, uint64_t b,
+                                              uint32_t d, uint32_t src_c, int c, double share,
+                                              uint64_t de) {
+  const int sub = (threadIdx.x & 31) % GL;
+  const unsigned gm = group_mask<GL>();
+  const unsigned most = __reduce_max_sync(0xffffffffu, (unsigned)de);  // warp-uniform trip count
+  for (uint64_t q0 = 0; q0 < most; q0 += 4 * GL) {
     uint32_t t[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint64_t qq = q0 + lane + 32 * k;
+      const uint64_t qq = q0 + sub + GL * k;
       t[k] = qq < de ? (d ? __ldg(nbr + b + qq) : src_c) : 0xFFFFFFFFu;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) relax_scatter(C, t[k], c, share, t[k] != 0xFFFFFFFFu, 0xffffffffu);
-  }
-}
-
-// One level, one warp per frontier entry (host-driven drain: observed or
-// traced calls). Per-column counters accumulate in shared memory and are
-// flushed once per block.
-__global__ void __launch_bounds__(256) k_frontier(const __grid_constant__ FrontierParams P,
-                                                  HeavyEntry* heavy, unsigned* heavy_cnt) {
-  __shared__ double sh_dr[KMAX];
-  __shared__ unsigned long long sh_np[KMAX], sh_nn[KMAX];
-  __shared__ double sh_thr[KMAX];
-  const int K = P.K;
-  for (int i = threadIdx.x; i < K; i += blockDim.x)
-    sh_dr[i] = 0, sh_np[i] = 0, sh_nn[i] = 0, sh_thr[i] = P.thr[i];
-  __syncthreads();
-  const ScatterCtx C{P.res, P.deg, sh_thr, P.stamp, P.level_tag, P.next, P.seg_cap, K, P.col_cnt};
-  const LevelAcc la{sh_dr, sh_np, sh_nn};
-  const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t w = w0; w < P.total; w += nw) {
-    int c = 0;
-    while (w >= P.pre[c + 1]) ++c;
-    if (!((P.col_live >> c) & 1ull)) continue;
-    const uint64_t pos = w - P.pre[c];
-    const uint32_t v = P.cur[(uint64_t)c * P.seg_cap + pos];
-    pop_entry(C, P.off, P.nbr, P.x, P.alpha, P.src[c], P.limit, P.col_stop, P.col_resv, v, c, pos,
-              P.pre[c + 1] - P.pre[c], la, heavy, heavy_cnt);
-  }
-  __syncthreads();
-  for (int cc = threadIdx.x; cc < K; cc += blockDim.x) {
-    if (sh_dr[cc] != 0.0) atomicAdd(P.col_dr + cc, sh_dr[cc]);
-    if (sh_np[cc]) atomicAdd(P.col_np + cc, sh_np[cc]);
-    if (sh_nn[cc]) atomicAdd(P.col_nn + cc, sh_nn[cc]);
+    for (int k = 0; k < 4; ++k) relax_scatter(C, t[k], c, share, t[k] != 0xFFFFFFFFu, gm);
   }
 }
 
 // The scatter of one HEAVY_CHUNK-edge chunk of a heavy entry by one block,
 // four neighbour ids per thread loaded before the first atomic. Every lane of
 // a chunk shares the entry's column, so appends group the whole warp.
-constexpr uint32_t HEAVY_CHUNK = 1024;
-__device__ __forceinline__ void heavy_chunk(const ScatterCtx& C, const uint32_t* nbr,
+template <bool DET>
+__device__ __forceinline__ void heavy_chunk(const ScatterCtx<DET>& C, const uint32_t* nbr,
                                             const HeavyEntry& e, uint32_t first) {
   const uint32_t end = e.deg - first < HEAVY_CHUNK ? e.deg : first + HEAVY_CHUNK;
   const uint32_t q0 = first + threadIdx.x;
@@ -202,49 +130,43 @@ __device__ __forceinline__ void heavy_chunk(const ScatterCtx& C, const uint32_t*
   for (int i = 0; i < 4; ++i) relax_scatter(C, t[i], (int)e.c, e.share, t[i] != 0xFFFFFFFFu, 0xffffffffu);
 }
 
-struct HeavyChunk {
-  uint32_t h;      // heavy entry
-  uint32_t first;  // first out-edge of the chunk, relative to the entry
-};
-
-// host-built chunk list (host-driven drain), a block per chunk
-__global__ void __launch_bounds__(256) k_frontier_heavy_chunks(const __grid_constant__ FrontierParams P,
-                                                               const HeavyEntry* heavy,
-                                                               const HeavyChunk* chunks,
-                                                               unsigned nchunks) {
-  __shared__ double sh_thr[KMAX];
-  for (int i = threadIdx.x; i < P.K; i += blockDim.x) sh_thr[i] = P.thr[i];
-  __syncthreads();
-  const ScatterCtx C{P.res, P.deg, sh_thr, P.stamp, P.level_tag, P.next, P.seg_cap, P.K, P.col_cnt};
-  for (unsigned ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
-    const HeavyChunk k = chunks[ch];
-    heavy_chunk(C, P.nbr, heavy[k.h], k.first);
-  }
-}
-
-// ---- persistent drain: all levels of a drain in one cooperative launch -----
-// (drain_queue, push.cpp:34-59, level by level). The host-driven loop reads
-// the level counters back after every level (several round trips per level);
-// here every block derives the next level from the reduced counters itself:
-//   entries phase (warp per entry, heavy entries queued) | grid barrier |
-//   heavy phase (chunks of HEAVY_CHUNK edges, enumerated on the device from
-//   a block-wide scan of the heavy entries' chunk counts) | grid barrier |
-//   every block: r_sum -= alpha * pushed, queue sizes, stop tests -> next
-//   level's live columns and segment prefix.
-// Level counters are triple-buffered (slot = level % 3): slot level+1 is
+// ---- the drain: all levels of drain_queue (push.cpp:34-59) in one
+// cooperative launch, or one level per launch for observed / traced calls.
+// Per level:
+//   entries (warp per entry; heavy entries queued) | grid barrier |
+//   heavy entries (chunks of HEAVY_CHUNK edges, enumerated on the device from
+//   a block-wide scan of their chunk counts) | grid barrier |
+//   every block derives the next level from the reduced counters:
+//   r_sum -= alpha * pushed, queue sizes, the stop tests.
+// Level counters are triple-buffered (slot = level % 3); slot level+1 is
 // cleared during `level` by block 0, two barriers after its last reader.
+//
+// Fast mode: the pop (atomicExch) races with the same level's scatters to the
+// same entry, and the queue-limit test (push.cpp:38) runs before every pop
+// against the out-degrees reserved by the pops so far.
+// DET (PPRG_DETERMINISTIC): bitwise-reproducible. Every pop of a level
+// happens before any of its scatters (pop phase | grid barrier | scatter
+// phase), residues are fixed-point integers while the drain runs (exact,
+// order-independent sums), the queue limit is tested at level boundaries,
+// and the pushed mass is summed as integers. The set of entries of every
+// level is then a function of the inputs; their order in a segment is not,
+// and nothing depends on it.
 struct DrainCtl {
   GridBarrier gbar;
   unsigned long long cnt[3][KMAX];   // appends per column (next queue size)
   unsigned long long np[3][KMAX];    // edge pushes
   unsigned long long nn[3][KMAX];    // node pushes
   unsigned long long resv[3][KMAX];  // out-degrees reserved by pops (queue-limit test)
-  double dr[3][KMAX];                // alpha * pushed residue
+  unsigned long long qdeg[3][KMAX];  // DET: sum of deg_eff over the appended entries
+  double dr[3][KMAX];                // alpha * pushed residue (fast mode)
+  unsigned long long dq[3][KMAX];    // pushed residue, fixed point (DET)
   unsigned stop[3][KMAX];            // queue outgrew the limit
   unsigned heavy_cnt[3];
   unsigned levels_run;
   double out_rsum[KMAX];
   unsigned long long out_np[KMAX];
+  unsigned long long out_q[KMAX];
+  unsigned long long out_qdeg[KMAX];
   unsigned out_levels[KMAX];
   unsigned long long out_live;
 };
@@ -260,10 +182,12 @@ struct DrainParams {
   uint64_t seg_cap;
   HeavyEntry* heavy;
   DrainCtl* ctl;
+  unsigned long long* popv;          // DET: popped value of segment slot [c*seg_cap + pos]
   unsigned long long limit;          // queue limit (~0: none)
   unsigned long long live0;          // columns draining
   double lam_stop;                   // r_sum stop (0: none)
   double alpha;
+  uint64_t n;
   unsigned tag0;                     // level L stamps tag0 + L + 1 (no wrap: host-checked)
   unsigned max_levels;
   int K;
@@ -271,36 +195,54 @@ struct DrainParams {
   double thr[KMAX];
   double r_sum0[KMAX];
   unsigned long long q0[KMAX];       // first level's queue sizes
+  unsigned long long qdeg0[KMAX];    // DET: first level's sum of deg_eff
+  double sc[KMAX];                   // DET: fixed-point scale 2^S_c (all residues < 2^61 / sc)
 };
 
 constexpr int DRAIN_NT = 256;
 constexpr unsigned DRAIN_HSH = 2048;  // heavy entries whose chunk prefix is kept in shared memory
 
+template <bool DET, int GL>
 __global__ void __launch_bounds__(DRAIN_NT) k_drain(const __grid_constant__ DrainParams D) {
-  __shared__ double s_rsum[KMAX], s_thr[KMAX];
+  constexpr int NG = 32 / GL;  // entries per warp at a time
+  __shared__ double s_rsum[KMAX], s_thr[KMAX], s_sc[KMAX];
   __shared__ uint32_t s_src[KMAX];
-  __shared__ unsigned long long s_q[KMAX], s_pre[KMAX + 1], s_np[KMAX];
+  __shared__ unsigned long long s_q[KMAX], s_pre[KMAX + 1], s_np[KMAX], s_qd[KMAX];
   __shared__ unsigned s_lv[KMAX];
   __shared__ unsigned long long s_live;
   __shared__ double sh_dr[KMAX];
-  __shared__ unsigned long long sh_np[KMAX], sh_nn[KMAX];
+  __shared__ unsigned long long sh_np[KMAX], sh_nn[KMAX], sh_dq[KMAX];
   __shared__ unsigned s_hpre[DRAIN_HSH + 1];
   using Scan = cub::BlockScan<unsigned, DRAIN_NT>;
   __shared__ typename Scan::TempStorage scan_tmp;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int gid = lane / GL, sub = lane % GL;  // entry group of this lane, lane in the group
   const int K = D.K;
   DrainCtl* ctl = D.ctl;
   if (tid < KMAX) {
     s_rsum[tid] = D.r_sum0[tid];
-    s_thr[tid] = D.thr[tid];
+    s_sc[tid] = D.sc[tid];
+    s_thr[tid] = DET ? D.thr[tid] * D.sc[tid] : D.thr[tid];
     s_src[tid] = D.src[tid];
     s_q[tid] = D.q0[tid];
+    s_qd[tid] = D.qdeg0[tid];
     s_np[tid] = 0;
     s_lv[tid] = 0;
   }
   if (tid == 0) s_live = D.live0;
   __syncthreads();
+  const uint64_t gtid = blockIdx.x * (uint64_t)DRAIN_NT + tid;
+  const uint64_t gthreads = (uint64_t)gridDim.x * DRAIN_NT;
+  const uint64_t nk = D.n * (uint64_t)K;
   unsigned long long gen = 0;
+  if constexpr (DET) {  // residues of the draining columns to fixed point
+    for (uint64_t i = gtid; i < nk; i += gthreads) {
+      const int c = (int)(i % K);
+      if ((D.live0 >> c) & 1ull)
+        reinterpret_cast<long long*>(D.res)[i] = __double2ll_rn(D.res[i] * s_sc[c]);
+    }
+    grid_barrier2(&ctl->gbar, ++gen);
+  }
   uint32_t level = 0;
   for (;; ++level) {
     const int slot = (int)(level % 3);
@@ -312,7 +254,7 @@ __global__ void __launch_bounds__(DRAIN_NT) k_drain(const __grid_constant__ Drai
       }
       for (int c = K; c <= KMAX; ++c) s_pre[c] = t;
     }
-    if (tid < KMAX) sh_dr[tid] = 0.0, sh_np[tid] = 0, sh_nn[tid] = 0;
+    if (tid < KMAX) sh_dr[tid] = 0.0, sh_np[tid] = 0, sh_nn[tid] = 0, sh_dq[tid] = 0;
     __syncthreads();
     const unsigned long long total = s_pre[K];
     if (total == 0 || level >= D.max_levels) break;  // identical in every block
@@ -322,35 +264,112 @@ __global__ void __launch_bounds__(DRAIN_NT) k_drain(const __grid_constant__ Drai
       ctl->np[ns][tid] = 0;
       ctl->nn[ns][tid] = 0;
       ctl->resv[ns][tid] = 0;
+      ctl->qdeg[ns][tid] = 0;
       ctl->dr[ns][tid] = 0.0;
+      ctl->dq[ns][tid] = 0;
       ctl->stop[ns][tid] = 0;
       if (tid == 0) ctl->heavy_cnt[ns] = 0;
     }
-    const ScatterCtx C{D.res, D.deg, s_thr, D.stamp, D.tag0 + level + 1, D.seg[(level + 1) & 1],
-                       D.seg_cap, K, ctl->cnt[slot]};
-    const LevelAcc la{sh_dr, sh_np, sh_nn};
+    const ScatterCtx<DET> C{D.res, D.deg, s_thr, s_sc, D.stamp, D.tag0 + level + 1,
+                            D.seg[(level + 1) & 1], D.seg_cap, K, ctl->cnt[slot],
+                            DET && D.limit != ~0ull ? ctl->qdeg[slot] : nullptr};
     const uint32_t* cur = D.seg[level & 1];
-    {
-      const uint64_t w0 = (blockIdx.x * (uint64_t)DRAIN_NT + tid) >> 5;
-      const uint64_t nw = ((uint64_t)gridDim.x * DRAIN_NT) >> 5;
-      for (uint64_t w = w0; w < total; w += nw) {
-        int c = 0;
-        while (w >= s_pre[c + 1]) ++c;
-        const uint64_t pos = w - s_pre[c];
-        const uint32_t v = cur[(uint64_t)c * D.seg_cap + pos];
-        pop_entry(C, D.off, D.nbr, D.x, D.alpha, s_src[c], D.limit, ctl->stop[slot], ctl->resv[slot], v,
-                  c, pos, s_pre[c + 1] - s_pre[c], la, D.heavy, &ctl->heavy_cnt[slot]);
+    // entries are taken NG = 32/GL at a time per warp, GL lanes per entry:
+    // the pop chain (claim, then scatter, then append) of NG entries is in
+    // flight at once instead of one
+    const uint64_t w0 = (gtid >> 5) * NG, nw = (gthreads >> 5) * NG;
+    // ---- pops (fast mode: and their scatters) ------------------------------
+    for (uint64_t w = w0; w < total; w += nw) {
+      const uint64_t e = w + gid;
+      const bool valid = e < total;
+      int c = 0;
+      uint64_t pos = 0, seg_i = 0, de = 1, b = 0, i = 0;
+      uint32_t d = 0;
+      if (valid) {
+        while (e >= s_pre[c + 1]) ++c;
+        pos = e - s_pre[c];
+        seg_i = (uint64_t)c * D.seg_cap + pos;
+        const uint32_t v = cur[seg_i];
+        i = (uint64_t)v * K + c;
+        d = D.deg[v];
+        de = d ? d : 1;
+        b = D.off[v];
       }
+      double r = 0.0;
+      unsigned long long rq = 0;
+      if (valid && sub == 0) {
+        if constexpr (DET) {
+          rq = atomicExch(reinterpret_cast<unsigned long long*>(D.res) + i, 0ull);
+          D.popv[seg_i] = rq;
+          r = (double)(long long)rq / s_sc[c];
+        } else {
+          bool stop = false;
+          if (D.limit != ~0ull) {
+            stop = *(volatile unsigned*)(ctl->stop[slot] + c) != 0;
+            if (!stop) {
+              // appends of the pops before this one are bounded by their
+              // out-degrees, reserved at pop time, so concurrent warps see the
+              // queue growth at once
+              const unsigned long long reserved = atomicAdd(ctl->resv[slot] + c, de);
+              if (s_pre[c + 1] - s_pre[c] - pos + reserved > D.limit) {
+                stop = true;
+                ctl->stop[slot][c] = 1;
+              }
+            }
+          }
+          if (!stop)
+            r = __longlong_as_double((long long)atomicExch((unsigned long long*)(D.res + i), 0ull));
+        }
+      }
+      r = __shfl_sync(0xffffffffu, r, gid * GL);
+      const bool ok = r > 0.0;
+      const double share = (1.0 - D.alpha) * r / (double)de;
+      if (ok && sub == 0) {
+        D.x[i] += r;
+        if constexpr (DET) atomicAdd(&sh_dq[c], rq);
+        else atomicAdd(&sh_dr[c], D.alpha * r);
+        atomicAdd(&sh_np[c], (unsigned long long)de);
+        atomicAdd(&sh_nn[c], 1ull);
+        if (de > HEAVY_DEG) D.heavy[atomicAdd(&ctl->heavy_cnt[slot], 1u)] = HeavyEntry{b, d, (uint32_t)c, share};
+      }
+      if constexpr (!DET)
+        group_scatter<DET, GL>(C, D.nbr, b, d, s_src[c], c, share, ok && de <= HEAVY_DEG ? de : 0);
     }
     __syncthreads();
     if (tid < K) {
       if (sh_dr[tid] != 0.0) atomicAdd(&ctl->dr[slot][tid], sh_dr[tid]);
+      if (sh_dq[tid]) atomicAdd(&ctl->dq[slot][tid], sh_dq[tid]);
       if (sh_np[tid]) atomicAdd(&ctl->np[slot][tid], sh_np[tid]);
       if (sh_nn[tid]) atomicAdd(&ctl->nn[slot][tid], sh_nn[tid]);
     }
     grid_barrier2(&ctl->gbar, ++gen);
+    if constexpr (DET) {  // ---- scatters, after every pop of the level ----------
+      for (uint64_t w = w0; w < total; w += nw) {
+        const uint64_t e = w + gid;
+        int c = 0;
+        uint64_t de = 0, b = 0;
+        uint32_t d = 0;
+        double share = 0.0;
+        if (e < total) {
+          while (e >= s_pre[c + 1]) ++c;
+          const uint64_t seg_i = (uint64_t)c * D.seg_cap + (e - s_pre[c]);
+          const long long rq = (long long)__ldcg(D.popv + seg_i);
+          if (rq > 0) {
+            const uint32_t v = __ldcg(cur + seg_i);
+            d = D.deg[v];
+            const uint64_t dd = d ? d : 1;
+            if (dd <= HEAVY_DEG) {
+              de = dd;
+              b = D.off[v];
+              share = (1.0 - D.alpha) * ((double)rq / s_sc[c]) / (double)dd;
+            }
+          }
+        }
+        group_scatter<DET, GL>(C, D.nbr, b, d, s_src[c], c, share, de);
+      }
+    }
     const unsigned nh = __ldcg(&ctl->heavy_cnt[slot]);
-    if (nh) {
+    if (nh) {  // ---- heavy entries ------------------------------------------
       if (nh <= DRAIN_HSH) {
         // chunk prefix of the heavy entries (every block computes the same)
         unsigned run = 0;
@@ -388,23 +407,41 @@ __global__ void __launch_bounds__(DRAIN_NT) k_drain(const __grid_constant__ Drai
           for (uint32_t f = 0; f < e.deg; f += HEAVY_CHUNK) heavy_chunk(C, D.nbr, e, f);
         }
       }
-      grid_barrier2(&ctl->gbar, ++gen);
     }
-    // the next level, identically in every block (drain_queue's loop test)
+    if (DET || nh) grid_barrier2(&ctl->gbar, ++gen);
+    // ---- the next level, identically in every block (drain_queue's loop test)
     if (tid < K && ((s_live >> tid) & 1ull)) {
-      s_rsum[tid] -= __ldcg(&ctl->dr[slot][tid]);
+      if constexpr (DET)
+        s_rsum[tid] -= D.alpha * ((double)(long long)__ldcg(&ctl->dq[slot][tid]) / s_sc[tid]);
+      else
+        s_rsum[tid] -= __ldcg(&ctl->dr[slot][tid]);
       s_np[tid] += __ldcg(&ctl->np[slot][tid]);
       s_lv[tid] += 1;
       const unsigned long long q = __ldcg(&ctl->cnt[slot][tid]);
       s_q[tid] = q;
-      const bool still = q > 0 && q <= D.limit && !(D.lam_stop > 0 && s_rsum[tid] <= D.lam_stop);
+      // DET: a level runs only if no sequence of its pops can take the queue
+      // past the limit (its entries' deg_eff bound their appends); the fast
+      // mode stops mid-level at the first pop that could
+      const unsigned long long qd = __ldcg(&ctl->qdeg[slot][tid]);
+      s_qd[tid] = qd;
+      const bool still = q > 0 && (DET && D.limit != ~0ull ? q + qd <= D.limit : q <= D.limit) &&
+                         !(D.lam_stop > 0 && s_rsum[tid] <= D.lam_stop);
       if (__ldcg(&ctl->stop[slot][tid]) || !still) atomicAnd(&s_live, ~(1ull << tid));
     }
     __syncthreads();
   }
+  if constexpr (DET) {  // back to doubles (every scatter completed before the last barrier)
+    for (uint64_t i = gtid; i < nk; i += gthreads) {
+      const int c = (int)(i % K);
+      if ((D.live0 >> c) & 1ull)
+        D.res[i] = (double)reinterpret_cast<const long long*>(D.res)[i] / s_sc[c];
+    }
+  }
   if (blockIdx.x == 0 && tid < KMAX) {
     ctl->out_rsum[tid] = s_rsum[tid];
     ctl->out_np[tid] = s_np[tid];
+    ctl->out_q[tid] = s_q[tid];
+    ctl->out_qdeg[tid] = s_qd[tid];
     ctl->out_levels[tid] = s_lv[tid];
     if (tid == 0) {
       ctl->out_live = s_live;
@@ -438,6 +475,41 @@ __global__ void k_scan_active(const double* res, const uint32_t* deg, uint64_t n
       out[(uint64_t)c * seg_cap + b + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)(i / K);
     }
   }
+}
+
+// Deterministic per-column sums (PPRG_DETERMINISTIC): out[c] = scale *
+// sum over rows r of a[row(r)*K + c], row(r) = rows ? rows[r] : r. A fixed
+// grid of DSUM_BLOCKS blocks; thread t of a block owns column t % K and a
+// fixed stride of rows, summed in order; the block's row groups meet in a
+// fixed order in shared memory, and k_dsum_final adds the blocks' partials in
+// block order. Same bits on every run and every device.
+constexpr int DSUM_BLOCKS = 296;
+constexpr int DSUM_NT = 256;
+__global__ void __launch_bounds__(DSUM_NT) k_dsum_part(const double* a, const uint32_t* rows,
+                                                       uint64_t nrows, int K, double* part) {
+  __shared__ double sh[DSUM_NT];
+  const int tid = threadIdx.x;
+  const int groups = DSUM_NT / K;  // K divides 256 (a power of two <= 64)
+  const int c = tid % K, grp = tid / K;
+  double s = 0.0;
+  for (uint64_t r = (uint64_t)blockIdx.x * groups + grp; r < nrows; r += (uint64_t)gridDim.x * groups) {
+    const uint64_t row = rows ? rows[r] : r;
+    s += a[row * K + c];
+  }
+  sh[tid] = s;
+  __syncthreads();
+  if (tid < K) {
+    double t = 0.0;
+    for (int g2 = 0; g2 < groups; ++g2) t += sh[g2 * K + tid];
+    part[(uint64_t)blockIdx.x * K + tid] = t;
+  }
+}
+__global__ void k_dsum_final(const double* part, int nblocks, int K, double scale, double* out) {
+  const int c = threadIdx.x;
+  if (c >= K) return;
+  double t = 0.0;
+  for (int b = 0; b < nblocks; ++b) t += part[(uint64_t)b * K + c];
+  out[c] = scale * t;
 }
 
 // per-column sums of an [n*K] array (exact r_sum recompute, push.cpp:9-15).

@@ -171,6 +171,14 @@ struct StepSink {
   std::vector<double> hr, hq;
 };
 extern thread_local StepSink* g_obs;
+// Deterministic mode of the current call (PPRG_DETERMINISTIC): bitwise-
+// reproducible results, set by the C ABI for the duration of one call.
+extern thread_local bool t_det;
+struct DetScope {
+  bool prev;
+  explicit DetScope(bool on) : prev(t_det) { t_det = on; }
+  ~DetScope() { t_det = prev; }
+};
 uint64_t host_now_ns();
 uint64_t device_now_ns(Graph& g);
 

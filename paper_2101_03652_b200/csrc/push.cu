@@ -25,6 +25,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include <cub/cub.cuh>
@@ -66,10 +67,9 @@ struct Workspace {
   DevBuf<double> dcols;                 // col_dr[K], colsum[K], D[K]
   DevBuf<uint32_t> d_src;
   DevBuf<HeavyEntry> heavy;
-  DevBuf<unsigned> heavy_cnt;
-  DevBuf<unsigned> col_stop;
-  DevBuf<unsigned long long> heavy_chunks;
   DevBuf<DrainCtl> drain_ctl;
+  DevBuf<unsigned long long> popv;      // deterministic drains: popped value per segment slot
+  DevBuf<double> dsum_part;             // deterministic column sums: per-block partials
   unsigned level_tag = 0;
 };
 
@@ -92,11 +92,9 @@ static void ws_alloc(Workspace& w, Graph& g, int K) {
   w.fb.alloc(nk + 1);
   w.ctl.alloc(1);
   w.counters.alloc(1 + 5 * KMAX);
-  w.col_stop.alloc(KMAX);
   w.dcols.alloc(3 * KMAX);
   w.d_src.alloc(KMAX);
   w.heavy.alloc((g.m / HEAVY_DEG + 1) * (uint64_t)K + 1);
-  w.heavy_cnt.alloc(1);
 }
 
 static void ws_tiles(Workspace& w, Graph& g, uint64_t ntiles, uint64_t nhubs) {
@@ -156,13 +154,12 @@ inline unsigned grid_for(uint64_t items, int tb = 256) {
   return (unsigned)b;
 }
 
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
-
   const size_t wide_bytes = 8ull * (RMAX_W + 1) + 8ull * RMAX_W + 8ull * (NT / 32) * K +
                             4ull * (3 * RMAX_W + 1) + 16;
   const size_t smem = K >= WIDE_K ? wide_bytes : P.k1w ? k1w_bytes : Tile<K>::bytes;
-  auto kern = k_sweeps<K, MODE>;
+  auto kern = k_sweeps<K, MODE, DET>;
   static bool attr_set = false;
   if (!attr_set) {
     const size_t most = K >= WIDE_K ? wide_bytes : std::max(k1w_bytes, Tile<K>::bytes);
@@ -199,18 +196,24 @@ void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
   PPRG_CUDA(cudaGetLastError());
 }
 
-template <int MODE>
-void dispatch_sweeps(Graph& g, int K, SweepParams& P, bool coop) {
+template <int MODE, bool DET>
+void dispatch_sweeps_t(Graph& g, int K, SweepParams& P, bool coop) {
   switch (K) {
-    case 1: launch_sweeps<1, MODE>(g, P, coop); break;
-    case 2: launch_sweeps<2, MODE>(g, P, coop); break;
-    case 4: launch_sweeps<4, MODE>(g, P, coop); break;
-    case 8: launch_sweeps<8, MODE>(g, P, coop); break;
-    case 16: launch_sweeps<16, MODE>(g, P, coop); break;
-    case 32: launch_sweeps<32, MODE>(g, P, coop); break;
-    case 64: launch_sweeps<64, MODE>(g, P, coop); break;
+    case 1: launch_sweeps<1, MODE, DET>(g, P, coop); break;
+    case 2: launch_sweeps<2, MODE, DET>(g, P, coop); break;
+    case 4: launch_sweeps<4, MODE, DET>(g, P, coop); break;
+    case 8: launch_sweeps<8, MODE, DET>(g, P, coop); break;
+    case 16: launch_sweeps<16, MODE, DET>(g, P, coop); break;
+    case 32: launch_sweeps<32, MODE, DET>(g, P, coop); break;
+    case 64: launch_sweeps<64, MODE, DET>(g, P, coop); break;
     default: fail(EINTERNAL, "unsupported column block");
   }
+}
+// the deterministic sweeps (k_sweeps<K, MODE, true>) when the call asked for them
+template <int MODE>
+void dispatch_sweeps(Graph& g, int K, SweepParams& P, bool coop) {
+  if (t_det) dispatch_sweeps_t<MODE, true>(g, K, P, coop);
+  else dispatch_sweeps_t<MODE, false>(g, K, P, coop);
 }
 
 int round_k(uint32_t k) {
@@ -342,6 +345,8 @@ struct Block {
   uint32_t k;
   uint64_t ntiles = 0;
   const TileDesc* desc = nullptr;
+  const Graph::Plan* plan = nullptr;
+  double* yfin = nullptr;  // y after the global phase (deterministic sweeps alternate y0 / y1)
   uint64_t nhubs = 0;
   double alpha;
   std::vector<uint32_t> src;
@@ -361,12 +366,14 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   const int K = round_k(k);
   uint64_t ntiles = 0;
   const TileDesc* dsc = nullptr;
+  const Graph::Plan* plan = nullptr;
   uint64_t nhubs = 0;
   if (need_pull) {
     const Graph::Plan& pl = g.tile_plan(tile_edges(g, K), tile_rmax(g, K), tile_hub(g, K));
     dsc = pl.tiles.get();
     ntiles = pl.ntiles;
     nhubs = pl.nhubs;
+    plan = &pl;
   }
   if (own) {
     if (!own->K) ws_alloc(*own, g, K);
@@ -376,6 +383,8 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   Block b(g, w, K, k, alpha);
   b.ntiles = ntiles;
   b.desc = dsc;
+  b.plan = plan;
+  b.yfin = w.y0.get();
   b.nhubs = nhubs;
   for (uint32_t c = 0; c < k; ++c) b.src[c] = sources[c];
   for (int c = k; c < K; ++c) b.src[c] = sources[0];  // padding columns are inert
@@ -413,6 +422,49 @@ SweepParams base_params(Block& b) {
   return P;
 }
 
+// Per-column sums of an interleaved [row * K + c] array into dst[0..K)
+// (device): dst[c] = scale * sum over rows (rows[r] if given, else r < nrows).
+// Deterministic mode: fixed-grid, fixed-order partials (k_dsum_*); else fp64
+// atomics (k_colsum; rows / scale unsupported there).
+void det_colsum(Block& b, const double* a, const uint32_t* rows, uint64_t nrows, double scale,
+                double* dst) {
+  Workspace& w = b.w;
+  cudaStream_t st = b.g.stream;
+  if (w.dsum_part.n < (size_t)DSUM_BLOCKS * KMAX) w.dsum_part.alloc((size_t)DSUM_BLOCKS * KMAX);
+  k_dsum_part<<<DSUM_BLOCKS, DSUM_NT, 0, st>>>(a, rows, nrows, b.K, w.dsum_part.get());
+  k_dsum_final<<<1, KMAX, 0, st>>>(w.dsum_part.get(), DSUM_BLOCKS, b.K, scale, dst);
+  PPRG_CUDA(cudaGetLastError());
+}
+
+// Deterministic sweeps: the tile plan cut into waves of ~equal in-edges at
+// row-start tiles (hub pieces of one row stay in one wave). PPRG_DET_WAVES
+// (default 8): 1 = Jacobi sweeps; more waves read more of the sweep's own
+// updates (Gauss-Seidel between waves) and take fewer sweeps.
+void set_waves(Block& b, SweepParams& P) {
+  static const int W = [] {
+    const char* e = std::getenv("PPRG_DET_WAVES");
+    const int v = e ? std::atoi(e) : 8;
+    return v < 1 ? 1 : v > WMAX ? WMAX : v;
+  }();
+  const std::vector<TileDesc>& t = b.plan->host;
+  uint64_t total = 0;
+  for (const TileDesc& d : t) total += d.ne;
+  P.wave_tile[0] = 0;
+  P.wave_node[0] = 0;  // sources without in-edges are written before wave 0
+  uint32_t w = 1;
+  uint64_t acc = 0;
+  for (uint64_t j = 0; j < t.size() && (int)w < W; ++j) {
+    if (acc * W >= total * w && t[j].piece == 0 && j > P.wave_tile[w - 1]) {
+      P.wave_tile[w] = j;
+      d2h_small(&P.wave_node[w], b.g.cin_row.get() + t[j].r0, 4, b.g.stream);
+      ++w;
+    }
+    acc += t[j].ne;
+  }
+  P.wave_tile[w] = t.size();
+  P.nwaves = w;
+}
+
 // Observed calls: column 0's reserve / residue (device, interleaved with the
 // block's K) to the host sink.
 void emit_step(Block& b, const double* reserve_src, double reserve_scale, const double* residue_src,
@@ -434,11 +486,14 @@ void emit_step(Block& b, const double* reserve_src, double reserve_scale, const 
 
 // Frontier levels (drain_queue, push.cpp:34-59) for every column in
 // `state == 0`. The initial frontier is seed_source (push.cpp:61-66) or, for
-// refine, every active node in id order (push.cpp:212-218). A level is
-// drained in FIFO-ordered chunks so the reference's loop conditions --
-// queue size <= limit and r_sum > lambda_stop, checked before every pop --
-// are re-checked every chunk: the queue size of column c at that point is its
-// unprocessed entries of this level plus its entries appended to the next.
+// refine, every active node in id order (push.cpp:212-218). The reference's
+// loop conditions -- queue size <= limit and r_sum > lambda_stop, checked
+// before every pop -- are tested on the device (k_drain): the queue size of
+// column c at a pop is its unprocessed entries of this level plus the
+// out-degrees reserved by the level's pops so far (fast mode), or the level's
+// size at level boundaries (deterministic mode).
+// Unobserved calls run every level in one launch; observed / traced calls
+// (and PPRG_DEBUG_LOCAL) one level per launch, reporting after each.
 void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool from_scan,
                   std::vector<int>& state, CallStats* call) {
   Graph& g = b.g;
@@ -446,221 +501,141 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
   const int K = b.K;
   const uint64_t n = g.n, nk = n * (uint64_t)K;
   cudaStream_t st = g.stream;
-  FrontierParams F;
-  std::memset(&F, 0, sizeof F);
-  F.off = g.off.get();
-  F.nbr = g.nbr.get();
-  F.deg = g.deg.get();
-  F.res = w.res.get();
-  F.x = w.x.get();
-  F.stamp = w.stamp.get();
-  F.K = K;
-  F.alpha = b.alpha;
-  F.seg_cap = n;
-  F.limit = limit == UINT64_MAX ? ~0ull : (unsigned long long)limit;
-  for (int c = 0; c < K; ++c) {
-    F.src[c] = b.src[c];
-    F.thr[c] = r_max;
-  }
-  const int NC = 1 + 5 * KMAX;
-  unsigned long long* col_cnt = w.counters.get() + 1;
-  unsigned long long* col_np = col_cnt + KMAX;
-  unsigned long long* col_nn = col_np + KMAX;
-  double* col_dr = w.dcols.get();
-  unsigned* d_stop = w.col_stop.get();
+  const bool det = t_det;
   uint32_t* cur = w.fa.get();
   uint32_t* nxt = w.fb.get();
-  std::vector<uint64_t> qsize(K, 0);
-  auto next_tag = [&] {
-    if (++w.level_tag == 0) {
-      PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, st));
-      w.level_tag = 1;
-    }
-    return w.level_tag;
-  };
+  std::vector<uint64_t> qsize(K, 0), qdeg(K, 0);
+  if (++w.level_tag == 0 || w.level_tag >= 0x80000000u) {  // keep tag + levels from wrapping
+    PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, st));
+    w.level_tag = 1;
+  }
   unsigned long long live0 = 0;
   for (uint32_t c = 0; c < b.k; ++c)
     if (state[c] == 0) live0 |= 1ull << c;
-  std::vector<unsigned long long> hc(NC);
   if (from_scan) {
+    const int NC = 1 + 5 * KMAX;
+    unsigned long long* col_cnt = w.counters.get() + 1;
     std::vector<double> thr(KMAX, r_max);
+    std::vector<unsigned long long> hc(NC);
     PPRG_CUDA(cudaMemcpyAsync(w.dcols.get() + KMAX, thr.data(), 8 * KMAX, cudaMemcpyHostToDevice, st));
     PPRG_CUDA(cudaMemsetAsync(w.counters.get(), 0, 8 * NC, st));
     k_scan_active<<<grid_for(nk), 256, 0, st>>>(w.res.get(), g.deg.get(), n, K, w.dcols.get() + KMAX,
-                                                live0, w.stamp.get(), next_tag(), cur, n, col_cnt);
+                                                live0, w.stamp.get(), w.level_tag, cur, n, col_cnt);
     d2h_small(hc.data(), w.counters.get(), 8 * NC, st);
-    PPRG_CUDA(cudaStreamSynchronize(st));
     for (int c = 0; c < K; ++c) qsize[c] = hc[1 + c];
     call->kernel_launches += 1;
   } else {
     std::vector<uint32_t> hdeg(K);
     for (int c = 0; c < K; ++c)
       d2h_small(&hdeg[c], g.deg.get() + b.src[c], 4, st);
-    PPRG_CUDA(cudaStreamSynchronize(st));
     for (uint32_t c = 0; c < b.k; ++c)  // seed_source, push.cpp:61-66
       if (state[c] == 0 && 1.0 > (double)(hdeg[c] ? hdeg[c] : 1) * r_max) {
         PPRG_CUDA(cudaMemcpyAsync(cur + (uint64_t)c * n, &b.src[c], 4, cudaMemcpyHostToDevice, st));
         qsize[c] = 1;
+        qdeg[c] = hdeg[c] ? hdeg[c] : 1;
       }
   }
-  std::vector<double> hdr(KMAX);
-  std::vector<unsigned> hstop(KMAX);
   unsigned long long live = 0;
+  // (deterministic mode with a queue limit: the level's deg_eff sum too, see k_drain)
+  const bool det_limit = det && limit != UINT64_MAX && !from_scan;
   auto still_live = [&](uint32_t c, uint64_t queued) {
-    return queued > 0 && queued <= limit && !(lam_stop > 0 && b.r_sum[c] <= lam_stop);
+    return queued > 0 && (det_limit ? queued + qdeg[c] : queued) <= limit &&
+           !(lam_stop > 0 && b.r_sum[c] <= lam_stop);
   };
   for (uint32_t c = 0; c < b.k; ++c) {
     if (state[c] != 0) continue;
     if (still_live(c, qsize[c])) live |= 1ull << c;
     else state[c] = 1;
   }
-  // Unobserved calls: every level in one persistent launch (k_drain), one
-  // read-back per drain instead of several per level.
-  static const bool host_levels = std::getenv("PPRG_HOST_LEVELS") != nullptr;
-  if (live && !g_obs && !g_trace && !host_levels && !std::getenv("PPRG_DEBUG_LOCAL")) {
-    if (!w.drain_ctl.get()) w.drain_ctl.alloc(1);
-    if (w.level_tag >= 0x80000000u) {  // level L stamps level_tag + L + 1: keep it from wrapping
-      PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, st));
-      w.level_tag = 0;
-    }
-    DrainParams D;
-    std::memset(&D, 0, sizeof D);
-    D.off = g.off.get();
-    D.nbr = g.nbr.get();
-    D.deg = g.deg.get();
-    D.res = w.res.get();
-    D.x = w.x.get();
-    D.stamp = w.stamp.get();
+  static const bool debug = std::getenv("PPRG_DEBUG_LOCAL") != nullptr;
+  const bool stepwise = g_obs || g_trace || debug;
+  if (!w.drain_ctl.get()) w.drain_ctl.alloc(1);
+  if (det && w.popv.n < nk) w.popv.alloc(nk);
+  DrainParams D;
+  std::memset(&D, 0, sizeof D);
+  D.off = g.off.get();
+  D.nbr = g.nbr.get();
+  D.deg = g.deg.get();
+  D.res = w.res.get();
+  D.x = w.x.get();
+  D.stamp = w.stamp.get();
+  D.seg_cap = n;
+  D.heavy = w.heavy.get();
+  D.ctl = w.drain_ctl.get();
+  D.popv = det ? w.popv.get() : nullptr;
+  D.limit = limit == UINT64_MAX ? ~0ull : (unsigned long long)limit;
+  D.lam_stop = lam_stop;
+  D.alpha = b.alpha;
+  D.n = n;
+  D.K = K;
+  for (int c = 0; c < K; ++c) {
+    D.src[c] = b.src[c];
+    D.thr[c] = r_max;
+    // DET fixed point: every residue and every sum of residues of column c
+    // stays below its r_sum <= 2^e, so scale by 2^(61 - e)
+    int e = 0;
+    std::frexp(b.r_sum[c] > 0 ? b.r_sum[c] : 1.0, &e);
+    D.sc[c] = std::ldexp(1.0, 61 - e);
+  }
+  // lanes per frontier entry (PPRG_DRAIN_GL: 4, 8, 16 or 32). A whole warp
+  // per entry measured best: 8 lanes per entry (4 entries per warp in
+  // flight) took the configs[3] frontier 0.63 -> 0.76 ms per query, 4 lanes
+  // 0.94 ms (profiles/r02_drain_gl_ab.txt)
+  static const int gl = [] {
+    const char* e = std::getenv("PPRG_DRAIN_GL");
+    const int v = e ? std::atoi(e) : 32;
+    return v == 4 || v == 8 || v == 16 ? v : 32;
+  }();
+  auto pick = [&](auto det_tag) {
+    constexpr bool DT = decltype(det_tag)::value;
+    return gl == 4 ? k_drain<DT, 4> : gl == 16 ? k_drain<DT, 16> : gl == 32 ? k_drain<DT, 32> : k_drain<DT, 8>;
+  };
+  auto kern = det ? pick(std::true_type{}) : pick(std::false_type{});
+  static int per_sm[2] = {0, 0};
+  int& ps = per_sm[det];
+  if (!ps) PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, DRAIN_NT, 0));
+  if (ps < 1) fail(EINTERNAL, "drain kernel cannot be resident");
+  while (live) {
     D.seg[0] = cur;
     D.seg[1] = nxt;
-    D.seg_cap = n;
-    D.heavy = w.heavy.get();
-    D.ctl = w.drain_ctl.get();
-    D.limit = limit == UINT64_MAX ? ~0ull : (unsigned long long)limit;
     D.live0 = live;
-    D.lam_stop = lam_stop;
-    D.alpha = b.alpha;
     D.tag0 = w.level_tag;
-    D.max_levels = 0xFFFFFFFFu - w.level_tag - 1;
-    D.K = K;
+    D.max_levels = stepwise ? 1u : 0xFFFFFFFFu - w.level_tag - 1;
     for (int c = 0; c < K; ++c) {
-      D.src[c] = b.src[c];
-      D.thr[c] = r_max;
       D.r_sum0[c] = b.r_sum[c];
       D.q0[c] = ((live >> c) & 1ull) ? qsize[c] : 0;
+      D.qdeg0[c] = qdeg[c];
     }
     PPRG_CUDA(cudaMemsetAsync(D.ctl, 0, sizeof(DrainCtl), st));
-    static int per_sm = [] {
-      int v = 0;
-      PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_drain, DRAIN_NT, 0));
-      return v;
-    }();
-    if (per_sm < 1) fail(EINTERNAL, "drain kernel cannot be resident");
     void* args[] = {(void*)&D};
-    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)k_drain, dim3((unsigned)(per_sm * g.sm_count)),
-                                          dim3(DRAIN_NT), args, 0, st));
+    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)(ps * g.sm_count)), dim3(DRAIN_NT),
+                                          args, 0, st));
     PPRG_CUDA(cudaGetLastError());
     call->kernel_launches += 1;
     DrainCtl hd;
     d2h_small(&hd, D.ctl, sizeof hd, st);
-    if (hd.out_live) fail(EINTERNAL, "drain: level limit reached");
     w.level_tag += hd.levels_run;
+    if (debug && hd.levels_run) {
+      unsigned long long nn = 0, np = 0, app = 0, tot = 0;
+      for (uint32_t c = 0; c < b.k; ++c)
+        nn += hd.nn[0][c], np += hd.np[0][c], app += hd.cnt[0][c], tot += ((live >> c) & 1ull) ? qsize[c] : 0;
+      std::fprintf(stderr, "level: entries %llu heavy %u node_pushes %llu edge_pushes %llu appended %llu\n",
+                   tot, hd.heavy_cnt[0], nn, np, app);
+    }
     for (uint32_t c = 0; c < b.k; ++c) {
       if (!((live >> c) & 1ull)) continue;
       b.r_sum[c] = hd.out_rsum[c];
       b.pushes[c] += hd.out_np[c];
       b.levels[c] += hd.out_levels[c];
+      qsize[c] = hd.out_q[c];
+      qdeg[c] = hd.out_qdeg[c];
     }
-    live = 0;
-  }
-  while (live) {
-    uint64_t total = 0;
-    for (int c = 0; c < K; ++c) {
-      F.pre[c] = total;
-      total += ((live >> c) & 1ull) ? qsize[c] : 0;
-    }
-    F.pre[K] = total;
-    for (int c = K + 1; c <= KMAX; ++c) F.pre[c] = total;
-    if (!total) break;
-    PPRG_CUDA(cudaMemsetAsync(w.counters.get(), 0, 8 * NC, st));
-    PPRG_CUDA(cudaMemsetAsync(col_dr, 0, 8 * KMAX, st));
-    PPRG_CUDA(cudaMemsetAsync(d_stop, 0, 4 * KMAX, st));
-    PPRG_CUDA(cudaMemsetAsync(w.heavy_cnt.get(), 0, 4, st));
-    // the segments of the live columns are read in place (pre[] skips the others)
-    F.cur = cur;
-    F.next = nxt;
-    F.total = total;
-    F.col_cnt = col_cnt;
-    F.col_dr = col_dr;
-    F.col_np = col_np;
-    F.col_nn = col_nn;
-    F.col_stop = d_stop;
-    F.col_resv = col_nn + KMAX;
-    F.col_live = live;
-    F.level_tag = next_tag();
-    // live columns are contiguous in pre[] but their segments sit at c*n: the
-    // kernel maps (c, pos) -> cur[c*n + pos]
-    {
-      // grid-stride over the entries with at most PPRG_FRONTIER_BPS blocks per SM
-      // (0 = one warp per entry): fewer short-lived blocks and block barriers.
-      // 24 measured best: configs[2] local phase 8.5 -> 6.8 ms per 64-source
-      // block, configs[3] frontier 40.9 -> 35.7 ms per 64 queries.
-      static const int bps = [] {
-        const char* e = std::getenv("PPRG_FRONTIER_BPS");
-        return e ? std::atoi(e) : 24;
-      }();
-      unsigned grid = grid_for(total * 32);
-      if (bps > 0 && grid > (unsigned)(bps * g.sm_count)) grid = (unsigned)(bps * g.sm_count);
-      k_frontier<<<grid, 256, 0, st>>>(F, w.heavy.get(), w.heavy_cnt.get());
-    }
-    PPRG_CUDA(cudaGetLastError());
-    call->kernel_launches += 1;
-    unsigned nheavy = 0;
-    d2h_small(&nheavy, w.heavy_cnt.get(), 4, st);
-    PPRG_CUDA(cudaStreamSynchronize(st));
-    if (nheavy) {
-      std::vector<HeavyEntry> hv(nheavy);
-      d2h_small(hv.data(), w.heavy.get(), sizeof(HeavyEntry) * nheavy, st);
-      // chunks of HEAVY_CHUNK out-edges per heavy entry (the kernel's work list)
-      std::vector<HeavyChunk> chunks;
-      for (unsigned h = 0; h < nheavy; ++h)
-        for (uint32_t f = 0; f < hv[h].deg; f += HEAVY_CHUNK) chunks.push_back(HeavyChunk{h, f});
-      const unsigned nch = (unsigned)chunks.size();
-      w.heavy_chunks.ensure((sizeof(HeavyChunk) * nch + 7) / 8);
-      PPRG_CUDA(cudaMemcpyAsync(w.heavy_chunks.get(), chunks.data(), sizeof(HeavyChunk) * nch,
-                                cudaMemcpyHostToDevice, st));
-      const unsigned cap = (unsigned)g.sm_count * 8;
-      k_frontier_heavy_chunks<<<nch < cap ? nch : cap, 256, 0, st>>>(
-          F, w.heavy.get(), reinterpret_cast<const HeavyChunk*>(w.heavy_chunks.get()), nch);
-      PPRG_CUDA(cudaGetLastError());
-      call->kernel_launches += 1;
-    }
-    d2h_small(hc.data(), w.counters.get(), 8 * NC, st);
-    d2h_small(hdr.data(), col_dr, 8 * KMAX, st);
-    d2h_small(hstop.data(), d_stop, 4 * KMAX, st);
-    PPRG_CUDA(cudaStreamSynchronize(st));
-    if (std::getenv("PPRG_DEBUG_LOCAL")) {
-      unsigned long long nn = 0, np = 0, app = 0;
-      for (uint32_t c = 0; c < b.k; ++c) nn += hc[1 + 2 * KMAX + c], np += hc[1 + KMAX + c], app += hc[1 + c];
-      std::fprintf(stderr, "level: entries %llu heavy %u node_pushes %llu edge_pushes %llu appended %llu\n",
-                   (unsigned long long)total, nheavy, nn, np, app);
-    }
-    const bool observed_col0 = g_obs && (live & 1ull);
-    for (uint32_t c = 0; c < b.k; ++c) {
-      if (!((live >> c) & 1ull)) continue;
-      b.r_sum[c] -= hdr[c];
-      b.pushes[c] += hc[1 + KMAX + c];
-      b.levels[c] += 1;
-      if (g_trace && c == 0)
-        g_trace->pts.push_back(TracePoint{b.pushes[0], b.r_sum[0], host_now_ns() - g_trace->host_t0});
-      qsize[c] = hc[1 + c];
-      if (hstop[c] || !still_live(c, qsize[c])) {
-        live &= ~(1ull << c);
-        state[c] = 1;
-      }
-    }
-    if (observed_col0) emit_step(b, w.x.get(), b.alpha, w.res.get(), b.r_sum[0], b.pushes[0]);
-    std::swap(cur, nxt);
+    if (g_trace && (live & 1ull))
+      g_trace->pts.push_back(TracePoint{b.pushes[0], b.r_sum[0], host_now_ns() - g_trace->host_t0});
+    if (g_obs && (live & 1ull)) emit_step(b, w.x.get(), b.alpha, w.res.get(), b.r_sum[0], b.pushes[0]);
+    if (hd.levels_run & 1u) std::swap(cur, nxt);
+    if (!stepwise && hd.out_live) fail(EINTERNAL, "drain: level limit reached");
+    live = hd.out_live;
   }
   for (uint32_t c = 0; c < b.k; ++c)
     if (state[c] == 0) state[c] = 1;
@@ -671,8 +646,12 @@ void exact_rsum(Block& b, const std::vector<int>& which) {
   Graph& g = b.g;
   cudaStream_t st = g.stream;
   const uint64_t nk = g.n * (uint64_t)b.K;
-  PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
-  k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), g.n, b.K, b.w.dcols.get() + KMAX);
+  if (t_det) {
+    det_colsum(b, b.w.res.get(), nullptr, g.n, 1.0, b.w.dcols.get() + KMAX);
+  } else {
+    PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
+    k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), g.n, b.K, b.w.dcols.get() + KMAX);
+  }
   std::vector<double> exact(KMAX);
   d2h_small(exact.data(), b.w.dcols.get() + KMAX, 8 * KMAX, st);
   PPRG_CUDA(cudaStreamSynchronize(st));
@@ -719,6 +698,12 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   PPRG_CUDA(cudaMemsetAsync(w.dcols.get() + 2 * KMAX, 0, 8 * KMAX, st));
   k_init_pull<<<grid_reduce(nk), 256, 0, st>>>(w.x.get(), g.deg.get(), g.inv_deg.get(), g.n, b.K,
                                             b.alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
+  if (t_det) {
+    // D = (1-a) * sum of x over the dead ends in a fixed order; both y buffers
+    // start equal
+    det_colsum(b, w.x.get(), g.dead.get(), g.n_dead, 1.0 - b.alpha, w.dcols.get() + 2 * KMAX);
+    PPRG_CUDA(cudaMemcpyAsync(w.y1.get(), w.y0.get(), 8 * nk, cudaMemcpyDeviceToDevice, st));
+  }
   d2h_small(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, st);
   PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
   PPRG_CUDA(cudaStreamSynchronize(st));
@@ -751,6 +736,12 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   P.E = Et;
   P.x = w.x.get();
   P.y[0] = P.y[1] = w.y0.get();
+  if (t_det) {
+    P.y[1] = w.y1.get();
+    set_waves(b, P);
+  }
+  double* ycur = P.y[0];  // y as of the last completed sweep
+  double* ynext = P.y[1];
   SweepTrace trace;
   trace.attach(P);
   EventTimer tm(st);
@@ -768,9 +759,12 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
       if (sweep >= 200000) fail(EINTERNAL, "power push: sweep limit reached");
       SweepParams Q = P;
       Q.max_sweeps = 1;
+      Q.y[0] = ycur;
+      Q.y[1] = ynext;
       for (int c = 0; c < b.K; ++c) Q.init[c] = stv[c];
       PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
       dispatch_sweeps<M_POWERPUSH>(g, b.K, Q, true);
+      if (t_det) std::swap(ycur, ynext);
       SweepCtl one;
       d2h_small(&one, w.ctl.get(), sizeof one, st);
       PPRG_CUDA(cudaStreamSynchronize(st));
@@ -782,7 +776,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
       // explicit residues of the pull form (the final pass, outputs only)
       SweepParams F = base_params(b);
       F.x = w.x.get();
-      F.y[0] = F.y[1] = w.y0.get();
+      F.y[0] = F.y[1] = ycur;
       F.push_res = w.res.get();
       F.out_reserve = snap.get();
       F.out_residue = snap.get() + g.n;
@@ -815,7 +809,9 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
     dispatch_sweeps<M_POWERPUSH>(g, b.K, P, true);
     tm.stop();
     d2h_small(&hc, w.ctl.get(), sizeof hc, st);
+    if (t_det && (hc.total_sweeps & 1u)) std::swap(ycur, ynext);  // sweep s writes y[(s + 1) & 1]
   }
+  b.yfin = ycur;
   call->sweep_ms += tm.ms();
   trace.fold(st, hc.total_sweeps, b.pushes[0], 0);
   call->alg_bytes += hc.alg_bytes;
@@ -890,7 +886,7 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
   Q.res_inter = residues_inplace ? w.res.get() : nullptr;
   Q.push_res = w.res.get();
   Q.x = w.x.get();
-  Q.y[0] = Q.y[1] = w.y0.get();
+  Q.y[0] = Q.y[1] = b.yfin;
   for (int c = 0; c < b.K; ++c) {
     Q.final_pull[c] = b.scan[c];
     Q.init[c].r_sum = b.r_sum[c];
@@ -929,7 +925,7 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
   call->final_ms += tf.ms();
   for (uint32_t c = 0; c < k; ++c) {
     if (!b.scan[c]) continue;
-    const double exact = fc.pushed[0][c];
+    const double exact = fc.pushed[0][c] / fc.out_scale[c];
     if (std::fabs(exact - b.r_sum[c]) > 1e-6)
       fail(EINTERNAL, "push: r_sum drifted more than 1e-6 from the residues");
     b.r_sum[c] = exact;
@@ -1001,8 +997,12 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
     std::vector<int> all(KMAX, 1);
     std::fill(b.r_sum.begin(), b.r_sum.end(), 0.0);
     {  // r_sum of the incoming state (no drift check: it is the caller's)
-      PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
-      k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), n, b.K, b.w.dcols.get() + KMAX);
+      if (t_det) {
+        det_colsum(b, b.w.res.get(), nullptr, n, 1.0, b.w.dcols.get() + KMAX);
+      } else {
+        PPRG_CUDA(cudaMemsetAsync(b.w.dcols.get() + KMAX, 0, 8 * KMAX, st));
+        k_colsum<<<grid_reduce(nk), 256, 0, st>>>(b.w.res.get(), n, b.K, b.w.dcols.get() + KMAX);
+      }
       d2h_small(b.r_sum.data(), b.w.dcols.get() + KMAX, 8 * KMAX, st);
       PPRG_CUDA(cudaStreamSynchronize(st));
     }
@@ -1084,6 +1084,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       k_seed<<<1, KMAX, 0, st>>>(w.r0.get(), w.d_src.get(), b.K, 1.0);
       k_init_pull<<<grid_reduce(nk), 256, 0, st>>>(w.r0.get(), g.deg.get(), g.inv_deg.get(), n, b.K,
                                                 alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
+      if (t_det) det_colsum(b, w.r0.get(), g.dead.get(), g.n_dead, 1.0 - alpha, w.dcols.get() + 2 * KMAX);
       d2h_small(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, st);
       PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
       PPRG_CUDA(cudaStreamSynchronize(st));

@@ -13,6 +13,7 @@ namespace pprg {
 
 constexpr int KMAX = 64;
 constexpr int EMAX = 64;   // max epochs
+constexpr int WMAX = 16;   // max waves of a deterministic sweep
 #ifndef PPRG_NT
 #define PPRG_NT 128
 #endif
@@ -28,6 +29,7 @@ enum SweepMode : int { M_POWERPUSH = 0, M_POWITR = 1, M_SIMFWD = 2, M_FINAL = 3 
 
 thread_local TraceSink* g_trace = nullptr;
 thread_local StepSink* g_obs = nullptr;
+thread_local bool t_det = false;
 
 uint64_t host_now_ns() {
   return (uint64_t)std::chrono::duration_cast<std::chrono::nanoseconds>(
@@ -58,6 +60,8 @@ struct SweepCtl {
   // clamped to 0 in the outputs, counted and summed here and checked on the host)
   unsigned long long neg_count;
   double neg_sum;
+  double out_scale[KMAX];              // final pass: pushed[0][c] / out_scale[c] = residue sum
+  unsigned wticket[3][WMAX];           // deterministic sweeps: tile ticket of each wave
 };
 
 struct SweepParams {
@@ -96,6 +100,12 @@ struct SweepParams {
   uint32_t trace_cap;
   uint64_t own_lo, own_hi;      // node range this launch owns (vertex partition; else [0, n))
   unsigned long long handoff_np;  // refine epoch: hand off to the frontier below this many edge pushes
+  // deterministic sweeps: the tile list cut into nwaves waves of contiguous
+  // rows; wave w = tiles [wave_tile[w], wave_tile[w+1]), whose rows start at
+  // node wave_node[w]
+  uint32_t nwaves;
+  uint64_t wave_tile[WMAX + 1];
+  uint32_t wave_node[WMAX];
   uint32_t src[KMAX];
   int final_pull[KMAX];        // finalize: 1 = residue from pull form
   double thr[EMAX];            // epoch r_max (lambda is per call, so shared by columns)
@@ -105,12 +115,37 @@ struct SweepParams {
 
 struct ColSh {
   double r_sum, D;
+  double scp, scd;  // deterministic sweeps: fixed-point scales 2^S of this sweep's pushed / D sums
   int epoch, done;
   unsigned sweeps;
   uint32_t src;  // the column's source (a shared copy: P.src[c] with a per-lane c
                  // would be a divergent, serialised constant-bank load)
   unsigned long long pushes;
 };
+
+// Gather operand of a sweep. Fast mode: one y, updated in place (rows read
+// whatever value a neighbour's row has when the gather lands). Deterministic
+// sweeps: rows of the earlier waves of this sweep are read from this sweep's
+// buffer yn, every other row from the previous sweep's yo, so no inflow
+// depends on timing.
+struct YG {
+  const double* yo;
+  const double* yn;
+  uint32_t lo;  // first node of the current wave
+};
+template <bool DET>
+__device__ __forceinline__ const double* ysrc(const YG& y, uint32_t id) {
+  if constexpr (DET) return id < y.lo ? y.yn : y.yo;
+  else return y.yo;
+}
+// One term of a per-column sum. Deterministic sweeps sum integers (term *
+// 2^S rounded, exact in fp64 while every partial sum stays below 2^53), so
+// the fp64 atomics that combine them give the same bits in any order.
+template <bool DET>
+__device__ __forceinline__ double qterm(double v, double sc) {
+  if constexpr (DET) return rint(v * sc);
+  else return v;
+}
 
 // Tile geometry: a row-aligned tile holds at most T = SWEEP_ELEMS/K in-edges
 // and at most RMAX rows (host-built plan, Graph::tile_plan). Its gathered
@@ -152,49 +187,53 @@ constexpr int PK_SHIFT = 40;
 // The per-(row, column) decision: push form of push.cpp:182-193 in pull
 // representation, the PowItr update of push.cpp:90-99, or the final explicit
 // residue. `acc` is the sum over in-neighbours v of y_v.
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, const double* thr_cur,
                                        uint32_t u, int c, double acc, double xo, double rc,
-                                       uint32_t dg, double inv, const double* yg, double* rnxt,
+                                       uint32_t dg, double inv, const YG& yg, double* rnxt,
                                        double* ynxt, Acc& a) {
   const uint64_t ix = (uint64_t)u * K + c;
   const bool is_src = u == cs[c].src;
   const double alpha = P.alpha, oma = 1.0 - P.alpha;
   if constexpr (MODE == M_POWERPUSH) {
-    if (cs[c].done) return;
+    if (cs[c].done) {
+      if (DET && dg) ynxt[ix] = oma * xo * inv;  // every row's y into this sweep's buffer
+      return;
+    }
     const double inflow = acc + (is_src ? 1.0 + cs[c].D : 0.0);
     const double r = inflow - xo;
     if (r > (dg ? (double)dg : 1.0) * thr_cur[c]) {
       st_state(P.x + ix, inflow);
-      if (dg) {
+      if (!DET && dg) {
         const double yv = oma * inflow * inv;
         P.y[0][ix] = yv;
         for (int p = 0; p < P.npeers; ++p) P.peer_y[p][ix] = yv;  // fused exchange
       }
-      a.push += r;
+      a.push += qterm<DET>(r, cs[c].scp);
       a.np += dg ? dg : 1;
       a.nn += 1;
       a.et += dg;
       xo = inflow;
     }
-    if (!dg) a.d += oma * xo;
+    if (DET && dg) ynxt[ix] = oma * xo * inv;  // the same bits as the pushed value
+    if (!dg) a.d += qterm<DET>(oma * xo, cs[c].scd);
   } else if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) {
     if (cs[c].done) {
       rnxt[ix] = rc;
-      ynxt[ix] = __ldcg(yg + ix);
+      ynxt[ix] = __ldcg(yg.yo + ix);
       return;
     }
     const double nxt = acc + (is_src ? cs[c].D : 0.0);
     P.x[ix] = xo + alpha * rc;  // reserve += alpha * r
     rnxt[ix] = nxt;
     ynxt[ix] = oma * nxt * inv;
-    a.push += nxt;  // sum of next = the exact r_sum (push.cpp:101-103)
+    a.push += qterm<DET>(nxt, cs[c].scp);  // sum of next = the exact r_sum (push.cpp:101-103)
     if (MODE == M_POWITR || rc != 0.0) {
       a.np += dg ? dg : 1;
       a.nn += 1;
       a.et += dg;
     }
-    if (!dg) a.d += oma * nxt;
+    if (!dg) a.d += qterm<DET>(oma * nxt, cs[c].scd);
   } else {  // M_FINAL
     double res;
     if (P.final_pull[c]) {
@@ -213,17 +252,17 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
       if (P.out_reserve) P.out_reserve[(uint64_t)c * P.n + u] = alpha * xo;
       if (P.out_residue) P.out_residue[(uint64_t)c * P.n + u] = res;
     }
-    a.push += res;
+    a.push += qterm<DET>(res, cs[c].scp);
   }
 }
 
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __forceinline__ void decide_at(const SweepParams& P, const ColSh* cs,
                                           const double* thr_cur, uint32_t u, int c, double acc,
-                                          uint32_t dg, double inv, const double* yg,
+                                          uint32_t dg, double inv, const YG& yg,
                                           const double* rcur, double* rnxt, double* ynxt, Acc& a) {
   const uint64_t ix = (uint64_t)u * K + c;
-  decide<K, MODE>(P, cs, thr_cur, u, c, acc, __ldcg(P.x + ix),
+  decide<K, MODE, DET>(P, cs, thr_cur, u, c, acc, __ldcg(P.x + ix),
                   (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0, dg, inv, yg,
                   rnxt, ynxt, a);
 }
@@ -234,10 +273,10 @@ __device__ __forceinline__ void decide_at(const SweepParams& P, const ColSh* cs,
 // its partial, the last arriver acquires all of them before the block barrier
 // hands them to the deciding threads; partials read back from L2). Only hub
 // pieces pay this protocol.
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, uint64_t j,
                                        double* hubsh, int* flag, const ColSh* cs, const double* thr_cur,
-                                       const double* yg, const double* rcur, double* rnxt,
+                                       const YG& yg, const double* rcur, double* rnxt,
                                        double* ynxt, Acc& a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = tid % K;
@@ -249,12 +288,15 @@ __device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, 
     const uint32_t i1 = __ldg(P.in_nbr + d.e0 + (f + NT) / K);
     const uint32_t i2 = __ldg(P.in_nbr + d.e0 + (f + 2 * NT) / K);
     const uint32_t i3 = __ldg(P.in_nbr + d.e0 + (f + 3 * NT) / K);
-    s0 += yg[(uint64_t)i0 * K + c];
-    s1 += yg[(uint64_t)i1 * K + c];
-    s2 += yg[(uint64_t)i2 * K + c];
-    s3 += yg[(uint64_t)i3 * K + c];
+    s0 += ysrc<DET>(yg, i0)[(uint64_t)i0 * K + c];
+    s1 += ysrc<DET>(yg, i1)[(uint64_t)i1 * K + c];
+    s2 += ysrc<DET>(yg, i2)[(uint64_t)i2 * K + c];
+    s3 += ysrc<DET>(yg, i3)[(uint64_t)i3 * K + c];
   }
-  for (; f < total; f += NT) s0 += yg[(uint64_t)__ldg(P.in_nbr + d.e0 + f / K) * K + c];
+  for (; f < total; f += NT) {
+    const uint32_t i0 = __ldg(P.in_nbr + d.e0 + f / K);
+    s0 += ysrc<DET>(yg, i0)[(uint64_t)i0 * K + c];
+  }
   double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
   for (int o = 16; o >= K && o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -282,17 +324,17 @@ __device__ __noinline__ void hub_piece(const SweepParams& P, const TileDesc& d, 
     double acc = 0.0;
     for (uint32_t p = 0; p < d.npieces; ++p) acc += __ldcg(part + (uint64_t)p * K);
     const uint32_t u = __ldg(P.crow + d.r0);
-    decide_at<K, MODE>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
-                       rcur, rnxt, ynxt, a);
+    decide_at<K, MODE, DET>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0),
+                            yg, rcur, rnxt, ynxt, a);
   }
 }
 
 // One row-aligned tile: gather y of every in-edge into shared memory (all
 // loads of the tile issued together), then one thread per (row, column) sums
 // its row and decides; rows longer than LONG are summed by a whole warp.
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& d, char* smem,
-                                          const ColSh* cs, const double* thr_cur, const double* yg,
+                                          const ColSh* cs, const double* thr_cur, const YG& yg,
                                           const double* rcur, double* rnxt, double* ynxt, Acc& a,
                                           const BlockAcc& ba, uint32_t* nlong,
                                           const unsigned long long* dn_slot, TileDesc* dn) {
@@ -329,7 +371,7 @@ __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& 
 #pragma unroll
       for (int i = 0; i < U; ++i) {
         const uint32_t f = f0 + tid + i * NT;
-        if (f < total) vals[f] = yg[(uint64_t)id[i] * K + (f % K)];
+        if (f < total) vals[f] = ysrc<DET>(yg, id[i])[(uint64_t)id[i] * K + (f % K)];
       }
     }
   }
@@ -351,7 +393,7 @@ __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& 
       s1 += vals[(q + 1) * K + c];
     }
     if (q < e) s0 += vals[q * K + c];
-    decide<K, MODE>(P, cs, thr_cur, u, c, s0 + s1, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a);
+    decide<K, MODE, DET>(P, cs, thr_cur, u, c, s0 + s1, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a);
   }
   // ---- long rows: one warp per row -----------------------------------------
   {
@@ -375,15 +417,15 @@ __device__ __forceinline__ void tile_rows(const SweepParams& P, const TileDesc& 
         for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
       if (es == 0) {
         if constexpr (CPL == 1) {
-          decide_at<K, MODE>(P, cs, thr_cur, snode[r], kc, s[0], sdeg[r], sinv[r], yg, rcur, rnxt,
-                             ynxt, a);
+          decide_at<K, MODE, DET>(P, cs, thr_cur, snode[r], kc, s[0], sdeg[r], sinv[r], yg, rcur,
+                                  rnxt, ynxt, a);
         } else {  // K = 64: lane kc decides columns kc and kc+32; counters via shared atomics
 #pragma unroll
           for (int q = 0; q < CPL; ++q) {
             Acc b2;
             const int cc = kc + q * KC;
-            decide_at<K, MODE>(P, cs, thr_cur, snode[r], cc, s[q], sdeg[r], sinv[r], yg, rcur,
-                               rnxt, ynxt, b2);
+            decide_at<K, MODE, DET>(P, cs, thr_cur, snode[r], cc, s[q], sdeg[r], sinv[r], yg, rcur,
+                                    rnxt, ynxt, b2);
             if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
             if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
             if (b2.np) atomicAdd(&ba.np[cc], b2.np);
@@ -428,20 +470,21 @@ constexpr size_t k1w_bytes = 8ull * (NT / 32) * K1W_R;
 
 __device__ __forceinline__ uint32_t le_mask(int j) { return 0xFFFFFFFFu >> (31 - j); }
 
-template <int MODE>
+template <int MODE, bool DET>
 __device__ __forceinline__ void sweep_k1_warps(const SweepParams& P, const ColSh* cs,
-                                               const double* thr_cur, const double* yg,
+                                               const double* thr_cur, const YG& yg,
                                                const double* rcur, double* rnxt, double* ynxt,
-                                               Acc& a, double* sacc_all, unsigned* ticket) {
+                                               Acc& a, double* sacc_all, unsigned* ticket,
+                                               uint64_t t0, uint64_t t1) {
   constexpr int G = K1W_T / 32;
   constexpr bool RC = MODE == M_POWITR || MODE == M_SIMFWD;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double* sacc = sacc_all + warp * K1W_R;
-  const uint64_t nt = P.ntiles;
+  const uint64_t nt = t1;  // tasks [t0, t1)
   auto grab = [&]() -> uint64_t {
     unsigned b = 0;
     if (lane == 0) b = atomicAdd(ticket, K1W_CH);
-    return __shfl_sync(0xffffffffu, b, 0);
+    return t0 + __shfl_sync(0xffffffffu, b, 0);
   };
   uint64_t base = grab();
   uint64_t nbase = base < nt ? grab() : nt;
@@ -465,7 +508,8 @@ __device__ __forceinline__ void sweep_k1_warps(const SweepParams& P, const ColSh
             id[g] = pe < d.ne ? ld_stream(P.in_nbr + d.e0 + pe) : 0u;
           }
 #pragma unroll
-          for (int g = 0; g < G; ++g) v[g] = rb + 32 * g + lane < d.ne ? ld_gather(yg + id[g]) : 0.0;
+          for (int g = 0; g < G; ++g)
+            v[g] = rb + 32 * g + lane < d.ne ? ld_gather(ysrc<DET>(yg, id[g]) + id[g]) : 0.0;
           sum += ((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]));
         }
 #pragma unroll
@@ -489,7 +533,7 @@ __device__ __forceinline__ void sweep_k1_warps(const SweepParams& P, const ColSh
           for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
           if (lane == 0) {
             const uint32_t u = __ldg(P.crow + d.r0);
-            decide<1, MODE>(P, cs, thr_cur, u, 0, acc, __ldcg(P.x + u),
+            decide<1, MODE, DET>(P, cs, thr_cur, u, 0, acc, __ldcg(P.x + u),
                             RC ? __ldcg(rcur + u) : 0.0, __ldg(P.cdeg + d.r0),
                             __ldg(P.cinv + d.r0), yg, rnxt, ynxt, a);
           }
@@ -531,7 +575,8 @@ __device__ __forceinline__ void sweep_k1_warps(const SweepParams& P, const ColSh
           id[g] = pe < d.ne ? ld_stream(P.in_nbr + d.e0 + pe) : 0u;
         }
 #pragma unroll
-        for (int g = 0; g < G; ++g) v[g] = rb + 32 * g + lane < d.ne ? ld_gather(yg + id[g]) : 0.0;
+        for (int g = 0; g < G; ++g)
+          v[g] = rb + 32 * g + lane < d.ne ? ld_gather(ysrc<DET>(yg, id[g]) + id[g]) : 0.0;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const uint32_t w0 = rb + 32 * g;
@@ -554,10 +599,10 @@ __device__ __forceinline__ void sweep_k1_warps(const SweepParams& P, const ColSh
         }
       }
       if ((uint32_t)lane < d.nr)
-        decide<1, MODE>(P, cs, thr_cur, u0, 0, sacc[lane], xo0, rc0, dg0, inv0, yg, rnxt, ynxt, a);
+        decide<1, MODE, DET>(P, cs, thr_cur, u0, 0, sacc[lane], xo0, rc0, dg0, inv0, yg, rnxt, ynxt, a);
       if ((uint32_t)lane + 32 < d.nr)
-        decide<1, MODE>(P, cs, thr_cur, u1, 0, sacc[lane + 32], xo1, rc1, dg1, inv1, yg, rnxt,
-                        ynxt, a);
+        decide<1, MODE, DET>(P, cs, thr_cur, u1, 0, sacc[lane + 32], xo1, rc1, dg1, inv1, yg, rnxt,
+                             ynxt, a);
       __syncwarp();
       d = dn;
     }
@@ -602,8 +647,8 @@ __host__ __device__ constexpr int wide_kc() {
 #ifndef PPRG_G
 #define PPRG_G 8
 #endif
-template <int K>
-__device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double* yg, uint64_t b,
+template <int K, bool DET>
+__device__ __forceinline__ void warp_row_sum(const SweepParams& P, const YG& yg, uint64_t b,
                                              uint64_t e, double (&s)[K / wide_kc<K>()],
                                              bool have_first = false, uint32_t first_id = 0) {
   constexpr int KC = wide_kc<K>();
@@ -611,7 +656,7 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double*
   constexpr int ES = 32 / KC;
   constexpr int G = PPRG_G;
   const int lane = threadIdx.x & 31, es = lane / KC, kc = lane % KC;
-  const double* ybase = yg + kc * CPL;
+  const double* ybase = yg.yo + kc * CPL;  // (fast mode: one y)
   double acc[CPL][2];
 #pragma unroll
   for (int q = 0; q < CPL; ++q) acc[q][0] = acc[q][1] = 0.0;
@@ -628,7 +673,7 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double*
       for (int g = 0; g < G; ++g) {
         const int j = j0 + g * ES + es;
         const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
-        const double* src = ybase + (uint64_t)id * K;
+        const double* src = (DET ? ysrc<DET>(yg, id) + kc * CPL : ybase) + (uint64_t)id * K;
         if constexpr (CPL == 2) {
           const double2 v2 = ld_gather2(src);
           v[g][0] = v2.x;
@@ -659,10 +704,10 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const double*
 // and the piece protocol of hub_piece follows (partial slot, release-ordered
 // counter, last piece decides from the partials in piece order). Measured on
 // configs[2]: sweep kernel -4% against the column-per-thread hub_piece.
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc d, uint64_t j,
                                             double* hubsh, int* flag, const ColSh* cs,
-                                            const double* thr_cur, const double* yg,
+                                            const double* thr_cur, const YG& yg,
                                             const double* rcur, double* rnxt, double* ynxt,
                                             double* sh_push, double* sh_d,
                                             unsigned long long* sh_np, unsigned long long* sh_nn,
@@ -678,7 +723,7 @@ __device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc
   const uint64_t e0 = d.e0 + d.ne;
   const uint64_t e = b + chunk < e0 ? b + chunk : e0;
   double s[CPL];
-  warp_row_sum<K>(P, yg, b < e ? b : e, e, s);
+  warp_row_sum<K, DET>(P, yg, b < e ? b : e, e, s);
   if (lane < KC)
 #pragma unroll
     for (int q = 0; q < CPL; ++q) hubsh[warp * K + (lane % KC) * CPL + q] = s[q];
@@ -703,8 +748,8 @@ __device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc
     for (uint32_t p = 0; p < d.npieces; ++p) acc += __ldcg(part + (uint64_t)p * K);
     const uint32_t u = __ldg(P.crow + d.r0);
     Acc a;
-    decide_at<K, MODE>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
-                       rcur, rnxt, ynxt, a);
+    decide_at<K, MODE, DET>(P, cs, thr_cur, u, tid, acc, __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), yg,
+                            rcur, rnxt, ynxt, a);
     if (a.push != 0.0) atomicAdd(&sh_push[tid], a.push);
     if (a.d != 0.0) atomicAdd(&sh_d[tid], a.d);
     if (a.np) atomicAdd(&sh_np[tid], a.np);
@@ -715,44 +760,48 @@ __device__ __noinline__ void hub_piece_wide(const SweepParams& P, const TileDesc
 
 // decide<K, M_POWERPUSH> with the column's threshold and source in registers
 // (thr = +inf: the column is done).
-template <int K>
+template <int K, bool DET>
 __device__ __forceinline__ void decide_pp(const SweepParams& P, const ColSh* cs, double thr,
                                           uint32_t src, uint32_t u, int c, double acc, double xo,
-                                          uint32_t dg, double inv, Acc& a) {
-  if (thr == CUDART_INF) return;
+                                          uint32_t dg, double inv, double* ynxt, Acc& a) {
   const uint64_t ix = (uint64_t)u * K + c;
   const double oma = 1.0 - P.alpha;
+  if (thr == CUDART_INF) {
+    if (DET && dg) ynxt[ix] = oma * xo * inv;  // every row's y into this sweep's buffer
+    return;
+  }
   const double inflow = acc + (u == src ? 1.0 + cs[c].D : 0.0);
   const double r = inflow - xo;
   if (r > (dg ? (double)dg : 1.0) * thr) {
     st_state(P.x + ix, inflow);
-    if (dg) {
+    if (!DET && dg) {
       const double yv = oma * inflow * inv;
       P.y[0][ix] = yv;
       for (int p = 0; p < P.npeers; ++p) P.peer_y[p][ix] = yv;  // fused exchange
     }
-    a.push += r;
+    a.push += qterm<DET>(r, cs[c].scp);
     a.np += dg ? dg : 1;
     a.nn += 1;
     a.et += dg;
     xo = inflow;
   }
-  if (!dg) a.d += oma * xo;
+  if (DET && dg) ynxt[ix] = oma * xo * inv;
+  if (!dg) a.d += qterm<DET>(oma * xo, cs[c].scd);
 }
 
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* cs,
                                             const double* thr_cur, const uint32_t* csrc,
                                             uint32_t u, const double* s,
                                             const double* xo, const double* rc, uint32_t dg,
-                                            double inv, const double* yg, double* rnxt,
+                                            double inv, const YG& yg, double* rnxt,
                                             double* ynxt, Acc& a, const BlockAcc& ba,
                                             double* pacc = nullptr) {
   constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   const int kc = (threadIdx.x & 31) % KC;
   if constexpr (CPL == 1) {
-    decide<K, MODE>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], dg, inv, yg, rnxt, ynxt, a);
+    decide<K, MODE, DET>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], dg, inv, yg, rnxt, ynxt, a);
   } else {  // K = 64: lane kc owns columns 2kc, 2kc+1; counters via shared atomics
     // the lane's two thresholds and sources in one conflict-free 16 / 8-byte
     // shared load each (a done column's threshold is +inf)
@@ -763,9 +812,9 @@ __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* c
       Acc b2;
       const int cc = kc * CPL + q;
       if constexpr (MODE == M_POWERPUSH)
-        decide_pp<K>(P, cs, q ? th.y : th.x, q ? sr.y : sr.x, u, cc, s[q], xo[q], dg, inv, b2);
+        decide_pp<K, DET>(P, cs, q ? th.y : th.x, q ? sr.y : sr.x, u, cc, s[q], xo[q], dg, inv, ynxt, b2);
       else
-        decide<K, MODE>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
+        decide<K, MODE, DET>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
       if (PPRG_PUSH_REG && pacc) pacc[q] += b2.push;  // flushed once per tile
       else if (b2.push != 0.0) atomicAdd(&ba.push[cc], b2.push);
       if (b2.d != 0.0) atomicAdd(&ba.d[cc], b2.d);
@@ -795,11 +844,11 @@ __device__ __forceinline__ uint32_t* wide_long_count(char* smem) {
 #endif
 constexpr uint32_t LONG_W = PPRG_LONG_W;
 
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileDesc& d, char* smem,
                                                const ColSh* cs, const double* thr_cur,
                                                const uint32_t* csrc,
-                                               const double* yg, const double* rcur, double* rnxt,
+                                               const YG& yg, const double* rcur, double* rnxt,
                                                double* ynxt, Acc& a, const BlockAcc& ba,
                                                uint32_t* rowctr,
                                                const unsigned long long* dn_slot, TileDesc* dn) {
@@ -862,8 +911,8 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
         if constexpr (CPL != 2) xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
         rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
       }
-      warp_row_sum<K>(P, yg, b, e, s, true, ids);
-      if (es0) decide_cols<K, MODE>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
+      warp_row_sum<K, DET>(P, yg, b, e, s, true, ids);
+      if (es0) decide_cols<K, MODE, DET>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
     }
     r = rn;
     ids = ids_n;
@@ -876,7 +925,7 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
     const uint64_t chunk = ((e - b) + NW - 1) / NW;
     const uint64_t wb = b + warp * chunk, we = wb + chunk < e ? wb + chunk : e;
     double s[CPL];
-    warp_row_sum<K>(P, yg, wb < e ? wb : e, we, s);
+    warp_row_sum<K, DET>(P, yg, wb < e ? wb : e, we, s);
     if (es0)
 #pragma unroll
       for (int q = 0; q < CPL; ++q) spart[warp * K + kc * CPL + q] = s[q];
@@ -893,7 +942,7 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
         for (int w = 0; w < NW; ++w) t += spart[w * K + kc * CPL + q];
         s[q] = t;
       }
-      decide_cols<K, MODE>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
+      decide_cols<K, MODE, DET>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
     }
     __syncthreads();
   }
@@ -910,9 +959,9 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
 
 // Sources with in-degree 0 are not rows of the compacted transpose; their
 // only inflow is the unit start mass plus the dead-end mass D (block 0).
-template <int K, int MODE>
+template <int K, int MODE, bool DET>
 __device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* cs,
-                                            const double* thr_cur, const double* yg,
+                                            const double* thr_cur, const YG& yg,
                                             const double* rcur, double* rnxt, double* ynxt,
                                             Acc& a) {
   const int tid = threadIdx.x;
@@ -921,12 +970,11 @@ __device__ __forceinline__ void source_rows(const SweepParams& P, const ColSh* c
   if (u < P.own_lo || u >= P.own_hi) return;  // another partition's row
   if (__ldg(P.in_off_full + u + 1) != __ldg(P.in_off_full + u)) return;
   const uint64_t ix = (uint64_t)u * K + tid;
-  decide<K, MODE>(P, cs, thr_cur, u, tid, 0.0, __ldcg(P.x + ix),
+  decide<K, MODE, DET>(P, cs, thr_cur, u, tid, 0.0, __ldcg(P.x + ix),
                   (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0, __ldg(P.deg + u),
                   __ldg(P.inv_deg + u), yg, rnxt, ynxt, a);
 }
 
-template <int K, int MODE>
 #ifndef PPRG_MINB
 #define PPRG_MINB 8
 #endif
@@ -936,6 +984,23 @@ template <int K, int MODE>
 #ifndef PPRG_MINB_K1
 #define PPRG_MINB_K1 6
 #endif
+// Fixed-point scale 2^(52 - e) for a per-column sum bounded by `bound` < 2^e:
+// every scaled term and partial sum stays an integer below 2^53.
+__device__ __forceinline__ double det_scale(double bound) {
+  int e;
+  frexp(bound > 1e-280 ? bound : 1e-280, &e);
+  return ldexp(1.0, 52 - e);
+}
+
+// The persistent sweep kernel: every epoch and sweep of a query block in one
+// cooperative launch (see DESIGN 3). DET: deterministic sweeps -- the tile
+// list runs as P.nwaves waves of contiguous rows separated by grid barriers;
+// a row of wave w gathers this sweep's y for rows of waves < w and the
+// previous sweep's y for all others (y double-buffered: every row writes its
+// y into this sweep's buffer, pushed or not), and the per-column sums are
+// fixed-point integers (qterm). Results are then a function of the inputs
+// alone: no timing, no atomic order.
+template <int K, int MODE, bool DET>
 __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K1 : PPRG_MINB_NARROW))
     k_sweeps(const __grid_constant__ SweepParams P) {
   using TC = Tile<K>;
@@ -960,6 +1025,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
     cs[tid].sweeps = P.init[tid].sweeps;
     cs[tid].pushes = P.init[tid].pushes;
     cs[tid].src = P.src[tid];
+    cs[tid].scp = cs[tid].scd = 1.0;
     csrc[tid] = P.src[tid];
   }
   __syncthreads();
@@ -974,7 +1040,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
       int any = 0;
       for (int cc = 0; cc < K; ++cc) any |= !cs[cc].done;
       sh_any = any && (MODE == M_FINAL ? sweep == 0 : sweep < P.max_sweeps);
-      if (sh_any && !P.k1w) sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
+      if (!DET && sh_any && !P.k1w) sh_tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
       sh_nlong = 0;
       if constexpr (K >= WIDE_K) *wide_long_count<K>(smem_dyn) = 0;
     }
@@ -982,6 +1048,15 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
       // a done column's threshold is +inf (decide_pp's done test); decide()
       // checks cs[].done itself
       thr_cur[tid] = MODE != M_POWERPUSH ? 0.0 : cs[tid].done ? CUDART_INF : P.thr[cs[tid].epoch];
+      if constexpr (DET) {
+        // bounds of this sweep's sums (identical in every block): PowerPush
+        // pushes at most r_sum / alpha (Gauss-Seidel within a sweep), D grows by
+        // at most that; PowItr / the final pass sum at most r_sum
+        const double rs = cs[tid].r_sum > 0 ? cs[tid].r_sum : 0.0;
+        const double bp = MODE == M_POWERPUSH ? 2.0 * rs / P.alpha : 2.0 * rs;
+        cs[tid].scp = det_scale(bp);
+        cs[tid].scd = det_scale(MODE == M_POWERPUSH ? cs[tid].D + bp : bp);
+      }
       sh_push[tid] = 0.0;
       sh_d[tid] = 0.0;
       sh_np[tid] = 0;
@@ -995,6 +1070,8 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
     if (blockIdx.x == 0 && tid == 0 && MODE != M_FINAL) {
       const int nb = (sweep + 1) % 3;  // last read two barriers ago; safe to clear
       ctl->ticket[nb] = 0;
+      if (DET)
+        for (int w = 0; w < WMAX; ++w) ctl->wticket[nb][w] = 0;
       for (int cc = 0; cc < K; ++cc) {
         ctl->pushed[nb][cc] = 0;
         ctl->npush[nb][cc] = 0;
@@ -1003,43 +1080,91 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
         ctl->et[nb][cc] = 0;
       }
     }
-    const double* yg = P.y[MODE == M_POWERPUSH || MODE == M_FINAL ? 0 : (sweep & 1)];
+    const int par = (MODE == M_POWERPUSH && !DET) || MODE == M_FINAL ? 0 : (int)(sweep & 1);
+    YG yg{P.y[par], P.y[par ^ 1], 0u};
     const double* rcur = P.r[sweep & 1];
     double* rnxt = P.r[(sweep + 1) & 1];
     double* ynxt = P.y[(sweep + 1) & 1];
     Acc a;
-    // Tiles in ticket (= id) order; the next ticket is fetched one tile ahead
-    // and the next descriptor is loaded inside the current tile.
-    if (K == 1 && PPRG_K1W && P.k1w) {
-      sweep_k1_warps<MODE>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a,
-                           reinterpret_cast<double*>(smem_dyn), &ctl->ticket[buf]);
-    } else {
-    unsigned long long j = sh_tile[0];
-    TileDesc d = P.desc[j < P.ntiles ? j : 0];
-    for (uint32_t it = 0;; ++it) {
-      if (j >= P.ntiles) break;
-      if (tid == 0) sh_tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
-      TileDesc dn = d;
-      if (d.npieces > 1) {
-        if constexpr (K >= WIDE_K)
-          hub_piece_wide<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt,
-                                  sh_push, sh_d, sh_np, sh_nn, sh_et);
-        else
-          hub_piece<K, MODE>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
-        dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
-        __syncthreads();
-      } else if constexpr (K >= WIDE_K) {
-        tile_rows_wide<K, MODE>(P, d, smem_dyn, cs, thr_cur, csrc, yg, rcur, rnxt, ynxt, a, ba,
-                                &sh_nlong, &sh_tile[(it + 1) & 1], &dn);
-      } else {
-        tile_rows<K, MODE>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba, &sh_nlong,
-                           &sh_tile[(it + 1) & 1], &dn);
+    // Tiles [t0, t1) in ticket (= id) order from counter ctr; the next ticket
+    // is fetched one tile ahead and the next descriptor loaded inside the
+    // current tile. The first ticket is in sh_tile[0].
+    auto run_tiles = [&](unsigned* ctr, uint64_t t0, uint64_t t1) {
+      if (K == 1 && PPRG_K1W && P.k1w) {
+        sweep_k1_warps<MODE, DET>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a,
+                                  reinterpret_cast<double*>(smem_dyn), ctr, t0, t1);
+        return;
       }
-      j = sh_tile[(it + 1) & 1];
-      d = dn;
+      unsigned long long j = sh_tile[0];
+      TileDesc d = P.desc[j < t1 ? j : 0];
+      for (uint32_t it = 0;; ++it) {
+        if (j >= t1) break;
+        if (tid == 0) sh_tile[(it + 1) & 1] = t0 + atomicAdd(ctr, 1u);
+        TileDesc dn = d;
+        if (d.npieces > 1) {
+          if constexpr (K >= WIDE_K)
+            hub_piece_wide<K, MODE, DET>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt,
+                                         sh_push, sh_d, sh_np, sh_nn, sh_et);
+          else
+            hub_piece<K, MODE, DET>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+          dn = P.desc[sh_tile[(it + 1) & 1] < t1 ? sh_tile[(it + 1) & 1] : 0];
+          __syncthreads();
+        } else if constexpr (K >= WIDE_K) {
+          tile_rows_wide<K, MODE, DET>(P, d, smem_dyn, cs, thr_cur, csrc, yg, rcur, rnxt, ynxt, a, ba,
+                                       &sh_nlong, &sh_tile[(it + 1) & 1], &dn);
+        } else {
+          tile_rows<K, MODE, DET>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba, &sh_nlong,
+                                  &sh_tile[(it + 1) & 1], &dn);
+        }
+        j = sh_tile[(it + 1) & 1];
+        d = dn;
+      }
+    };
+    if constexpr (!DET) {
+      if (K == 1 && PPRG_K1W && P.k1w) {
+        sweep_k1_warps<MODE, DET>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a,
+                                  reinterpret_cast<double*>(smem_dyn), &ctl->ticket[buf], 0, P.ntiles);
+      } else {
+        unsigned long long j = sh_tile[0];
+        TileDesc d = P.desc[j < P.ntiles ? j : 0];
+        for (uint32_t it = 0;; ++it) {
+          if (j >= P.ntiles) break;
+          if (tid == 0) sh_tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
+          TileDesc dn = d;
+          if (d.npieces > 1) {
+            if constexpr (K >= WIDE_K)
+              hub_piece_wide<K, MODE, DET>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt,
+                                           sh_push, sh_d, sh_np, sh_nn, sh_et);
+            else
+              hub_piece<K, MODE, DET>(P, d, j, sh_hub, &sh_flag, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+            dn = P.desc[sh_tile[(it + 1) & 1] < P.ntiles ? sh_tile[(it + 1) & 1] : 0];
+            __syncthreads();
+          } else if constexpr (K >= WIDE_K) {
+            tile_rows_wide<K, MODE, DET>(P, d, smem_dyn, cs, thr_cur, csrc, yg, rcur, rnxt, ynxt, a, ba,
+                                         &sh_nlong, &sh_tile[(it + 1) & 1], &dn);
+          } else {
+            tile_rows<K, MODE, DET>(P, d, smem_dyn, cs, thr_cur, yg, rcur, rnxt, ynxt, a, ba, &sh_nlong,
+                                    &sh_tile[(it + 1) & 1], &dn);
+          }
+          j = sh_tile[(it + 1) & 1];
+          d = dn;
+        }
+      }
+      source_rows<K, MODE, DET>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+    } else {
+      // sources without in-edges first (their inflow does not depend on the
+      // sweep's other rows); then the waves
+      source_rows<K, MODE, DET>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
+      const uint32_t nwv = MODE == M_POWERPUSH && P.nwaves > 1 ? P.nwaves : 1;
+      for (uint32_t wv = 0; wv < nwv; ++wv) {
+        const uint64_t t0 = nwv > 1 ? P.wave_tile[wv] : 0, t1 = nwv > 1 ? P.wave_tile[wv + 1] : P.ntiles;
+        yg.lo = nwv > 1 ? P.wave_node[wv] : 0u;  // wave_node[0] = 0: sources without in-edges are in yn
+        if (tid == 0 && !P.k1w) sh_tile[0] = t0 + atomicAdd(&ctl->wticket[buf][wv], 1u);
+        __syncthreads();
+        run_tiles(&ctl->wticket[buf][wv], t0, t1);
+        if (wv + 1 < nwv) grid_barrier2(&ctl->gbar, ++gen);
+      }
     }
-    }
-    source_rows<K, MODE>(P, cs, thr_cur, yg, rcur, rnxt, ynxt, a);
     // block-level flush of this sweep's accumulators: reduce over the lanes of
     // the same column first (shuffles), then one shared atomic per warp/column
     {
@@ -1075,6 +1200,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
       if (sh_et[tid]) atomicAdd(&ctl->et[buf][tid], sh_et[tid]);
     }
     if (MODE == M_FINAL) {
+      if (blockIdx.x == 0 && tid < K) ctl->out_scale[tid] = cs[tid].scp;
       __syncthreads();
       break;
     }
@@ -1083,11 +1209,11 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
     if (tid < K) {
       const int cc = tid;
       if (!cs[cc].done) {
-        const double pushed = __ldcg(&ctl->pushed[buf][cc]);
+        const double pushed = __ldcg(&ctl->pushed[buf][cc]) / cs[cc].scp;
         const unsigned long long np = __ldcg(&ctl->npush[buf][cc]);
         cs[cc].sweeps += 1;
         cs[cc].pushes += np;
-        cs[cc].D = __ldcg(&ctl->dsum[buf][cc]);
+        cs[cc].D = __ldcg(&ctl->dsum[buf][cc]) / cs[cc].scd;
         if (P.trace && cc == 0 && blockIdx.x == 0 && sweep < P.trace_cap) {
           unsigned long long t;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

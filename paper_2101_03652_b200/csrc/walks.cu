@@ -114,7 +114,30 @@ struct McParams {
   uint64_t seed;
   double* est;
   uint32_t src[64];
+  double sc[64];  // deterministic mode: fixed-point scale of column c's sum (qterm)
 };
+
+// Deterministic mode: walk contributions are summed as integers (the
+// contribution * 2^S rounded; exact fp64 sums while every partial sum stays
+// below 2^53) into a zeroed accumulator, so the order of the atomics does not
+// matter; k_est_combine then adds the reserve: est = base_scale * base + acc / sc.
+template <bool DET>
+__device__ __forceinline__ double mc_term(double v, const McParams& P, int c) {
+  if constexpr (DET) return rint(v * P.sc[c]);
+  else return v;
+}
+__global__ void k_est_combine(const double* base, double base_scale, uint64_t nk, int K,
+                              const double* sc, double* est) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nk;
+       i += (uint64_t)gridDim.x * blockDim.x)
+    est[i] = (base ? base_scale * base[i] : 0.0) + est[i] / sc[i % K];
+}
+// fixed-point scale for a column whose contributions sum to at most `bound`
+inline double det_scale_host(double bound) {
+  int e = 0;
+  std::frexp(bound > 1e-280 ? bound : 1e-280, &e);
+  return std::ldexp(1.0, 52 - e);
+}
 
 // One walk's terminal: a stored index terminal (index prefix,
 // speedppr.cpp:66-71) or a fresh Philox walk keyed (seed, source, (k, v)).
@@ -125,6 +148,7 @@ __device__ __forceinline__ uint32_t mc_terminal(const McParams& P, uint32_t v, i
 
 // Entries (v, c) with W_v <= 32 walks: one thread each, its walks in a loop;
 // larger entries go to a list for k_mc_big (warp per entry).
+template <bool DET>
 __global__ void k_mc_entries(const __grid_constant__ McParams P, uint64_t* big,
                              unsigned long long* nbig) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < P.nk;
@@ -137,7 +161,7 @@ __global__ void k_mc_entries(const __grid_constant__ McParams P, uint64_t* big,
     }
     const uint32_t v = (uint32_t)(i / P.K);
     const int c = (int)(i % P.K);
-    const double contribution = P.res[i] / (double)wc;  // speedppr.cpp:41
+    const double contribution = mc_term<DET>(P.res[i] / (double)wc, P, c);  // speedppr.cpp:41
     // four walks' terminals resolved before their adds (independent loads in flight)
     uint32_t kk = 0;
     for (; kk + 4 <= (uint32_t)wc; kk += 4) {
@@ -152,6 +176,7 @@ __global__ void k_mc_entries(const __grid_constant__ McParams P, uint64_t* big,
   }
 }
 
+template <bool DET>
 __global__ void k_mc_big(const __grid_constant__ McParams P, const uint64_t* big,
                          const unsigned long long* nbig_p) {
   const unsigned long long nbig = *nbig_p;
@@ -163,7 +188,7 @@ __global__ void k_mc_big(const __grid_constant__ McParams P, const uint64_t* big
     const uint32_t v = (uint32_t)(i / P.K);
     const int c = (int)(i % P.K);
     const unsigned long long wc = P.cnt[i];
-    const double contribution = P.res[i] / (double)wc;
+    const double contribution = mc_term<DET>(P.res[i] / (double)wc, P, c);
     unsigned long long kk = lane;
     for (; kk + 96 < wc; kk += 128) {  // four walks per lane resolved before their adds
       uint32_t t[4];
@@ -179,7 +204,8 @@ __global__ void k_mc_big(const __grid_constant__ McParams P, const uint64_t* big
 
 // pure-sampling branch (speedppr.cpp:90-102): W walks from s, weight 1/W
 __global__ void k_mc_pure(const uint64_t* off, const uint32_t* nbr, uint64_t W, int K, int k,
-                          const uint32_t* src, double alpha, uint64_t seed, double* est) {
+                          const uint32_t* src, double alpha, uint64_t seed, double* est,
+                          double det_w) {  // deterministic mode: the integer 1/W * 2^S, else 0
   const uint64_t total = W * (uint64_t)k;
   for (uint64_t w = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; w < total;
        w += (uint64_t)gridDim.x * blockDim.x) {
@@ -187,7 +213,7 @@ __global__ void k_mc_pure(const uint64_t* off, const uint32_t* nbr, uint64_t W, 
     const uint32_t kk = (uint32_t)(w % W);
     const uint32_t s = src[c];
     const uint32_t t = philox_walk(off, nbr, s, s, alpha, seed, kk, s, s);
-    atomicAdd(est + (uint64_t)t * K + c, 1.0 / (double)W);
+    atomicAdd(est + (uint64_t)t * K + c, det_w > 0.0 ? det_w : 1.0 / (double)W);
   }
 }
 
@@ -332,8 +358,18 @@ void monte_carlo(Graph& g, const WalkIndex* idx, uint32_t s, double alpha, uint6
   DevBuf<uint64_t> big(n);
   DevBuf<unsigned> bad(1);
   DevBuf<uint32_t> dsrc(1);
+  const bool det = t_det;
+  DevBuf<double> base(det ? n : 0), dsc(det ? 1 : 0);
   PPRG_CUDA(cudaMemcpyAsync(res.get(), h_residue, 8 * n, cudaMemcpyHostToDevice, st));
-  PPRG_CUDA(cudaMemcpyAsync(est.get(), h_reserve, 8 * n, cudaMemcpyHostToDevice, st));
+  PPRG_CUDA(cudaMemcpyAsync(det ? base.get() : est.get(), h_reserve, 8 * n, cudaMemcpyHostToDevice, st));
+  double hsc = 1.0;
+  if (det) {
+    double rs = 0.0;  // the contributions sum to the residue mass
+    for (uint64_t v = 0; v < n; ++v) rs += h_residue[v] > 0 ? h_residue[v] : 0.0;
+    hsc = det_scale_host(2.0 * rs);
+    PPRG_CUDA(cudaMemsetAsync(est.get(), 0, 8 * n, st));
+    PPRG_CUDA(cudaMemcpyAsync(dsc.get(), &hsc, 8, cudaMemcpyHostToDevice, st));
+  }
   PPRG_CUDA(cudaMemsetAsync(bad.get(), 0, 4, st));
   PPRG_CUDA(cudaMemsetAsync(colw.get(), 0, 8 * 65, st));
   k_mc_counts<<<std::min<unsigned>(gridn(n), g.sm_count * 8), 256, 0, st>>>(
@@ -356,8 +392,15 @@ void monte_carlo(Graph& g, const WalkIndex* idx, uint32_t s, double alpha, uint6
   P.seed = seed;
   P.est = est.get();
   P.src[0] = s;
-  k_mc_entries<<<gridn(n), 256, 0, st>>>(P, big.get(), colw.get() + 64);
-  k_mc_big<<<g.sm_count * 8, 256, 0, st>>>(P, big.get(), colw.get() + 64);
+  P.sc[0] = hsc;
+  if (det) {
+    k_mc_entries<true><<<gridn(n), 256, 0, st>>>(P, big.get(), colw.get() + 64);
+    k_mc_big<true><<<g.sm_count * 8, 256, 0, st>>>(P, big.get(), colw.get() + 64);
+    k_est_combine<<<gridn(n), 256, 0, st>>>(base.get(), 1.0, n, 1, dsc.get(), est.get());
+  } else {
+    k_mc_entries<false><<<gridn(n), 256, 0, st>>>(P, big.get(), colw.get() + 64);
+    k_mc_big<false><<<g.sm_count * 8, 256, 0, st>>>(P, big.get(), colw.get() + 64);
+  }
   PPRG_CUDA(cudaGetLastError());
   unsigned long long hw = 0;
   PPRG_CUDA(cudaMemcpyAsync(h_est, est.get(), 8 * n, cudaMemcpyDeviceToHost, st));
@@ -388,7 +431,7 @@ namespace {
 struct McState {
   DevBuf<unsigned long long> cnt, colw;
   DevBuf<uint64_t> big;
-  DevBuf<double> est, stage[2];
+  DevBuf<double> est, stage[2], sc;
   DevBuf<unsigned> bad;
   uint64_t nk = 0;
   unsigned slot = 0;
@@ -447,8 +490,16 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
       PPRG_CUDA(cudaMemcpyAsync(dsrc.get(), sources + b0, 4 * kb, cudaMemcpyHostToDevice, st));
       PPRG_CUDA(cudaMemsetAsync(est.get(), 0, 8 * n * K, st));
       if (W > 0xffffffffull) fail(EINVAL_, "speedppr: walk budget exceeds 2^32 walks per query");
+      // deterministic mode: walk counts (exact integers), divided by W after
       k_mc_pure<<<gridn(W * kb), 256, 0, st>>>(g.off.get(), g.nbr.get(), W, K, kb, dsrc.get(), alpha,
-                                              seed, est.get());
+                                              seed, est.get(), t_det ? 1.0 : 0.0);
+      if (t_det) {
+        std::vector<double> hs(K, (double)W);
+        DevBuf<double> dsc(K);
+        PPRG_CUDA(cudaMemcpyAsync(dsc.get(), hs.data(), 8 * K, cudaMemcpyHostToDevice, st));
+        k_est_combine<<<gridn(n * K), 256, 0, st>>>(nullptr, 0.0, n * (uint64_t)K, K, dsc.get(), est.get());
+        PPRG_CUDA(cudaStreamSynchronize(st));  // dsc is freed at scope exit
+      }
       double* dst = est_out ? (out_on_device ? est_out + (uint64_t)b0 * n : outb.get()) : nullptr;
       if (dst) k_unpack_est<<<gridn(n * K), 256, 0, st>>>(est.get(), n, K, kb, dst);
       if (est_out && !out_on_device)
@@ -482,7 +533,9 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
     PPRG_CUDA(cudaMemsetAsync(mc.colw.get(), 0, 8 * 65, st));
     k_mc_counts<<<std::min<unsigned>(gridn(nk), g.sm_count * 8), 256, 0, st>>>(
         pv.res, g.deg.get(), n, K, kb, (double)W, mc.cnt.get(), mc.bad.get(), mc.colw.get());
-    k_est_init<<<gridn(nk), 256, 0, st>>>(pv.x, nk, alpha, mc.est.get());
+    const bool det = t_det;
+    if (det) PPRG_CUDA(cudaMemsetAsync(mc.est.get(), 0, 8 * nk, st));
+    else k_est_init<<<gridn(nk), 256, 0, st>>>(pv.x, nk, alpha, mc.est.get());
     McParams P;
     std::memset(&P, 0, sizeof P);
     P.off = g.off.get();
@@ -499,8 +552,20 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
     for (int c = 0; c < K; ++c) P.src[c] = pv.src[c];
     // Entries run thread-per-(v, c); entries over 32 walks are queued and run
     // warp-per-entry by a fixed-size grid that reads the queue length on device.
-    k_mc_entries<<<gridn(nk), 256, 0, st>>>(P, mc.big.get(), nbig);
-    k_mc_big<<<g.sm_count * 8, 256, 0, st>>>(P, mc.big.get(), nbig);
+    if (det) {
+      // column c's contributions sum to its residue mass after refine
+      std::vector<double> hs(K, 1.0);
+      for (uint32_t c = 0; c < kb; ++c) hs[c] = P.sc[c] = det_scale_host(2.0 * cs[c].r_sum);
+      for (int c = kb; c < K; ++c) P.sc[c] = 1.0;
+      if (!mc.sc.get()) mc.sc.alloc(64);
+      PPRG_CUDA(cudaMemcpyAsync(mc.sc.get(), hs.data(), 8 * K, cudaMemcpyHostToDevice, st));
+      k_mc_entries<true><<<gridn(nk), 256, 0, st>>>(P, mc.big.get(), nbig);
+      k_mc_big<true><<<g.sm_count * 8, 256, 0, st>>>(P, mc.big.get(), nbig);
+      k_est_combine<<<gridn(nk), 256, 0, st>>>(pv.x, alpha, nk, K, mc.sc.get(), mc.est.get());
+    } else {
+      k_mc_entries<false><<<gridn(nk), 256, 0, st>>>(P, mc.big.get(), nbig);
+      k_mc_big<false><<<g.sm_count * 8, 256, 0, st>>>(P, mc.big.get(), nbig);
+    }
     PPRG_CUDA(cudaGetLastError());
     if (est_out && out_on_device) {
       k_unpack_est<<<gridn(nk), 256, 0, st>>>(mc.est.get(), n, K, kb, est_out + (uint64_t)b0 * n);

@@ -13,8 +13,10 @@ sys.path.insert(0, ROOT)
 import paper_2101_03652_b200 as P  # noqa: E402
 
 ALPHA, LAM = 0.2, 1e-8
+if os.environ.get("AB_DET"):
+    P.set_deterministic(True)
 which = sys.argv[1].split(",") if len(sys.argv) > 1 else ["0", "2", "3"]
-rec = {"env": {k: v for k, v in os.environ.items() if k.startswith("PPRG_")}}
+rec = {"env": {k: v for k, v in os.environ.items() if k.startswith(("PPRG_", "AB_"))}}
 
 
 def split(cs, k):

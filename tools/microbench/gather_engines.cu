@@ -688,6 +688,35 @@ int main(int argc, char** argv) {
     TMA(4, 1, 3)
     TMA(2, 1, 6)
     TMA(3, 2, 2)
+#define LGS(D, WPB, BPS)                                                                           \
+  {                                                                                                \
+    const size_t sm = (size_t)D * K * 8 * WPB;                                                     \
+    CK(cudaFuncSetAttribute(k_lgs<D, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));  \
+    rep("lgs D=" #D " wpb=" #WPB " bps=" #BPS,                                                      \
+        timeit([&] { k_lgs<D, WPB><<<sms * BPS, WPB * 32, sm>>>(dpc, npc, dnbr, y, out); }, 5));    \
+    CK(cudaGetLastError());                                                                        \
+  }
+#define BULK(D, WPB, BPS)                                                                          \
+  {                                                                                                \
+    const size_t sm = (size_t)D * K * 8 * WPB;                                                     \
+    CK(cudaFuncSetAttribute(k_bulk<D, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)); \
+    rep("bulk D=" #D " wpb=" #WPB " bps=" #BPS,                                                     \
+        timeit([&] { k_bulk<D, WPB><<<sms * BPS, WPB * 32, sm>>>(dpc, npc, dnbr, y, out); }, 5));   \
+    CK(cudaGetLastError());                                                                        \
+  }
+    LGS(8, 4, 8)
+    LGS(16, 4, 6)
+    LGS(16, 8, 3)
+    LGS(24, 4, 4)
+    LGS(32, 4, 3)
+    LGS(32, 2, 6)
+    BULK(8, 4, 8)
+    BULK(16, 4, 6)
+    BULK(16, 8, 3)
+    BULK(32, 4, 3)
+    BULK(32, 2, 6)
+    rep("regpp G=4", timeit([&] { k_regpp<4><<<sms * 8, 128>>>(dpc, npc, dnbr, y, out); }, 5));
+    rep("regpp G=8", timeit([&] { k_regpp<8><<<sms * 8, 128>>>(dpc, npc, dnbr, y, out); }, 5));
     // correctness: stream and reg must give the same sums
     std::vector<double> a(npc * K), b(npc * K);
     CK(cudaMemset(y, 0, 8 * n * K));
@@ -719,6 +748,21 @@ int main(int argc, char** argv) {
       md = 0;
       for (uint64_t i = 0; i < npc * K; ++i) md = std::max(md, std::abs(a[i] - b[i]));
       printf("tma vs reg max |diff| = %g\n", md);
+    }
+    {
+      const size_t sm = (size_t)16 * K * 8 * 4;
+      k_lgs<16, 4><<<sms * 6, 128, sm>>>(dpc, npc, dnbr, y, out);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(b.data(), out, 8 * npc * K, cudaMemcpyDeviceToHost));
+      md = 0;
+      for (uint64_t i = 0; i < npc * K; ++i) md = std::max(md, std::abs(a[i] - b[i]));
+      printf("lgs vs reg max |diff| = %g\n", md);
+      k_bulk<16, 4><<<sms * 6, 128, sm>>>(dpc, npc, dnbr, y, out);
+      CK(cudaGetLastError());
+      CK(cudaMemcpy(b.data(), out, 8 * npc * K, cudaMemcpyDeviceToHost));
+      md = 0;
+      for (uint64_t i = 0; i < npc * K; ++i) md = std::max(md, std::abs(a[i] - b[i]));
+      printf("bulk vs reg max |diff| = %g\n", md);
     }
     CK(cudaMemset(y, 0, 8 * n * K));
   }
