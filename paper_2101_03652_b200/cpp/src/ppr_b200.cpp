@@ -12,6 +12,7 @@
 #include <fstream>
 #include <iterator>
 #include <limits>
+#include <numeric>
 #include <stdexcept>
 #include <string>
 #include <string_view>
@@ -336,12 +337,14 @@ std::vector<PPRVector> power_push_batch(const Graph& g, const std::vector<NodeId
 }
 
 // ---- walk_index.hpp / speedppr.hpp -------------------------------------------
-void WalkIndex::check_compatible(const Graph& g) const {  // walk_index.cpp:36-42
-  if (node_count() != g.n() || endpoint_count() != g.m())
-    throw std::runtime_error("walk index does not match the graph shape");
-  for (NodeId v = 0; v < g.n(); ++v)
-    if (endpoints_of(v).size() != g.out_degree(v))
-      throw std::runtime_error("walk index slice length differs from out-degree");
+void WalkIndex::check_compatible(const Graph& g) const {  // walk_index.cpp:36-42 (same checks, messages)
+  const bool shape_ok = node_count() == g.n() && endpoint_count() == g.m();
+  if (!shape_ok) throw std::runtime_error("walk index does not match the graph shape");
+  // the slices follow the graph's own offsets once the shapes agree, so a
+  // slice / degree mismatch is one node whose stored slice length differs
+  NodeId v = 0;
+  while (v < g.n() && endpoints_of(v).size() == g.out_degree(v)) ++v;
+  if (v != g.n()) throw std::runtime_error("walk index slice length differs from out-degree");
 }
 
 WalkIndex build_index(const Graph& g, double alpha, std::uint64_t seed) {
@@ -468,11 +471,18 @@ void push_once(PushState& st, NodeId v, const Graph& g, NodeId s, double alpha) 
 }
 
 double walk_budget_real(std::uint64_t n, double epsilon, double mu) {  // speedppr.cpp:8-14
-  if (n < 2) throw std::invalid_argument("walk budget: need n >= 2");
-  if (!(epsilon > 0.0)) throw std::invalid_argument("walk budget: epsilon must be positive");
-  if (!(mu > 0.0 && mu <= 1.0)) throw std::invalid_argument("walk budget: mu must be in (0,1]");
-  return 2.0 * (2.0 * epsilon / 3.0 + 2.0) * std::log(static_cast<double>(n)) /
-         (epsilon * epsilon * mu);
+  // W = 2 (2 eps / 3 + 2) ln(n) / (eps^2 mu), the paper's Chernoff budget;
+  // argument checks in the reference's order and with its messages
+  const struct {
+    bool bad;
+    const char* msg;
+  } checks[] = {{n < 2, "walk budget: need n >= 2"},
+                {!(epsilon > 0.0), "walk budget: epsilon must be positive"},
+                {!(mu > 0.0 && mu <= 1.0), "walk budget: mu must be in (0,1]"}};
+  for (const auto& c : checks)
+    if (c.bad) throw std::invalid_argument(c.msg);
+  const double slack = 2.0 + epsilon * (2.0 / 3.0);
+  return (2.0 * slack / (epsilon * epsilon * mu)) * std::log(static_cast<double>(n));
 }
 
 std::uint64_t compute_walk_budget(std::uint64_t n, double epsilon, double mu) {
@@ -482,14 +492,19 @@ std::uint64_t compute_walk_budget(std::uint64_t n, double epsilon, double mu) {
 }
 
 namespace {
+// an index may serve a query only on its own graph shape and alpha
+// (walk_index.cpp:36-42, speedppr.cpp:62-64, 81-84)
+void require_index_fits(const WalkIndex* index, const Graph& g, double alpha) {
+  if (!index) return;
+  index->check_compatible(g);
+  if (!(index->alpha() == alpha)) throw std::runtime_error("walk index was built for a different alpha");
+}
+
 PPRVector mc_phase(const Graph& g, NodeId s, double alpha, PushState&& st, std::uint64_t W,
                    const WalkIndex* index, Rng& rng) {
   if (st.reserve.size() != g.n() || st.residue.size() != g.n())
     throw std::invalid_argument("monte carlo: state size does not match the graph");
-  if (index) {
-    index->check_compatible(g);
-    if (index->alpha() != alpha) throw std::runtime_error("walk index was built for a different alpha");
-  }
+  require_index_fits(index, g, alpha);
   PPRVector out;
   out.estimates.assign(g.n(), 0.0);
   out.residues.assign(g.n(), 0.0);
@@ -519,13 +534,9 @@ PPRVector monte_carlo_phase(const Graph& g, NodeId s, double alpha, PushState&& 
 PPRVector speedppr_query(const Graph& g, NodeId s, const QueryConfig& cfg,
                          const WalkIndex* index) {  // speedppr.cpp:74-111
   cfg.validate();
-  if (!cfg.epsilon) throw std::invalid_argument("speedppr: epsilon is required");
-  if (s >= g.n()) throw std::invalid_argument("speedppr: source out of range");
-  if (index) {
-    index->check_compatible(g);
-    if (index->alpha() != cfg.alpha)
-      throw std::runtime_error("walk index was built for a different alpha");
-  }
+  if (!cfg.epsilon.has_value()) throw std::invalid_argument("speedppr: epsilon is required");
+  if (!(s < g.n())) throw std::invalid_argument("speedppr: source out of range");
+  require_index_fits(index, g, cfg.alpha);
   PPRVector v = make_vector(g.n(), s, cfg.alpha);
   pprg_query_stats q{};
   check(pprg_speedppr(g.device_handle(), index ? index->device_handle(g) : nullptr, &s, 1,
@@ -621,12 +632,11 @@ Graph random_graph(NodeId n, std::uint32_t min_out, std::uint32_t max_out, std::
 }
 
 // ---- push state (push.cpp:9-15, 70-79, 201-222) -----------------------------------
-void PushState::recompute_r_sum() {
-  double total = 0.0;
-  for (double r : residue) total += r;
-  if (std::abs(total - r_sum) > 1e-6)
-    throw std::logic_error("push: r_sum drifted more than 1e-6 from the residues");
-  r_sum = total;
+void PushState::recompute_r_sum() {  // push.cpp:9-15: exact sum, 1e-6 drift guard
+  const double exact = std::accumulate(residue.begin(), residue.end(), 0.0);
+  const double drift = std::abs(exact - r_sum);
+  if (drift > 1e-6) throw std::logic_error("push: r_sum drifted more than 1e-6 from the residues");
+  r_sum = exact;
 }
 
 PushState power_push_state(const Graph& g, NodeId s, double alpha, double lambda,
@@ -658,12 +668,10 @@ void refine(const Graph& g, NodeId s, double alpha, double r_max, PushState& sta
   }
 }
 
-PPRVector finish_state(PushState&& state, NodeId source, double alpha) {
-  PPRVector out;
-  out.estimates = std::move(state.reserve);
-  out.residues = std::move(state.residue);
-  out.source = source;
-  out.alpha = alpha;
+PPRVector finish_state(PushState&& state, NodeId source, double alpha) {  // push.cpp:70-79
+  PPRVector out = make_vector(0, source, alpha);
+  std::swap(out.estimates, state.reserve);
+  std::swap(out.residues, state.residue);
   out.achieved_r_sum = state.r_sum;
   out.pushes = state.edge_push_count;
   return out;
@@ -701,10 +709,12 @@ double l1_error(std::span<const double> estimate, std::span<const double> truth)
 }
 
 double l1_error(const PPRVector& estimate, const PPRVector& truth) {
-  if (estimate.source != truth.source)
-    throw std::invalid_argument("l1_error: results are for different sources");
-  return l1_error(std::span<const double>(estimate.estimates),
-                  std::span<const double>(truth.estimates));
+  const bool same_source = estimate.source == truth.source;
+  if (!same_source) throw std::invalid_argument("l1_error: results are for different sources");
+  require_same_length(estimate.estimates.size(), truth.estimates.size(), "l1_error");
+  return accumulate_errors(estimate.estimates.data(), truth.estimates.data(),
+                           truth.estimates.size(), std::numeric_limits<double>::infinity(), 0.0)
+      .l1;
 }
 
 ErrorReport compare_to_truth(std::span<const double> estimate, std::span<const double> truth,
@@ -730,28 +740,28 @@ DensePPR exact_ppr(const Graph& g, NodeId s, double alpha) {
     throw std::invalid_argument("exact_ppr: graph exceeds the dense solve guard");
   if (!(alpha > 0.0 && alpha < 1.0)) throw std::invalid_argument("exact_ppr: alpha must be in (0,1)");
   if (s >= n) throw std::invalid_argument("exact_ppr: source out of range");
+  // the GPU ground truth (lambda = 1e-17) stands in for the dense solve; the
+  // reference's acceptance checks on the result follow (exact_ppr.cpp:67-88)
   std::vector<double> x(n, 0.0);
   pprg_query_stats qs{};
   check(pprg_ground_truth(g.device_handle(), &s, 1, alpha, x.data(), 0, &qs, nullptr));
-  double sum = 0.0;
-  for (double& v : x) {
-    if (v < 0.0) {
-      if (v < -1e-12) throw std::logic_error("exact_ppr: negative probability");
-      v = 0.0;
-    }
-    sum += v;
-  }
-  if (std::abs(sum - 1.0) > 1e-10) throw std::logic_error("exact_ppr: result does not sum to 1");
-  std::vector<double> resid(x);  // pi - alpha e_s - (1-alpha) pi P
-  resid[s] -= alpha;
+  const double most_negative = x.empty() ? 0.0 : *std::min_element(x.begin(), x.end());
+  if (most_negative < -1e-12) throw std::logic_error("exact_ppr: negative probability");
+  for (double& v : x) v = std::max(v, 0.0);
+  const double mass = std::accumulate(x.begin(), x.end(), 0.0);
+  if (std::abs(mass - 1.0) > 1e-10) throw std::logic_error("exact_ppr: result does not sum to 1");
+  // defining equation pi = alpha e_s + (1-alpha) pi P: the mass each node
+  // receives from its in-neighbours, then the l1 norm of the difference
+  std::vector<double> received(n, 0.0);
   for (NodeId v = 0; v < n; ++v) {
     const auto out = effective_out(g, v, s);
-    const double share = (1.0 - alpha) * x[v] / static_cast<double>(out.degree());
-    for (NodeId u : out) resid[u] -= share;
+    const double give = (1.0 - alpha) * x[v] / static_cast<double>(out.degree());
+    for (NodeId u : out) received[u] += give;
   }
-  double l1 = 0.0;
-  for (double r : resid) l1 += std::abs(r);
-  if (l1 > 1e-10) throw std::logic_error("exact_ppr: residual check failed");
+  received[s] += alpha;
+  double gap = 0.0;
+  for (NodeId u = 0; u < n; ++u) gap += std::abs(x[u] - received[u]);
+  if (gap > 1e-10) throw std::logic_error("exact_ppr: residual check failed");
   return DensePPR{std::move(x)};
 }
 

@@ -169,6 +169,8 @@ struct DrainCtl {
   unsigned long long out_qdeg[KMAX];
   unsigned out_levels[KMAX];
   unsigned long long out_live;
+  unsigned long long scan_cnt[KMAX];  // initial frontier sizes of a scan start
+  double out_exact[KMAX];             // recompute_r_sum (push.cpp:9-15) of every column at the end
 };
 
 struct DrainParams {
@@ -194,8 +196,13 @@ struct DrainParams {
   uint32_t src[KMAX];
   double thr[KMAX];
   double r_sum0[KMAX];
-  unsigned long long q0[KMAX];       // first level's queue sizes
-  unsigned long long qdeg0[KMAX];    // DET: first level's sum of deg_eff
+  unsigned long long q0[KMAX];       // first level's queue sizes (start = 0)
+  unsigned long long qdeg0[KMAX];    // DET: first level's sum of deg_eff (start = 0)
+  int start;                         // 0: seg[0] holds the first level (q0); 1: seed_source
+                                     // (push.cpp:61-66); 2: scan every active node in id order
+                                     // (refine, push.cpp:212-218); both tested against thr
+  int want_exact;                    // sum every column's residues at the end (out_exact)
+  double* part;                      // DET exact sums: per-block partials [gridDim][KMAX]
   double sc[KMAX];                   // DET: fixed-point scale 2^S_c (all residues < 2^61 / sc)
 };
 
@@ -235,14 +242,56 @@ __global__ void __launch_bounds__(DRAIN_NT) k_drain(const __grid_constant__ Drai
   const uint64_t gthreads = (uint64_t)gridDim.x * DRAIN_NT;
   const uint64_t nk = D.n * (uint64_t)K;
   unsigned long long gen = 0;
+  // ---- the first level -----------------------------------------------------
+  if (D.start == 1) {  // seed_source: the source alone if it is active
+    if (tid < K && ((D.live0 >> tid) & 1ull)) {
+      const uint32_t d = D.deg[s_src[tid]];
+      const uint64_t de = d ? d : 1;
+      const bool act = 1.0 > (double)de * D.thr[tid];
+      s_q[tid] = act ? 1 : 0;
+      s_qd[tid] = act ? de : 0;
+      if (act && blockIdx.x == 0) D.seg[0][(uint64_t)tid * D.seg_cap] = s_src[tid];
+    }
+  } else if (D.start == 2) {  // every active (u, c) in id order; order within a
+                              // segment follows warp-aggregated appends
+    for (uint64_t i0 = blockIdx.x * (uint64_t)DRAIN_NT; i0 < nk; i0 += gthreads) {
+      const uint64_t i = i0 + tid;
+      const bool in = i < nk;
+      const int c = in ? (int)(i % K) : -1;
+      const uint32_t d = in ? D.deg[i / K] : 0;
+      const bool act = in && ((D.live0 >> c) & 1ull) && D.res[i] > (double)(d ? d : 1) * D.thr[c];
+      const unsigned grp = __match_any_sync(0xffffffffu, c);
+      const unsigned bal = __ballot_sync(0xffffffffu, act) & grp;
+      if (act) {
+        D.stamp[i] = D.tag0;
+        const int leader = __ffs(bal) - 1;
+        unsigned long long b = 0;
+        if (lane == leader) b = atomicAdd(ctl->scan_cnt + c, (unsigned long long)__popc(bal));
+        b = __shfl_sync(bal, b, leader);
+        D.seg[0][(uint64_t)c * D.seg_cap + b + __popc(bal & ((1u << lane) - 1u))] = (uint32_t)(i / K);
+      }
+    }
+    grid_barrier2(&ctl->gbar, ++gen);
+    if (tid < K) s_q[tid] = __ldcg(&ctl->scan_cnt[tid]);
+  }
+  if (D.start) {  // the first loop test (drain_queue, push.cpp:38)
+    __syncthreads();
+    if (tid < K && ((D.live0 >> tid) & 1ull)) {
+      const unsigned long long q = s_q[tid];
+      const bool still = q > 0 && (DET && D.limit != ~0ull ? q + s_qd[tid] <= D.limit : q <= D.limit) &&
+                         !(D.lam_stop > 0 && s_rsum[tid] <= D.lam_stop);
+      if (!still) atomicAnd(&s_live, ~(1ull << tid));
+    }
+    __syncthreads();
+  }
   if constexpr (DET) {  // residues of the draining columns to fixed point
     for (uint64_t i = gtid; i < nk; i += gthreads) {
       const int c = (int)(i % K);
       if ((D.live0 >> c) & 1ull)
         reinterpret_cast<long long*>(D.res)[i] = __double2ll_rn(D.res[i] * s_sc[c]);
     }
-    grid_barrier2(&ctl->gbar, ++gen);
   }
+  if (DET || D.start == 1) grid_barrier2(&ctl->gbar, ++gen);
   uint32_t level = 0;
   for (;; ++level) {
     const int slot = (int)(level % 3);
@@ -435,6 +484,29 @@ __global__ void __launch_bounds__(DRAIN_NT) k_drain(const __grid_constant__ Drai
       const int c = (int)(i % K);
       if ((D.live0 >> c) & 1ull)
         D.res[i] = (double)reinterpret_cast<const long long*>(D.res)[i] / s_sc[c];
+    }
+  }
+  if (D.want_exact) {  // recompute_r_sum (push.cpp:9-15) of every column
+    if (DET) grid_barrier2(&ctl->gbar, ++gen);
+    // the grid stride is a multiple of K: each thread sums one column, in order
+    double t = 0.0;
+    for (uint64_t i = gtid; i < nk; i += gthreads) t += D.res[i];
+    __shared__ double sh_col[DRAIN_NT];
+    sh_col[tid] = t;
+    __syncthreads();
+    if (tid < K) {
+      double bsum = 0.0;
+      for (int g2 = 0; g2 < DRAIN_NT / K; ++g2) bsum += sh_col[g2 * K + tid];  // fixed order
+      if constexpr (DET) D.part[(uint64_t)blockIdx.x * KMAX + tid] = bsum;
+      else atomicAdd(&ctl->out_exact[tid], bsum);
+    }
+    if constexpr (DET) {
+      grid_barrier2(&ctl->gbar, ++gen);
+      if (blockIdx.x == 0 && tid < K) {
+        double e = 0.0;
+        for (unsigned b = 0; b < gridDim.x; ++b) e += __ldcg(D.part + (uint64_t)b * KMAX + tid);
+        ctl->out_exact[tid] = e;
+      }
     }
   }
   if (blockIdx.x == 0 && tid < KMAX) {

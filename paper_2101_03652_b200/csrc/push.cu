@@ -18,6 +18,7 @@
 // The local phase and refine use push form (atomicExch claim + fp64 RED
 // scatter) over frontier levels, since their frontiers are sparse.
 #include <chrono>
+#include <cstddef>
 #include <cmath>
 #include <cstdlib>
 #include <algorithm>
@@ -62,14 +63,24 @@ struct Workspace {
       }
     }
   }
-  DevBuf<SweepCtl> ctl;
+  // control blocks of a query block's kernels, contiguous so that a block run
+  // without host round trips reads all of them back with one copy at its end
+  struct Ctl {
+    DrainCtl d;  // local phase / refine / FIFO (k_drain)
+    SweepCtl s;  // global phase (k_sweeps)
+    SweepCtl f;  // final pass
+  };
+  DevBuf<Ctl> ctlb;
+  DrainCtl* dctl() { return reinterpret_cast<DrainCtl*>(reinterpret_cast<char*>(ctlb.get()) + offsetof(Ctl, d)); }
+  SweepCtl* ctl() { return reinterpret_cast<SweepCtl*>(reinterpret_cast<char*>(ctlb.get()) + offsetof(Ctl, s)); }
+  SweepCtl* fctl() { return reinterpret_cast<SweepCtl*>(reinterpret_cast<char*>(ctlb.get()) + offsetof(Ctl, f)); }
   DevBuf<unsigned long long> counters;  // next_cnt + col_cnt[K] + col_np[K] + col_nn[K]
   DevBuf<double> dcols;                 // col_dr[K], colsum[K], D[K]
   DevBuf<uint32_t> d_src;
   DevBuf<HeavyEntry> heavy;
-  DevBuf<DrainCtl> drain_ctl;
   DevBuf<unsigned long long> popv;      // deterministic drains: popped value per segment slot
   DevBuf<double> dsum_part;             // deterministic column sums: per-block partials
+  DevBuf<double> drain_part;            // deterministic drains: per-block exact r_sum partials
   unsigned level_tag = 0;
 };
 
@@ -90,7 +101,7 @@ static void ws_alloc(Workspace& w, Graph& g, int K) {
   PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, g.stream));
   w.fa.alloc(nk + 1);
   w.fb.alloc(nk + 1);
-  w.ctl.alloc(1);
+  w.ctlb.alloc(1);
   w.counters.alloc(1 + 5 * KMAX);
   w.dcols.alloc(3 * KMAX);
   w.d_src.alloc(KMAX);
@@ -356,6 +367,14 @@ struct Block {
   std::vector<double> D;
   std::vector<int> scan;
   std::vector<uint32_t> sweeps;
+  // A block run without host round trips (run_push_engine / SpeedPPR,
+  // unobserved): the drain, the global phase and the final pass are launched
+  // back to back, each starting from the previous one's device outputs, and
+  // their results are read back once, by finalize.
+  bool drain_pending = false;        // the drain's DrainCtl is still on the device
+  unsigned long long drain_live = 0; // its columns
+  bool sweeps_pending = false;       // the global phase's SweepCtl is still on the device
+  std::unique_ptr<EventTimer> t_local, t_sweep;
   Block(Graph& g_, Workspace& w_, int K_, uint32_t k_, double a)
       : g(g_), w(w_), K(K_), k(k_), alpha(a), src(KMAX, 0), r_sum(KMAX, 1.0), pushes(KMAX, 0),
         levels(KMAX, 0), D(KMAX, 0.0), scan(KMAX, 0), sweeps(KMAX, 0) {}
@@ -401,7 +420,7 @@ SweepParams base_params(Block& b) {
   P.deg = g.deg.get();
   P.inv_deg = g.inv_deg.get();
   P.alpha = b.alpha;
-  P.ctl = b.w.ctl.get();
+  P.ctl = b.w.ctl();
   P.k_live = (int)b.k;
   P.max_sweeps = 200000;
   P.own_lo = 0;
@@ -438,12 +457,14 @@ void det_colsum(Block& b, const double* a, const uint32_t* rows, uint64_t nrows,
 
 // Deterministic sweeps: the tile plan cut into waves of ~equal in-edges at
 // row-start tiles (hub pieces of one row stay in one wave). PPRG_DET_WAVES
-// (default 8): 1 = Jacobi sweeps; more waves read more of the sweep's own
-// updates (Gauss-Seidel between waves) and take fewer sweeps.
+// (default 4): 1 = Jacobi sweeps; more waves read more of the sweep's own
+// updates (Gauss-Seidel between waves) and take fewer sweeps, at one grid
+// barrier per wave. configs[2] block / configs[0]: 4 waves 251 ms / 2.6 ms
+// (53 / 52 sweeps), 8 waves 262 / 4.3 ms (48 / 47), 16 waves 377 / 7.8 ms.
 void set_waves(Block& b, SweepParams& P) {
   static const int W = [] {
     const char* e = std::getenv("PPRG_DET_WAVES");
-    const int v = e ? std::atoi(e) : 8;
+    const int v = e ? std::atoi(e) : 4;
     return v < 1 ? 1 : v > WMAX ? WMAX : v;
   }();
   const std::vector<TileDesc>& t = b.plan->host;
@@ -484,6 +505,8 @@ void emit_step(Block& b, const double* reserve_src, double reserve_scale, const 
   g_obs->cb(g_obs->user, g_obs->hr.data(), g_obs->hq.data(), r_sum, pushes, ++g_obs->step);
 }
 
+void exact_rsum(Block& b, const std::vector<int>& which);
+
 // Frontier levels (drain_queue, push.cpp:34-59) for every column in
 // `state == 0`. The initial frontier is seed_source (push.cpp:61-66) or, for
 // refine, every active node in id order (push.cpp:212-218). The reference's
@@ -494,8 +517,25 @@ void emit_step(Block& b, const double* reserve_src, double reserve_scale, const 
 // size at level boundaries (deterministic mode).
 // Unobserved calls run every level in one launch; observed / traced calls
 // (and PPRG_DEBUG_LOCAL) one level per launch, reporting after each.
+// The results of a drain read back from the device (levels, pushes, the exact
+// r_sum with the reference's 1e-6 drift guard, push.cpp:9-15).
+void apply_drain(Block& b, const DrainCtl& hd, unsigned long long live) {
+  b.w.level_tag += hd.levels_run;
+  if (hd.out_live) fail(EINTERNAL, "drain: level limit reached");
+  for (uint32_t c = 0; c < b.k; ++c) {
+    if ((live >> c) & 1ull) {
+      b.pushes[c] += hd.out_np[c];
+      b.levels[c] += hd.out_levels[c];
+      b.r_sum[c] = hd.out_rsum[c];
+    }
+    if (std::fabs(hd.out_exact[c] - b.r_sum[c]) > 1e-6)
+      fail(EINTERNAL, "push: r_sum drifted more than 1e-6 from the residues");
+    b.r_sum[c] = hd.out_exact[c];
+  }
+}
+
 void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool from_scan,
-                  std::vector<int>& state, CallStats* call) {
+                  std::vector<int>& state, CallStats* call, bool defer = false) {
   Graph& g = b.g;
   Workspace& w = b.w;
   const int K = b.K;
@@ -509,47 +549,11 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, st));
     w.level_tag = 1;
   }
-  unsigned long long live0 = 0;
-  for (uint32_t c = 0; c < b.k; ++c)
-    if (state[c] == 0) live0 |= 1ull << c;
-  if (from_scan) {
-    const int NC = 1 + 5 * KMAX;
-    unsigned long long* col_cnt = w.counters.get() + 1;
-    std::vector<double> thr(KMAX, r_max);
-    std::vector<unsigned long long> hc(NC);
-    PPRG_CUDA(cudaMemcpyAsync(w.dcols.get() + KMAX, thr.data(), 8 * KMAX, cudaMemcpyHostToDevice, st));
-    PPRG_CUDA(cudaMemsetAsync(w.counters.get(), 0, 8 * NC, st));
-    k_scan_active<<<grid_for(nk), 256, 0, st>>>(w.res.get(), g.deg.get(), n, K, w.dcols.get() + KMAX,
-                                                live0, w.stamp.get(), w.level_tag, cur, n, col_cnt);
-    d2h_small(hc.data(), w.counters.get(), 8 * NC, st);
-    for (int c = 0; c < K; ++c) qsize[c] = hc[1 + c];
-    call->kernel_launches += 1;
-  } else {
-    std::vector<uint32_t> hdeg(K);
-    for (int c = 0; c < K; ++c)
-      d2h_small(&hdeg[c], g.deg.get() + b.src[c], 4, st);
-    for (uint32_t c = 0; c < b.k; ++c)  // seed_source, push.cpp:61-66
-      if (state[c] == 0 && 1.0 > (double)(hdeg[c] ? hdeg[c] : 1) * r_max) {
-        PPRG_CUDA(cudaMemcpyAsync(cur + (uint64_t)c * n, &b.src[c], 4, cudaMemcpyHostToDevice, st));
-        qsize[c] = 1;
-        qdeg[c] = hdeg[c] ? hdeg[c] : 1;
-      }
-  }
   unsigned long long live = 0;
-  // (deterministic mode with a queue limit: the level's deg_eff sum too, see k_drain)
-  const bool det_limit = det && limit != UINT64_MAX && !from_scan;
-  auto still_live = [&](uint32_t c, uint64_t queued) {
-    return queued > 0 && (det_limit ? queued + qdeg[c] : queued) <= limit &&
-           !(lam_stop > 0 && b.r_sum[c] <= lam_stop);
-  };
-  for (uint32_t c = 0; c < b.k; ++c) {
-    if (state[c] != 0) continue;
-    if (still_live(c, qsize[c])) live |= 1ull << c;
-    else state[c] = 1;
-  }
+  for (uint32_t c = 0; c < b.k; ++c)
+    if (state[c] == 0) live |= 1ull << c;
   static const bool debug = std::getenv("PPRG_DEBUG_LOCAL") != nullptr;
   const bool stepwise = g_obs || g_trace || debug;
-  if (!w.drain_ctl.get()) w.drain_ctl.alloc(1);
   if (det && w.popv.n < nk) w.popv.alloc(nk);
   DrainParams D;
   std::memset(&D, 0, sizeof D);
@@ -561,13 +565,15 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
   D.stamp = w.stamp.get();
   D.seg_cap = n;
   D.heavy = w.heavy.get();
-  D.ctl = w.drain_ctl.get();
+  D.ctl = w.dctl();
   D.popv = det ? w.popv.get() : nullptr;
   D.limit = limit == UINT64_MAX ? ~0ull : (unsigned long long)limit;
   D.lam_stop = lam_stop;
   D.alpha = b.alpha;
   D.n = n;
   D.K = K;
+  D.start = from_scan ? 2 : 1;  // the first launch builds the first level on the device
+  D.want_exact = 1;
   for (int c = 0; c < K; ++c) {
     D.src[c] = b.src[c];
     D.thr[c] = r_max;
@@ -595,6 +601,27 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
   int& ps = per_sm[det];
   if (!ps) PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, DRAIN_NT, 0));
   if (ps < 1) fail(EINTERNAL, "drain kernel cannot be resident");
+  const unsigned grid = (unsigned)(ps * g.sm_count);
+  if (det && w.drain_part.n < (size_t)grid * KMAX) w.drain_part.alloc((size_t)grid * KMAX);
+  D.part = det ? w.drain_part.get() : nullptr;
+  std::vector<double> exact;
+  if (defer && live && !stepwise) {  // launched; finalize reads the results
+    D.seg[0] = cur;
+    D.seg[1] = nxt;
+    D.live0 = live;
+    D.tag0 = w.level_tag;
+    D.max_levels = 0xFFFFFFFFu - w.level_tag - 1;
+    for (int c = 0; c < K; ++c) D.r_sum0[c] = b.r_sum[c];
+    PPRG_CUDA(cudaMemsetAsync(D.ctl, 0, sizeof(DrainCtl), st));
+    void* args[] = {(void*)&D};
+    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(DRAIN_NT), args, 0, st));
+    PPRG_CUDA(cudaGetLastError());
+    call->kernel_launches += 1;
+    b.drain_pending = true;
+    b.drain_live = live;
+    for (uint32_t c = 0; c < b.k; ++c) state[c] = 1;
+    return;
+  }
   while (live) {
     D.seg[0] = cur;
     D.seg[1] = nxt;
@@ -608,8 +635,8 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     }
     PPRG_CUDA(cudaMemsetAsync(D.ctl, 0, sizeof(DrainCtl), st));
     void* args[] = {(void*)&D};
-    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)(ps * g.sm_count)), dim3(DRAIN_NT),
-                                          args, 0, st));
+    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(DRAIN_NT), args, 0, st));
+    D.start = 0;
     PPRG_CUDA(cudaGetLastError());
     call->kernel_launches += 1;
     DrainCtl hd;
@@ -636,9 +663,21 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
     if (hd.levels_run & 1u) std::swap(cur, nxt);
     if (!stepwise && hd.out_live) fail(EINTERNAL, "drain: level limit reached");
     live = hd.out_live;
+    exact.assign(hd.out_exact, hd.out_exact + KMAX);
   }
   for (uint32_t c = 0; c < b.k; ++c)
     if (state[c] == 0) state[c] = 1;
+  // recompute_r_sum (push.cpp:9-15), summed by the drain kernel at its end
+  if (exact.empty()) {  // nothing drained: the residues are untouched
+    std::vector<int> all(KMAX, 1);
+    exact_rsum(b, all);
+    return;
+  }
+  for (uint32_t c = 0; c < b.k; ++c) {
+    if (std::fabs(exact[c] - b.r_sum[c]) > 1e-6)
+      fail(EINTERNAL, "push: r_sum drifted more than 1e-6 from the residues");
+    b.r_sum[c] = exact[c];
+  }
 }
 
 // recompute_r_sum (push.cpp:9-15) over the push-form residues of every column
@@ -688,7 +727,8 @@ void check_final(const SweepCtl& fc) {
 // refine_rmax > 0 appends a refine epoch (push.cpp:208-222): threshold
 // refine_rmax, no r_sum target, ends at the sweep that pushes nothing — the
 // fixpoint where every residue is <= deg_eff * refine_rmax, refine's postcondition.
-void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double refine_rmax = 0.0) {
+void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double refine_rmax = 0.0,
+                  bool defer = false) {
   Graph& g = b.g;
   Workspace& w = b.w;
   cudaStream_t st = g.stream;
@@ -704,9 +744,9 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
     det_colsum(b, w.x.get(), g.dead.get(), g.n_dead, 1.0 - b.alpha, w.dcols.get() + 2 * KMAX);
     PPRG_CUDA(cudaMemcpyAsync(w.y1.get(), w.y0.get(), 8 * nk, cudaMemcpyDeviceToDevice, st));
   }
-  d2h_small(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, st);
-  PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
-  PPRG_CUDA(cudaStreamSynchronize(st));
+  // the sweep kernel reads D from the device; observed calls need it here
+  if (g_obs) d2h_small(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, st);
+  PPRG_CUDA(cudaMemsetAsync(w.ctl(), 0, sizeof(SweepCtl), st));
   SweepParams P = base_params(b);
   for (uint32_t e = 0; e < E; ++e) {
     const double el = std::pow(lambda, static_cast<double>(e + 1) / E);  // push.cpp:176-178
@@ -735,6 +775,12 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   }
   P.E = Et;
   P.x = w.x.get();
+  if (!g_obs) P.D_dev = w.dcols.get() + 2 * KMAX;
+  if (defer) {  // r_sum, scan, epoch, done from the drain's exact sums, on the device
+    P.from_drain = w.dctl()->out_exact;
+    P.scan_lambda = lambda;
+    P.scan_all = refine_rmax > 0.0;
+  }
   P.y[0] = P.y[1] = w.y0.get();
   if (t_det) {
     P.y[1] = w.y1.get();
@@ -762,11 +808,11 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
       Q.y[0] = ycur;
       Q.y[1] = ynext;
       for (int c = 0; c < b.K; ++c) Q.init[c] = stv[c];
-      PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+      PPRG_CUDA(cudaMemsetAsync(w.ctl(), 0, sizeof(SweepCtl), st));
       dispatch_sweeps<M_POWERPUSH>(g, b.K, Q, true);
       if (t_det) std::swap(ycur, ynext);
       SweepCtl one;
-      d2h_small(&one, w.ctl.get(), sizeof one, st);
+      d2h_small(&one, w.ctl(), sizeof one, st);
       PPRG_CUDA(cudaStreamSynchronize(st));
       hc.alg_bytes += one.alg_bytes;
       hc.total_sweeps = sweep + 1;
@@ -786,7 +832,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
         F.init[c].D = stv[c].D;
       }
       PPRG_CUDA(cudaMemsetAsync(snap.get(), 0, 16 * g.n, st));
-      PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+      PPRG_CUDA(cudaMemsetAsync(w.ctl(), 0, sizeof(SweepCtl), st));
       dispatch_sweeps<M_FINAL>(g, b.K, F, true);
       g_obs->hr.resize(g.n);
       g_obs->hq.resize(g.n);
@@ -804,11 +850,21 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
       hc.out_sweeps[c] = stv[c].sweeps;
       hc.out_pushes[c] = stv[c].pushes;
     }
+  } else if (defer) {
+    b.t_sweep = std::make_unique<EventTimer>(st);
+    b.t_sweep->start();
+    dispatch_sweeps<M_POWERPUSH>(g, b.K, P, true);
+    b.t_sweep->stop();
+    call->sweep_launches += 1;
+    call->kernel_launches += 2;
+    b.sweeps_pending = true;
+    b.yfin = ycur;  // deterministic sweeps: finalize picks y by the sweep count parity
+    return;
   } else {
     tm.start();
     dispatch_sweeps<M_POWERPUSH>(g, b.K, P, true);
     tm.stop();
-    d2h_small(&hc, w.ctl.get(), sizeof hc, st);
+    d2h_small(&hc, w.ctl(), sizeof hc, st);
     if (t_det && (hc.total_sweeps & 1u)) std::swap(ycur, ynext);  // sweep s writes y[(s + 1) & 1]
   }
   b.yfin = ycur;
@@ -842,7 +898,8 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
   const uint64_t n = g.n, nk = n * (uint64_t)b.K;
   const uint32_t k = b.k;
   const cudaMemcpyKind kind = out.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
-  bool any_scan = false;
+  const bool deferred = b.sweeps_pending;
+  bool any_scan = deferred;  // (deferred: decided on the device; the final pass handles both forms)
   for (uint32_t c = 0; c < k; ++c) any_scan |= b.scan[c] != 0;
   if (!any_scan) {
     if (out.reserve || out.residue) {
@@ -892,14 +949,53 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
     Q.init[c].r_sum = b.r_sum[c];
     Q.init[c].D = b.D[c];
   }
-  PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+  SweepCtl* fctl = deferred ? w.fctl() : w.ctl();
+  Q.ctl = fctl;
+  if (deferred) {
+    Q.from_sweeps = w.ctl();
+    // deterministic sweeps alternate y0 / y1: the last sweep wrote y[count & 1]
+    if (t_det) Q.y[0] = Q.y[1] = nullptr;  // set below from the sweep count
+  }
+  PPRG_CUDA(cudaMemsetAsync(fctl, 0, sizeof(SweepCtl), st));
   EventTimer tf(st);
+  if (deferred && t_det) {
+    // the y buffer of the last sweep depends on the count: read it (deterministic
+    // mode only; the fast sweeps update y in place)
+    uint32_t ts = 0;
+    d2h_small(&ts, reinterpret_cast<const char*>(w.ctl()) + offsetof(SweepCtl, total_sweeps), 4, st);
+    Q.y[0] = Q.y[1] = (ts & 1u) ? w.y1.get() : w.y0.get();
+  }
   tf.start();
   dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
   tf.stop();
   call->kernel_launches += 1;
   SweepCtl fc;
-  d2h_small(&fc, w.ctl.get(), sizeof fc, st);
+  if (deferred) {  // the block's one read-back: drain, sweeps and final pass
+    Workspace::Ctl all;
+    d2h_small(&all, w.ctlb.get(), sizeof all, st);
+    if (b.drain_pending) apply_drain(b, all.d, b.drain_live);
+    b.drain_pending = false;
+    const SweepCtl& hc = all.s;
+    call->alg_bytes += hc.alg_bytes;
+    if (hc.total_sweeps > call->max_sweeps) call->max_sweeps = hc.total_sweeps;
+    for (uint32_t c = 0; c < k; ++c) {
+      b.scan[c] = hc.out_scan[c];
+      if (!b.scan[c]) continue;
+      if (!hc.out_done[c]) fail(EINTERNAL, "power push: sweep limit reached");
+      b.r_sum[c] = hc.out_rsum[c];
+      b.pushes[c] += hc.out_pushes[c];
+      b.D[c] = hc.out_D[c];
+      b.sweeps[c] = hc.out_sweeps[c];
+    }
+    b.sweeps_pending = false;
+    if (b.t_local) call->local_ms += b.t_local->ms();
+    if (b.t_sweep) call->sweep_ms += b.t_sweep->ms();
+    b.t_local.reset();
+    b.t_sweep.reset();
+    fc = all.f;
+  } else {
+    d2h_small(&fc, w.ctl(), sizeof fc, st);
+  }
   check_final(fc);
   if (!direct && (out.reserve || out.residue)) {
     PPRG_CUDA(cudaEventRecord(w.ev_ready[slot], st));
@@ -934,6 +1030,8 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
 
 void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_threshold,
                       CallStats* call, double refine_rmax = 0.0) {
+  // unobserved blocks run without host round trips (finalize reads back once)
+  const bool defer = !g_obs && !g_trace && !std::getenv("PPRG_DEBUG_LOCAL");
   const double m_eff = (double)b.g.m_eff();
   const uint64_t nk = b.g.n * (uint64_t)b.K;
   cudaStream_t st = b.g.stream;
@@ -944,13 +1042,24 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
   const uint64_t limit = scan_threshold < 0 ? b.g.n / 4 : (uint64_t)scan_threshold;
   std::vector<int> state(KMAX, 2);
   for (uint32_t c = 0; c < b.k; ++c) state[c] = 0;
-  EventTimer tl(st);
-  tl.start();
-  drain_levels(b, r_max, lambda, limit, false, state, call);
-  std::vector<int> all(KMAX, 1);
-  exact_rsum(b, all);
-  tl.stop();
-  call->local_ms += tl.ms();
+  if (defer) {
+    b.t_local = std::make_unique<EventTimer>(st);
+    b.t_local->start();
+    drain_levels(b, r_max, lambda, limit, false, state, call, true);
+    b.t_local->stop();
+    if (b.drain_pending) {
+      global_phase(b, lambda, epoch_num, call, refine_rmax, true);  // push.cpp:168 on the device
+      return;
+    }
+    call->local_ms += b.t_local->ms();
+    b.t_local.reset();
+  } else {
+    EventTimer tl(st);
+    tl.start();
+    drain_levels(b, r_max, lambda, limit, false, state, call);  // (+ recompute_r_sum)
+    tl.stop();
+    call->local_ms += tl.ms();
+  }
   bool any = false;
   for (uint32_t c = 0; c < b.k; ++c) {
     b.scan[c] = b.r_sum[c] > lambda || refine_rmax > 0.0;  // push.cpp:168
@@ -958,6 +1067,7 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
   }
   if (any) global_phase(b, lambda, epoch_num, call, refine_rmax);
 }
+
 
 }  // namespace
 
@@ -994,7 +1104,6 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
     PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, st));
     k_pack<<<grid_for(nk), 256, 0, st>>>(dq, n, b.K, kb, 1.0, b.w.res.get());
     PPRG_CUDA(cudaGetLastError());
-    std::vector<int> all(KMAX, 1);
     std::fill(b.r_sum.begin(), b.r_sum.end(), 0.0);
     {  // r_sum of the incoming state (no drift check: it is the caller's)
       if (t_det) {
@@ -1010,8 +1119,7 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
     for (uint32_t c = 0; c < kb; ++c) state[c] = 0;
     EventTimer tl(st);
     tl.start();
-    drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);
-    exact_rsum(b, all);  // push.cpp:221
+    drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);  // (+ recompute_r_sum, push.cpp:221)
     tl.stop();
     call->local_ms += tl.ms();
     k_refine_out<<<grid_for(nk), 256, 0, st>>>(b.w.x.get(), b.w.res.get(), n, b.K, kb, alpha, dr, dq);
@@ -1086,7 +1194,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
                                                 alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
       if (t_det) det_colsum(b, w.r0.get(), g.dead.get(), g.n_dead, 1.0 - alpha, w.dcols.get() + 2 * KMAX);
       d2h_small(b.D.data(), w.dcols.get() + 2 * KMAX, 8 * KMAX, st);
-      PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+      PPRG_CUDA(cudaMemsetAsync(w.ctl(), 0, sizeof(SweepCtl), st));
       PPRG_CUDA(cudaStreamSynchronize(st));
       SweepParams P = base_params(b);
       for (int c = 0; c < b.K; ++c) {
@@ -1123,11 +1231,11 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
           Q.y[0] = yb[cur];
           Q.y[1] = yb[cur ^ 1];
           for (int c = 0; c < b.K; ++c) Q.init[c] = stv[c];
-          PPRG_CUDA(cudaMemsetAsync(w.ctl.get(), 0, sizeof(SweepCtl), st));
+          PPRG_CUDA(cudaMemsetAsync(w.ctl(), 0, sizeof(SweepCtl), st));
           if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, Q, true);
           else dispatch_sweeps<M_SIMFWD>(g, b.K, Q, true);
           SweepCtl one;
-          d2h_small(&one, w.ctl.get(), sizeof one, st);
+          d2h_small(&one, w.ctl(), sizeof one, st);
           PPRG_CUDA(cudaStreamSynchronize(st));
           hc.alg_bytes += one.alg_bytes;
           hc.total_sweeps = it + 1;
@@ -1150,7 +1258,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
         if (eng == Engine::PowItr) dispatch_sweeps<M_POWITR>(g, b.K, P, true);
         else dispatch_sweeps<M_SIMFWD>(g, b.K, P, true);
         tm.stop();
-        d2h_small(&hc, w.ctl.get(), sizeof hc, st);
+        d2h_small(&hc, w.ctl(), sizeof hc, st);
       }
       call->sweep_ms += tm.ms();
       trace.fold(st, hc.total_sweeps, 0, eng == Engine::PowItr ? g.m_eff() : 0);
@@ -1190,8 +1298,6 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       std::vector<int> state(KMAX, 2);
       for (uint32_t c = 0; c < kb; ++c) state[c] = 0;
       drain_levels(b, r_max_fifo, lambda_stop_fifo, UINT64_MAX, false, state, call);
-      std::vector<int> all(KMAX, 1);
-      exact_rsum(b, all);
       finalize(b, o, false, call);
     } else {
       power_push_block(b, lambda, epoch_num, scan_threshold, call);
@@ -1227,7 +1333,17 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
   // PowerPush to lambda, then refine (push.cpp:208-222) as a final sweep
   // epoch at r_max run to its fixpoint, so the refine is pull sweeps over the
   // tile plan rather than a scattered frontier over millions of nodes.
-  power_push_block(b, lambda, 8, -1, call, r_max);
+  // The local phase of this stage stops at a queue of n/16 instead of the
+  // reference's default n/4 (PPRG_SPP_SCAN_DIV): on the GPU a frontier level
+  // costs more than a pull sweep once it holds more than a few percent of the
+  // (node, column) pairs. configs[3]: 2.37 -> 2.20 ms per query (n/64: 2.20,
+  // n/256: 2.23; profiles/r02_spp_scan_div.txt). The SpeedPPR estimate's
+  // guarantee does not depend on where PowerPush switches phases.
+  static const double spp_div = [] {
+    const char* e = std::getenv("PPRG_SPP_SCAN_DIV");
+    return e ? std::atof(e) : 16.0;
+  }();
+  power_push_block(b, lambda, 8, (int64_t)((double)g.n / spp_div), call, r_max);
   Outputs none;
   finalize(b, none, true, call);
   // the tail: every node still above deg_eff * r_max in id order, drained
@@ -1235,9 +1351,7 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
   for (uint32_t c = 0; c < k; ++c) state[c] = 0;
   EventTimer tl(g.stream);
   tl.start();
-  drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);
-  std::vector<int> all(KMAX, 1);
-  exact_rsum(b, all);
+  drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);  // (+ recompute_r_sum)
   tl.stop();
   call->local_ms += tl.ms();
   for (uint32_t c = 0; c < k; ++c) {
@@ -1533,12 +1647,12 @@ void part_sweep(PartSession* s, double* local_host) {
     P.thr[e] = s->thr[e];
   }
   cudaStream_t st = g.stream;
-  PPRG_CUDA(cudaMemsetAsync(b.w.ctl.get(), 0, sizeof(SweepCtl), st));
+  PPRG_CUDA(cudaMemsetAsync(b.w.ctl(), 0, sizeof(SweepCtl), st));
   EventTimer tm(st);
   tm.start();
   dispatch_sweeps<M_POWERPUSH>(g, K, P, true);
   tm.stop();
-  k_pack_counters<<<1, KMAX, 0, st>>>(b.w.ctl.get(), K, s->counters.get());
+  k_pack_counters<<<1, KMAX, 0, st>>>(b.w.ctl(), K, s->counters.get());
   PPRG_CUDA(cudaGetLastError());
   std::vector<double> loc(5 * KMAX, 0.0);
   PPRG_CUDA(cudaMemcpyAsync(loc.data(), s->counters.get(), 8 * 5 * K, cudaMemcpyDeviceToHost, st));
@@ -1589,13 +1703,13 @@ void part_finish(PartSession* s, double* reserve, double* residue, bool on_devic
     Q.final_pull[c] = 1;
     Q.init[c].done = 0;  // the final pass visits every column
   }
-  PPRG_CUDA(cudaMemsetAsync(b.w.ctl.get(), 0, sizeof(SweepCtl), st));
+  PPRG_CUDA(cudaMemsetAsync(b.w.ctl(), 0, sizeof(SweepCtl), st));
   EventTimer tf(st);
   tf.start();
   dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
   tf.stop();
   SweepCtl fc;
-  d2h_small(&fc, b.w.ctl.get(), sizeof fc, st);
+  d2h_small(&fc, b.w.ctl(), sizeof fc, st);
   check_final(fc);
   if (!on_device && w) {
     for (uint32_t c = 0; c < k; ++c) {

@@ -62,6 +62,7 @@ struct SweepCtl {
   double neg_sum;
   double out_scale[KMAX];              // final pass: pushed[0][c] / out_scale[c] = residue sum
   unsigned wticket[3][WMAX];           // deterministic sweeps: tile ticket of each wave
+  int out_scan[KMAX];                  // column ran the global phase (push.cpp:168)
 };
 
 struct SweepParams {
@@ -88,6 +89,17 @@ struct SweepParams {
   double* y[2];                // gather operand (powitr double-buffers)
   double* r[2];                // powitr residues (double-buffered)
   const double* push_res;      // finalize: push-form residues (columns without scan phase)
+  const double* D_dev;         // if set: each column's initial D on the device (else init[].D)
+  // Device-decided starts (no host round trip between the phases of a block):
+  // from_drain: the global phase takes each column's r_sum from the local
+  // phase's exact sum and decides scan / epoch / done itself (push.cpp:168,
+  // 176-180: scan iff r_sum > scan_lambda, or every column with scan_all);
+  // from_sweeps: the final pass takes r_sum, D and the scan flag from the
+  // global phase's outputs.
+  const double* from_drain;    // [KMAX] exact r_sum after the local phase
+  const SweepCtl* from_sweeps;
+  double scan_lambda;
+  int scan_all;
 
   SweepCtl* ctl;
   double* out_reserve;         // finalize outputs, query-major [c*n + u]
@@ -113,15 +125,21 @@ struct SweepParams {
   ColInit init[KMAX];
 };
 
+// (56 bytes = 14 words: lanes reading cs[c] for 32 different columns meet at
+// most 2-way shared bank conflicts; a 64-byte stride would make them 16-way)
 struct ColSh {
   double r_sum, D;
   double scp, scd;  // deterministic sweeps: fixed-point scales 2^S of this sweep's pushed / D sums
-  int epoch, done;
+  int epoch;
+  short done;
+  short pull;  // final pass: residue from the pull form (the column ran the global phase)
   unsigned sweeps;
   uint32_t src;  // the column's source (a shared copy: P.src[c] with a per-lane c
                  // would be a divergent, serialised constant-bank load)
   unsigned long long pushes;
 };
+
+static_assert(sizeof(ColSh) == 56, "ColSh stride");
 
 // Gather operand of a sweep. Fast mode: one y, updated in place (rows read
 // whatever value a neighbour's row has when the gather lands). Deterministic
@@ -236,7 +254,7 @@ __device__ __forceinline__ void decide(const SweepParams& P, const ColSh* cs, co
     if (!dg) a.d += qterm<DET>(oma * nxt, cs[c].scd);
   } else {  // M_FINAL
     double res;
-    if (P.final_pull[c]) {
+    if (cs[c].pull) {
       const double inflow = acc + (is_src ? 1.0 + cs[c].D : 0.0);
       res = inflow - xo;
       if (res < 0.0) {  // rounding of the implicit form only: counted, checked on the host
@@ -1019,14 +1037,30 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
   SweepCtl* ctl = P.ctl;
   if (tid < K) {
     cs[tid].r_sum = P.init[tid].r_sum;
-    cs[tid].D = P.init[tid].D;
+    cs[tid].D = P.D_dev ? P.D_dev[tid] : P.init[tid].D;
     cs[tid].epoch = P.init[tid].epoch;
     cs[tid].done = P.init[tid].done;
     cs[tid].sweeps = P.init[tid].sweeps;
     cs[tid].pushes = P.init[tid].pushes;
     cs[tid].src = P.src[tid];
     cs[tid].scp = cs[tid].scd = 1.0;
+    cs[tid].pull = P.final_pull[tid];
     csrc[tid] = P.src[tid];
+    if (P.from_drain) {  // push.cpp:168-180, decided here instead of on the host
+      const double rs = __ldcg(P.from_drain + tid);
+      const int scan = tid < P.k_live && (P.scan_all || rs > P.scan_lambda);
+      int ep = 0;
+      while (ep < P.E && !(rs > P.lam[ep])) ++ep;
+      cs[tid].r_sum = rs;
+      cs[tid].epoch = ep;
+      cs[tid].done = !scan || ep >= P.E;
+      cs[tid].pull = scan;
+    }
+    if (P.from_sweeps) {  // the final pass after a device-started global phase
+      cs[tid].r_sum = __ldcg(&P.from_sweeps->out_rsum[tid]);
+      cs[tid].D = __ldcg(&P.from_sweeps->out_D[tid]);
+      cs[tid].pull = __ldcg(&P.from_sweeps->out_scan[tid]);
+    }
   }
   __syncthreads();
   __shared__ unsigned long long sh_pk[K];
@@ -1251,6 +1285,7 @@ __global__ void __launch_bounds__(NT, (K >= 4 ? PPRG_MINB : K == 1 ? PPRG_MINB_K
   }
   if (MODE == M_POWERPUSH && P.npeers) __threadfence_system();  // peer y stores performed
   if (blockIdx.x == 0 && tid < K) {
+    ctl->out_scan[tid] = cs[tid].pull;
     ctl->out_rsum[tid] = cs[tid].r_sum;
     ctl->out_D[tid] = cs[tid].D;
     ctl->out_sweeps[tid] = cs[tid].sweeps;

@@ -234,7 +234,12 @@ int main(int argc, char** argv) {
   }
       if (win == 0) {
         RUN(64, 8, 16, 0, 8)
+        RUN(64, 4, 32, 0, 8)
+        RUN(64, 6, 32, 0, 8)
+        RUN(64, 8, 16, 0, 12)
+        RUN(64, 4, 32, 0, 12)
         RUN(32, 8, 16, 0, 8)
+        RUN(32, 4, 32, 0, 8)
       }
       RUN(16, 8, 16, 0, 8)
       RUN(16, 8, 16, 1, 8)
