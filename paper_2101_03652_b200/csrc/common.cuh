@@ -183,6 +183,22 @@ __device__ __forceinline__ void st_state(double* p, double v) {
   *p = v;
 #endif
 }
+// four adjacent columns in one 32-byte access (LDG.E.ENL2.256, sm_100)
+struct dbl4 {
+  double v[4];
+};
+__device__ __forceinline__ dbl4 ld_state4(const double* p) {
+  dbl4 r;
+  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ dbl4 ld_gather4(const double* p) {
+  dbl4 r;
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ double2 ld_gather2(const double* p) {
 #if PPRG_HINTS == 3
   double2 v;

@@ -648,12 +648,23 @@ constexpr uint32_t RMAX_W = PPRG_RMAX_W;
 // 16 lanes x 16 B, two in-edges per warp load instruction (5.5% faster per
 // sweep than 32 lanes x 8 B on configs[2]; for K = 4..16 the same split was
 // 12-40% slower, so they keep one column per lane).
+// Round 2 (PPRG_VEC4, sm_100's 32-byte LDG.E.ENL2.256): K = 64 as 16 lanes x
+// 32 B and K = 32 as 8 lanes x 32 B -- two (four) in-edges per warp load
+// instruction at the same registers in flight (4 loads of 4 doubles per
+// lane). The bare gather over the configs[2] transpose: 2.73 instead of 3.16
+// ms per 64-column sweep (profiles/r02_microbench_narrow_k_v2.log).
 #ifndef PPRG_VEC2
 #define PPRG_VEC2 1
 #endif
+#ifndef PPRG_VEC4
+#define PPRG_VEC4 1
+#endif
 template <int K>
 __host__ __device__ constexpr int wide_kc() {
-  return K >= 64 ? 32 : (PPRG_VEC2 && K == 32) ? 16 : (K < 32 ? K : 32);
+  return (PPRG_VEC4 && K >= 32) ? K / 4
+         : K >= 64              ? 32
+         : (PPRG_VEC2 && K == 32) ? 16
+                                  : (K < 32 ? K : 32);
 }
 
 // Sum of y over the in-edges [b, e) of one row for my columns, by one warp.
@@ -665,6 +676,9 @@ __host__ __device__ constexpr int wide_kc() {
 #ifndef PPRG_G
 #define PPRG_G 8
 #endif
+#ifndef PPRG_G4
+#define PPRG_G4 4  // row loads in flight per lane with 32-byte lanes (same registers as 8 x 16 B)
+#endif
 template <int K, bool DET>
 __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const YG& yg, uint64_t b,
                                              uint64_t e, double (&s)[K / wide_kc<K>()],
@@ -672,12 +686,15 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const YG& yg,
   constexpr int KC = wide_kc<K>();
   constexpr int CPL = K / KC;
   constexpr int ES = 32 / KC;
-  constexpr int G = PPRG_G;
+  constexpr int G = CPL == 4 ? PPRG_G4 : PPRG_G;
+  constexpr int NA = CPL == 4 ? 1 : 2;  // accumulators per column (register budget)
   const int lane = threadIdx.x & 31, es = lane / KC, kc = lane % KC;
   const double* ybase = yg.yo + kc * CPL;  // (fast mode: one y)
-  double acc[CPL][2];
+  double acc[CPL][NA];
 #pragma unroll
-  for (int q = 0; q < CPL; ++q) acc[q][0] = acc[q][1] = 0.0;
+  for (int q = 0; q < CPL; ++q)
+#pragma unroll
+    for (int t = 0; t < NA; ++t) acc[q][t] = 0.0;
   // the ids of the next 32 in-edges are loaded one chunk ahead, so their
   // latency hides behind this chunk's gathers (rows longer than 32 in-edges)
   uint32_t nextid = have_first ? first_id : (b + lane < e ? ld_stream(P.in_nbr + b + lane) : 0u);
@@ -692,7 +709,11 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const YG& yg,
         const int j = j0 + g * ES + es;
         const uint32_t id = __shfl_sync(0xffffffffu, myid, j < cnt ? j : cnt - 1);
         const double* src = (DET ? ysrc<DET>(yg, id) + kc * CPL : ybase) + (uint64_t)id * K;
-        if constexpr (CPL == 2) {
+        if constexpr (CPL == 4) {
+          const dbl4 v4 = ld_gather4(src);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[g][q] = v4.v[q];
+        } else if constexpr (CPL == 2) {
           const double2 v2 = ld_gather2(src);
           v[g][0] = v2.x;
           v[g][1] = v2.y;
@@ -704,13 +725,13 @@ __device__ __forceinline__ void warp_row_sum(const SweepParams& P, const YG& yg,
       for (int g = 0; g < G; ++g) {
         const bool ok = j0 + g * ES + es < cnt;
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) acc[q][g & 1] += ok ? v[g][q] : 0.0;
+        for (int q = 0; q < CPL; ++q) acc[q][g % NA] += ok ? v[g][q] : 0.0;
       }
     }
   }
 #pragma unroll
   for (int q = 0; q < CPL; ++q) {
-    s[q] = acc[q][0] + acc[q][1];
+    s[q] = NA == 2 ? acc[q][0] + acc[q][NA - 1] : acc[q][0];
 #pragma unroll
     for (int o = KC; o < 32; o <<= 1) s[q] += __shfl_xor_sync(0xffffffffu, s[q], o);
   }
@@ -807,30 +828,58 @@ __device__ __forceinline__ void decide_pp(const SweepParams& P, const ColSh* cs,
   if (!dg) a.d += qterm<DET>(oma * xo, cs[c].scd);
 }
 
+// Decision layout of the wide path: the columns a lane decides for a row.
+// 16-byte and 8-byte lanes (CPL <= 2) decide the columns they loaded. With
+// 32-byte lanes (CPL = 4) only KC = K/4 lanes load a row's columns, but after
+// warp_row_sum's xor reduction every lane holds every sum of its kc, so all 32
+// lanes decide: DPL = K/32 columns each, starting at dc0.
+template <int K>
+struct DecLayout {
+  static constexpr int KC = wide_kc<K>();
+  static constexpr int CPL = K / KC;
+  static constexpr int DPL = CPL == 4 ? K / 32 : CPL;  // columns decided per lane
+  int sb;   // index of the lane's first decided column in its s[CPL]
+  int dc0;  // the lane's first decided column
+  bool on;  // this lane decides
+  __device__ __forceinline__ DecLayout() {
+    const int lane = threadIdx.x & 31, kc = lane % KC;
+    sb = CPL == 4 ? DPL * (lane / KC) : 0;
+    dc0 = kc * CPL + sb;
+    on = CPL == 4 ? true : lane < KC;
+  }
+};
+
 template <int K, int MODE, bool DET>
 __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* cs,
                                             const double* thr_cur, const uint32_t* csrc,
-                                            uint32_t u, const double* s,
+                                            uint32_t u, const DecLayout<K>& L, const double* s,
                                             const double* xo, const double* rc, uint32_t dg,
                                             double inv, const YG& yg, double* rnxt,
                                             double* ynxt, Acc& a, const BlockAcc& ba,
                                             double* pacc = nullptr) {
-  constexpr int KC = wide_kc<K>();
-  constexpr int CPL = K / KC;
-  const int kc = (threadIdx.x & 31) % KC;
-  if constexpr (CPL == 1) {
-    decide<K, MODE, DET>(P, cs, thr_cur, u, kc, s[0], xo[0], rc[0], dg, inv, yg, rnxt, ynxt, a);
-  } else {  // K = 64: lane kc owns columns 2kc, 2kc+1; counters via shared atomics
-    // the lane's two thresholds and sources in one conflict-free 16 / 8-byte
-    // shared load each (a done column's threshold is +inf)
-    const double2 th = reinterpret_cast<const double2*>(thr_cur)[kc];
-    const uint2 sr = reinterpret_cast<const uint2*>(csrc)[kc];
+  constexpr int CPL = DecLayout<K>::CPL;
+  constexpr int DPL = DecLayout<K>::DPL;
+  if constexpr (CPL == 1) {  // one column per lane: the thread's own counters (column = tid % K)
+    decide<K, MODE, DET>(P, cs, thr_cur, u, L.dc0, s[0], xo[0], rc[0], dg, inv, yg, rnxt, ynxt, a);
+  } else {  // counters via shared atomics
+    // the lane's thresholds and sources in one vector shared load each (a
+    // done column's threshold is +inf)
+    double th[DPL];
+    uint32_t sr[DPL];
+    if constexpr (DPL == 2) {
+      const double2 t2 = reinterpret_cast<const double2*>(thr_cur)[L.dc0 / 2];
+      const uint2 s2 = reinterpret_cast<const uint2*>(csrc)[L.dc0 / 2];
+      th[0] = t2.x, th[1] = t2.y, sr[0] = s2.x, sr[1] = s2.y;
+    } else {
+      th[0] = thr_cur[L.dc0];
+      sr[0] = csrc[L.dc0];
+    }
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
+    for (int q = 0; q < DPL; ++q) {
       Acc b2;
-      const int cc = kc * CPL + q;
+      const int cc = L.dc0 + q;
       if constexpr (MODE == M_POWERPUSH)
-        decide_pp<K, DET>(P, cs, q ? th.y : th.x, q ? sr.y : sr.x, u, cc, s[q], xo[q], dg, inv, ynxt, b2);
+        decide_pp<K, DET>(P, cs, th[q], sr[q], u, cc, s[q], xo[q], dg, inv, ynxt, b2);
       else
         decide<K, MODE, DET>(P, cs, thr_cur, u, cc, s[q], xo[q], rc[q], dg, inv, yg, rnxt, ynxt, b2);
       if (PPRG_PUSH_REG && pacc) pacc[q] += b2.push;  // flushed once per tile
@@ -841,6 +890,34 @@ __device__ __forceinline__ void decide_cols(const SweepParams& P, const ColSh* c
         if (!b2.et) atomicAdd(&ba.nd[cc], 1u);  // a dead end's push (np 1, no out-edges)
       }
     }
+  }
+}
+
+// the lane's DPL decided sums out of its CPL row sums, by selects (a dynamic
+// index would put s[] in local memory)
+template <int K>
+__device__ __forceinline__ void pick_sums(const DecLayout<K>& L, const double* s, double* sd) {
+  constexpr int CPL = DecLayout<K>::CPL;
+  constexpr int DPL = DecLayout<K>::DPL;
+#pragma unroll
+  for (int q = 0; q < DPL; ++q) {
+    double v = s[q];
+#pragma unroll
+    for (int j = 1; j < CPL / DPL; ++j) v = L.sb == j * DPL ? s[j * DPL + q] : v;
+    sd[q] = v;
+  }
+}
+
+// the lane's DPL state values of row u (issued early; they land during the gathers)
+template <int K, int DPL>
+__device__ __forceinline__ void load_cols(const double* a, uint32_t u, int dc0, bool on, double* out) {
+  const double* p = a + (uint64_t)u * K + dc0;
+  if constexpr (DPL == 2) {
+    const double2 v = on ? ld_state2(p) : make_double2(0.0, 0.0);
+    out[0] = v.x;
+    out[1] = v.y;
+  } else {
+    out[0] = on ? ld_state(p) : 0.0;
   }
 }
 
@@ -880,11 +957,13 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
   uint32_t* sdeg = snode + RMAX_W;
   uint32_t* slong = sdeg + RMAX_W;                     // [RMAX_W] long rows; slong[RMAX_W] = count
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int es0 = lane < KC;  // lanes holding the reduced sums
+  const int es0 = lane < KC;  // lanes holding the reduced sums of their kc (first edge slot)
   const int kc = lane % KC;
-  double pacc[CPL];  // pushed mass of my columns in this tile (PPRG_PUSH_REG)
+  const DecLayout<K> L;
+  constexpr int DPL = DecLayout<K>::DPL;
+  double pacc[DPL];  // pushed mass of my decided columns in this tile (PPRG_PUSH_REG)
 #pragma unroll
-  for (int q = 0; q < CPL; ++q) pacc[q] = 0.0;
+  for (int q = 0; q < DPL; ++q) pacc[q] = 0.0;
   const uint32_t nr = d.nr;
   for (uint32_t t = tid; t <= nr; t += NT) soff[t] = __ldg(P.in_off + d.r0 + t);
   for (uint32_t t = tid; t < nr; t += NT) {
@@ -917,20 +996,18 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
     const uint32_t ids_n = first_ids(rn);
     if (e - b <= LONG_W) {
       const uint32_t u = snode[r];
-      double xo[CPL], rc[CPL], s[CPL];
-      if constexpr (CPL == 2) {  // issued early (one 16-byte load); lands during the edge loop
-        const double2 x2 = es0 ? ld_state2(P.x + (uint64_t)u * K + kc * 2) : make_double2(0.0, 0.0);
-        xo[0] = x2.x;
-        xo[1] = x2.y;
-      }
+      double xo[DPL], rc[DPL], s[CPL];
+      load_cols<K, DPL>(P.x, u, L.dc0, L.on, xo);  // issued early; lands during the edge loop
+      if constexpr (MODE == M_POWITR || MODE == M_SIMFWD) load_cols<K, DPL>(rcur, u, L.dc0, L.on, rc);
+      else
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) {  // issued early; lands during the edge loop
-        const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
-        if constexpr (CPL != 2) xo[q] = es0 ? ld_state(P.x + ix) : 0.0;
-        rc[q] = (es0 && (MODE == M_POWITR || MODE == M_SIMFWD)) ? __ldcg(rcur + ix) : 0.0;
-      }
+        for (int q = 0; q < DPL; ++q) rc[q] = 0.0;
       warp_row_sum<K, DET>(P, yg, b, e, s, true, ids);
-      if (es0) decide_cols<K, MODE, DET>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
+      double sd[DPL];
+      pick_sums<K>(L, s, sd);
+      if (L.on)
+        decide_cols<K, MODE, DET>(P, cs, thr_cur, csrc, u, L, sd, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt,
+                                  a, ba, pacc);
     }
     r = rn;
     ids = ids_n;
@@ -948,26 +1025,27 @@ __device__ __forceinline__ void tile_rows_wide(const SweepParams& P, const TileD
 #pragma unroll
       for (int q = 0; q < CPL; ++q) spart[warp * K + kc * CPL + q] = s[q];
     __syncthreads();
-    if (warp == 0 && es0) {
+    if (warp == 0 && L.on) {
       const uint32_t u = snode[r];
-      double xo[CPL], rc[CPL];
+      double xo[DPL], rc[DPL], sd[DPL];
 #pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        const uint64_t ix = (uint64_t)u * K + kc * CPL + q;
+      for (int q = 0; q < DPL; ++q) {
+        const uint64_t ix = (uint64_t)u * K + L.dc0 + q;
         xo[q] = __ldcg(P.x + ix);
         rc[q] = (MODE == M_POWITR || MODE == M_SIMFWD) ? __ldcg(rcur + ix) : 0.0;
         double t = 0.0;
-        for (int w = 0; w < NW; ++w) t += spart[w * K + kc * CPL + q];
-        s[q] = t;
+        for (int w = 0; w < NW; ++w) t += spart[w * K + L.dc0 + q];
+        sd[q] = t;
       }
-      decide_cols<K, MODE, DET>(P, cs, thr_cur, csrc, u, s, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a, ba, pacc);
+      decide_cols<K, MODE, DET>(P, cs, thr_cur, csrc, u, L, sd, xo, rc, sdeg[r], sinv[r], yg, rnxt, ynxt, a,
+                                ba, pacc);
     }
     __syncthreads();
   }
-  if (PPRG_PUSH_REG && es0)
+  if (PPRG_PUSH_REG && L.on)
 #pragma unroll
-    for (int q = 0; q < CPL; ++q)
-      if (pacc[q] != 0.0) atomicAdd(&ba.push[kc * CPL + q], pacc[q]);
+    for (int q = 0; q < DPL; ++q)
+      if (pacc[q] != 0.0) atomicAdd(&ba.push[L.dc0 + q], pacc[q]);
   __syncthreads();
   if (tid == 0) {
     *rowctr = 0;
