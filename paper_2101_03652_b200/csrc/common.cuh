@@ -23,6 +23,9 @@ enum { OK = 0, EINVAL_ = 1, EDATA = 2, EINTERNAL = 3, ECUDA = 4, ENCCL = 5 };
       ::pprg::fail(::pprg::ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// in destructors: errors are ignored (a failed call already reported its own)
+#define PPRG_CUDA_NOTHROW(call) ((void)(call))
+
 // ---- Philox4x32-10 (Salmon et al. SC'11) -----------------------------------
 struct U4 {
   uint32_t x, y, z, w;

@@ -308,11 +308,114 @@ uint64_t sort_clean(DevBuf<uint64_t>& keys, uint64_t cnt, int key_bits, cudaStre
 }  // namespace
 
 Graph::~Graph() {
+  DeviceGuard dg(device);
+  for (size_t i = 0; i < lanes.size(); ++i) {
+    if (i > 0 && lanes[i].stream) {
+      cudaStreamSynchronize(lanes[i].stream);
+      cudaStreamDestroy(lanes[i].stream);
+    }
+    if (lanes[i].done) cudaEventDestroy(lanes[i].done);
+  }
   if (stream) {
-    DeviceGuard dg(device);
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
+}
+
+// ---- execution lanes --------------------------------------------------------
+thread_local const LaneCtx* t_lane = nullptr;
+
+// Lanes of a graph: PPRG_LANES (default 2) on graphs below PPRG_LANE_MAX_M
+// in-edges (default 16M), where one query's persistent kernels are latency-
+// bound and a half-device grid costs it little (configs[0]: 1.74 vs 1.71 ms;
+// a quarter: 2.25 ms, profiles/r02_grid_frac.txt); one lane above, where a
+// query needs the whole device.
+static void init_lanes(Graph& g) {
+  static const int want = [] {
+    const char* e = std::getenv("PPRG_LANES");
+    const int v = e ? std::atoi(e) : 2;
+    return v < 1 ? 1 : v > 8 ? 8 : v;
+  }();
+  static const uint64_t max_m = [] {
+    const char* e = std::getenv("PPRG_LANE_MAX_M");
+    return e ? std::strtoull(e, nullptr, 10) : 16000000ull;
+  }();
+  const int nl = g.m < max_m ? want : 1;
+  g.lanes.resize(nl);
+  cudaEvent_t built;
+  PPRG_CUDA(cudaEventCreateWithFlags(&built, cudaEventDisableTiming));
+  PPRG_CUDA(cudaEventRecord(built, g.stream));  // the graph's build and uploads
+  for (int i = 0; i < nl; ++i) {
+    Graph::Lane& L = g.lanes[i];
+    if (i == 0) {
+      L.stream = g.stream;
+    } else {
+      PPRG_CUDA(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+      PPRG_CUDA(cudaStreamWaitEvent(L.stream, built, 0));
+    }
+    PPRG_CUDA(cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming));
+    PPRG_CUDA(cudaEventRecord(L.done, L.stream));
+  }
+  PPRG_CUDA(cudaEventDestroy(built));
+}
+
+// A query takes one free lane, or -- exclusive -- all of them. Ordering on
+// the device: an exclusive query's stream (lane 0) waits for every lane's last
+// work, and after it every lane waits for it, so a whole-device persistent
+// kernel never runs beside another lane's kernel; lanes' own kernels take
+// 1/nlanes (x 0.95) of the resident blocks each and always fit together.
+LaneGuard::LaneGuard(Graph& g, bool exclusive) : g_(g), all_(false), prev_(t_lane) {
+  std::unique_lock<std::mutex> lk(g.lane_mu);
+  if (g.lanes.empty()) init_lanes(g);
+  const int nl = (int)g.lanes.size();
+  auto all_free = [&] {
+    for (const Graph::Lane& L : g.lanes)
+      if (L.busy) return false;
+    return true;
+  };
+  if (exclusive || nl == 1) {
+    ++g.exclusive_waiters;
+    g.lane_cv.wait(lk, all_free);
+    --g.exclusive_waiters;
+    for (Graph::Lane& L : g.lanes) L.busy = true;
+    for (int i = 1; i < nl; ++i) PPRG_CUDA(cudaStreamWaitEvent(g.lanes[0].stream, g.lanes[i].done, 0));
+    all_ = true;
+    ctx_ = LaneCtx{0, g.lanes[0].stream, 1.0};
+  } else {
+    int pick = -1;
+    g.lane_cv.wait(lk, [&] {
+      if (g.exclusive_waiters) return false;
+      for (int i = 0; i < nl; ++i)
+        if (!g.lanes[i].busy) {
+          pick = i;
+          return true;
+        }
+      return false;
+    });
+    g.lanes[pick].busy = true;
+    ctx_ = LaneCtx{pick, g.lanes[pick].stream, 0.95 / nl};
+  }
+  t_lane = &ctx_;
+}
+
+LaneGuard::~LaneGuard() {
+  t_lane = prev_;
+  std::lock_guard<std::mutex> lk(g_.lane_mu);
+  if (all_) {
+    PPRG_CUDA_NOTHROW(cudaEventRecord(g_.lanes[0].done, g_.lanes[0].stream));
+    for (size_t i = 0; i < g_.lanes.size(); ++i) {
+      if (i > 0) {
+        PPRG_CUDA_NOTHROW(cudaStreamWaitEvent(g_.lanes[i].stream, g_.lanes[0].done, 0));
+        PPRG_CUDA_NOTHROW(cudaEventRecord(g_.lanes[i].done, g_.lanes[i].stream));
+      }
+      g_.lanes[i].busy = false;
+    }
+  } else {
+    Graph::Lane& L = g_.lanes[ctx_.lane];
+    PPRG_CUDA_NOTHROW(cudaEventRecord(L.done, L.stream));
+    L.busy = false;
+  }
+  g_.lane_cv.notify_all();
 }
 
 void Graph::finish_build() {
@@ -354,6 +457,7 @@ void Graph::finish_build() {
 }
 
 void Graph::ensure_transpose() {
+  std::lock_guard<std::recursive_mutex> lk(build_mu);
   if (in_off.get()) return;
   cudaStream_t st = stream;
   in_off.alloc(n + 1);
@@ -410,6 +514,7 @@ void Graph::ensure_transpose() {
 }
 
 const uint2* Graph::tile_desc(uint32_t T, uint64_t* ntiles) {
+  std::lock_guard<std::recursive_mutex> lk(build_mu);
   ensure_transpose();
   *ntiles = m / T + 1;
   auto it = tile_d.find(T);
@@ -424,6 +529,7 @@ const uint2* Graph::tile_desc(uint32_t T, uint64_t* ntiles) {
 }
 
 const uint32_t* Graph::split_rows(uint32_t T, uint64_t* count) {
+  std::lock_guard<std::recursive_mutex> lk(build_mu);
   ensure_transpose();
   auto it = tile_split.find(T);
   if (it != tile_split.end()) {
@@ -458,6 +564,7 @@ const uint32_t* Graph::split_rows(uint32_t T, uint64_t* count) {
 // added to the current tile while it keeps <= T in-edges and <= R rows; a row
 // with more than T in-edges becomes ceil(deg/T) hub pieces of its own.
 const Graph::Plan& Graph::tile_plan(uint32_t T, uint32_t R, uint32_t H) {
+  std::lock_guard<std::recursive_mutex> lk(build_mu);
   ensure_transpose();
   if (H < T) H = T;
   const uint64_t key = ((uint64_t)T << 40) | ((uint64_t)H << 16) | R;

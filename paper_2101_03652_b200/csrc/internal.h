@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <condition_variable>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -47,6 +48,22 @@ struct Graph {
   std::map<uint32_t, DevBuf<uint32_t>> tile_split;  // per tile size: compact rows spanning tiles
   std::mutex mu;
   cudaStream_t stream = nullptr;
+  // ---- execution lanes (concurrent queries from many host
+  // threads, each on its own stream and scratch). A query takes one lane:
+  // its stream, its workspaces, and a 1/nlanes share of every persistent
+  // kernel's resident blocks, so the lanes' cooperative kernels always fit on
+  // the device together. Column blocks of >= 4 columns take every lane (the
+  // whole device); graphs of >= PPRG_LANE_MAX_M in-edges have one lane.
+  struct Lane {
+    cudaStream_t stream = nullptr;  // lanes[0] uses `stream`
+    cudaEvent_t done = nullptr;     // recorded when the lane is released
+    bool busy = false;
+  };
+  std::vector<Lane> lanes;
+  std::mutex lane_mu;
+  std::condition_variable lane_cv;
+  int exclusive_waiters = 0;
+  std::recursive_mutex build_mu;  // lazily derived structures (transpose, tile plans)
 
   ~Graph();
   void finish_build();  // deg / inv_deg / dead-ends from off; validates
@@ -142,6 +159,30 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
 void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double alpha,
                          double lambda, double r_max, ColumnStats* cols, CallStats* call,
                          PushView* view);
+
+// The lane the calling thread's query runs on (set by LaneGuard).
+struct LaneCtx {
+  int lane;
+  cudaStream_t stream;
+  double frac;  // share of a persistent kernel's resident blocks
+};
+extern thread_local const LaneCtx* t_lane;
+inline cudaStream_t qstream(const Graph& g) { return t_lane ? t_lane->stream : g.stream; }
+inline int qlane() { return t_lane ? t_lane->lane : 0; }
+// Acquire a lane (exclusive: all of them) for the scope of one query call.
+class LaneGuard {
+ public:
+  LaneGuard(Graph& g, bool exclusive);
+  ~LaneGuard();
+  LaneGuard(const LaneGuard&) = delete;
+  LaneGuard& operator=(const LaneGuard&) = delete;
+
+ private:
+  Graph& g_;
+  bool all_;
+  LaneCtx ctx_;
+  const LaneCtx* prev_;
+};
 
 // Progress trace of a traced single-source call (the reference's
 // CheckpointRecorder, sweep.hpp:30-45, at sweep / level granularity). A

@@ -98,7 +98,7 @@ static void ws_alloc(Workspace& w, Graph& g, int K) {
   w.r1.alloc(nk);
   w.res.alloc(nk);
   w.stamp.alloc(nk);
-  PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, g.stream));
+  PPRG_CUDA(cudaMemsetAsync(w.stamp.get(), 0, 4 * nk, qstream(g)));
   w.fa.alloc(nk + 1);
   w.fb.alloc(nk + 1);
   w.ctlb.alloc(1);
@@ -113,13 +113,14 @@ static void ws_tiles(Workspace& w, Graph& g, uint64_t ntiles, uint64_t nhubs) {
   if ((ntiles + 1) * K > w.hub_acc.n) w.hub_acc.alloc((ntiles + 1) * K);
   if (nhubs + 1 > w.hub_cnt.n) {
     w.hub_cnt.alloc(nhubs + 1);
-    PPRG_CUDA(cudaMemsetAsync(w.hub_cnt.get(), 0, 4 * (nhubs + 1), g.stream));
+    PPRG_CUDA(cudaMemsetAsync(w.hub_cnt.get(), 0, 4 * (nhubs + 1), qstream(g)));
   }
 }
 
+// one workspace per (graph, lane, columns): concurrent lanes never share scratch
 static Workspace& workspace(Graph& g, int K, uint64_t ntiles, uint64_t nhubs) {
   std::lock_guard<std::mutex> lk(g_ws_mu);
-  auto& slot = g_ws[&g][K];
+  auto& slot = g_ws[&g][qlane() * 256 + K];
   if (!slot) {
     slot = std::make_unique<Workspace>();
     ws_alloc(*slot, g, K);
@@ -139,7 +140,6 @@ static void sync_host_copies(const Graph& g) {
 
 void graph_sync(Graph& g) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
   sync_host_copies(g);
 }
 
@@ -165,6 +165,20 @@ inline unsigned grid_for(uint64_t items, int tb = 256) {
   return (unsigned)b;
 }
 
+// Blocks of a cooperative (persistent) launch: the query lane's share of the
+// resident slots (LaneGuard), times PPRG_GRID_FRAC (probe: what a smaller grid
+// costs one call).
+unsigned coop_grid(const Graph& g, int per_sm) {
+  static const double frac = [] {
+    const char* e = std::getenv("PPRG_GRID_FRAC");
+    const double v = e ? std::atof(e) : 1.0;
+    return v > 0.0 && v <= 1.0 ? v : 1.0;
+  }();
+  const unsigned full = (unsigned)(per_sm * g.sm_count);
+  const unsigned want = (unsigned)(frac * (t_lane ? t_lane->frac : 1.0) * full);
+  return want < 1 ? 1 : want;
+}
+
 template <int K, int MODE, bool DET>
 void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
   const size_t wide_bytes = 8ull * (RMAX_W + 1) + 8ull * RMAX_W + 8ull * (NT / 32) * K +
@@ -181,7 +195,7 @@ void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
     int per_sm = 0;
     PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem));
     if (per_sm < 1) fail(EINTERNAL, "sweep kernel cannot be resident");
-    unsigned grid = (unsigned)(per_sm * g.sm_count);
+    unsigned grid = coop_grid(g, per_sm);
     // narrow path on small graphs: at least ~2 tiles per block, so fewer rows
     // are in flight (closer to the reference's sequential scan): configs[0]
     // takes 71 sweeps instead of 83 and 9% less time. The wide path keeps the
@@ -195,14 +209,14 @@ void launch_sweeps(Graph& g, SweepParams& P, bool cooperative) {
                                     : P.k1w ? 2.0 * (NT / 32) : (K < WIDE_K ? 2.0 : 0.0);
     if (tpb > 0 && P.ntiles > 0) {
       const double want = (double)P.ntiles / tpb;
-      const unsigned lo = (unsigned)g.sm_count;
+      const unsigned lo = std::min((unsigned)g.sm_count, grid);  // (never above the lane share)
       if (want < grid) grid = want < lo ? lo : (unsigned)want;
     }
     void* args[] = {(void*)&P};
-    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, smem, g.stream));
+    PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(NT), args, smem, qstream(g)));
   } else {
     const uint64_t grid = P.ntiles < (uint64_t)g.sm_count * 8 ? P.ntiles : (uint64_t)g.sm_count * 8;
-    kern<<<(unsigned)(grid ? grid : 1), NT, smem, g.stream>>>(P);
+    kern<<<(unsigned)(grid ? grid : 1), NT, smem, qstream(g)>>>(P);
   }
   PPRG_CUDA(cudaGetLastError());
 }
@@ -271,10 +285,10 @@ struct SweepTrace {
 
 uint64_t device_now_ns(Graph& g) {
   DevBuf<unsigned long long> t(1);
-  k_stamp<<<1, 1, 0, g.stream>>>(t.get());
+  k_stamp<<<1, 1, 0, qstream(g)>>>(t.get());
   unsigned long long h = 0;
-  PPRG_CUDA(cudaMemcpyAsync(&h, t.get(), 8, cudaMemcpyDeviceToHost, g.stream));
-  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+  PPRG_CUDA(cudaMemcpyAsync(&h, t.get(), 8, cudaMemcpyDeviceToHost, qstream(g)));
+  PPRG_CUDA(cudaStreamSynchronize(qstream(g)));
   return h;
 }
 
@@ -407,7 +421,7 @@ Block make_block(Graph& g, const uint32_t* sources, uint32_t k, double alpha, bo
   b.nhubs = nhubs;
   for (uint32_t c = 0; c < k; ++c) b.src[c] = sources[c];
   for (int c = k; c < K; ++c) b.src[c] = sources[0];  // padding columns are inert
-  PPRG_CUDA(cudaMemcpyAsync(w.d_src.get(), b.src.data(), 4 * KMAX, cudaMemcpyHostToDevice, g.stream));
+  PPRG_CUDA(cudaMemcpyAsync(w.d_src.get(), b.src.data(), 4 * KMAX, cudaMemcpyHostToDevice, qstream(g)));
   return b;
 }
 
@@ -448,7 +462,7 @@ SweepParams base_params(Block& b) {
 void det_colsum(Block& b, const double* a, const uint32_t* rows, uint64_t nrows, double scale,
                 double* dst) {
   Workspace& w = b.w;
-  cudaStream_t st = b.g.stream;
+  cudaStream_t st = qstream(b.g);
   if (w.dsum_part.n < (size_t)DSUM_BLOCKS * KMAX) w.dsum_part.alloc((size_t)DSUM_BLOCKS * KMAX);
   k_dsum_part<<<DSUM_BLOCKS, DSUM_NT, 0, st>>>(a, rows, nrows, b.K, w.dsum_part.get());
   k_dsum_final<<<1, KMAX, 0, st>>>(w.dsum_part.get(), DSUM_BLOCKS, b.K, scale, dst);
@@ -477,7 +491,7 @@ void set_waves(Block& b, SweepParams& P) {
   for (uint64_t j = 0; j < t.size() && (int)w < W; ++j) {
     if (acc * W >= total * w && t[j].piece == 0 && j > P.wave_tile[w - 1]) {
       P.wave_tile[w] = j;
-      d2h_small(&P.wave_node[w], b.g.cin_row.get() + t[j].r0, 4, b.g.stream);
+      d2h_small(&P.wave_node[w], b.g.cin_row.get() + t[j].r0, 4, qstream(b.g));
       ++w;
     }
     acc += t[j].ne;
@@ -493,7 +507,7 @@ void emit_step(Block& b, const double* reserve_src, double reserve_scale, const 
   if (!g_obs) return;
   Graph& g = b.g;
   const uint64_t n = g.n, nk = n * (uint64_t)b.K;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   DevBuf<double> tmp(2 * n);
   k_unpack<<<grid_for(nk), 256, 0, st>>>(reserve_src, n, b.K, 1, reserve_scale, tmp.get());
   k_unpack<<<grid_for(nk), 256, 0, st>>>(residue_src, n, b.K, 1, 1.0, tmp.get() + n);
@@ -540,7 +554,7 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
   Workspace& w = b.w;
   const int K = b.K;
   const uint64_t n = g.n, nk = n * (uint64_t)K;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   const bool det = t_det;
   uint32_t* cur = w.fa.get();
   uint32_t* nxt = w.fb.get();
@@ -601,7 +615,7 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
   int& ps = per_sm[det];
   if (!ps) PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, DRAIN_NT, 0));
   if (ps < 1) fail(EINTERNAL, "drain kernel cannot be resident");
-  const unsigned grid = (unsigned)(ps * g.sm_count);
+  const unsigned grid = coop_grid(g, ps);
   if (det && w.drain_part.n < (size_t)grid * KMAX) w.drain_part.alloc((size_t)grid * KMAX);
   D.part = det ? w.drain_part.get() : nullptr;
   std::vector<double> exact;
@@ -683,7 +697,7 @@ void drain_levels(Block& b, double r_max, double lam_stop, uint64_t limit, bool 
 // recompute_r_sum (push.cpp:9-15) over the push-form residues of every column
 void exact_rsum(Block& b, const std::vector<int>& which) {
   Graph& g = b.g;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   const uint64_t nk = g.n * (uint64_t)b.K;
   if (t_det) {
     det_colsum(b, b.w.res.get(), nullptr, g.n, 1.0, b.w.dcols.get() + KMAX);
@@ -731,7 +745,7 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
                   bool defer = false) {
   Graph& g = b.g;
   Workspace& w = b.w;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   const uint64_t nk = g.n * (uint64_t)b.K;
   const double m_eff = (double)g.m_eff();
   if (E + (refine_rmax > 0.0) > EMAX) fail(EINVAL_, "epoch_num exceeds 64");
@@ -894,7 +908,7 @@ namespace {
 void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* call) {
   Graph& g = b.g;
   Workspace& w = b.w;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   const uint64_t n = g.n, nk = n * (uint64_t)b.K;
   const uint32_t k = b.k;
   const cudaMemcpyKind kind = out.on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
@@ -1034,7 +1048,7 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
   const bool defer = !g_obs && !g_trace && !std::getenv("PPRG_DEBUG_LOCAL");
   const double m_eff = (double)b.g.m_eff();
   const uint64_t nk = b.g.n * (uint64_t)b.K;
-  cudaStream_t st = b.g.stream;
+  cudaStream_t st = qstream(b.g);
   PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, st));
   PPRG_CUDA(cudaMemsetAsync(b.w.res.get(), 0, 8 * nk, st));
   k_seed<<<1, KMAX, 0, st>>>(b.w.res.get(), b.w.d_src.get(), b.K, 1.0);
@@ -1079,7 +1093,7 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
                   double* reserve, double* residue, bool on_device, ColumnStats* cols,
                   CallStats* call) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, round_k(k < (uint32_t)KMAX ? k : (uint32_t)KMAX) >= WIDE_K);  // 8(b) lanes
   if (!(r_max > 0.0)) fail(EINVAL_, "refine: r_max must be positive");  // push.cpp:210
   for (uint32_t c = 0; c < k; ++c)
     if (sources[c] >= g.n) fail(EINVAL_, "source out of range");
@@ -1088,7 +1102,7 @@ void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, d
   for (uint32_t b0 = 0; b0 < k; b0 += KMAX) {
     const uint32_t kb = k - b0 < (uint32_t)KMAX ? k - b0 : (uint32_t)KMAX;
     Block b = make_block(g, sources + b0, kb, alpha, false);
-    cudaStream_t st = g.stream;
+    cudaStream_t st = qstream(g);
     const uint64_t nk = n * (uint64_t)b.K;
     double* hr = reserve + (uint64_t)b0 * n;
     double* hq = residue + (uint64_t)b0 * n;
@@ -1159,7 +1173,7 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
                      double lambda_stop_fifo, const Outputs& out, ColumnStats* cols,
                      CallStats* call) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, round_k(block_columns(g.n, k)) >= WIDE_K);  // 8(b) lanes: wide blocks take the device
   for (uint32_t c = 0; c < k; ++c)
     if (sources[c] >= g.n) fail(EINVAL_, "source out of range");
   const uint64_t rb0 = t_readback_kernels;
@@ -1178,11 +1192,11 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
     if (o.residue) o.residue += (uint64_t)b0 * g.n;
     Block b = make_block(g, sources + b0, kb, alpha, pull);
     ColumnStats* cs = cols + b0;
-    EventTimer tdev(g.stream);
+    EventTimer tdev(qstream(g));
     tdev.start();
     if (eng == Engine::PowItr || eng == Engine::SimFwdPush) {
       const uint64_t n = g.n, nk = n * (uint64_t)b.K;
-      cudaStream_t st = g.stream;
+      cudaStream_t st = qstream(g);
       Workspace& w = b.w;
       PPRG_CUDA(cudaMemsetAsync(w.x.get(), 0, 8 * nk, st));
       PPRG_CUDA(cudaMemsetAsync(w.r0.get(), 0, 8 * nk, st));
@@ -1292,9 +1306,9 @@ void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, 
       PPRG_CUDA(cudaStreamSynchronize(st));
     } else if (eng == Engine::Fifo) {
       const uint64_t nk = g.n * (uint64_t)b.K;
-      PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, g.stream));
-      PPRG_CUDA(cudaMemsetAsync(b.w.res.get(), 0, 8 * nk, g.stream));
-      k_seed<<<1, KMAX, 0, g.stream>>>(b.w.res.get(), b.w.d_src.get(), b.K, 1.0);
+      PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, qstream(g)));
+      PPRG_CUDA(cudaMemsetAsync(b.w.res.get(), 0, 8 * nk, qstream(g)));
+      k_seed<<<1, KMAX, 0, qstream(g)>>>(b.w.res.get(), b.w.d_src.get(), b.K, 1.0);
       std::vector<int> state(KMAX, 2);
       for (uint32_t c = 0; c < kb; ++c) state[c] = 0;
       drain_levels(b, r_max_fifo, lambda_stop_fifo, UINT64_MAX, false, state, call);
@@ -1349,7 +1363,7 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
   // the tail: every node still above deg_eff * r_max in id order, drained
   std::vector<int> state(KMAX, 2);
   for (uint32_t c = 0; c < k; ++c) state[c] = 0;
-  EventTimer tl(g.stream);
+  EventTimer tl(qstream(g));
   tl.start();
   drain_levels(b, r_max, 0.0, UINT64_MAX, true, state, call);  // (+ recompute_r_sum)
   tl.stop();
@@ -1505,7 +1519,7 @@ PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t
                         uint32_t k, double alpha, double lambda, uint32_t E, int64_t scan_threshold,
                         double* partial_host, uint64_t* lo_out, uint64_t* hi_out) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);  // the partitioned query takes the whole device
   if (nparts < 1 || part >= nparts) fail(EINVAL_, "partition: part must be < nparts");
   if (k < 1 || k > KMAX) fail(EINVAL_, "partition: 1..64 sources per session");
   if (!(lambda > 0.0 && lambda <= 1.0)) fail(EINVAL_, "power_push: lambda must be in (0,1]");
@@ -1551,7 +1565,7 @@ PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t
   if (s->hi < s->lo) s->hi = s->lo;
   s->desc = pl.tiles.get() + s->t0;
   // ---- local phase (push.cpp:163-166) on the full graph -----------------------
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   const uint64_t nk = g.n * (uint64_t)K;
   PPRG_CUDA(cudaMemsetAsync(b.w.x.get(), 0, 8 * nk, st));
   PPRG_CUDA(cudaMemsetAsync(b.w.res.get(), 0, 8 * nk, st));
@@ -1585,7 +1599,7 @@ PartSession* part_begin(Graph& g, uint32_t nparts, uint32_t part, const uint32_t
 bool part_start(PartSession* s, const double* summed) {
   Graph& g = *s->g;
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);  // the partitioned query takes the whole device
   Block& b = *s->b;
   const int K = b.K;
   const double m_eff = (double)g.m_eff();
@@ -1605,10 +1619,10 @@ bool part_start(PartSession* s, const double* summed) {
   ps.n = (int)s->peers.size();
   for (int p = 0; p < ps.n; ++p) ps.y[p] = s->peers[p];
   if (s->hi > s->lo)
-    k_part_y<<<grid_for((s->hi - s->lo) * K), 256, 0, g.stream>>>(b.w.x.get(), g.inv_deg.get(), s->lo,
+    k_part_y<<<grid_for((s->hi - s->lo) * K), 256, 0, qstream(g)>>>(b.w.x.get(), g.inv_deg.get(), s->lo,
                                                                   s->hi, K, b.alpha, b.w.y0.get(), ps);
   PPRG_CUDA(cudaGetLastError());
-  PPRG_CUDA(cudaStreamSynchronize(g.stream));
+  PPRG_CUDA(cudaStreamSynchronize(qstream(g)));
   s->call.kernel_launches += 1;
   return any;
 }
@@ -1636,7 +1650,7 @@ void part_set_peers(PartSession* s, double* const* peer_y, uint32_t npeers) {
 void part_sweep(PartSession* s, double* local_host) {
   Graph& g = *s->g;
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);  // the partitioned query takes the whole device
   Block& b = *s->b;
   const int K = b.K;
   SweepParams P = part_params(s);
@@ -1646,7 +1660,7 @@ void part_sweep(PartSession* s, double* local_host) {
     P.lam[e] = s->lam[e];
     P.thr[e] = s->thr[e];
   }
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   PPRG_CUDA(cudaMemsetAsync(b.w.ctl(), 0, sizeof(SweepCtl), st));
   EventTimer tm(st);
   tm.start();
@@ -1681,9 +1695,9 @@ bool part_advance(PartSession* s, const double* summed) {
 void part_finish(PartSession* s, double* reserve, double* residue, bool on_device, double* rpart) {
   Graph& g = *s->g;
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);  // the partitioned query takes the whole device
   Block& b = *s->b;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   const uint64_t n = g.n;
   const uint32_t k = b.k;
   SweepParams Q = part_params(s);
@@ -1756,10 +1770,10 @@ double* part_x(PartSession* s) { return s->b->w.x.get(); }
 void part_resum(PartSession* s, double* partial_host) {
   Graph& g = *s->g;
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);  // the partitioned query takes the whole device
   Block& b = *s->b;
   const int K = b.K;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   PPRG_CUDA(cudaMemsetAsync(s->sums.get(), 0, 16 * KMAX, st));
   if (s->hi > s->lo)
     k_part_sums<<<grid_reduce((s->hi - s->lo) * K), 256, 0, st>>>(b.w.x.get(), g.deg.get(), s->lo,

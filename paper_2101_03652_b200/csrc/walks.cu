@@ -237,7 +237,7 @@ void cub_run(F&& f) {
 
 std::unique_ptr<WalkIndex> index_build(Graph& g, double alpha, uint64_t seed) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);
   auto w = std::make_unique<WalkIndex>();
   w->device = g.device;
   w->alpha = alpha;
@@ -255,7 +255,7 @@ std::unique_ptr<WalkIndex> index_build(Graph& g, double alpha, uint64_t seed) {
 std::unique_ptr<WalkIndex> index_from_host(Graph& g, double alpha, uint64_t seed,
                                            const uint32_t* h_endpoints) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);
   auto w = std::make_unique<WalkIndex>();
   w->device = g.device;
   w->alpha = alpha;
@@ -287,7 +287,7 @@ __global__ void k_cmp_u64(const uint64_t* a, const uint64_t* b, uint64_t n, unsi
 // the graph like WalkIndex's constructor + check_compatible (walk_index.cpp:19-42).
 std::unique_ptr<WalkIndex> index_load(Graph& g, const std::string& path) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);
   FileCloser fc;
   fc.f = std::fopen(path.c_str(), "rb");
   if (!fc.f) fail(EDATA, "cannot open walk index: " + path);
@@ -330,7 +330,7 @@ std::unique_ptr<WalkIndex> index_load(Graph& g, const std::string& path) {
 
 void index_save(Graph& g, const WalkIndex& w, const std::string& path) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);
   FileCloser fc;
   fc.f = std::fopen(path.c_str(), "wb");
   if (!fc.f) fail(EDATA, "cannot open for writing: " + path);
@@ -349,10 +349,10 @@ void index_save(Graph& g, const WalkIndex& w, const std::string& path) {
 void monte_carlo(Graph& g, const WalkIndex* idx, uint32_t s, double alpha, uint64_t W, uint64_t seed,
                  const double* h_reserve, const double* h_residue, double* h_est, uint64_t* walks) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, false);  // one source: a lane
   if (s >= g.n) fail(EINVAL_, "monte carlo: source out of range");
   const uint64_t n = g.n;
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   DevBuf<double> res(n), est(n);
   DevBuf<unsigned long long> cnt(n), colw(65);
   DevBuf<uint64_t> big(n);
@@ -413,7 +413,7 @@ void walk_terminals(Graph& g, const uint32_t* h_start, const uint32_t* h_k, cons
                     uint64_t count, uint32_t source, uint32_t tag, double alpha, uint64_t seed,
                     uint32_t* h_out) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, true);
   if (!count) return;
   DevBuf<uint32_t> s(count), kk(count), v(count), o(count);
   PPRG_CUDA(cudaMemcpyAsync(s.get(), h_start, 4 * count, cudaMemcpyHostToDevice, g.stream));
@@ -463,7 +463,7 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
               double epsilon, double mu, uint64_t seed, double* est_out, bool out_on_device,
               ColumnStats* cols, CallStats* call) {
   DeviceGuard dg(g.device);
-  std::lock_guard<std::mutex> lk(g.mu);
+  LaneGuard lk(g, k > 2);  // narrow batches share the device by lanes
   for (uint32_t c = 0; c < k; ++c)
     if (sources[c] >= g.n) fail(EINVAL_, "speedppr: source out of range");
   const uint64_t n = g.n;
@@ -472,7 +472,7 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
   const uint64_t W = (uint64_t)std::ceil(2.0 * (2.0 * epsilon / 3.0 + 2.0) * std::log((double)n) /
                                          (epsilon * epsilon * mu_eff));  // speedppr.cpp:8-18
   const uint64_t m_eff = g.m_eff();
-  cudaStream_t st = g.stream;
+  cudaStream_t st = qstream(g);
   const cudaMemcpyKind kind = out_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
   cudaEvent_t e0, e1;
   PPRG_CUDA(cudaEventCreate(&e0));

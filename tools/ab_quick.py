@@ -34,6 +34,16 @@ if "0" in which:
         outs, cs = P.power_push_batch(g, s, ALPHA, LAM, keep=False)
         ts.append(time.perf_counter() - t0)
     rec["configs[0]"] = {"ms_median": 1e3 * float(np.median(ts)), **split(cs, 1)}
+if "1" in which:
+    g = P.generate_rmat(17, 8, 1)
+    s = P.sample_sources(np.diff(g.out_offsets()), 64, 2)
+    P.power_push_batch(g, s, ALPHA, LAM, keep=False)
+    ts = []
+    for _ in range(10):
+        t0 = time.perf_counter()
+        outs, cs = P.power_push_batch(g, s, ALPHA, LAM, keep=False)
+        ts.append(time.perf_counter() - t0)
+    rec["configs[1]"] = {"ms_median": 1e3 * float(np.median(ts)), **split(cs, 1)}
 if "2" in which:
     g = P.generate_rmat(22, 16, 3)
     s = P.sample_sources(np.diff(g.out_offsets()), 256, 3)[:64]
