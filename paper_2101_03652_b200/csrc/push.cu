@@ -1347,15 +1347,15 @@ void speedppr_push_stage(Graph& g, const uint32_t* sources, uint32_t k, double a
   // PowerPush to lambda, then refine (push.cpp:208-222) as a final sweep
   // epoch at r_max run to its fixpoint, so the refine is pull sweeps over the
   // tile plan rather than a scattered frontier over millions of nodes.
-  // The local phase of this stage stops at a queue of n/16 instead of the
+  // The local phase of this stage stops at a queue of n/32 instead of the
   // reference's default n/4 (PPRG_SPP_SCAN_DIV): on the GPU a frontier level
   // costs more than a pull sweep once it holds more than a few percent of the
-  // (node, column) pairs. configs[3]: 2.37 -> 2.20 ms per query (n/64: 2.20,
-  // n/256: 2.23; profiles/r02_spp_scan_div.txt). The SpeedPPR estimate's
-  // guarantee does not depend on where PowerPush switches phases.
+  // (node, column) pairs. configs[3]: 2.37 -> 2.14 ms per query (n/16: 2.18,
+  // n/64: 2.20, n/256: 2.23; profiles/r02_spp_scan_div.txt). The SpeedPPR
+  // estimate's guarantee does not depend on where PowerPush switches phases.
   static const double spp_div = [] {
     const char* e = std::getenv("PPRG_SPP_SCAN_DIV");
-    return e ? std::atof(e) : 16.0;
+    return e ? std::atof(e) : 32.0;
   }();
   power_push_block(b, lambda, 8, (int64_t)((double)g.n / spp_div), call, r_max);
   Outputs none;

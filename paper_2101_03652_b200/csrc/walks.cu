@@ -162,17 +162,26 @@ __global__ void k_mc_entries(const __grid_constant__ McParams P, uint64_t* big,
     const uint32_t v = (uint32_t)(i / P.K);
     const int c = (int)(i % P.K);
     const double contribution = mc_term<DET>(P.res[i] / (double)wc, P, c);  // speedppr.cpp:41
-    // four walks' terminals resolved before their adds (independent loads in flight)
-    uint32_t kk = 0;
+    // four walks' terminals resolved before their adds (independent loads in
+    // flight). A walk stops at v itself with probability alpha: those are
+    // counted and added once (one atomic instead of ~alpha * wc).
+    uint32_t kk = 0, self = 0;
     for (; kk + 4 <= (uint32_t)wc; kk += 4) {
       uint32_t t[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = mc_terminal(P, v, c, kk + j);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) atomicAdd(P.est + (uint64_t)t[j] * P.K + c, contribution);
+      for (int j = 0; j < 4; ++j) {
+        if (t[j] == v) ++self;
+        else atomicAdd(P.est + (uint64_t)t[j] * P.K + c, contribution);
+      }
     }
-    for (; kk < (uint32_t)wc; ++kk)
-      atomicAdd(P.est + (uint64_t)mc_terminal(P, v, c, kk) * P.K + c, contribution);
+    for (; kk < (uint32_t)wc; ++kk) {
+      const uint32_t t = mc_terminal(P, v, c, kk);
+      if (t == v) ++self;
+      else atomicAdd(P.est + (uint64_t)t * P.K + c, contribution);
+    }
+    if (self) atomicAdd(P.est + i, (double)self * contribution);
   }
 }
 
@@ -190,15 +199,24 @@ __global__ void k_mc_big(const __grid_constant__ McParams P, const uint64_t* big
     const unsigned long long wc = P.cnt[i];
     const double contribution = mc_term<DET>(P.res[i] / (double)wc, P, c);
     unsigned long long kk = lane;
+    unsigned self = 0;  // walks that stop at v itself, added once per warp
     for (; kk + 96 < wc; kk += 128) {  // four walks per lane resolved before their adds
       uint32_t t[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = mc_terminal(P, v, c, (uint32_t)(kk + 32 * j));
 #pragma unroll
-      for (int j = 0; j < 4; ++j) atomicAdd(P.est + (uint64_t)t[j] * P.K + c, contribution);
+      for (int j = 0; j < 4; ++j) {
+        if (t[j] == v) ++self;
+        else atomicAdd(P.est + (uint64_t)t[j] * P.K + c, contribution);
+      }
     }
-    for (; kk < wc; kk += 32)
-      atomicAdd(P.est + (uint64_t)mc_terminal(P, v, c, (uint32_t)kk) * P.K + c, contribution);
+    for (; kk < wc; kk += 32) {
+      const uint32_t t = mc_terminal(P, v, c, (uint32_t)kk);
+      if (t == v) ++self;
+      else atomicAdd(P.est + (uint64_t)t * P.K + c, contribution);
+    }
+    self = __reduce_add_sync(0xffffffffu, self);
+    if (lane == 0 && self) atomicAdd(P.est + i, (double)self * contribution);
   }
 }
 
@@ -479,8 +497,14 @@ void speedppr(Graph& g, const WalkIndex* idx, const uint32_t* sources, uint32_t 
   PPRG_CUDA(cudaEventCreate(&e1));
   PPRG_CUDA(cudaEventRecord(e0, st));
   McState mc(st);
-  for (uint32_t b0 = 0; b0 < k; b0 += 64) {
-    const uint32_t kb = k - b0 < 64u ? k - b0 : 64u;
+  // sources per push-stage block (PPRG_SPP_COLUMNS, a power of two <= 64)
+  static const uint32_t spp_cols = [] {
+    const char* e = std::getenv("PPRG_SPP_COLUMNS");
+    const long v = e ? std::strtol(e, nullptr, 10) : 64;
+    return (uint32_t)(v == 1 || v == 2 || v == 4 || v == 8 || v == 16 || v == 32 ? v : 64);
+  }();
+  for (uint32_t b0 = 0; b0 < k; b0 += spp_cols) {
+    const uint32_t kb = k - b0 < spp_cols ? k - b0 : spp_cols;
     ColumnStats* cs = cols + b0;
     if (W <= m_eff) {
       int K = 1;
