@@ -196,6 +196,10 @@ __device__ __forceinline__ dbl4 ld_state4(const double* p) {
                : "=d"(r.v[0]), "=d"(r.v[1]), "=d"(r.v[2]), "=d"(r.v[3]) : "l"(p));
   return r;
 }
+__device__ __forceinline__ void st_state4(double* p, const dbl4& r) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};"
+               :: "l"(p), "d"(r.v[0]), "d"(r.v[1]), "d"(r.v[2]), "d"(r.v[3]) : "memory");
+}
 __device__ __forceinline__ dbl4 ld_gather4(const double* p) {
   dbl4 r;
   asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"

@@ -1,0 +1,746 @@
+// Delta sweeps: the PowerPush global phase (push.cpp:168-197) for wide column
+// blocks on graphs whose gather operand does not fit in L2. Included by
+// push.cu after sweep_kernel.cuh.
+//
+// k_sweeps gathers, per in-edge, the neighbour's cumulative y row (8K bytes:
+// 512 B at 64 columns). Here the residue is explicit and a push publishes only
+// this sweep's *increment* per out-edge, as a 16-bit float (e8m8, unsigned):
+// 2K bytes per in-edge (one 128-byte line at 64 columns), a quarter of the
+// gather traffic, and the gathered array (n x K x 2 B) is a quarter of y.
+//
+// Exactness. A push of row u with residue r (push.cpp:17-27) moves r' <= r:
+//     h  = e8m8 of (1-a) r / deg_eff, rounded DOWN        (the published share)
+//     r' = value(h) * deg_eff / (1-a)                     (the mass that leaves)
+//     x_u += r' (reserve = a x), r_u -= r', every out-neighbour later adds value(h).
+// The rounding remainder (< 2^-8 of r) simply stays in r_u, so mass is
+// conserved to fp64 rounding, residues stay >= 0, r_sum -= a r' (push.cpp:25)
+// stays exact, and the loop still ends at r_sum <= lambda: the 16-bit format
+// costs convergence rate (<0.4% of a row's residue left behind per push), not
+// accuracy. Sums of shares are formed in fp64 (a share's fp64 high word is
+// h << 12: decode is a shift and a mask, no conversion instruction).
+//
+// Exactly-once. Every published share must be added by every out-neighbour
+// exactly once, so the asynchronous "read whatever is there" of k_sweeps is
+// not available. Rows are cut into W waves of contiguous ids (equal in-edges);
+// shares are double-buffered by sweep parity; a row of wave w in sweep t reads
+//     d[t & 1][v]        if wave(v) <= w - L   (published earlier in this sweep)
+//     d[(t-1) & 1][v]    otherwise             (published in the previous sweep)
+// with lag L = 2: a tile of wave w starts once every tile of the waves <= w-2
+// has finished (per-wave completion counters, acquire/release), so wave w-1's
+// tail overlaps wave w's start and no grid barrier sits between waves. One
+// grid barrier per sweep closes the sweep (counters, epoch decisions), as in
+// k_sweeps. Gauss-Seidel between waves: 46-48 sweeps on configs[2] against 44.
+// After the last pushing sweep one more sweep consumes the shares in flight.
+#pragma once
+#include "sweep_kernel.cuh"
+
+namespace pprg {
+
+constexpr int DS_NT = 128;
+constexpr int DS_NW = DS_NT / 32;
+constexpr int DS_G = 4;             // 16-byte row loads in flight per lane
+constexpr uint32_t DS_RMAX = 256;   // rows per tile
+constexpr uint32_t DS_SHORT = 32;   // rows up to this many in-edges: one lane group each
+constexpr uint32_t DS_LONG = 384;   // rows beyond this: all warps of the block
+constexpr int DS_WMAX = 64;         // waves per sweep
+constexpr int DS_EXP = 769;         // value(h) = fp64{h << 12, 0} * 2^769: e8m8 spans 2^-253 .. 4
+#ifndef PPRG_DS_PIPE
+#define PPRG_DS_PIPE 0  // 1: two batches of row loads in flight per lane (needs 4 blocks per SM: slower)
+#endif
+#ifndef PPRG_DS_MINB
+#define PPRG_DS_MINB 5
+#endif
+
+struct DeltaParams {
+  uint64_t n, m;
+  const uint64_t* in_off;   // compacted transpose rows
+  const uint32_t* crow;
+  const uint32_t* cdeg;
+  const double* cinv;
+  const uint64_t* in_off_full;
+  const uint32_t* in_nbr;
+  const uint32_t* deg;
+  const double* inv_deg;
+  const TileDesc* desc;
+  uint64_t ntiles;
+  double* hub_acc;          // [ntiles][K] raw partial sums of hub pieces
+  unsigned* hub_cnt;
+  int k_live, E;
+  double alpha, inv_oma;    // inv_oma = 1 / (1 - alpha)
+  double* x;                // [n][K] pushed mass
+  double* r;                // [n][K] explicit residues
+  uint4* dsh;               // [n][2][K] u16 shares: row v of sweep parity p at 2 v + p
+  const double* from_drain; // exact r_sum after the local phase
+  double scan_lambda;
+  SweepCtl* ctl;
+  uint32_t max_sweeps;
+  uint32_t nwaves, lag;
+  uint32_t wave_tile[DS_WMAX + 1];
+  uint32_t wave_node[DS_WMAX + 1];
+  uint32_t src[KMAX];
+  double thr[EMAX], lam[EMAX];
+};
+
+__device__ __forceinline__ uint4 ld_share(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double share_value(uint32_t h) {  // raw (unscaled) value of a share
+  return __hiloint2double((int)(h << 12), 0);
+}
+// the 8 shares of one 16-byte group added to their columns' sums
+__device__ __forceinline__ void add_shares(double (&acc)[8], const uint4& v) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    acc[2 * i] += __hiloint2double((int)((w[i] << 12) & 0x0FFFF000u), 0);
+    acc[2 * i + 1] += __hiloint2double((int)((w[i] >> 4) & 0x0FFFF000u), 0);
+  }
+}
+
+// Per-block shared state of the delta sweeps.
+template <int K>
+struct DeltaSh {
+  static constexpr int LPR = K / 8;    // lanes per row (16 B = 8 columns each)
+  static constexpr int ES = 32 / LPR;  // rows (lane groups) per warp instruction
+  uint64_t soff[DS_RMAX + 1];
+  double sinv[DS_RMAX];
+  double spart[DS_NW][K];              // long rows / hub pieces: per-warp raw partials
+  double pacc[DS_NW * ES][K];          // pushed mass, one array per lane group (no atomics)
+  double thr[LPR * 10];                // this sweep's thresholds, column c at (c/8)*10 + c%8
+  double dd[K];                        // dead-end mass of the previous sweep (to the source)
+  double dead[K];                      // dead-end mass pushed in this sweep
+  double r_sum[K];
+  unsigned long long pushes[K];
+  uint32_t snode[DS_RMAX], sdeg[DS_RMAX];
+  uint32_t smed[DS_RMAX], slong[DS_RMAX];
+  uint32_t csrc[K];
+  unsigned nn[K], np[K], nd[K];
+  unsigned sweeps[K];
+  int epoch[K];
+  int done[K];
+  uint32_t bloom[64];                  // 2048 bits: (node & 2047) of every source
+  uint32_t cnt[2][4];                  // per tile parity: rowctr, medctr, nmed, nlong
+  unsigned long long tile[2];
+  int any, flag;
+  uint32_t known;                      // leading waves of this sweep known complete
+};
+
+// Gather operand of one tile. The two share buffers are interleaved by row
+// (row v of parity p at index 2 v + p), so the buffer choice is an index bit.
+template <int K>
+struct DRow {
+  const uint4* base;  // shares + this lane's 16-byte column group
+  uint32_t bound;     // ids below: published earlier in this sweep (parity par), others par ^ 1
+  uint32_t par;
+  __device__ __forceinline__ const uint4* at(uint32_t id) const {
+    const uint32_t sel = id < bound ? par : par ^ 1u;
+    return base + (uint64_t)(2u * id + sel) * (K / 8);
+  }
+};
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Raw share sums of ES short rows at once: lane group es sums row [b, b + len)
+// (len = 0: no row). The group's LPR lanes load LPR ids per chunk, coalesced.
+template <int K>
+__device__ __forceinline__ void group_sum(const DeltaParams& P, const DRow<K>& X, uint64_t b,
+                                          uint32_t len, uint32_t maxlen, uint32_t first_ids,
+                                          double (&acc)[8]) {
+  constexpr int LPR = K / 8;
+  constexpr int NB = LPR / DS_G;  // batches of DS_G loads per id chunk (2 at K = 64, 1 at K = 32)
+  const int lane = threadIdx.x & 31, kc = lane % LPR, base = lane - kc;
+  uint32_t nextid = first_ids;
+  for (uint32_t p0 = 0; p0 < maxlen; p0 += LPR) {
+    const uint32_t myid = nextid;
+    if (p0 + LPR < maxlen) nextid = p0 + LPR + kc < len ? ld_stream(P.in_nbr + b + p0 + LPR + kc) : 0u;
+#if PPRG_DS_PIPE
+    // every load of the chunk is issued before the first add
+    uint4 v[NB][DS_G];
+#pragma unroll
+    for (int h = 0; h < NB; ++h) {
+      if (h && p0 + h * DS_G >= maxlen) break;  // warp-uniform
+#pragma unroll
+      for (int g = 0; g < DS_G; ++g) {
+        const uint32_t id = __shfl_sync(0xffffffffu, myid, base + h * DS_G + g);
+        v[h][g] = p0 + h * DS_G + g < len ? ld_share(X.at(id)) : make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int h = 0; h < NB; ++h) {
+      if (h && p0 + h * DS_G >= maxlen) break;
+#pragma unroll
+      for (int g = 0; g < DS_G; ++g) add_shares(acc, v[h][g]);
+    }
+#else
+#pragma unroll
+    for (int h = 0; h < NB; ++h) {
+      if (h && p0 + h * DS_G >= maxlen) break;  // warp-uniform
+      uint4 v[DS_G];
+#pragma unroll
+      for (int g = 0; g < DS_G; ++g) {
+        const uint32_t id = __shfl_sync(0xffffffffu, myid, base + h * DS_G + g);
+        v[g] = p0 + h * DS_G + g < len ? ld_share(X.at(id)) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int g = 0; g < DS_G; ++g) add_shares(acc, v[g]);
+    }
+#endif
+  }
+}
+
+// Raw share sums of the in-edges [b, e) by the whole warp: lane groups take
+// every ES-th edge, in batches of DS_G loads per lane, two batches in flight
+// (the next batch is issued before the current one is added). Afterwards
+// every lane holds the totals of its 8 columns.
+template <int K>
+__device__ __forceinline__ void warp_sum(const DeltaParams& P, const DRow<K>& X, uint64_t b,
+                                         uint64_t e, double (&acc)[8]) {
+  constexpr int LPR = K / 8, ES = 32 / LPR;
+  constexpr uint32_t BE = ES * DS_G;  // edges per batch: 16 at K = 64, 32 at K = 32
+  const int lane = threadIdx.x & 31, es = lane / LPR;
+  const uint32_t ne = (uint32_t)(e - b);
+  const uint32_t nb = (ne + BE - 1) / BE;
+  auto ld_ids = [&](uint32_t chunk) -> uint32_t {
+    const uint32_t pe = chunk * 32 + lane;
+    return pe < ne ? ld_stream(P.in_nbr + b + pe) : 0u;
+  };
+  auto issue = [&](uint4(&v)[DS_G], uint32_t t, uint32_t ids) {
+#pragma unroll
+    for (int g = 0; g < DS_G; ++g) {
+      const uint32_t j = t * BE + g * ES + es;
+      const uint32_t id = __shfl_sync(0xffffffffu, ids, j & 31);
+      v[g] = j < ne ? ld_share(X.at(id)) : make_uint4(0, 0, 0, 0);
+    }
+  };
+#if !PPRG_DS_PIPE
+  {
+    uint4 v[DS_G];
+    uint32_t idc = ld_ids(0), idn = ld_ids(1);
+    for (uint32_t t = 0; t < nb; ++t) {
+      if (t && (t * BE) % 32 == 0) {
+        idc = idn;
+        idn = ld_ids(t * BE / 32 + 1);
+      }
+      issue(v, t, idc);
+#pragma unroll
+      for (int g = 0; g < DS_G; ++g) add_shares(acc, v[g]);
+    }
+  }
+#else
+  uint4 v0[DS_G], v1[DS_G];
+  uint32_t idc = ld_ids(0), idn = ld_ids(1);
+  if (nb) issue(v0, 0, idc);
+  for (uint32_t t = 0; t < nb; t += 2) {
+    // batch t + 1
+    if constexpr (BE == 32) {
+      idc = idn;
+      idn = ld_ids(t + 2);
+    }
+    if (t + 1 < nb) issue(v1, t + 1, idc);
+#pragma unroll
+    for (int g = 0; g < DS_G; ++g) add_shares(acc, v0[g]);
+    // batch t + 2
+    idc = idn;
+    idn = ld_ids(BE == 32 ? t + 3 : t / 2 + 2);
+    if (t + 2 < nb) issue(v0, t + 2, idc);
+    if (t + 1 < nb)
+#pragma unroll
+      for (int g = 0; g < DS_G; ++g) add_shares(acc, v1[g]);
+  }
+#endif
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+}
+
+// The decision for 8 columns [8 kc, 8 kc + 8) of row u by one lane: add the
+// gathered shares to the residues, push the columns above their threshold
+// (push.cpp:182-193) in the share format, write this sweep's shares.
+// acc: raw share sums. slot: the lane group's pushed-mass array.
+template <int K>
+__device__ __forceinline__ void decide8(const DeltaParams& P, DeltaSh<K>& S, uint4* dcur,
+                                        uint32_t u, uint32_t dg, double inv,
+                                        const double (&acc)[8], int kc, int slot) {
+  const uint64_t ix = (uint64_t)u * K + kc * 8;
+  const dbl4 ra = ld_state4(P.r + ix), rb = ld_state4(P.r + ix + 4);
+  // (x too, before any decision: one memory latency per row instead of two; nearly
+  // every visited row pushes in some column)
+  const dbl4 xa = ld_state4(P.x + ix), xb = ld_state4(P.x + ix + 4);
+  double rr[8];
+  const double up = ldexp(1.0, DS_EXP);
+  bool chg = false;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    rr[q] = fma(acc[q], up, q < 4 ? ra.v[q] : rb.v[q - 4]);
+    chg |= acc[q] != 0.0;
+  }
+  if ((S.bloom[(u >> 5) & 63] >> (u & 31)) & 1u) {  // maybe a source: last sweep's dead-end mass
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (u == S.csrc[kc * 8 + q] && S.dd[kc * 8 + q] != 0.0) {
+        rr[q] += S.dd[kc * 8 + q];
+        chg = true;
+      }
+  }
+  const double dthr = dg ? (double)dg : 1.0;
+  unsigned pm = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) pm |= (rr[q] > dthr * S.thr[kc * 10 + q]) ? 1u << q : 0u;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+  if (pm) {
+    double xx[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) xx[q] = q < 4 ? xa.v[q] : xb.v[q - 4];
+    const double oma = 1.0 - P.alpha;
+    const double c1 = oma * inv * ldexp(1.0, -DS_EXP);  // residue -> raw share
+    const double c2 = dthr * P.inv_oma * up;            // raw share -> mass leaving the row
+    double* pa = &S.pacc[slot][kc * 8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      if (!((pm >> q) & 1u)) continue;
+      double rp;
+      if (dg) {
+        uint32_t h = (uint32_t)__double2hiint(rr[q] * c1) >> 12;
+        h = h > 0xFFFFu ? 0xFFFFu : h;
+        if (h < 256u) continue;  // below the format's range: stays a residue
+        rp = fmin(share_value(h) * c2, rr[q]);
+        w[q >> 1] |= h << (16 * (q & 1));
+      } else {  // dead end: everything leaves, (1-a) of it to the source next sweep
+        rp = rr[q];
+        atomicAdd(&S.dead[kc * 8 + q], oma * rp);
+        atomicAdd(&S.nd[kc * 8 + q], 1u);
+      }
+      xx[q] += rp;
+      rr[q] -= rp;
+      pa[q] += rp;
+      atomicAdd(&S.nn[kc * 8 + q], 1u);
+      atomicAdd(&S.np[kc * 8 + q], dg ? dg : 1u);
+    }
+    dbl4 oa, ob;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) oa.v[q] = xx[q], ob.v[q] = xx[q + 4];
+    st_state4(P.x + ix, oa);
+    st_state4(P.x + ix + 4, ob);
+    chg = true;
+  }
+  if (chg) {
+    dbl4 oa, ob;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) oa.v[q] = rr[q], ob.v[q] = rr[q + 4];
+    st_state4(P.r + ix, oa);
+    st_state4(P.r + ix + 4, ob);
+  }
+  if (dg) dcur[(uint64_t)(2u * u) * (K / 8) + kc] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// One row-aligned tile: short rows by lane groups (ES rows per warp pass),
+// medium rows by warps, long rows by the block. cnt = this tile's counters
+// {rowctr, medctr, nmed, nlong} (the caller alternates two sets, so no barrier
+// is spent on resetting them).
+template <int K>
+__device__ __forceinline__ void delta_tile(const DeltaParams& P, DeltaSh<K>& S, const TileDesc& d,
+                                           const DRow<K>& X, uint4* dcur, uint32_t* cnt) {
+  constexpr int LPR = K / 8, ES = 32 / LPR;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kc = lane % LPR, es = lane / LPR;
+  const uint32_t nr = d.nr;
+  for (uint32_t t = tid; t <= nr; t += DS_NT) S.soff[t] = __ldg(P.in_off + d.r0 + t);
+  for (uint32_t t = tid; t < nr; t += DS_NT) {
+    S.snode[t] = __ldg(P.crow + d.r0 + t);
+    S.sdeg[t] = __ldg(P.cdeg + d.r0 + t);
+    S.sinv[t] = __ldg(P.cinv + d.r0 + t);
+    const uint64_t len = __ldg(P.in_off + d.r0 + t + 1) - __ldg(P.in_off + d.r0 + t);
+    if (len > DS_LONG) S.slong[atomicAdd(&cnt[3], 1u)] = t;
+    else if (len > DS_SHORT) S.smed[atomicAdd(&cnt[2], 1u)] = t;
+  }
+  __syncthreads();  // (also hands over the wave wait of thread 0)
+  // ---- short rows ----------------------------------------------------------
+  // Groups of ES rows are taken one ahead: the next group's first in-edge ids
+  // are loaded and its state rows prefetched into L2 before this group's
+  // gathers, so a group costs one exposed memory latency (the gathers).
+  auto grab = [&]() -> uint32_t {
+    uint32_t g0 = 0;
+    if (lane == 0) g0 = atomicAdd(&cnt[0], (uint32_t)ES);
+    return __shfl_sync(0xffffffffu, g0, 0);
+  };
+  auto prep = [&](uint32_t g0, uint64_t& b, uint32_t& len) -> uint32_t {
+    b = 0;
+    len = 0;
+    const uint32_t rr = g0 + es;
+    if (rr < nr) {
+      b = S.soff[rr];
+      const uint64_t l = S.soff[rr + 1] - b;
+      len = l <= DS_SHORT ? (uint32_t)l : 0u;
+    }
+    if (!len) return 0u;
+    const uint64_t ix = (uint64_t)S.snode[rr] * K + kc * 8;
+    prefetch_l2(P.r + ix);
+    prefetch_l2(P.x + ix);
+    return (uint32_t)kc < len ? ld_stream(P.in_nbr + b + kc) : 0u;
+  };
+  {
+    uint32_t g0 = grab();
+    uint64_t b;
+    uint32_t len;
+    uint32_t ids = prep(g0, b, len);
+    while (g0 < nr) {
+      const uint32_t gn = grab();
+      uint64_t bn;
+      uint32_t lenn;
+      const uint32_t idsn = prep(gn, bn, lenn);
+      const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
+      if (maxlen) {
+        double acc[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+        group_sum<K>(P, X, b, len, maxlen, ids, acc);
+        const uint32_t rr = g0 + es;
+        if (len) decide8<K>(P, S, dcur, S.snode[rr], S.sdeg[rr], S.sinv[rr], acc, kc, warp * ES + es);
+      }
+      g0 = gn;
+      b = bn;
+      len = lenn;
+      ids = idsn;
+    }
+  }
+  // ---- medium rows: one warp per row -----------------------------------------
+  for (;;) {
+    uint32_t i = 0;
+    if (lane == 0) i = atomicAdd(&cnt[1], 1u);
+    i = __shfl_sync(0xffffffffu, i, 0);
+    if (i >= cnt[2]) break;
+    const uint32_t rr = S.smed[i];
+    if (es == 0) {
+      const uint64_t ix = (uint64_t)S.snode[rr] * K + kc * 8;
+      prefetch_l2(P.r + ix);
+      prefetch_l2(P.x + ix);
+    }
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    warp_sum<K>(P, X, S.soff[rr], S.soff[rr + 1], acc);
+    if (es == 0) decide8<K>(P, S, dcur, S.snode[rr], S.sdeg[rr], S.sinv[rr], acc, kc, warp * ES);
+  }
+  // ---- long rows: all warps split the edges ---------------------------------
+  const uint32_t nl = cnt[3];
+  for (uint32_t li = 0; li < nl; ++li) {
+    const uint32_t rr = S.slong[li];
+    const uint64_t b = S.soff[rr], e = S.soff[rr + 1];
+    const uint64_t chunk = ((e - b) + DS_NW - 1) / DS_NW;
+    const uint64_t wb = b + warp * chunk, we = wb + chunk < e ? wb + chunk : e;
+    if (warp == 0 && es == 0) {
+      const uint64_t ix = (uint64_t)S.snode[rr] * K + kc * 8;
+      prefetch_l2(P.r + ix);
+      prefetch_l2(P.x + ix);
+    }
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    warp_sum<K>(P, X, wb < e ? wb : e, we, acc);
+    if (es == 0)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) S.spart[warp][kc * 8 + q] = acc[q];
+    __syncthreads();
+    if (warp == 0 && es == 0) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double t = 0.0;
+        for (int w = 0; w < DS_NW; ++w) t += S.spart[w][kc * 8 + q];
+        acc[q] = t;
+      }
+      decide8<K>(P, S, dcur, S.snode[rr], S.sdeg[rr], S.sinv[rr], acc, kc, 0);
+    }
+    __syncthreads();
+  }
+}
+
+// One piece of a hub row (more in-edges than a tile): raw partial sums per
+// piece, the last piece to arrive adds them in piece order and decides.
+template <int K>
+__device__ __forceinline__ void delta_hub_piece(const DeltaParams& P, DeltaSh<K>& S,
+                                                const TileDesc& d, uint64_t j, const DRow<K>& X,
+                                                uint4* dcur) {
+  constexpr int LPR = K / 8;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kc = lane % LPR, es = lane / LPR;
+  const uint64_t chunk = ((uint64_t)d.ne + DS_NW - 1) / DS_NW;
+  const uint64_t b = d.e0 + (uint64_t)warp * chunk, e0 = d.e0 + d.ne;
+  const uint64_t e = b + chunk < e0 ? b + chunk : e0;
+  double acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+  warp_sum<K>(P, X, b < e ? b : e, e, acc);
+  if (es == 0)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) S.spart[warp][kc * 8 + q] = acc[q];
+  __syncthreads();
+  if (tid < K) {
+    double t = 0.0;
+    for (int w = 0; w < DS_NW; ++w) t += S.spart[w][tid];
+    P.hub_acc[j * K + tid] = t;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                 : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
+    S.flag = old == d.npieces - 1;
+    if (S.flag) P.hub_cnt[d.hub] = 0;
+  }
+  __syncthreads();
+  if (S.flag && warp == 0 && es == 0) {
+    const double* part = P.hub_acc + (j - d.piece) * K + kc * 8;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      double t = 0.0;
+      for (uint32_t p = 0; p < d.npieces; ++p) t += __ldcg(part + (uint64_t)p * K + q);
+      acc[q] = t;
+    }
+    decide8<K>(P, S, dcur, __ldg(P.crow + d.r0), __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), acc,
+               kc, 0);
+  }
+  __syncthreads();
+}
+
+// Sources without in-edges are not rows of the compacted transpose: their only
+// inflow is the dead-end mass. Run with tile 0 (wave 0), one column per thread.
+template <int K>
+__device__ __forceinline__ void delta_source_rows(const DeltaParams& P, DeltaSh<K>& S,
+                                                  uint4* dcur) {
+  const int c = threadIdx.x;
+  if (c < K) {
+    const uint32_t u = S.csrc[c];
+    if (__ldg(P.in_off_full + u + 1) == __ldg(P.in_off_full + u)) {
+      const uint64_t ix = (uint64_t)u * K + c;
+      double rr = __ldcg(P.r + ix) + S.dd[c];
+      const uint32_t dg = __ldg(P.deg + u);
+      const double dthr = dg ? (double)dg : 1.0;
+      uint32_t h = 0;
+      if (rr > dthr * S.thr[(c / 8) * 10 + c % 8]) {
+        const double oma = 1.0 - P.alpha;
+        double rp = 0.0;
+        if (dg) {
+          h = (uint32_t)__double2hiint(rr * (oma * __ldg(P.inv_deg + u) * ldexp(1.0, -DS_EXP))) >> 12;
+          h = h > 0xFFFFu ? 0xFFFFu : h;
+          if (h < 256u) h = 0;
+          rp = fmin(share_value(h) * (dthr * P.inv_oma * ldexp(1.0, DS_EXP)), rr);
+        } else {
+          rp = rr;
+          atomicAdd(&S.dead[c], oma * rp);
+          atomicAdd(&S.nd[c], 1u);
+        }
+        if (rp > 0.0) {
+          P.x[ix] = __ldcg(P.x + ix) + rp;
+          rr -= rp;
+          atomicAdd(&S.pacc[0][c], rp);
+          atomicAdd(&S.nn[c], 1u);
+          atomicAdd(&S.np[c], dg ? dg : 1u);
+        }
+      }
+      P.r[ix] = rr;
+      // (other columns of this node's share row stay 0: it has no in-edges, so
+      // it holds residue only in the columns it is the source of)
+      reinterpret_cast<uint16_t*>(dcur)[2 * (uint64_t)u * K + c] = (uint16_t)h;
+    }
+  }
+  __syncthreads();
+}
+
+template <int K>
+__global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_constant__ DeltaParams P) {
+  constexpr int LPR = K / 8, ES = 32 / LPR;
+  extern __shared__ __align__(16) char ds_smem[];
+  DeltaSh<K>& S = *reinterpret_cast<DeltaSh<K>*>(ds_smem);
+  const int tid = threadIdx.x;
+  SweepCtl* ctl = P.ctl;
+  for (int i = tid; i < 64; i += DS_NT) S.bloom[i] = 0;
+  if (tid < 8) (&S.cnt[0][0])[tid] = 0;
+  __syncthreads();
+  if (tid < K) {
+    const double rs = __ldcg(P.from_drain + tid);
+    const int scan = tid < P.k_live && rs > P.scan_lambda;  // push.cpp:168
+    int ep = 0;
+    while (ep < P.E && !(rs > P.lam[ep])) ++ep;
+    S.r_sum[tid] = rs;
+    S.epoch[tid] = ep;
+    S.done[tid] = !scan || ep >= P.E;
+    S.sweeps[tid] = 0;
+    S.pushes[tid] = 0;
+    S.csrc[tid] = P.src[tid];
+    S.dd[tid] = 0.0;
+    atomicOr(&S.bloom[(P.src[tid] >> 5) & 63], 1u << (P.src[tid] & 31));
+    if (blockIdx.x == 0) ctl->out_scan[tid] = scan;
+  }
+  __syncthreads();
+  unsigned long long gen = 0;
+  bool draining = false;  // the extra sweep that only consumes the shares in flight
+  for (uint32_t sweep = 0;; ++sweep) {
+    const int buf = sweep % 3;
+    if (tid == 0) {
+      int any = 0;
+      for (int c = 0; c < K; ++c) any |= !S.done[c];
+      S.any = any;
+      S.known = 0;
+    }
+    if (tid < 8) (&S.cnt[0][0])[tid] = 0;
+    for (int i = tid; i < DS_NW * ES * K; i += DS_NT) (&S.pacc[0][0])[i] = 0.0;
+    if (tid < K) {
+      S.thr[(tid / 8) * 10 + tid % 8] = S.done[tid] ? CUDART_INF : P.thr[S.epoch[tid]];
+      S.dead[tid] = 0.0;
+      S.nn[tid] = S.np[tid] = S.nd[tid] = 0;
+    }
+    __syncthreads();
+    if (!S.any) {
+      if (draining || sweep == 0) break;
+      draining = true;
+    }
+    if (sweep >= P.max_sweeps) break;
+    if (tid == 0) S.tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
+    if (blockIdx.x == 0 && tid == 0) {
+      const int nb = (sweep + 1) % 3;  // last read two barriers ago
+      ctl->ticket[nb] = 0;
+      for (int w = 0; w < DS_WMAX; ++w) ctl->wdone[nb][w] = 0;
+      for (int c = 0; c < K; ++c) {
+        ctl->pushed[nb][c] = 0;
+        ctl->npush[nb][c] = 0;
+        ctl->nnode[nb][c] = 0;
+        ctl->dsum[nb][c] = 0;
+        ctl->et[nb][c] = 0;
+      }
+    }
+    __syncthreads();
+    const uint32_t par = sweep & 1u;
+    uint4* dcur = P.dsh + par * LPR;  // row u of this sweep: dcur[2 u LPR + kc]
+    uint32_t wave = 0;
+    unsigned long long j = S.tile[0];
+    for (uint32_t it = 0; j < P.ntiles; ++it) {
+      if (tid == 0) S.tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
+      while (j >= P.wave_tile[wave + 1]) ++wave;
+      const TileDesc d = P.desc[j];
+      // every tile of the waves <= wave - lag must have finished (their shares
+      // are read from this sweep's buffer)
+      const uint32_t need = wave >= P.lag ? wave - P.lag + 1 : 0;
+      if (tid == 0) {
+        uint32_t kn = S.known;
+        if (kn < need) {
+          while (kn < need) {
+            const unsigned full = P.wave_tile[kn + 1] - P.wave_tile[kn];
+            while (ld_acquire32(&ctl->wdone[buf][kn]) < full) __nanosleep(100);
+            ++kn;
+          }
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          S.known = kn;
+        }
+      }
+      if (tid < 4) S.cnt[(it + 1) & 1][tid] = 0;  // the next tile's counters
+      DRow<K> X{P.dsh + (tid & 31) % LPR, need ? P.wave_node[need] : 0u, par};
+      if (j == 0) {
+        __syncthreads();
+        delta_source_rows<K>(P, S, dcur);
+      }
+      if (d.npieces > 1) {
+        __syncthreads();
+        delta_hub_piece<K>(P, S, d, j, X, dcur);
+      } else {
+        delta_tile<K>(P, S, d, X, dcur, S.cnt[it & 1]);
+      }
+      __syncthreads();
+      if (tid == 0) {  // this tile's shares are published
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->wdone[buf][wave]) : "memory");
+      }
+      j = S.tile[(it + 1) & 1];
+    }
+    __syncthreads();
+    // flush the block's sums: lane-group arrays -> one value per column
+    if (tid < K) {
+      double p = 0.0;
+      for (int s = 0; s < DS_NW * ES; ++s) p += S.pacc[s][tid];
+      if (p != 0.0) atomicAdd(&ctl->pushed[buf][tid], p);
+      if (S.dead[tid] != 0.0) atomicAdd(&ctl->dsum[buf][tid], S.dead[tid]);
+      if (S.np[tid]) atomicAdd(&ctl->npush[buf][tid], (unsigned long long)S.np[tid]);
+      if (S.nn[tid]) atomicAdd(&ctl->nnode[buf][tid], (unsigned long long)S.nn[tid]);
+      if (S.np[tid]) atomicAdd(&ctl->et[buf][tid], (unsigned long long)(S.np[tid] - S.nd[tid]));
+    }
+    grid_barrier2(&ctl->gbar, ++gen);
+    if (tid < K) {
+      const double pushed = __ldcg(&ctl->pushed[buf][tid]);
+      const unsigned long long np = __ldcg(&ctl->npush[buf][tid]);
+      S.dd[tid] = __ldcg(&ctl->dsum[buf][tid]);
+      if (!S.done[tid]) {
+        S.sweeps[tid] += 1;
+        S.pushes[tid] += np;
+        S.r_sum[tid] -= P.alpha * pushed;
+        if (np == 0) S.epoch[tid] += 1;  // fixpoint: nothing active at this threshold
+        while (S.epoch[tid] < P.E && !(S.r_sum[tid] > P.lam[S.epoch[tid]])) S.epoch[tid] += 1;
+        if (S.epoch[tid] >= P.E) S.done[tid] = 1;
+      }
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+      // B = 8(n+1) + 8 k n + 4 E_t + 24 P_t over the live columns
+      unsigned long long pt = 0, et = 0;
+      for (int c = 0; c < P.k_live; ++c) {
+        pt += __ldcg(&ctl->nnode[buf][c]);
+        const unsigned long long e = __ldcg(&ctl->et[buf][c]);
+        et = e > et ? e : et;
+      }
+      ctl->alg_bytes += 8ull * (P.n + 1) + 8ull * P.k_live * P.n + 4ull * et + 24ull * pt;
+      ctl->total_sweeps = sweep + 1;
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid < K) {
+    ctl->out_rsum[tid] = S.r_sum[tid];
+    ctl->out_D[tid] = 0.0;
+    ctl->out_sweeps[tid] = S.sweeps[tid];
+    ctl->out_done[tid] = S.done[tid];
+    ctl->out_epoch[tid] = S.epoch[tid];
+    ctl->out_pushes[tid] = S.pushes[tid];
+  }
+}
+
+// After the delta sweeps: query-major outputs through a shared-memory
+// transpose (32 rows x K columns per step, 256-byte output segments) and the
+// exact residue sum per column (push.cpp:9-15) into fctl->pushed[0].
+template <int K>
+__global__ void __launch_bounds__(256) k_delta_final(const double* x, const double* r, uint64_t n,
+                                                     int k_live, double alpha, double* out_reserve,
+                                                     double* out_residue, SweepCtl* fctl) {
+  __shared__ double tx[32][K + 1], tr[32][K + 1];
+  __shared__ double csum[K];
+  const int tid = threadIdx.x;
+  if (tid < K) csum[tid] = 0.0;
+  double loc = 0.0;  // column tid % K (256 % K == 0)
+  for (uint64_t u0 = (uint64_t)blockIdx.x * 32; u0 < n; u0 += (uint64_t)gridDim.x * 32) {
+    const uint32_t rows = n - u0 < 32 ? (uint32_t)(n - u0) : 32u;
+    __syncthreads();
+    for (uint32_t i = tid; i < rows * K; i += 256) {
+      const double rv = __ldcs(r + u0 * K + i);
+      tr[i / K][i % K] = rv;
+      loc += rv;
+      if (out_reserve) tx[i / K][i % K] = __ldcs(x + u0 * K + i);
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < 32u * k_live; i += 256) {
+      const uint32_t c = i / 32, rr = i % 32;
+      if (rr < rows) {
+        if (out_reserve) __stcs(out_reserve + (uint64_t)c * n + u0 + rr, alpha * tx[rr][c]);
+        if (out_residue) __stcs(out_residue + (uint64_t)c * n + u0 + rr, tr[rr][c]);
+      }
+    }
+  }
+  __syncthreads();
+  if (loc != 0.0) atomicAdd(&csum[tid % K], loc);
+  __syncthreads();
+  if (tid < K) {
+    if (csum[tid] != 0.0) atomicAdd(&fctl->pushed[0][tid], csum[tid]);
+    if (blockIdx.x == 0) fctl->out_scale[tid] = 1.0;
+  }
+}
+
+}  // namespace pprg

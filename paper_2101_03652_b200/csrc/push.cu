@@ -35,6 +35,7 @@
 
 #include "sweep_kernel.cuh"
 #include "frontier_kernels.cuh"
+#include "delta_sweep.cuh"
 
 namespace pprg {
 
@@ -82,6 +83,10 @@ struct Workspace {
   DevBuf<double> dsum_part;             // deterministic column sums: per-block partials
   DevBuf<double> drain_part;            // deterministic drains: per-block exact r_sum partials
   unsigned level_tag = 0;
+  // delta sweeps: the wave cut of their tile plan (host, built once per plan)
+  const void* dw_plan = nullptr;
+  uint32_t dw_waves = 0;
+  std::vector<uint32_t> dw_tile, dw_node;
 };
 
 static std::mutex g_ws_mu;
@@ -388,6 +393,7 @@ struct Block {
   bool drain_pending = false;        // the drain's DrainCtl is still on the device
   unsigned long long drain_live = 0; // its columns
   bool sweeps_pending = false;       // the global phase's SweepCtl is still on the device
+  bool delta = false;                // the global phase ran as delta sweeps (explicit residues in w.res)
   std::unique_ptr<EventTimer> t_local, t_sweep;
   Block(Graph& g_, Workspace& w_, int K_, uint32_t k_, double a)
       : g(g_), w(w_), K(K_), k(k_), alpha(a), src(KMAX, 0), r_sum(KMAX, 1.0), pushes(KMAX, 0),
@@ -736,6 +742,140 @@ void check_final(const SweepCtl& fc) {
                         " negative implicit residues summing to " + std::to_string(fc.neg_sum));
 }
 
+// ---- delta sweeps (delta_sweep.cuh) -------------------------------------------
+// PPRG_DELTA: 0 = never, 1 = every eligible block, unset = blocks whose gather
+// operand y (n x K x 8 B) is beyond twice the L2.
+bool delta_on(const Graph& g, int K) {
+  static const int mode = [] {
+    const char* e = std::getenv("PPRG_DELTA");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (K < 32 || mode == 0 || t_det) return false;
+  if (g.m_eff() >= (1ull << 32) || g.n >= (1ull << 31) || g.n_rows == 0) return false;
+  if (mode > 0) return true;
+  return g.n * (uint64_t)K * 8 > (256ull << 20);
+}
+uint32_t ds_tile_edges() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("PPRG_DS_TILE");
+    const int t = e ? std::atoi(e) : 2048;
+    return (uint32_t)(t < 256 ? 256 : t);
+  }();
+  return v;
+}
+
+template <int K>
+void launch_dsweeps(Graph& g, DeltaParams& P) {
+  auto kern = k_dsweeps<K>;
+  const size_t smem = sizeof(DeltaSh<K>);
+  static bool attr_set = false;
+  if (!attr_set) {
+    PPRG_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  int per_sm = 0;
+  PPRG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DS_NT, smem));
+  if (per_sm < 1) fail(EINTERNAL, "delta sweep kernel cannot be resident");
+  const unsigned grid = coop_grid(g, per_sm);
+  void* args[] = {(void*)&P};
+  PPRG_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(grid), dim3(DS_NT), args, smem, qstream(g)));
+  PPRG_CUDA(cudaGetLastError());
+}
+
+// The global phase of a device-started block as delta sweeps: explicit
+// residues (w.res, left by the local phase), 16-bit shares in w.y0.
+void delta_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
+  Graph& g = b.g;
+  Workspace& w = b.w;
+  cudaStream_t st = qstream(g);
+  const uint64_t nk = g.n * (uint64_t)b.K;
+  const double m_eff = (double)g.m_eff();
+  const Graph::Plan& pl = g.tile_plan(ds_tile_edges(), DS_RMAX, ds_tile_edges());
+  ws_tiles(w, g, pl.ntiles, pl.nhubs);
+  static const uint32_t W = [] {
+    const char* e = std::getenv("PPRG_DS_WAVES");
+    const int v = e ? std::atoi(e) : 32;
+    return (uint32_t)(v < 1 ? 1 : v > DS_WMAX ? DS_WMAX : v);
+  }();
+  static const uint32_t L = [] {
+    const char* e = std::getenv("PPRG_DS_LAG");
+    const int v = e ? std::atoi(e) : 2;
+    return (uint32_t)(v < 1 ? 1 : v);
+  }();
+  if (w.dw_plan != &pl || w.dw_waves != W) {
+    // waves of ~equal in-edges, cut at row-start tiles (a hub row's pieces stay in one wave)
+    const std::vector<TileDesc>& t = pl.host;
+    uint64_t total = 0;
+    for (const TileDesc& d : t) total += d.ne;
+    w.dw_tile.assign(1, 0u);
+    uint64_t acc = 0;
+    for (uint64_t j = 0; j < t.size() && w.dw_tile.size() < W; ++j) {
+      if (acc * W >= total * w.dw_tile.size() && t[j].piece == 0 && j > w.dw_tile.back())
+        w.dw_tile.push_back((uint32_t)j);
+      acc += t[j].ne;
+    }
+    w.dw_node.assign(w.dw_tile.size(), 0u);
+    for (size_t i = 1; i < w.dw_tile.size(); ++i)
+      d2h_small(&w.dw_node[i], g.cin_row.get() + t[w.dw_tile[i]].r0, 4, st);
+    PPRG_CUDA(cudaStreamSynchronize(st));
+    w.dw_tile.push_back((uint32_t)t.size());
+    w.dw_node.push_back(0xFFFFFFFFu);
+    w.dw_plan = &pl;
+    w.dw_waves = W;
+  }
+  DeltaParams P;
+  std::memset(&P, 0, sizeof P);
+  P.n = g.n;
+  P.m = g.m;
+  P.in_off = g.cin_off.get();
+  P.crow = g.cin_row.get();
+  P.cdeg = g.cin_deg.get();
+  P.cinv = g.cin_inv.get();
+  P.in_off_full = g.in_off.get();
+  P.in_nbr = g.in_nbr.get();
+  P.deg = g.deg.get();
+  P.inv_deg = g.inv_deg.get();
+  P.desc = pl.tiles.get();
+  P.ntiles = pl.ntiles;
+  P.hub_acc = w.hub_acc.get();
+  P.hub_cnt = w.hub_cnt.get();
+  P.k_live = (int)b.k;
+  P.E = (int)E;
+  P.alpha = b.alpha;
+  P.inv_oma = 1.0 / (1.0 - b.alpha);
+  P.x = w.x.get();
+  P.r = w.res.get();
+  P.dsh = reinterpret_cast<uint4*>(w.y0.get());
+  P.from_drain = w.dctl()->out_exact;
+  P.scan_lambda = lambda;
+  P.ctl = w.ctl();
+  P.max_sweeps = 200000;
+  P.nwaves = (uint32_t)w.dw_tile.size() - 1;
+  P.lag = L;
+  for (uint32_t i = 0; i <= P.nwaves; ++i) {
+    P.wave_tile[i] = w.dw_tile[i];
+    P.wave_node[i] = w.dw_node[i];
+  }
+  for (uint32_t i = P.nwaves + 1; i <= (uint32_t)DS_WMAX; ++i) P.wave_tile[i] = 0xFFFFFFFFu;
+  for (int c = 0; c < b.K; ++c) P.src[c] = b.src[c];
+  for (uint32_t e = 0; e < E; ++e) {
+    const double el = std::pow(lambda, static_cast<double>(e + 1) / E);  // push.cpp:176-178
+    P.lam[e] = stop_lambda(el, e, E);
+    P.thr[e] = el / m_eff;
+  }
+  PPRG_CUDA(cudaMemsetAsync(w.y0.get(), 0, 4 * nk, st));  // both share buffers
+  PPRG_CUDA(cudaMemsetAsync(w.ctl(), 0, sizeof(SweepCtl), st));
+  b.t_sweep = std::make_unique<EventTimer>(st);
+  b.t_sweep->start();
+  if (b.K == 64) launch_dsweeps<64>(g, P);
+  else launch_dsweeps<32>(g, P);
+  b.t_sweep->stop();
+  call->sweep_launches += 1;
+  call->kernel_launches += 1;
+  b.sweeps_pending = true;
+  b.delta = true;
+}
+
 // Global phase: epochs of asynchronous pull sweeps in one persistent
 // cooperative kernel (push.cpp:168-197) for the columns with scan[c] set.
 // refine_rmax > 0 appends a refine epoch (push.cpp:208-222): threshold
@@ -749,6 +889,10 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   const uint64_t nk = g.n * (uint64_t)b.K;
   const double m_eff = (double)g.m_eff();
   if (E + (refine_rmax > 0.0) > EMAX) fail(EINVAL_, "epoch_num exceeds 64");
+  if (defer && refine_rmax == 0.0 && delta_on(g, b.K)) {
+    delta_phase(b, lambda, E, call);
+    return;
+  }
   PPRG_CUDA(cudaMemsetAsync(w.dcols.get() + 2 * KMAX, 0, 8 * KMAX, st));
   k_init_pull<<<grid_reduce(nk), 256, 0, st>>>(w.x.get(), g.deg.get(), g.inv_deg.get(), g.n, b.K,
                                             b.alpha, w.y0.get(), w.dcols.get() + 2 * KMAX);
@@ -952,8 +1096,8 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
   Q.out_reserve = out.reserve ? (direct ? out.reserve : w.stage_res[slot].get()) : nullptr;
   Q.out_residue = out.residue ? (direct ? out.residue : w.stage_rsd[slot].get()) : nullptr;
   // rows with in-degree 0 (other than sources) are never visited: they hold 0
-  if (Q.out_reserve) PPRG_CUDA(cudaMemsetAsync(Q.out_reserve, 0, 8 * n * k, st));
-  if (Q.out_residue) PPRG_CUDA(cudaMemsetAsync(Q.out_residue, 0, 8 * n * k, st));
+  if (Q.out_reserve && !b.delta) PPRG_CUDA(cudaMemsetAsync(Q.out_reserve, 0, 8 * n * k, st));
+  if (Q.out_residue && !b.delta) PPRG_CUDA(cudaMemsetAsync(Q.out_residue, 0, 8 * n * k, st));
   Q.res_inter = residues_inplace ? w.res.get() : nullptr;
   Q.push_res = w.res.get();
   Q.x = w.x.get();
@@ -980,7 +1124,19 @@ void finalize(Block& b, const Outputs& out, bool residues_inplace, CallStats* ca
     Q.y[0] = Q.y[1] = (ts & 1u) ? w.y1.get() : w.y0.get();
   }
   tf.start();
-  dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
+  if (b.delta) {
+    // explicit residues already (w.res): transpose into the outputs, exact r_sum
+    const unsigned grid = (unsigned)std::min<uint64_t>((n + 31) / 32, 148ull * 8);
+    if (b.K == 64)
+      k_delta_final<64><<<grid, 256, 0, st>>>(w.x.get(), w.res.get(), n, (int)k, b.alpha,
+                                              Q.out_reserve, Q.out_residue, fctl);
+    else
+      k_delta_final<32><<<grid, 256, 0, st>>>(w.x.get(), w.res.get(), n, (int)k, b.alpha,
+                                              Q.out_reserve, Q.out_residue, fctl);
+    PPRG_CUDA(cudaGetLastError());
+  } else {
+    dispatch_sweeps<M_FINAL>(g, b.K, Q, true);
+  }
   tf.stop();
   call->kernel_launches += 1;
   SweepCtl fc;

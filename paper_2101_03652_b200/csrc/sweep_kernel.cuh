@@ -63,6 +63,7 @@ struct SweepCtl {
   double out_scale[KMAX];              // final pass: pushed[0][c] / out_scale[c] = residue sum
   unsigned wticket[3][WMAX];           // deterministic sweeps: tile ticket of each wave
   int out_scan[KMAX];                  // column ran the global phase (push.cpp:168)
+  unsigned wdone[3][64];               // delta sweeps: finished tiles of each wave
 };
 
 struct SweepParams {
