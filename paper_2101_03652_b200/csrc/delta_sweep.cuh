@@ -39,13 +39,25 @@ namespace pprg {
 constexpr int DS_NT = 128;
 constexpr int DS_NW = DS_NT / 32;
 constexpr int DS_G = 4;             // 16-byte row loads in flight per lane
-constexpr uint32_t DS_RMAX = 256;   // rows per tile
+constexpr uint32_t DS_IDS = 512;    // in-edges per task at most
+constexpr uint32_t DS_TASK_R = 32;  // rows per task (lane i holds row i's data)
 constexpr uint32_t DS_SHORT = 32;   // rows up to this many in-edges: one lane group each
-constexpr uint32_t DS_LONG = 384;   // rows beyond this: all warps of the block
 constexpr int DS_WMAX = 64;         // waves per sweep
 constexpr int DS_EXP = 769;         // value(h) = fp64{h << 12, 0} * 2^769: e8m8 spans 2^-253 .. 4
 #ifndef PPRG_DS_PIPE
 #define PPRG_DS_PIPE 0  // 1: two batches of row loads in flight per lane (needs 4 blocks per SM: slower)
+#endif
+#ifndef PPRG_DS_PFROWS
+#define PPRG_DS_PFROWS 0
+#endif
+#ifndef PPRG_DS_HALF
+#define PPRG_DS_HALF 0
+#endif
+#ifndef PPRG_DS_PFTASK
+#define PPRG_DS_PFTASK 1
+#endif
+#ifndef PPRG_DS_L1STATE
+#define PPRG_DS_L1STATE 1
 #endif
 #ifndef PPRG_DS_MINB
 #define PPRG_DS_MINB 5
@@ -100,32 +112,27 @@ __device__ __forceinline__ void add_shares(double (&acc)[8], const uint4& v) {
   }
 }
 
-// Per-block shared state of the delta sweeps.
+// Per-block shared state of the delta sweeps (the warps of a block work
+// independently; the block only shares the per-column state and sums).
 template <int K>
 struct DeltaSh {
   static constexpr int LPR = K / 8;    // lanes per row (16 B = 8 columns each)
   static constexpr int ES = 32 / LPR;  // rows (lane groups) per warp instruction
-  uint64_t soff[DS_RMAX + 1];
-  double sinv[DS_RMAX];
-  double spart[DS_NW][K];              // long rows / hub pieces: per-warp raw partials
   double pacc[DS_NW * ES][K];          // pushed mass, one array per lane group (no atomics)
+  uint32_t sids[DS_NW][DS_IDS];        // each warp's task: its in-edge ids
   double thr[LPR * 10];                // this sweep's thresholds, column c at (c/8)*10 + c%8
   double dd[K];                        // dead-end mass of the previous sweep (to the source)
   double dead[K];                      // dead-end mass pushed in this sweep
+  double srcpush[K];                   // mass pushed by sources without in-edges
   double r_sum[K];
   unsigned long long pushes[K];
-  uint32_t snode[DS_RMAX], sdeg[DS_RMAX];
-  uint32_t smed[DS_RMAX], slong[DS_RMAX];
   uint32_t csrc[K];
   unsigned nn[K], np[K], nd[K];
   unsigned sweeps[K];
   int epoch[K];
   int done[K];
   uint32_t bloom[64];                  // 2048 bits: (node & 2047) of every source
-  uint32_t cnt[2][4];                  // per tile parity: rowctr, medctr, nmed, nlong
-  unsigned long long tile[2];
-  int any, flag;
-  uint32_t known;                      // leading waves of this sweep known complete
+  int any;
 };
 
 // Gather operand of one tile. The two share buffers are interleaved by row
@@ -143,115 +150,59 @@ struct DRow {
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
-
-// Raw share sums of ES short rows at once: lane group es sums row [b, b + len)
-// (len = 0: no row). The group's LPR lanes load LPR ids per chunk, coalesced.
-template <int K>
-__device__ __forceinline__ void group_sum(const DeltaParams& P, const DRow<K>& X, uint64_t b,
-                                          uint32_t len, uint32_t maxlen, uint32_t first_ids,
-                                          double (&acc)[8]) {
-  constexpr int LPR = K / 8;
-  constexpr int NB = LPR / DS_G;  // batches of DS_G loads per id chunk (2 at K = 64, 1 at K = 32)
-  const int lane = threadIdx.x & 31, kc = lane % LPR, base = lane - kc;
-  uint32_t nextid = first_ids;
-  for (uint32_t p0 = 0; p0 < maxlen; p0 += LPR) {
-    const uint32_t myid = nextid;
-    if (p0 + LPR < maxlen) nextid = p0 + LPR + kc < len ? ld_stream(P.in_nbr + b + p0 + LPR + kc) : 0u;
-#if PPRG_DS_PIPE
-    // every load of the chunk is issued before the first add
-    uint4 v[NB][DS_G];
-#pragma unroll
-    for (int h = 0; h < NB; ++h) {
-      if (h && p0 + h * DS_G >= maxlen) break;  // warp-uniform
-#pragma unroll
-      for (int g = 0; g < DS_G; ++g) {
-        const uint32_t id = __shfl_sync(0xffffffffu, myid, base + h * DS_G + g);
-        v[h][g] = p0 + h * DS_G + g < len ? ld_share(X.at(id)) : make_uint4(0, 0, 0, 0);
-      }
-    }
-#pragma unroll
-    for (int h = 0; h < NB; ++h) {
-      if (h && p0 + h * DS_G >= maxlen) break;
-#pragma unroll
-      for (int g = 0; g < DS_G; ++g) add_shares(acc, v[h][g]);
-    }
+// State rows (r, x) are touched by exactly one warp per sweep and every sweep
+// starts with an L1 invalidation (the grid barrier's fence), so they may be
+// prefetched into and read through L1.
+__device__ __forceinline__ void prefetch_state(const void* p) {
+#if PPRG_DS_L1STATE
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 #else
-#pragma unroll
-    for (int h = 0; h < NB; ++h) {
-      if (h && p0 + h * DS_G >= maxlen) break;  // warp-uniform
-      uint4 v[DS_G];
-#pragma unroll
-      for (int g = 0; g < DS_G; ++g) {
-        const uint32_t id = __shfl_sync(0xffffffffu, myid, base + h * DS_G + g);
-        v[g] = p0 + h * DS_G + g < len ? ld_share(X.at(id)) : make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int g = 0; g < DS_G; ++g) add_shares(acc, v[g]);
-    }
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 #endif
+}
+__device__ __forceinline__ dbl4 ld_rowstate4(const double* p) {
+#if PPRG_DS_L1STATE
+  return ld_gather4(p);
+#else
+  return ld_state4(p);
+#endif
+}
+
+// Raw share sums of ES short rows at once: lane group es sums the in-edges
+// ids[0 .. len) of its row (len = 0: no row). ids: the task's in-edge ids in
+// shared memory (staged once per task, so no id load sits in a gather chain).
+template <int K>
+__device__ __forceinline__ void group_sum(const DRow<K>& X, const uint32_t* ids, uint32_t len,
+                                          uint32_t maxlen, double (&acc)[8]) {
+  for (uint32_t p0 = 0; p0 < maxlen; p0 += DS_G) {
+    uint4 v[DS_G];
+#pragma unroll
+    for (int g = 0; g < DS_G; ++g)
+      v[g] = p0 + g < len ? ld_share(X.at(ids[p0 + g])) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+    for (int g = 0; g < DS_G; ++g) add_shares(acc, v[g]);
   }
 }
 
-// Raw share sums of the in-edges [b, e) by the whole warp: lane groups take
-// every ES-th edge, in batches of DS_G loads per lane, two batches in flight
-// (the next batch is issued before the current one is added). Afterwards
-// every lane holds the totals of its 8 columns.
+// Raw share sums of the in-edges ids[0 .. ne) by the whole warp: lane groups
+// take every ES-th edge, DS_G loads per lane in flight. Afterwards every lane
+// holds the totals of its 8 columns.
 template <int K>
-__device__ __forceinline__ void warp_sum(const DeltaParams& P, const DRow<K>& X, uint64_t b,
-                                         uint64_t e, double (&acc)[8]) {
+__device__ __forceinline__ void warp_sum(const DRow<K>& X, const uint32_t* ids, uint32_t ne,
+                                         double (&acc)[8]) {
   constexpr int LPR = K / 8, ES = 32 / LPR;
   constexpr uint32_t BE = ES * DS_G;  // edges per batch: 16 at K = 64, 32 at K = 32
-  const int lane = threadIdx.x & 31, es = lane / LPR;
-  const uint32_t ne = (uint32_t)(e - b);
-  const uint32_t nb = (ne + BE - 1) / BE;
-  auto ld_ids = [&](uint32_t chunk) -> uint32_t {
-    const uint32_t pe = chunk * 32 + lane;
-    return pe < ne ? ld_stream(P.in_nbr + b + pe) : 0u;
-  };
-  auto issue = [&](uint4(&v)[DS_G], uint32_t t, uint32_t ids) {
+  const uint32_t es = (threadIdx.x & 31) / LPR;
+  for (uint32_t t0 = 0; t0 < ne; t0 += BE) {
+    uint4 v[DS_G];
 #pragma unroll
     for (int g = 0; g < DS_G; ++g) {
-      const uint32_t j = t * BE + g * ES + es;
-      const uint32_t id = __shfl_sync(0xffffffffu, ids, j & 31);
-      v[g] = j < ne ? ld_share(X.at(id)) : make_uint4(0, 0, 0, 0);
+      const uint32_t j = t0 + g * ES + es;
+      v[g] = j < ne ? ld_share(X.at(ids[j])) : make_uint4(0, 0, 0, 0);
     }
-  };
-#if !PPRG_DS_PIPE
-  {
-    uint4 v[DS_G];
-    uint32_t idc = ld_ids(0), idn = ld_ids(1);
-    for (uint32_t t = 0; t < nb; ++t) {
-      if (t && (t * BE) % 32 == 0) {
-        idc = idn;
-        idn = ld_ids(t * BE / 32 + 1);
-      }
-      issue(v, t, idc);
 #pragma unroll
-      for (int g = 0; g < DS_G; ++g) add_shares(acc, v[g]);
-    }
+    for (int g = 0; g < DS_G; ++g) add_shares(acc, v[g]);
   }
-#else
-  uint4 v0[DS_G], v1[DS_G];
-  uint32_t idc = ld_ids(0), idn = ld_ids(1);
-  if (nb) issue(v0, 0, idc);
-  for (uint32_t t = 0; t < nb; t += 2) {
-    // batch t + 1
-    if constexpr (BE == 32) {
-      idc = idn;
-      idn = ld_ids(t + 2);
-    }
-    if (t + 1 < nb) issue(v1, t + 1, idc);
-#pragma unroll
-    for (int g = 0; g < DS_G; ++g) add_shares(acc, v0[g]);
-    // batch t + 2
-    idc = idn;
-    idn = ld_ids(BE == 32 ? t + 3 : t / 2 + 2);
-    if (t + 2 < nb) issue(v0, t + 2, idc);
-    if (t + 1 < nb)
-#pragma unroll
-      for (int g = 0; g < DS_G; ++g) add_shares(acc, v1[g]);
-  }
-#endif
 #pragma unroll
   for (int q = 0; q < 8; ++q)
 #pragma unroll
@@ -263,14 +214,16 @@ __device__ __forceinline__ void warp_sum(const DeltaParams& P, const DRow<K>& X,
 // (push.cpp:182-193) in the share format, write this sweep's shares.
 // acc: raw share sums. slot: the lane group's pushed-mass array.
 template <int K>
-__device__ __forceinline__ void decide8(const DeltaParams& P, DeltaSh<K>& S, uint4* dcur,
-                                        uint32_t u, uint32_t dg, double inv,
-                                        const double (&acc)[8], int kc, int slot) {
+__device__ __noinline__ void decide8(const DeltaParams& P, DeltaSh<K>& S, uint4* dcur, uint32_t u,
+                                     uint32_t dg, double inv, double a0, double a1, double a2,
+                                     double a3, double a4, double a5, double a6, double a7, int kc,
+                                     int slot) {
+  const double acc[8] = {a0, a1, a2, a3, a4, a5, a6, a7};
   const uint64_t ix = (uint64_t)u * K + kc * 8;
-  const dbl4 ra = ld_state4(P.r + ix), rb = ld_state4(P.r + ix + 4);
+  const dbl4 ra = ld_rowstate4(P.r + ix), rb = ld_rowstate4(P.r + ix + 4);
   // (x too, before any decision: one memory latency per row instead of two; nearly
   // every visited row pushes in some column)
-  const dbl4 xa = ld_state4(P.x + ix), xb = ld_state4(P.x + ix + 4);
+  const dbl4 xa = ld_rowstate4(P.x + ix), xb = ld_rowstate4(P.x + ix + 4);
   double rr[8];
   const double up = ldexp(1.0, DS_EXP);
   bool chg = false;
@@ -338,217 +291,188 @@ __device__ __forceinline__ void decide8(const DeltaParams& P, DeltaSh<K>& S, uin
   if (dg) dcur[(uint64_t)(2u * u) * (K / 8) + kc] = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// One row-aligned tile: short rows by lane groups (ES rows per warp pass),
-// medium rows by warps, long rows by the block. cnt = this tile's counters
-// {rowctr, medctr, nmed, nlong} (the caller alternates two sets, so no barrier
-// is spent on resetting them).
+// One warp task (a TileDesc of the warp-task plan): a bundle of <= 32 whole
+// rows with <= DS_TASK_E in-edges, or one whole longer row, or one piece of a
+// row cut into DS_PIECE-edge pieces. No block barrier anywhere: lane i holds
+// bundle row i's data (offsets, node, degree) and hands it out by shuffle;
+// rows of <= DS_SHORT in-edges run ES at a time in lane groups, longer ones one
+// at a time over the whole warp; pieces leave raw partial sums in hub_acc and
+// the last piece to arrive decides the row.
 template <int K>
-__device__ __forceinline__ void delta_tile(const DeltaParams& P, DeltaSh<K>& S, const TileDesc& d,
-                                           const DRow<K>& X, uint4* dcur, uint32_t* cnt) {
+__device__ __forceinline__ void delta_task(const DeltaParams& P, DeltaSh<K>& S, const TileDesc& d,
+                                           uint64_t j, const DRow<K>& X, uint4* dcur) {
   constexpr int LPR = K / 8, ES = 32 / LPR;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int kc = lane % LPR, es = lane / LPR;
-  const uint32_t nr = d.nr;
-  for (uint32_t t = tid; t <= nr; t += DS_NT) S.soff[t] = __ldg(P.in_off + d.r0 + t);
-  for (uint32_t t = tid; t < nr; t += DS_NT) {
-    S.snode[t] = __ldg(P.crow + d.r0 + t);
-    S.sdeg[t] = __ldg(P.cdeg + d.r0 + t);
-    S.sinv[t] = __ldg(P.cinv + d.r0 + t);
-    const uint64_t len = __ldg(P.in_off + d.r0 + t + 1) - __ldg(P.in_off + d.r0 + t);
-    if (len > DS_LONG) S.slong[atomicAdd(&cnt[3], 1u)] = t;
-    else if (len > DS_SHORT) S.smed[atomicAdd(&cnt[2], 1u)] = t;
+  // the task's in-edge ids into shared memory, every load in flight at once
+  uint32_t* ids = S.sids[warp];
+#pragma unroll 4
+  for (uint32_t i = lane; i < d.ne; i += 32) {
+    const uint32_t id = ld_stream(P.in_nbr + d.e0 + i);
+    ids[i] = id;
+#if PPRG_DS_PFROWS
+    prefetch_l2(X.at(id));  // its share row on the way into L2
+#endif
   }
-  __syncthreads();  // (also hands over the wave wait of thread 0)
-  // ---- short rows ----------------------------------------------------------
-  // Groups of ES rows are taken one ahead: the next group's first in-edge ids
-  // are loaded and its state rows prefetched into L2 before this group's
-  // gathers, so a group costs one exposed memory latency (the gathers).
-  auto grab = [&]() -> uint32_t {
-    uint32_t g0 = 0;
-    if (lane == 0) g0 = atomicAdd(&cnt[0], (uint32_t)ES);
-    return __shfl_sync(0xffffffffu, g0, 0);
-  };
-  auto prep = [&](uint32_t g0, uint64_t& b, uint32_t& len) -> uint32_t {
-    b = 0;
-    len = 0;
-    const uint32_t rr = g0 + es;
-    if (rr < nr) {
-      b = S.soff[rr];
-      const uint64_t l = S.soff[rr + 1] - b;
-      len = l <= DS_SHORT ? (uint32_t)l : 0u;
+  __syncwarp();
+  if (d.npieces > 1) {  // ---- a piece of a hub row ------------------------------
+    double acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+    warp_sum<K>(X, ids, d.ne, acc);
+    if (es == 0)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) P.hub_acc[j * K + kc * 8 + q] = acc[q];
+    __syncwarp();
+    unsigned old = 0;
+    if (lane == 0) {
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                   : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
+      if (old == d.npieces - 1) P.hub_cnt[d.hub] = 0;
     }
-    if (!len) return 0u;
-    const uint64_t ix = (uint64_t)S.snode[rr] * K + kc * 8;
-    prefetch_l2(P.r + ix);
-    prefetch_l2(P.x + ix);
-    return (uint32_t)kc < len ? ld_stream(P.in_nbr + b + kc) : 0u;
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old != d.npieces - 1) return;
+    __syncwarp();
+    if (es == 0) {
+      const double* part = P.hub_acc + (j - d.piece) * K + kc * 8;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        double t = 0.0;
+        for (uint32_t p = 0; p < d.npieces; ++p) t += __ldcg(part + (uint64_t)p * K + q);
+        acc[q] = t;
+      }
+      decide8<K>(P, S, dcur, __ldg(P.crow + d.r0), __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0),
+                 acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], kc, warp * ES);
+    }
+    return;
+  }
+  // ---- whole rows: lane i holds row i --------------------------------------
+  uint32_t loff = 0, llen = 0, lnode = 0, ldeg = 0;
+  double linv = 0.0;
+  if ((uint32_t)lane < d.nr) {
+    const uint64_t o = __ldg(P.in_off + d.r0 + lane);
+    loff = (uint32_t)(o - d.e0);
+    llen = (uint32_t)(__ldg(P.in_off + d.r0 + lane + 1) - o);
+    lnode = __ldg(P.crow + d.r0 + lane);
+    ldeg = __ldg(P.cdeg + d.r0 + lane);
+    linv = __ldg(P.cinv + d.r0 + lane);
+  }
+  const unsigned longm = __ballot_sync(0xffffffffu, llen > DS_SHORT);
+  // short rows, ES per pass; the next pass's first in-edge ids are loaded and its
+  // state rows prefetched into L2 before this pass's gathers
+  auto prep = [&](uint32_t g0, uint32_t& off, uint32_t& len, uint32_t& node) {
+    const int srcl = (int)(g0 + es) & 31;
+    off = __shfl_sync(0xffffffffu, loff, srcl);
+    len = __shfl_sync(0xffffffffu, llen, srcl);
+    node = __shfl_sync(0xffffffffu, lnode, srcl);
+    if (g0 + es >= d.nr || len > DS_SHORT) len = 0;
+    if (!len) return;
+    const uint64_t ix = (uint64_t)node * K + kc * 8;
+    prefetch_state(P.r + ix);
+    prefetch_state(P.x + ix);
   };
-  {
-    uint32_t g0 = grab();
-    uint64_t b;
-    uint32_t len;
-    uint32_t ids = prep(g0, b, len);
-    while (g0 < nr) {
-      const uint32_t gn = grab();
-      uint64_t bn;
-      uint32_t lenn;
-      const uint32_t idsn = prep(gn, bn, lenn);
+  if (d.nr > 1 || !longm) {
+    uint32_t off, len, node;
+    prep(0, off, len, node);
+    for (uint32_t g0 = 0; g0 < d.nr; g0 += ES) {
+      uint32_t offn = 0, lenn = 0, noden = 0;
+      if (g0 + ES < d.nr) prep(g0 + ES, offn, lenn, noden);
       const uint32_t maxlen = __reduce_max_sync(0xffffffffu, len);
       if (maxlen) {
         double acc[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-        group_sum<K>(P, X, b, len, maxlen, ids, acc);
-        const uint32_t rr = g0 + es;
-        if (len) decide8<K>(P, S, dcur, S.snode[rr], S.sdeg[rr], S.sinv[rr], acc, kc, warp * ES + es);
+        group_sum<K>(X, ids + off, len, maxlen, acc);
+        const int srcl = (int)(g0 + es) & 31;
+        const uint32_t dg = __shfl_sync(0xffffffffu, ldeg, srcl);
+        const double inv = __shfl_sync(0xffffffffu, linv, srcl);
+        if (len)
+          decide8<K>(P, S, dcur, node, dg, inv, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5],
+                     acc[6], acc[7], kc, warp * ES + es);
       }
-      g0 = gn;
-      b = bn;
+      off = offn;
       len = lenn;
-      ids = idsn;
+      node = noden;
     }
   }
-  // ---- medium rows: one warp per row -----------------------------------------
-  for (;;) {
-    uint32_t i = 0;
-    if (lane == 0) i = atomicAdd(&cnt[1], 1u);
-    i = __shfl_sync(0xffffffffu, i, 0);
-    if (i >= cnt[2]) break;
-    const uint32_t rr = S.smed[i];
+  // longer rows, one at a time over the whole warp
+  for (unsigned m = longm; m; m &= m - 1) {
+    const int rl = __ffs(m) - 1;
+    const uint32_t off = __shfl_sync(0xffffffffu, loff, rl);
+    const uint32_t len = __shfl_sync(0xffffffffu, llen, rl);
+    const uint32_t node = __shfl_sync(0xffffffffu, lnode, rl);
+    const uint32_t dg = __shfl_sync(0xffffffffu, ldeg, rl);
+    const double inv = __shfl_sync(0xffffffffu, linv, rl);
     if (es == 0) {
-      const uint64_t ix = (uint64_t)S.snode[rr] * K + kc * 8;
-      prefetch_l2(P.r + ix);
-      prefetch_l2(P.x + ix);
+      const uint64_t ix = (uint64_t)node * K + kc * 8;
+      prefetch_state(P.r + ix);
+      prefetch_state(P.x + ix);
     }
     double acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    warp_sum<K>(P, X, S.soff[rr], S.soff[rr + 1], acc);
-    if (es == 0) decide8<K>(P, S, dcur, S.snode[rr], S.sdeg[rr], S.sinv[rr], acc, kc, warp * ES);
-  }
-  // ---- long rows: all warps split the edges ---------------------------------
-  const uint32_t nl = cnt[3];
-  for (uint32_t li = 0; li < nl; ++li) {
-    const uint32_t rr = S.slong[li];
-    const uint64_t b = S.soff[rr], e = S.soff[rr + 1];
-    const uint64_t chunk = ((e - b) + DS_NW - 1) / DS_NW;
-    const uint64_t wb = b + warp * chunk, we = wb + chunk < e ? wb + chunk : e;
-    if (warp == 0 && es == 0) {
-      const uint64_t ix = (uint64_t)S.snode[rr] * K + kc * 8;
-      prefetch_l2(P.r + ix);
-      prefetch_l2(P.x + ix);
-    }
-    double acc[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-    warp_sum<K>(P, X, wb < e ? wb : e, we, acc);
+    warp_sum<K>(X, ids + off, len, acc);
     if (es == 0)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) S.spart[warp][kc * 8 + q] = acc[q];
-    __syncthreads();
-    if (warp == 0 && es == 0) {
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        double t = 0.0;
-        for (int w = 0; w < DS_NW; ++w) t += S.spart[w][kc * 8 + q];
-        acc[q] = t;
-      }
-      decide8<K>(P, S, dcur, S.snode[rr], S.sdeg[rr], S.sinv[rr], acc, kc, 0);
-    }
-    __syncthreads();
+      decide8<K>(P, S, dcur, node, dg, inv, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6],
+                 acc[7], kc, warp * ES);
   }
 }
 
-// One piece of a hub row (more in-edges than a tile): raw partial sums per
-// piece, the last piece to arrive adds them in piece order and decides.
-template <int K>
-__device__ __forceinline__ void delta_hub_piece(const DeltaParams& P, DeltaSh<K>& S,
-                                                const TileDesc& d, uint64_t j, const DRow<K>& X,
-                                                uint4* dcur) {
-  constexpr int LPR = K / 8;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int kc = lane % LPR, es = lane / LPR;
-  const uint64_t chunk = ((uint64_t)d.ne + DS_NW - 1) / DS_NW;
-  const uint64_t b = d.e0 + (uint64_t)warp * chunk, e0 = d.e0 + d.ne;
-  const uint64_t e = b + chunk < e0 ? b + chunk : e0;
-  double acc[8];
-#pragma unroll
-  for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-  warp_sum<K>(P, X, b < e ? b : e, e, acc);
-  if (es == 0)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) S.spart[warp][kc * 8 + q] = acc[q];
-  __syncthreads();
-  if (tid < K) {
-    double t = 0.0;
-    for (int w = 0; w < DS_NW; ++w) t += S.spart[w][tid];
-    P.hub_acc[j * K + tid] = t;
+// The in-edge ids and row data of a task this warp will run next, into L2.
+__device__ __forceinline__ void prefetch_task(const DeltaParams& P, const TileDesc& d) {
+  const uint32_t lane = threadIdx.x & 31;
+  if (lane < 16) {
+    if (lane * 32 < d.ne) prefetch_l2(P.in_nbr + d.e0 + lane * 32);
+  } else if (d.npieces == 1) {
+    const uint32_t l = lane - 16, last = d.nr - 1;
+    if (l < 3) prefetch_l2(P.in_off + d.r0 + (l * 16 < d.nr ? l * 16 : d.nr));
+    else if (l < 5) prefetch_l2(P.crow + d.r0 + (l == 3 ? 0 : last));
+    else if (l < 7) prefetch_l2(P.cdeg + d.r0 + (l == 5 ? 0 : last));
+    else if (l < 10) prefetch_l2(P.cinv + d.r0 + (l == 7 ? 0 : l == 8 ? (last < 16 ? last : 16) : last));
   }
-  __syncthreads();
-  if (tid == 0) {
-    unsigned old;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
-                 : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
-    S.flag = old == d.npieces - 1;
-    if (S.flag) P.hub_cnt[d.hub] = 0;
-  }
-  __syncthreads();
-  if (S.flag && warp == 0 && es == 0) {
-    const double* part = P.hub_acc + (j - d.piece) * K + kc * 8;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      double t = 0.0;
-      for (uint32_t p = 0; p < d.npieces; ++p) t += __ldcg(part + (uint64_t)p * K + q);
-      acc[q] = t;
-    }
-    decide8<K>(P, S, dcur, __ldg(P.crow + d.r0), __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0), acc,
-               kc, 0);
-  }
-  __syncthreads();
 }
 
 // Sources without in-edges are not rows of the compacted transpose: their only
-// inflow is the dead-end mass. Run with tile 0 (wave 0), one column per thread.
+// inflow is the dead-end mass. Run by the warp that takes task 0 (wave 0).
 template <int K>
 __device__ __forceinline__ void delta_source_rows(const DeltaParams& P, DeltaSh<K>& S,
                                                   uint4* dcur) {
-  const int c = threadIdx.x;
-  if (c < K) {
+  const int lane = threadIdx.x & 31;
+  for (int c = lane; c < K; c += 32) {
     const uint32_t u = S.csrc[c];
-    if (__ldg(P.in_off_full + u + 1) == __ldg(P.in_off_full + u)) {
-      const uint64_t ix = (uint64_t)u * K + c;
-      double rr = __ldcg(P.r + ix) + S.dd[c];
-      const uint32_t dg = __ldg(P.deg + u);
-      const double dthr = dg ? (double)dg : 1.0;
-      uint32_t h = 0;
-      if (rr > dthr * S.thr[(c / 8) * 10 + c % 8]) {
-        const double oma = 1.0 - P.alpha;
-        double rp = 0.0;
-        if (dg) {
-          h = (uint32_t)__double2hiint(rr * (oma * __ldg(P.inv_deg + u) * ldexp(1.0, -DS_EXP))) >> 12;
-          h = h > 0xFFFFu ? 0xFFFFu : h;
-          if (h < 256u) h = 0;
-          rp = fmin(share_value(h) * (dthr * P.inv_oma * ldexp(1.0, DS_EXP)), rr);
-        } else {
-          rp = rr;
-          atomicAdd(&S.dead[c], oma * rp);
-          atomicAdd(&S.nd[c], 1u);
-        }
-        if (rp > 0.0) {
-          P.x[ix] = __ldcg(P.x + ix) + rp;
-          rr -= rp;
-          atomicAdd(&S.pacc[0][c], rp);
-          atomicAdd(&S.nn[c], 1u);
-          atomicAdd(&S.np[c], dg ? dg : 1u);
-        }
+    if (__ldg(P.in_off_full + u + 1) != __ldg(P.in_off_full + u)) continue;
+    const uint64_t ix = (uint64_t)u * K + c;
+    double rr = __ldcg(P.r + ix) + S.dd[c];
+    const uint32_t dg = __ldg(P.deg + u);
+    const double dthr = dg ? (double)dg : 1.0;
+    uint32_t h = 0;
+    if (rr > dthr * S.thr[(c / 8) * 10 + c % 8]) {
+      const double oma = 1.0 - P.alpha;
+      double rp = 0.0;
+      if (dg) {
+        h = (uint32_t)__double2hiint(rr * (oma * __ldg(P.inv_deg + u) * ldexp(1.0, -DS_EXP))) >> 12;
+        h = h > 0xFFFFu ? 0xFFFFu : h;
+        if (h < 256u) h = 0;
+        rp = fmin(share_value(h) * (dthr * P.inv_oma * ldexp(1.0, DS_EXP)), rr);
+      } else {
+        rp = rr;
+        atomicAdd(&S.dead[c], oma * rp);
+        atomicAdd(&S.nd[c], 1u);
       }
-      P.r[ix] = rr;
-      // (other columns of this node's share row stay 0: it has no in-edges, so
-      // it holds residue only in the columns it is the source of)
-      reinterpret_cast<uint16_t*>(dcur)[2 * (uint64_t)u * K + c] = (uint16_t)h;
+      if (rp > 0.0) {
+        P.x[ix] = __ldcg(P.x + ix) + rp;
+        rr -= rp;
+        atomicAdd(&S.srcpush[c], rp);
+        atomicAdd(&S.nn[c], 1u);
+        atomicAdd(&S.np[c], dg ? dg : 1u);
+      }
     }
+    P.r[ix] = rr;
+    // (other columns of this node's share row stay 0: it has no in-edges, so
+    // it holds residue only in the columns it is the source of)
+    reinterpret_cast<uint16_t*>(dcur)[2 * (uint64_t)u * K + c] = (uint16_t)h;
   }
-  __syncthreads();
+  __syncwarp();
 }
 
 template <int K>
@@ -556,10 +480,9 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
   constexpr int LPR = K / 8, ES = 32 / LPR;
   extern __shared__ __align__(16) char ds_smem[];
   DeltaSh<K>& S = *reinterpret_cast<DeltaSh<K>*>(ds_smem);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
   SweepCtl* ctl = P.ctl;
   for (int i = tid; i < 64; i += DS_NT) S.bloom[i] = 0;
-  if (tid < 8) (&S.cnt[0][0])[tid] = 0;
   __syncthreads();
   if (tid < K) {
     const double rs = __ldcg(P.from_drain + tid);
@@ -585,13 +508,12 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
       int any = 0;
       for (int c = 0; c < K; ++c) any |= !S.done[c];
       S.any = any;
-      S.known = 0;
     }
-    if (tid < 8) (&S.cnt[0][0])[tid] = 0;
     for (int i = tid; i < DS_NW * ES * K; i += DS_NT) (&S.pacc[0][0])[i] = 0.0;
     if (tid < K) {
       S.thr[(tid / 8) * 10 + tid % 8] = S.done[tid] ? CUDART_INF : P.thr[S.epoch[tid]];
       S.dead[tid] = 0.0;
+      S.srcpush[tid] = 0.0;
       S.nn[tid] = S.np[tid] = S.nd[tid] = 0;
     }
     __syncthreads();
@@ -600,7 +522,6 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
       draining = true;
     }
     if (sweep >= P.max_sweeps) break;
-    if (tid == 0) S.tile[0] = atomicAdd(&ctl->ticket[buf], 1u);
     if (blockIdx.x == 0 && tid == 0) {
       const int nb = (sweep + 1) % 3;  // last read two barriers ago
       ctl->ticket[nb] = 0;
@@ -613,53 +534,57 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
         ctl->et[nb][c] = 0;
       }
     }
-    __syncthreads();
+    // ---- the sweep: every warp takes tasks in id order, two per ticket -----
     const uint32_t par = sweep & 1u;
     uint4* dcur = P.dsh + par * LPR;  // row u of this sweep: dcur[2 u LPR + kc]
-    uint32_t wave = 0;
-    unsigned long long j = S.tile[0];
-    for (uint32_t it = 0; j < P.ntiles; ++it) {
-      if (tid == 0) S.tile[(it + 1) & 1] = atomicAdd(&ctl->ticket[buf], 1u);
-      while (j >= P.wave_tile[wave + 1]) ++wave;
-      const TileDesc d = P.desc[j];
-      // every tile of the waves <= wave - lag must have finished (their shares
-      // are read from this sweep's buffer)
-      const uint32_t need = wave >= P.lag ? wave - P.lag + 1 : 0;
-      if (tid == 0) {
-        uint32_t kn = S.known;
-        if (kn < need) {
-          while (kn < need) {
-            const unsigned full = P.wave_tile[kn + 1] - P.wave_tile[kn];
-            while (ld_acquire32(&ctl->wdone[buf][kn]) < full) __nanosleep(100);
-            ++kn;
+    auto grab = [&]() -> unsigned long long {
+      unsigned t = 0;
+      if (lane == 0) t = atomicAdd(&ctl->ticket[buf], 2u);
+      return __shfl_sync(0xffffffffu, t, 0);
+    };
+    uint32_t wave = 0, known = 0;
+    unsigned long long base = grab();
+    while (base < P.ntiles) {
+      const unsigned long long nbase = grab();  // one ahead
+      if (nbase < P.ntiles) prefetch_l2(P.desc + nbase);
+      for (unsigned long long j = base; j < base + 2 && j < P.ntiles; ++j) {
+        const TileDesc d = P.desc[j];
+#if PPRG_DS_PFTASK
+        {  // the following task's ids and row data on their way into L2
+          const unsigned long long jn = (j == base && j + 1 < P.ntiles) ? j + 1 : nbase;
+          if (jn < P.ntiles) prefetch_task(P, P.desc[jn]);
+        }
+#endif
+        while (j >= P.wave_tile[wave + 1]) ++wave;
+        // every task of the waves <= wave - lag must have finished (their shares
+        // are read from this sweep's buffer)
+        const uint32_t need = wave >= P.lag ? wave - P.lag + 1 : 0;
+        if (known < need) {
+          if (lane == 0) {
+            for (uint32_t kn = known; kn < need; ++kn) {
+              const unsigned full = P.wave_tile[kn + 1] - P.wave_tile[kn];
+              while (ld_acquire32(&ctl->wdone[buf][kn]) < full) __nanosleep(100);
+            }
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
           }
+          __syncwarp();
+          known = need;
+        }
+        DRow<K> X{P.dsh + lane % LPR, need ? P.wave_node[need] : 0u, par};
+        if (j == 0) delta_source_rows<K>(P, S, dcur);
+        delta_task<K>(P, S, d, j, X, dcur);
+        __syncwarp();
+        if (lane == 0) {  // this task's shares are published
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          S.known = kn;
+          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->wdone[buf][wave]) : "memory");
         }
       }
-      if (tid < 4) S.cnt[(it + 1) & 1][tid] = 0;  // the next tile's counters
-      DRow<K> X{P.dsh + (tid & 31) % LPR, need ? P.wave_node[need] : 0u, par};
-      if (j == 0) {
-        __syncthreads();
-        delta_source_rows<K>(P, S, dcur);
-      }
-      if (d.npieces > 1) {
-        __syncthreads();
-        delta_hub_piece<K>(P, S, d, j, X, dcur);
-      } else {
-        delta_tile<K>(P, S, d, X, dcur, S.cnt[it & 1]);
-      }
-      __syncthreads();
-      if (tid == 0) {  // this tile's shares are published
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->wdone[buf][wave]) : "memory");
-      }
-      j = S.tile[(it + 1) & 1];
+      base = nbase;
     }
     __syncthreads();
     // flush the block's sums: lane-group arrays -> one value per column
     if (tid < K) {
-      double p = 0.0;
+      double p = S.srcpush[tid];
       for (int s = 0; s < DS_NW * ES; ++s) p += S.pacc[s][tid];
       if (p != 0.0) atomicAdd(&ctl->pushed[buf][tid], p);
       if (S.dead[tid] != 0.0) atomicAdd(&ctl->dsum[buf][tid], S.dead[tid]);

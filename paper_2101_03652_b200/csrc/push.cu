@@ -755,12 +755,20 @@ bool delta_on(const Graph& g, int K) {
   if (mode > 0) return true;
   return g.n * (uint64_t)K * 8 > (256ull << 20);
 }
-uint32_t ds_tile_edges() {
-  static const uint32_t v = [] {
-    const char* e = std::getenv("PPRG_DS_TILE");
-    const int t = e ? std::atoi(e) : 2048;
-    return (uint32_t)(t < 256 ? 256 : t);
-  }();
+// The warp-task plan of the delta sweeps: bundles of <= 32 whole rows and
+// <= PPRG_DS_TASK in-edges, longer rows whole up to PPRG_DS_PIECE in-edges,
+// beyond that in pieces.
+uint32_t ds_env(const char* name, int dflt, int lo) {
+  const char* e = std::getenv(name);
+  const int t = e ? std::atoi(e) : dflt;
+  return (uint32_t)(t < lo ? lo : t > (int)DS_IDS ? (int)DS_IDS : t);  // (a task's ids sit in shared memory)
+}
+uint32_t ds_task_edges() {
+  static const uint32_t v = ds_env("PPRG_DS_TASK", 256, 32);
+  return v;
+}
+uint32_t ds_piece_edges() {
+  static const uint32_t v = ds_env("PPRG_DS_PIECE", 512, 64);
   return v;
 }
 
@@ -790,11 +798,11 @@ void delta_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
   cudaStream_t st = qstream(g);
   const uint64_t nk = g.n * (uint64_t)b.K;
   const double m_eff = (double)g.m_eff();
-  const Graph::Plan& pl = g.tile_plan(ds_tile_edges(), DS_RMAX, ds_tile_edges());
+  const Graph::Plan& pl = g.tile_plan(ds_task_edges(), DS_TASK_R, std::max(ds_task_edges(), ds_piece_edges()));
   ws_tiles(w, g, pl.ntiles, pl.nhubs);
   static const uint32_t W = [] {
     const char* e = std::getenv("PPRG_DS_WAVES");
-    const int v = e ? std::atoi(e) : 32;
+    const int v = e ? std::atoi(e) : 16;
     return (uint32_t)(v < 1 ? 1 : v > DS_WMAX ? DS_WMAX : v);
   }();
   static const uint32_t L = [] {
