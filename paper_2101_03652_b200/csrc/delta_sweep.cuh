@@ -38,17 +38,23 @@ namespace pprg {
 
 constexpr int DS_NT = 128;
 constexpr int DS_NW = DS_NT / 32;
-constexpr int DS_G = 4;             // 16-byte row loads in flight per lane
+#ifndef PPRG_DS_G
+#define PPRG_DS_G 6
+#endif
+constexpr int DS_G = PPRG_DS_G;  // 16-byte row loads in flight per lane
 constexpr uint32_t DS_IDS = 512;    // in-edges per task at most
 constexpr uint32_t DS_TASK_R = 32;  // rows per task (lane i holds row i's data)
-constexpr uint32_t DS_SHORT = 32;   // rows up to this many in-edges: one lane group each
+#ifndef PPRG_DS_SHORT
+#define PPRG_DS_SHORT 64
+#endif
+constexpr uint32_t DS_SHORT = PPRG_DS_SHORT;  // rows up to this many in-edges: one lane group each
 constexpr int DS_WMAX = 64;         // waves per sweep
 constexpr int DS_EXP = 769;         // value(h) = fp64{h << 12, 0} * 2^769: e8m8 spans 2^-253 .. 4
 #ifndef PPRG_DS_PIPE
 #define PPRG_DS_PIPE 0  // 1: two batches of row loads in flight per lane (needs 4 blocks per SM: slower)
 #endif
 #ifndef PPRG_DS_PFROWS
-#define PPRG_DS_PFROWS 0
+#define PPRG_DS_PFROWS 1
 #endif
 #ifndef PPRG_DS_HALF
 #define PPRG_DS_HALF 0
@@ -133,18 +139,22 @@ struct DeltaSh {
   int done[K];
   uint32_t bloom[64];                  // 2048 bits: (node & 2047) of every source
   int any;
+  uint32_t known;                      // leading waves of this sweep known complete (by some warp)
 };
 
-// Gather operand of one tile. The two share buffers are interleaved by row
-// (row v of parity p at index 2 v + p), so the buffer choice is an index bit.
+// Gather operand of one task. The two share buffers are interleaved by row
+// (row v of parity p at index 2 v + p), so the buffer choice is an index bit;
+// the staged ids already carry it (row()), so a gather address is one multiply-add.
 template <int K>
 struct DRow {
   const uint4* base;  // shares + this lane's 16-byte column group
   uint32_t bound;     // ids below: published earlier in this sweep (parity par), others par ^ 1
   uint32_t par;
-  __device__ __forceinline__ const uint4* at(uint32_t id) const {
-    const uint32_t sel = id < bound ? par : par ^ 1u;
-    return base + (uint64_t)(2u * id + sel) * (K / 8);
+  __device__ __forceinline__ uint32_t row(uint32_t id) const {
+    return 2u * id + (id < bound ? par : par ^ 1u);
+  }
+  __device__ __forceinline__ const uint4* at(uint32_t row) const {
+    return base + (uint64_t)row * (K / 8);
   }
 };
 __device__ __forceinline__ void prefetch_l2(const void* p) {
@@ -308,10 +318,10 @@ __device__ __forceinline__ void delta_task(const DeltaParams& P, DeltaSh<K>& S, 
   uint32_t* ids = S.sids[warp];
 #pragma unroll 4
   for (uint32_t i = lane; i < d.ne; i += 32) {
-    const uint32_t id = ld_stream(P.in_nbr + d.e0 + i);
-    ids[i] = id;
+    const uint32_t row = X.row(ld_stream(P.in_nbr + d.e0 + i));
+    ids[i] = row;
 #if PPRG_DS_PFROWS
-    prefetch_l2(X.at(id));  // its share row on the way into L2
+    prefetch_l2(X.at(row));  // its share row on the way into L2
 #endif
   }
   __syncwarp();
@@ -326,24 +336,35 @@ __device__ __forceinline__ void delta_task(const DeltaParams& P, DeltaSh<K>& S, 
     __syncwarp();
     unsigned old = 0;
     if (lane == 0) {
-      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+      // (release only: an acquire invalidates the SM's L1, so only the last
+      // arriver, who reads the other pieces' partials, pays for one)
+      asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;"
                    : "=r"(old) : "l"(P.hub_cnt + d.hub) : "memory");
-      if (old == d.npieces - 1) P.hub_cnt[d.hub] = 0;
+      if (old == d.npieces - 1) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        P.hub_cnt[d.hub] = 0;
+      }
     }
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old != d.npieces - 1) return;
     __syncwarp();
-    if (es == 0) {
+    {  // the last piece to arrive: the partials of all pieces, lane groups taking every ES-th
       const double* part = P.hub_acc + (j - d.piece) * K + kc * 8;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        double t = 0.0;
-        for (uint32_t p = 0; p < d.npieces; ++p) t += __ldcg(part + (uint64_t)p * K + q);
-        acc[q] = t;
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      for (uint32_t p = es; p < d.npieces; p += ES) {
+        const dbl4 a = ld_state4(part + (uint64_t)p * K), b = ld_state4(part + (uint64_t)p * K + 4);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += a.v[q], acc[q + 4] += b.v[q];
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int o = LPR; o < 32; o <<= 1) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+    }
+    if (es == 0)
       decide8<K>(P, S, dcur, __ldg(P.crow + d.r0), __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0),
                  acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], kc, warp * ES);
-    }
     return;
   }
   // ---- whole rows: lane i holds row i --------------------------------------
@@ -508,6 +529,7 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
       int any = 0;
       for (int c = 0; c < K; ++c) any |= !S.done[c];
       S.any = any;
+      S.known = 0;
     }
     for (int i = tid; i < DS_NW * ES * K; i += DS_NT) (&S.pacc[0][0])[i] = 0.0;
     if (tid < K) {
@@ -542,7 +564,7 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
       if (lane == 0) t = atomicAdd(&ctl->ticket[buf], 2u);
       return __shfl_sync(0xffffffffu, t, 0);
     };
-    uint32_t wave = 0, known = 0;
+    uint32_t wave = 0, known = 0, pending = 0;
     unsigned long long base = grab();
     while (base < P.ntiles) {
       const unsigned long long nbase = grab();  // one ahead
@@ -560,12 +582,21 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
         // are read from this sweep's buffer)
         const uint32_t need = wave >= P.lag ? wave - P.lag + 1 : 0;
         if (known < need) {
+          // One acquire per block and wave (it invalidates the SM's L1): the
+          // first warp to need a wave waits for it and publishes it to the
+          // block's other warps through shared memory.
           if (lane == 0) {
-            for (uint32_t kn = known; kn < need; ++kn) {
-              const unsigned full = P.wave_tile[kn + 1] - P.wave_tile[kn];
-              while (ld_acquire32(&ctl->wdone[buf][kn]) < full) __nanosleep(100);
+            uint32_t kn = *(volatile uint32_t*)&S.known;
+            if (kn < need) {
+              for (; kn < need; ++kn) {
+                const unsigned full = P.wave_tile[kn + 1] - P.wave_tile[kn];
+                while (ld_acquire32(&ctl->wdone[buf][kn]) < full) __nanosleep(200);
+              }
+              __threadfence_block();
+              atomicMax(&S.known, need);
+            } else {
+              __threadfence_block();
             }
-            asm volatile("fence.acq_rel.gpu;" ::: "memory");
           }
           __syncwarp();
           known = need;
@@ -573,10 +604,15 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
         DRow<K> X{P.dsh + lane % LPR, need ? P.wave_node[need] : 0u, par};
         if (j == 0) delta_source_rows<K>(P, S, dcur);
         delta_task<K>(P, S, d, j, X, dcur);
-        __syncwarp();
-        if (lane == 0) {  // this task's shares are published
-          asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(&ctl->wdone[buf][wave]) : "memory");
+        // this task's shares are published: signalled once per pair of tasks (or
+        // when the wave changes in between)
+        const bool last = j + 1 >= base + 2 || j + 1 >= P.ntiles;
+        ++pending;
+        if (last || j + 1 >= P.wave_tile[wave + 1]) {
+          __syncwarp();
+          if (lane == 0)  // (a release, not a fence: no L1 invalidation on the publishing side)
+            asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&ctl->wdone[buf][wave]), "r"(pending) : "memory");
+          pending = 0;
         }
       }
       base = nbase;

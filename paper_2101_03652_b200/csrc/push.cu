@@ -746,10 +746,8 @@ void check_final(const SweepCtl& fc) {
 // PPRG_DELTA: 0 = never, 1 = every eligible block, unset = blocks whose gather
 // operand y (n x K x 8 B) is beyond twice the L2.
 bool delta_on(const Graph& g, int K) {
-  static const int mode = [] {
-    const char* e = std::getenv("PPRG_DELTA");
-    return e ? std::atoi(e) : -1;
-  }();
+  const char* e = std::getenv("PPRG_DELTA");  // (read per call: tests switch it)
+  const int mode = e ? std::atoi(e) : -1;
   if (K < 32 || mode == 0 || t_det) return false;
   if (g.m_eff() >= (1ull << 32) || g.n >= (1ull << 31) || g.n_rows == 0) return false;
   if (mode > 0) return true;
@@ -802,12 +800,12 @@ void delta_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
   ws_tiles(w, g, pl.ntiles, pl.nhubs);
   static const uint32_t W = [] {
     const char* e = std::getenv("PPRG_DS_WAVES");
-    const int v = e ? std::atoi(e) : 16;
+    const int v = e ? std::atoi(e) : 64;
     return (uint32_t)(v < 1 ? 1 : v > DS_WMAX ? DS_WMAX : v);
   }();
   static const uint32_t L = [] {
     const char* e = std::getenv("PPRG_DS_LAG");
-    const int v = e ? std::atoi(e) : 2;
+    const int v = e ? std::atoi(e) : 6;
     return (uint32_t)(v < 1 ? 1 : v);
   }();
   if (w.dw_plan != &pl || w.dw_waves != W) {
