@@ -205,6 +205,12 @@ int pprg_ipc_close(int device, void* ptr);
 /* Columns (sources) per device block for a k-source call: the batch width the
  * engines use (a power of two, padding columns inert). Not in the reference. */
 int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out);
+/* Which kernel runs the global phase (push.cpp:168-197) of an unobserved
+ * k-source power_push call on this graph: *out = 1 for the delta sweeps
+ * (k_dsweeps: explicit residues, 16-bit per-sweep shares; wide blocks whose
+ * gather operand is far beyond L2, or PPRG_DELTA=1), 0 for k_sweeps (cumulative
+ * y rows). Results obey the same bounds either way. Not in the reference. */
+int pprg_uses_delta_sweeps(const pprg_graph* g, uint32_t k, int* out);
 
 /* One high-precision query with its progress series: the reference's
  * run_high_precision + CheckpointRecorder (sweep.cpp:25-61), recorded at

@@ -112,6 +112,7 @@ def load_library(path: str = lib_path):
                               vp]
     L.pprg_ground_truth.argtypes = [vp, vp, C.c_uint32, C.c_double, vp, C.c_uint32, vp, vp]
     L.pprg_block_columns.argtypes = [vp, C.c_uint32, C.POINTER(C.c_uint32)]
+    L.pprg_uses_delta_sweeps.argtypes = [vp, C.c_uint32, C.POINTER(C.c_int)]
     L.pprg_index_build.argtypes = [vp, C.c_double, C.c_uint64, C.POINTER(vp)]
     L.pprg_index_from_host.argtypes = [vp, C.c_double, C.c_uint64, vp, C.POINTER(vp)]
     L.pprg_index_export.argtypes = [vp, vp]
@@ -305,6 +306,12 @@ class Graph:
         out = C.c_uint32()
         _check(load_library().pprg_block_columns(self.handle, k, C.byref(out)))
         return out.value
+
+    def uses_delta_sweeps(self, k: int) -> bool:
+        """True if a k-source power_push call runs its global phase as delta sweeps."""
+        out = C.c_int()
+        _check(load_library().pprg_uses_delta_sweeps(self.handle, k, C.byref(out)))
+        return bool(out.value)
 
     def out_degree(self, v: int) -> int:
         off = self.out_offsets()

@@ -608,6 +608,13 @@ int pprg_block_columns(const pprg_graph* g, uint32_t k, uint32_t* out) {
   });
 }
 
+int pprg_uses_delta_sweeps(const pprg_graph* g, uint32_t k, int* out) {
+  return guard([&] {
+    require(g != nullptr && out != nullptr, "delta sweeps: null argument");
+    *out = pprg::delta_block(*g->g, k) ? 1 : 0;
+  });
+}
+
 int pprg_walk_budget(uint64_t n, double epsilon, double mu, uint64_t* out) {
   return guard([&] {
     // walk_budget_real, speedppr.cpp:8-14 (same checks)

@@ -153,6 +153,7 @@ struct PushView {
   std::vector<uint32_t> src;
 };
 uint32_t block_width(uint64_t n, uint32_t k);
+bool delta_block(Graph& g, uint32_t k);  // the global phase of a k-source block runs as delta sweeps
 void refine_state(Graph& g, const uint32_t* sources, uint32_t k, double alpha, double r_max,
                   double* reserve, double* residue, bool on_device, ColumnStats* cols,
                   CallStats* call);  // padded columns per block for k queries

@@ -1329,6 +1329,10 @@ uint32_t block_columns(uint64_t n, uint32_t k) {
 }
 
 uint32_t block_width(uint64_t n, uint32_t k) { return (uint32_t)round_k(block_columns(n, k)); }
+bool delta_block(Graph& g, uint32_t k) {
+  g.ensure_transpose();
+  return delta_on(g, (int)block_width(g.n, k));
+}
 
 void run_push_engine(Graph& g, Engine eng, const uint32_t* sources, uint32_t k, double alpha,
                      double lambda, uint32_t epoch_num, int64_t scan_threshold, double r_max_fifo,

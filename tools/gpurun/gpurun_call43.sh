@@ -1,0 +1,6 @@
+run() { tag=$1; shift; env "$@" timeout 300 python tools/ab_quick.py 2 > gpurun_out/c43_$tag.json 2>&1; echo "$tag $(tail -1 gpurun_out/c43_$tag.json | python -c "
+import sys,json
+d=json.loads(sys.stdin.read())['configs[2] 64-block']; print(round(d['sweep_ms'],1), d['max_sweeps'], round(d['sweep_ms']/d['max_sweeps'],3))")"; }
+run base
+for v in minb6 minb6g4; do run $v PPRG_LIB=$PWD/libv_$v/libpprg.so; done
+echo k32; PPRG_DELTA=0 python tools/k32_probe.py | tail -1; python tools/k32_probe.py | tail -1

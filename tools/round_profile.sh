@@ -9,6 +9,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${tag}.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
   --e2e-steps 1 > gpurun_out/launches_${tag}.log 2>&1
 echo "launches rc=$?"
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_sweeps -c 1 \
+timeout 900 ncu --set full --import-source on --clock-control none -k "regex:k_dsweeps|k_sweeps" -c 1 \
   -o gpurun_out/sweep_${tag} python tools/profile_one.py --queries 64 > gpurun_out/sweep_${tag}.log 2>&1
 echo "ncu rc=$?"
