@@ -90,6 +90,8 @@ struct DeltaParams {
   uint4* dsh;               // [n][2][K] u16 shares: row v of sweep parity p at 2 v + p
   const double* from_drain; // exact r_sum after the local phase
   double scan_lambda;
+  int scan_all;                   // refine epoch appended: every live column runs the sweeps
+  unsigned long long handoff_np;  // refine epoch: hand off to the frontier below this many edge pushes
   SweepCtl* ctl;
   uint32_t max_sweeps;
   uint32_t nwaves, lag;
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
   __syncthreads();
   if (tid < K) {
     const double rs = __ldcg(P.from_drain + tid);
-    const int scan = tid < P.k_live && rs > P.scan_lambda;  // push.cpp:168
+    const int scan = tid < P.k_live && (P.scan_all || rs > P.scan_lambda);  // push.cpp:168
     int ep = 0;
     while (ep < P.E && !(rs > P.lam[ep])) ++ep;
     S.r_sum[tid] = rs;
@@ -638,6 +640,7 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
         S.pushes[tid] += np;
         S.r_sum[tid] -= P.alpha * pushed;
         if (np == 0) S.epoch[tid] += 1;  // fixpoint: nothing active at this threshold
+        else if (S.epoch[tid] == P.E - 1 && np < P.handoff_np) S.epoch[tid] += 1;  // refine tail
         while (S.epoch[tid] < P.E && !(S.r_sum[tid] > P.lam[S.epoch[tid]])) S.epoch[tid] += 1;
         if (S.epoch[tid] >= P.E) S.done[tid] = 1;
       }

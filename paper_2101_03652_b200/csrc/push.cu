@@ -753,6 +753,16 @@ bool delta_on(const Graph& g, int K) {
   if (mode > 0) return true;
   return g.n * (uint64_t)K * 8 > (256ull << 20);
 }
+// SpeedPPR's push stage (a refine epoch appended) as delta sweeps: opt-in
+// (PPRG_DELTA_REFINE=1). Measured on configs[3]: the sweeps get cheaper (1.04
+// vs 1.35 ms per query) but their lagged fixpoint leaves the frontier tail more
+// work (1.30 vs 0.37 ms); handing off 4x later evens it out (2.15 ms per query
+// either way), so the refine stage stays on k_sweeps.
+bool delta_refine() {
+  const char* e = std::getenv("PPRG_DELTA_REFINE");
+  return e && std::atoi(e) != 0;
+}
+
 // The warp-task plan of the delta sweeps: bundles of <= 32 whole rows and
 // <= PPRG_DS_TASK in-edges, longer rows whole up to PPRG_DS_PIECE in-edges,
 // beyond that in pieces.
@@ -790,7 +800,7 @@ void launch_dsweeps(Graph& g, DeltaParams& P) {
 
 // The global phase of a device-started block as delta sweeps: explicit
 // residues (w.res, left by the local phase), 16-bit shares in w.y0.
-void delta_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
+void delta_phase(Block& b, double lambda, uint32_t E, CallStats* call, double refine_rmax) {
   Graph& g = b.g;
   Workspace& w = b.w;
   cudaStream_t st = qstream(g);
@@ -846,7 +856,7 @@ void delta_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
   P.hub_acc = w.hub_acc.get();
   P.hub_cnt = w.hub_cnt.get();
   P.k_live = (int)b.k;
-  P.E = (int)E;
+  P.E = (int)E + (refine_rmax > 0.0);
   P.alpha = b.alpha;
   P.inv_oma = 1.0 / (1.0 - b.alpha);
   P.x = w.x.get();
@@ -868,6 +878,14 @@ void delta_phase(Block& b, double lambda, uint32_t E, CallStats* call) {
     const double el = std::pow(lambda, static_cast<double>(e + 1) / E);  // push.cpp:176-178
     P.lam[e] = stop_lambda(el, e, E);
     P.thr[e] = el / m_eff;
+  }
+  if (refine_rmax > 0.0) {  // the refine epoch of global_phase (push.cpp:208-222), same hand-off
+    P.lam[E] = -1.0;
+    P.thr[E] = refine_rmax;
+    double f = 1.0 / 128;
+    if (const char* e = std::getenv("PPRG_REFINE_HANDOFF")) f = std::atof(e);
+    P.handoff_np = (unsigned long long)(f * m_eff);
+    P.scan_all = 1;
   }
   PPRG_CUDA(cudaMemsetAsync(w.y0.get(), 0, 4 * nk, st));  // both share buffers
   PPRG_CUDA(cudaMemsetAsync(w.ctl(), 0, sizeof(SweepCtl), st));
@@ -895,8 +913,8 @@ void global_phase(Block& b, double lambda, uint32_t E, CallStats* call, double r
   const uint64_t nk = g.n * (uint64_t)b.K;
   const double m_eff = (double)g.m_eff();
   if (E + (refine_rmax > 0.0) > EMAX) fail(EINVAL_, "epoch_num exceeds 64");
-  if (defer && refine_rmax == 0.0 && delta_on(g, b.K)) {
-    delta_phase(b, lambda, E, call);
+  if (defer && delta_on(g, b.K) && (refine_rmax == 0.0 || delta_refine())) {
+    delta_phase(b, lambda, E, call, refine_rmax);
     return;
   }
   PPRG_CUDA(cudaMemsetAsync(w.dcols.get() + 2 * KMAX, 0, 8 * KMAX, st));
