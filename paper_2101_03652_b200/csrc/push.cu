@@ -1233,7 +1233,19 @@ void power_push_block(Block& b, double lambda, uint32_t epoch_num, int64_t scan_
   PPRG_CUDA(cudaMemsetAsync(b.w.res.get(), 0, 8 * nk, st));
   k_seed<<<1, KMAX, 0, st>>>(b.w.res.get(), b.w.d_src.get(), b.K, 1.0);
   const double r_max = lambda / m_eff;  // push.cpp:157-160
-  const uint64_t limit = scan_threshold < 0 ? b.g.n / 4 : (uint64_t)scan_threshold;
+  // Default queue limit (push.cpp:161: n / 4). Blocks whose global phase runs as
+  // delta sweeps switch at n / 128: a sweep costs them 2.3 ms per 64 sources, less
+  // than the frontier levels between a queue of n/128 and n/4 entries (configs[2]
+  // block: local phase 6.1 -> 1.35 ms, 50 sweeps either way; PPRG_DS_SCAN_DIV).
+  uint64_t limit = scan_threshold < 0 ? b.g.n / 4 : (uint64_t)scan_threshold;
+  if (scan_threshold < 0 && defer && refine_rmax == 0.0 && delta_on(b.g, b.K)) {
+    static const double div = [] {
+      const char* e = std::getenv("PPRG_DS_SCAN_DIV");
+      const double v = e ? std::atof(e) : 128.0;
+      return v >= 1.0 ? v : 1.0;
+    }();
+    limit = (uint64_t)((double)b.g.n / div);
+  }
   std::vector<int> state(KMAX, 2);
   for (uint32_t c = 0; c < b.k; ++c) state[c] = 0;
   if (defer) {
