@@ -148,16 +148,24 @@ template <int K>
 struct DeltaSh {
   static constexpr int LPR = K / 8;    // lanes per row (16 B = 8 columns each)
   static constexpr int ES = 32 / LPR;  // rows (lane groups) per warp instruction
-  double pacc[DS_NW * ES][K];          // pushed mass, one array per lane group (no atomics)
+  // Per-lane sums of a sweep, [warp][column-in-lane q][lane]: every lane owns its
+  // 8 entries (no atomics) and a warp's accesses for one q are 32 consecutive
+  // words (no bank conflicts; as [lane group][column] arrays the same adds were
+  // 16-way conflicted and, with the shared atomics of the counters, kept the LSU
+  // data pipe 67% busy). Column c = 8 kc + q of lane group es sits at lane es LPR + kc.
+  double pacc[DS_NW][8][32];           // pushed mass
+  double pdead[DS_NW][8][32];          // (1-a) x mass pushed by dead-end rows (to the source next sweep)
+  unsigned long long pcnt[DS_NW][8][32];  // node pushes << 40 | edge pushes
   uint32_t sids[DS_NW][DS_IDS];        // each warp's task: its in-edge ids
   double thr[LPR * 10];                // this sweep's thresholds, column c at (c/8)*10 + c%8
   double dd[K];                        // dead-end mass of the previous sweep (to the source)
-  double dead[K];                      // dead-end mass pushed in this sweep
   double srcpush[K];                   // mass pushed by sources without in-edges
   double r_sum[K];
   unsigned long long pushes[K];
   uint32_t csrc[K];
-  unsigned nn[K], np[K], nd[K];
+  unsigned nd[K];                      // dead-end pushes (rare enough for shared atomics)
+  double srcdead[K];                   // dead-end mass pushed by sources without in-edges
+  unsigned srcnn[K], srcnp[K];
   unsigned sweeps[K];
   int epoch[K];
   int done[K];
@@ -246,7 +254,8 @@ __device__ __forceinline__ void warp_sum(const DRow<K>& X, const uint32_t* ids, 
 // The decision for 8 columns [8 kc, 8 kc + 8) of row u by one lane: add the
 // gathered shares to the residues, push the columns above their threshold
 // (push.cpp:182-193) in the share format, write this sweep's shares.
-// acc: raw share sums. slot: the lane group's pushed-mass array.
+// acc: raw share sums. slot: the calling lane's index in its warp's sum planes
+// (lane group es, column group kc -> es LPR + kc), warp: its warp.
 template <int K>
 __device__ __noinline__ void decide8(const DeltaParams& P, DeltaSh<K>& S, uint4* dcur, uint32_t u,
                                      uint32_t dg, double inv, double a0, double a1, double a2,
@@ -286,7 +295,9 @@ __device__ __noinline__ void decide8(const DeltaParams& P, DeltaSh<K>& S, uint4*
     const double oma = 1.0 - P.alpha;
     const double c1 = oma * inv * ldexp(1.0, -DS_EXP);  // residue -> raw share
     const double c2 = dthr * P.inv_oma * up;            // raw share -> mass leaving the row
-    double* pa = &S.pacc[slot][kc * 8];
+    const int wp = threadIdx.x >> 5;
+    double* pa = &S.pacc[wp][0][slot];            // my column q at pa[32 q]
+    unsigned long long* pc = &S.pcnt[wp][0][slot];
     if (dg) {
       // the words first (an odd column's value depends on its even neighbour's field)
       uint32_t hf[8];
@@ -302,22 +313,20 @@ __device__ __noinline__ void decide8(const DeltaParams& P, DeltaSh<K>& S, uint4*
         const double rp = fmin(val * c2, rr[q]);
         xx[q] += rp;
         rr[q] -= rp;
-        pa[q] += rp;
-        atomicAdd(&S.nn[kc * 8 + q], 1u);
-        atomicAdd(&S.np[kc * 8 + q], dg);
+        pa[32 * q] += rp;
+        pc[32 * q] += (1ull << 40) | dg;
       }
     } else {  // dead end: everything leaves, (1-a) of it to the source next sweep
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         if (!((pm >> q) & 1u)) continue;
         const double rp = rr[q];
-        atomicAdd(&S.dead[kc * 8 + q], oma * rp);
+        S.pdead[wp][q][slot] += oma * rp;
         atomicAdd(&S.nd[kc * 8 + q], 1u);
         xx[q] += rp;
         rr[q] -= rp;
-        pa[q] += rp;
-        atomicAdd(&S.nn[kc * 8 + q], 1u);
-        atomicAdd(&S.np[kc * 8 + q], 1u);
+        pa[32 * q] += rp;
+        pc[32 * q] += (1ull << 40) | 1ull;
       }
     }
     dbl4 oa, ob;
@@ -400,7 +409,7 @@ __device__ __forceinline__ void delta_task(const DeltaParams& P, DeltaSh<K>& S, 
     }
     if (es == 0)
       decide8<K>(P, S, dcur, __ldg(P.crow + d.r0), __ldg(P.cdeg + d.r0), __ldg(P.cinv + d.r0),
-                 acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], kc, warp * ES);
+                 acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6], acc[7], kc, lane);
     return;
   }
   // ---- whole rows: lane i holds row i --------------------------------------
@@ -445,7 +454,7 @@ __device__ __forceinline__ void delta_task(const DeltaParams& P, DeltaSh<K>& S, 
         const double inv = __shfl_sync(0xffffffffu, linv, srcl);
         if (len)
           decide8<K>(P, S, dcur, node, dg, inv, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5],
-                     acc[6], acc[7], kc, warp * ES + es);
+                     acc[6], acc[7], kc, lane);
       }
       off = offn;
       len = lenn;
@@ -471,7 +480,7 @@ __device__ __forceinline__ void delta_task(const DeltaParams& P, DeltaSh<K>& S, 
     warp_sum<K>(X, ids + off, len, acc);
     if (es == 0)
       decide8<K>(P, S, dcur, node, dg, inv, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], acc[6],
-                 acc[7], kc, warp * ES);
+                 acc[7], kc, lane);
   }
 }
 
@@ -521,7 +530,7 @@ __device__ __forceinline__ void delta_source_rows(const DeltaParams& P, DeltaSh<
         rp = h ? fmin(val * (dthr * P.inv_oma * ldexp(1.0, DS_EXP)), rr) : 0.0;
       } else {
         rp = rr;
-        atomicAdd(&S.dead[c], oma * rp);
+        atomicAdd(&S.srcdead[c], oma * rp);
         atomicAdd(&S.nd[c], 1u);
       }
     }
@@ -530,8 +539,8 @@ __device__ __forceinline__ void delta_source_rows(const DeltaParams& P, DeltaSh<
       P.x[ix] = __ldcg(P.x + ix) + rp;
       rr -= rp;
       atomicAdd(&S.srcpush[c], rp);
-      atomicAdd(&S.nn[c], 1u);
-      atomicAdd(&S.np[c], dg ? dg : 1u);
+      atomicAdd(&S.srcnn[c], 1u);
+      atomicAdd(&S.srcnp[c], dg ? dg : 1u);
     }
     if (on) P.r[ix] = rr;
     // (other columns of this node's share row stay 0: it has no in-edges, so
@@ -576,12 +585,16 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
       S.any = any;
       S.known = 0;
     }
-    for (int i = tid; i < DS_NW * ES * K; i += DS_NT) (&S.pacc[0][0])[i] = 0.0;
+    for (int i = tid; i < DS_NW * 8 * 32; i += DS_NT) {
+      (&S.pacc[0][0][0])[i] = 0.0;
+      (&S.pdead[0][0][0])[i] = 0.0;
+      (&S.pcnt[0][0][0])[i] = 0ull;
+    }
     if (tid < K) {
       S.thr[(tid / 8) * 10 + tid % 8] = S.done[tid] ? CUDART_INF : P.thr[S.epoch[tid]];
-      S.dead[tid] = 0.0;
+      S.srcdead[tid] = 0.0;
       S.srcpush[tid] = 0.0;
-      S.nn[tid] = S.np[tid] = S.nd[tid] = 0;
+      S.srcnn[tid] = S.srcnp[tid] = S.nd[tid] = 0;
     }
     __syncthreads();
     if (!S.any) {
@@ -665,13 +678,22 @@ __global__ void __launch_bounds__(DS_NT, PPRG_DS_MINB) k_dsweeps(const __grid_co
     __syncthreads();
     // flush the block's sums: lane-group arrays -> one value per column
     if (tid < K) {
-      double p = S.srcpush[tid];
-      for (int s = 0; s < DS_NW * ES; ++s) p += S.pacc[s][tid];
+      double p = S.srcpush[tid], dm = S.srcdead[tid];
+      unsigned long long np = S.srcnp[tid], nn = S.srcnn[tid];
+      const int kq = tid % 8, kk = tid / 8;  // column tid = 8 kk + kq
+      for (int wq = 0; wq < DS_NW; ++wq)
+        for (int e = 0; e < ES; ++e) {
+          p += S.pacc[wq][kq][e * LPR + kk];
+          dm += S.pdead[wq][kq][e * LPR + kk];
+          const unsigned long long pk = S.pcnt[wq][kq][e * LPR + kk];
+          np += pk & ((1ull << 40) - 1);
+          nn += pk >> 40;
+        }
       if (p != 0.0) atomicAdd(&ctl->pushed[buf][tid], p);
-      if (S.dead[tid] != 0.0) atomicAdd(&ctl->dsum[buf][tid], S.dead[tid]);
-      if (S.np[tid]) atomicAdd(&ctl->npush[buf][tid], (unsigned long long)S.np[tid]);
-      if (S.nn[tid]) atomicAdd(&ctl->nnode[buf][tid], (unsigned long long)S.nn[tid]);
-      if (S.np[tid]) atomicAdd(&ctl->et[buf][tid], (unsigned long long)(S.np[tid] - S.nd[tid]));
+      if (dm != 0.0) atomicAdd(&ctl->dsum[buf][tid], dm);
+      if (np) atomicAdd(&ctl->npush[buf][tid], np);
+      if (nn) atomicAdd(&ctl->nnode[buf][tid], nn);
+      if (np) atomicAdd(&ctl->et[buf][tid], np - S.nd[tid]);
     }
     grid_barrier2(&ctl->gbar, ++gen);
     if (tid < K) {
