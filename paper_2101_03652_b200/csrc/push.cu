@@ -772,7 +772,7 @@ uint32_t ds_env(const char* name, int dflt, int lo) {
   return (uint32_t)(t < lo ? lo : t > (int)DS_IDS ? (int)DS_IDS : t);  // (a task's ids sit in shared memory)
 }
 uint32_t ds_task_edges() {
-  static const uint32_t v = ds_env("PPRG_DS_TASK", 256, 32);
+  static const uint32_t v = ds_env("PPRG_DS_TASK", 192, 32);
   return v;
 }
 uint32_t ds_piece_edges() {
