@@ -36,10 +36,13 @@
 
 namespace pprg {
 
-constexpr int DS_NT = 128;
+#ifndef PPRG_DS_NT
+#define PPRG_DS_NT 128
+#endif
+constexpr int DS_NT = PPRG_DS_NT;
 constexpr int DS_NW = DS_NT / 32;
 #ifndef PPRG_DS_G
-#define PPRG_DS_G 6
+#define PPRG_DS_G 8
 #endif
 constexpr int DS_G = PPRG_DS_G;  // 16-byte row loads in flight per lane
 constexpr uint32_t DS_IDS = 512;    // in-edges per task at most
@@ -101,8 +104,16 @@ struct DeltaParams {
   double thr[EMAX], lam[EMAX];
 };
 
+#ifndef PPRG_DS_GATHER_NA
+#define PPRG_DS_GATHER_NA 0  // 1: share gathers do not allocate in L1
+#endif
 __device__ __forceinline__ uint4 ld_share(const uint4* p) {
   uint4 v;
+#if PPRG_DS_GATHER_NA
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+#endif
   asm volatile("ld.global.v4.u32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
   return v;

@@ -1,0 +1,7 @@
+run() { tag=$1; shift; env "$@" timeout 300 python tools/ab_quick.py 2 > gpurun_out/c57_$tag.json 2>&1; echo "$tag $(tail -1 gpurun_out/c57_$tag.json | python -c "
+import sys,json
+d=json.loads(sys.stdin.read())['configs[2] 64-block']; print(round(d['sweep_ms'],1), d['max_sweeps'], round(d['sweep_ms']/d['max_sweeps'],3))")"; }
+for r in 1 2; do
+run base_$r
+for v in na g7 nt96 g5; do run ${v}_$r PPRG_LIB=$PWD/libv_$v/libpprg.so; done
+done
