@@ -17,7 +17,8 @@
 // stays exact, and the loop still ends at r_sum <= lambda: the 16-bit format
 // costs convergence rate (<0.4% of a row's residue left behind per push), not
 // accuracy. Sums of shares are formed in fp64 (a share's fp64 high word is
-// h << 12: decode is a shift and a mask, no conversion instruction).
+// h << 12: decode is one widening multiply per share, no conversion
+// instruction; see add_shares for the two shares of a word).
 //
 // Exactly-once. Every published share must be added by every out-neighbour
 // exactly once, so the asynchronous "read whatever is there" of k_sweeps is
@@ -25,12 +26,15 @@
 // shares are double-buffered by sweep parity; a row of wave w in sweep t reads
 //     d[t & 1][v]        if wave(v) <= w - L   (published earlier in this sweep)
 //     d[(t-1) & 1][v]    otherwise             (published in the previous sweep)
-// with lag L = 2: a tile of wave w starts once every tile of the waves <= w-2
-// has finished (per-wave completion counters, acquire/release), so wave w-1's
-// tail overlaps wave w's start and no grid barrier sits between waves. One
-// grid barrier per sweep closes the sweep (counters, epoch decisions), as in
-// k_sweeps. Gauss-Seidel between waves: 46-48 sweeps on configs[2] against 44.
+// with lag L >= 2 (default: 64 waves, L = 6): a task of wave w starts once
+// every task of the waves <= w-L has finished (per-wave completion counters,
+// release adds and one acquire per block and wave), so a wave's tail overlaps
+// the next waves' start and no grid barrier sits between waves. One grid
+// barrier per sweep closes the sweep (counters, epoch decisions), as in
+// k_sweeps. Gauss-Seidel between waves: 50 sweeps on configs[2] against 44.
 // After the last pushing sweep one more sweep consumes the shares in flight.
+// Work units are warp tasks (delta_task); the blocks only share per-column
+// state and the per-sweep sums.
 #pragma once
 #include "sweep_kernel.cuh"
 
@@ -53,23 +57,18 @@ constexpr uint32_t DS_TASK_R = 32;  // rows per task (lane i holds row i's data)
 constexpr uint32_t DS_SHORT = PPRG_DS_SHORT;  // rows up to this many in-edges: one lane group each
 constexpr int DS_WMAX = 64;         // waves per sweep
 constexpr int DS_EXP = 769;         // value(h) = fp64{h << 12, 0} * 2^769: e8m8 spans 2^-253 .. 4
-#ifndef PPRG_DS_PIPE
-#define PPRG_DS_PIPE 0  // 1: two batches of row loads in flight per lane (needs 4 blocks per SM: slower)
-#endif
+// A/B switches (tools/build_variant.sh; measured in profiles/r02_delta_history.txt)
 #ifndef PPRG_DS_PFROWS
-#define PPRG_DS_PFROWS 1
-#endif
-#ifndef PPRG_DS_HALF
-#define PPRG_DS_HALF 0
+#define PPRG_DS_PFROWS 1   // a task's share rows prefetched into L2 when its ids are staged
 #endif
 #ifndef PPRG_DS_PFTASK
-#define PPRG_DS_PFTASK 1
+#define PPRG_DS_PFTASK 1   // the next task's ids and row data prefetched into L2
 #endif
 #ifndef PPRG_DS_L1STATE
-#define PPRG_DS_L1STATE 1
+#define PPRG_DS_L1STATE 1  // state rows (r, x) prefetched into and read through L1 (0: L2)
 #endif
 #ifndef PPRG_DS_MINB
-#define PPRG_DS_MINB 5
+#define PPRG_DS_MINB 5     // blocks per SM (96 registers); 4 and 6 are both slower
 #endif
 
 struct DeltaParams {
