@@ -108,3 +108,31 @@ def test_delta_small_blocks_keep_the_sweeps_path(P, delta):
     b, _ = P.power_push_batch(g, src, ALPHA, 1e-8)
     for q in range(8):
         assert np.max(np.abs(a[q].estimates - b[q].estimates)) <= 1e-8
+
+
+def test_delta_on_the_chung_lu_graph_of_configs3(P, monkeypatch):
+    """A second graph family at full size (the 2^22-node Chung-Lu graph of
+    configs[3]: power-law in- and out-degrees, 124M edges): the automatic choice
+    is the delta sweeps, and they agree with k_sweeps (which the configs tests pin
+    to the reference) within lambda, with exact mass."""
+    import torch
+    n = 1 << 22
+    g = P.generate_chung_lu(n, 146 * n // 4, 4)
+    src = P.sample_sources(np.diff(g.out_offsets()), 64, 4)
+    lam = 1e-8
+    monkeypatch.delenv("PPRG_DELTA", raising=False)
+    assert g.uses_delta_sweeps(64)
+    k, nn = len(src), g.n()
+    a = torch.empty((2, k, nn), dtype=torch.float64, device="cuda:0")
+    b = torch.empty((2, k, nn), dtype=torch.float64, device="cuda:0")
+    oa, ca = P.power_push_batch(g, src, ALPHA, lam, device_out=(a[0].data_ptr(), a[1].data_ptr()))
+    monkeypatch.setenv("PPRG_DELTA", "0")
+    assert not g.uses_delta_sweeps(64)
+    ob, cb = P.power_push_batch(g, src, ALPHA, lam, device_out=(b[0].data_ptr(), b[1].data_ptr()))
+    assert float((a[0] - b[0]).abs().max().item()) <= lam
+    mass = a[0].sum(dim=1) + a[1].sum(dim=1)
+    assert float((mass - 1.0).abs().max().item()) < 1e-11
+    assert float(a[1].min().item()) >= 0.0
+    for q in range(k):
+        assert oa[q].achieved_r_sum <= lam and ob[q].achieved_r_sum <= lam
+        assert abs(float(a[1][q].sum().item()) - oa[q].achieved_r_sum) <= 1e-12
